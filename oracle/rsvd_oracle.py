@@ -1,0 +1,398 @@
+"""ORACLE — test infrastructure only.
+
+A plain, slow, obviously-correct fp64 CPU implementation of the pass-efficient randomized
+SVD algorithms of arXiv 1804.07531 (Bjarkason, "Pass-efficient randomized algorithms for
+low-rank matrix approximation using any number of views").  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` leg may
+import it.  It shares no code with the CUDA path (``paper_1804_07531_b200``).
+
+Notation follows the paper (PAPER.md lines noted as P:<line>):
+    A is n_r x n_c; p = target rank; l = oversampling (sketch width p + l);
+    Omega_r is the range test matrix (n_c x (p+l)); Omega_c the co-range one (n_r x (p+l2)).
+The C ABI (BASELINE.json) calls the same two integers (k, p) — positionally identical:
+    oracle (p, l)  ==  ABI (k, p).
+
+Every routine is in float64 regardless of the input dtype (fp32 inputs are upcast once, so the
+oracle gives the exact-arithmetic answer for the given fp32 bytes).
+
+Conventions the paper leaves open:
+  * qr: Householder (numpy/LAPACK), thin, signs normalised so diag(R) >= 0 (reading R1).
+  * tsvd: LAPACK SVD, singular values descending (reading R2).
+  * Random test matrices are INPUTS (reading R3): the caller passes Omega_r / Omega_c, which
+    replace the paper's randn calls.
+
+Pins: see tests/test_oracle_pins.py.  Parity unpinned: the actual values of the randomized
+outputs on noisy / slowly decaying inputs have no closed form; they are pinned only indirectly
+(exact-rank recovery, diagonal closed forms, Alg.2==Alg.1 / Alg.9==Alg.2 identities, brute
+force at full sampling, Thm A.1, the Thm 3.1/4.1 bounds).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = [
+    "qr", "orth", "tsvd", "chol_lower", "jacobi_svd",
+    "std_subspace_iteration", "gen_subspace_iteration", "qrqc", "one_view_tropp",
+    "gen_block_krylov", "normal_matrix_tevd", "recommend_input", "svd_of",
+    "views_and_vectors", "rel_frobenius_error", "rel_spectral_error", "projector_distance",
+    "residual_fro", "half_power_lhs_rhs", "thm_bound",
+    "GOAL_SVD", "GOAL_LEFT", "GOAL_RIGHT", "GOAL_NORMAL",
+]
+
+
+# ============================================================ dense primitives
+
+def _f64(M) -> np.ndarray:
+    return np.asarray(M, dtype=np.float64)
+
+
+def qr(M):
+    """[Q, R] = qr(M): thin QR, Q n_r x n_c orthonormal, R n_c x n_c upper triangular.
+
+    Householder via LAPACK; column signs normalised so diag(R) >= 0 (reading R1: the paper
+    defines qr without a sign)."""
+    M = _f64(M)
+    Q, R = np.linalg.qr(M, mode="reduced")
+    s = np.where(np.diag(R) < 0, -1.0, 1.0)
+    return Q * s, R * s[:, None]
+
+
+def orth(M):
+    """Q = orth(M): orthonormal basis of range(M).  Used only where the paper writes orth;
+    for full-column-rank M this is qr(M).Q."""
+    return qr(M)[0]
+
+
+def tsvd(M, p):
+    """[U_p, Lambda_p, V_p] = tsvd(M, p): exact rank-p truncated SVD, M = U Lambda V^* (P:67)."""
+    M = _f64(M)
+    U, s, Vt = np.linalg.svd(M, full_matrices=False)
+    return U[:, :p], s[:p], Vt[:p, :].T
+
+
+def chol_lower(S):
+    """C_L = chol(S, LOWER) with S = C_L C_L^* (P:69); plain column Cholesky–Banachiewicz."""
+    S = _f64(S)
+    n = S.shape[0]
+    L = np.zeros_like(S)
+    for j in range(n):
+        d = S[j, j] - np.dot(L[j, :j], L[j, :j])
+        if d <= 0.0:
+            raise np.linalg.LinAlgError("chol: non-positive pivot")
+        L[j, j] = np.sqrt(d)
+        for i in range(j + 1, n):
+            L[i, j] = (S[i, j] - np.dot(L[i, :j], L[j, :j])) / L[j, j]
+    return L
+
+
+def jacobi_svd(M, tol=None, max_sweeps=60):
+    """Full SVD by cyclic one-sided (Hestenes) Jacobi: orthogonalise the columns of W = M J by
+    plane rotations until every pair is orthogonal to ``tol``; then sigma_i = ||W_i||,
+    U_i = W_i / sigma_i, V = J.  Independent of LAPACK; used to brute-force small cases."""
+    W = _f64(M).copy()
+    n_r, n_c = W.shape
+    transposed = False
+    if n_r < n_c:
+        W = W.T.copy()
+        n_r, n_c = n_c, n_r
+        transposed = True
+    J = np.eye(n_c)
+    tol = (n_c * np.finfo(np.float64).eps) if tol is None else tol
+    for _ in range(max_sweeps):
+        rotated = False
+        for i in range(n_c - 1):
+            for j in range(i + 1, n_c):
+                a = np.dot(W[:, i], W[:, i])
+                b = np.dot(W[:, j], W[:, j])
+                c = np.dot(W[:, i], W[:, j])
+                if abs(c) <= tol * np.sqrt(a * b) or c == 0.0:
+                    continue
+                rotated = True
+                zeta = (b - a) / (2.0 * c)
+                t = np.sign(zeta) / (abs(zeta) + np.sqrt(1.0 + zeta * zeta)) if zeta != 0 else 1.0
+                cs = 1.0 / np.sqrt(1.0 + t * t)
+                sn = cs * t
+                wi, wj = W[:, i].copy(), W[:, j].copy()
+                W[:, i] = cs * wi - sn * wj
+                W[:, j] = sn * wi + cs * wj
+                ji, jj = J[:, i].copy(), J[:, j].copy()
+                J[:, i] = cs * ji - sn * jj
+                J[:, j] = sn * ji + cs * jj
+        if not rotated:
+            break
+    else:
+        raise RuntimeError("jacobi_svd: not converged")
+    s = np.sqrt(np.sum(W * W, axis=0))
+    order = np.argsort(-s, kind="stable")
+    s = s[order]
+    W = W[:, order]
+    J = J[:, order]
+    U = np.zeros_like(W)
+    nz = s > 0
+    U[:, nz] = W[:, nz] / s[nz]
+    if transposed:
+        return J, s, U
+    return U, s, J
+
+
+# ============================================================ matrix access ("views")
+
+class _Op:
+    """A or its transpose as the algorithm's input matrix (P:198 'with either J or J^* as input').
+
+    ``apply(X)`` = (input) X ; ``adjoint(Y)`` = (input)^* Y.  Each call is one matrix view."""
+
+    def __init__(self, A, transpose=False):
+        self.A = _f64(A)
+        self.T = bool(transpose)
+        self.views = 0
+        self.vectors = 0
+
+    @property
+    def shape(self):
+        r, c = self.A.shape
+        return (c, r) if self.T else (r, c)
+
+    def apply(self, X):
+        self.views += 1
+        self.vectors += X.shape[1]
+        return (self.A.T @ X) if self.T else (self.A @ X)
+
+    def adjoint(self, Y):
+        self.views += 1
+        self.vectors += Y.shape[1]
+        return (self.A @ Y) if self.T else (self.A.T @ Y)
+
+
+# ============================================================ Algorithm 1
+
+def std_subspace_iteration(A, p, l, q, Omega_r, transpose=False, _op=None):
+    """Alg. 1 — randomized SVD using standard subspace iteration, 2(q+1) views.
+
+    Returns (U_p, Lambda_p, V_p) of the input matrix (A, or A^* if transpose)."""
+    op = _op or _Op(A, transpose)
+    Omega_r = _f64(Omega_r)
+    Qc, _ = qr(op.apply(Omega_r))                 # line 2
+    for _j in range(q):                           # lines 3-6
+        Qr, _ = qr(op.adjoint(Qc))
+        Qc, _ = qr(op.apply(Qr))
+    Qr, Rr = qr(op.adjoint(Qc))                   # line 7
+    Vh, lam, Uh = tsvd(Rr, p)                     # line 8: R_r = Vh Lam Uh^*
+    return Qc @ Uh, lam, Qr @ Vh                  # line 9
+
+
+# ============================================================ Algorithm 2
+
+def gen_subspace_iteration(A, p, l, v, Omega_r, transpose=False, _op=None):
+    """Alg. 2 — randomized SVD using generalized subspace iteration, any v >= 2.
+
+    Omega_r (n_c x (p+l)) replaces line 1's randn.  Returns (U_p, Lambda_p, V_p) of the input
+    matrix; odd j: [Q_c,R_c] = qr(A Q_r); even j: [Q_r,R_r] = qr(A^* Q_c)."""
+    if v < 2:
+        raise ValueError("Alg. 2 needs v >= 2 (P:142)")
+    op = _op or _Op(A, transpose)
+    Qr = _f64(Omega_r)                            # line 1
+    Qc = Rc = Rr = None
+    for j in range(1, v + 1):                     # lines 2-8
+        if j % 2 == 1:
+            Qc, Rc = qr(op.apply(Qr))
+        else:
+            Qr, Rr = qr(op.adjoint(Qc))
+    if v % 2 == 0:                                # lines 9-13
+        Vh, lam, Uh = tsvd(Rr, p)                 # R_r = Vh Lam Uh^*
+    else:
+        Uh, lam, Vh = tsvd(Rc, p)                 # R_c = Uh Lam Vh^*
+    return Qc @ Uh, lam, Qr @ Vh                  # line 14
+
+
+def qrqc(A, p, l, v, Omega_r, transpose=False, _op=None):
+    """Alg. 3 — QrQc: approximate range (v odd, returns Q_c) or co-range (v even, returns Q_r)
+    basis after v views."""
+    op = _op or _Op(A, transpose)
+    Qr = _f64(Omega_r)
+    Qc = None
+    for j in range(1, v + 1):
+        if j % 2 == 1:
+            Qc, _ = qr(op.apply(Qr))
+        else:
+            Qr, _ = qr(op.adjoint(Qc))
+    return Qr if v % 2 == 0 else Qc
+
+
+# ============================================================ Algorithm 7
+
+def one_view_tropp(A, p, l1, l2, lc, Omega_r, Omega_c, transpose=False, _op=None):
+    """Alg. 7 — randomized 1-view TSVD, Tropp variant with truncation parameter l_c.
+
+    Omega_r: n_c x (p+l1); Omega_c: n_r x (p+l2); 0 <= lc <= l1 <= l2.  lc = l1 gives the
+    baseline [Tropp Alg. 7].  The optional orth of the test matrices (line 2) is off
+    ('not used for the experiments').  Line 3's a) and b) are one logical pass; the
+    oracle counts it as one view."""
+    if not (0 <= lc <= l1 <= l2):
+        raise ValueError("Alg. 7 needs 0 <= l_c <= l_1 <= l_2 (P:663)")
+    op = _op or _Op(A, transpose)
+    Omega_r = _f64(Omega_r)
+    Omega_c = _f64(Omega_c)
+    Yc = op.apply(Omega_r)                        # line 3 a)
+    Yr = op.adjoint(Omega_c)                      # line 3 b)
+    op.views -= 1                                 # a) and b) together are ONE view
+    if lc < l1:                                   # lines 4-7
+        Qc, Rc = qr(Yc)
+        Qhc, _, _ = tsvd(Rc, p + lc)
+        Qc = Qc @ Qhc
+    else:                                         # line 9
+        Qc, _ = qr(Yc)
+    Qh, Rh = qr(Omega_c.T @ Qc)                   # line 11
+    X = np.linalg.solve(Rh, Qh.T @ Yr.T)          # line 12: X = Rh^{-1} Qh^* Y_r^*
+    Uh, lam, Vp = tsvd(X, p)                      # line 13
+    return Qc @ Uh, lam, Vp                       # line 14
+
+
+# ============================================================ Algorithm 9
+
+def gen_block_krylov(A, p, l, v, Omega_r, transpose=False, _op=None, return_basis=False):
+    """Alg. 9 — randomized SVD using the generalized block Krylov method, any v >= 2.
+
+    Blocks Q^j for j < v-1 are orthonormalised, the last block Q^{v-1} is left raw (lines 3-4);
+    K_c = [Q_c^1 Q_c^3 ... Q_c^{v-1}] (v even) or K_r = [Q_r^2 ... Q_r^{v-1}] (v odd) is
+    orthonormalised with qr (lines 9/14), then one more view and a tsvd."""
+    if v < 2:
+        raise ValueError("Alg. 9 needs v >= 2 (P:903)")
+    op = _op or _Op(A, transpose)
+    Q = {0: _f64(Omega_r)}                        # line 1: Q_r^0
+    for j in range(1, v):                         # lines 2-7
+        if j % 2 == 1:
+            B = op.apply(Q[j - 1])
+        else:
+            B = op.adjoint(Q[j - 1])
+        Q[j] = qr(B)[0] if j < v - 1 else B
+    if v % 2 == 0:                                # lines 8-12
+        Kc = np.hstack([Q[j] for j in range(1, v, 2)])
+        Qc, _ = qr(Kc)
+        Qr, Rr = qr(op.adjoint(Qc))
+        Vh, lam, Uh = tsvd(Rr, p)
+    else:                                         # lines 13-17
+        Kr = np.hstack([Q[j] for j in range(2, v, 2)])
+        Qr, _ = qr(Kr)
+        Qc, Rc = qr(op.apply(Qr))
+        Uh, lam, Vh = tsvd(Rc, p)
+    out = (Qc @ Uh, lam, Qr @ Vh)                 # line 18
+    if return_basis:
+        return out, (Qc, Qr)
+    return out
+
+
+# ============================================================ orientation / outputs
+
+GOAL_SVD, GOAL_LEFT, GOAL_RIGHT, GOAL_NORMAL = 0, 1, 2, 3
+
+
+def recommend_input(goal, v):
+    """Which matrix to feed Alg. 2/9 (0 = A, 1 = A^*):
+    even v: V (right) more accurate -> RIGHT/NORMAL use A; odd v: U more accurate -> use A^*.
+    LEFT goal uses the reverse rule.  SVD: A."""
+    if goal in (GOAL_RIGHT, GOAL_NORMAL):
+        return 0 if v % 2 == 0 else 1
+    if goal == GOAL_LEFT:
+        return 1 if v % 2 == 0 else 0
+    return 0
+
+
+def svd_of(A, algorithm, k, p, v=None, Omega=None, l2=None, lc=None, Phi=None, transpose=False):
+    """Run an algorithm on A (transpose=False) or on A^* (transpose=True) and return the TSVD
+    of A itself: (U, sigma, V) with A ~ U diag(sigma) V^T.  When the algorithm ran on A^*, its
+    (U, V) are A's (V, U) (reading R6)."""
+    op = _Op(A, transpose)
+    if algorithm == "subspace":
+        U, s, V = gen_subspace_iteration(None, k, p, v, Omega, _op=op)
+    elif algorithm == "krylov":
+        U, s, V = gen_block_krylov(None, k, p, v, Omega, _op=op)
+    elif algorithm == "single_pass":
+        lc = p if lc is None else lc
+        U, s, V = one_view_tropp(None, k, p, l2 - k, lc, Omega, Phi, _op=op)
+    else:
+        raise ValueError(algorithm)
+    if transpose:
+        U, V = V, U
+    return U, s, V, op
+
+
+def normal_matrix_tevd(A, k, p, v, Omega, algorithm="subspace", transpose=None):
+    """Normal-matrix estimate A^T A ~ V diag(sigma^2) V^T from Alg. 2/9 in the recommended
+    orientation: input = A for even v, A^* for odd v.
+    Returns (V, sigma^2)."""
+    if transpose is None:
+        transpose = bool(recommend_input(GOAL_NORMAL, v))
+    _, s, V, _ = svd_of(A, algorithm, k, p, v=v, Omega=Omega, transpose=transpose)
+    return V, s * s
+
+
+def views_and_vectors(algorithm, v, width):
+    """(views, matrix-vector products) of each algorithm: Alg. 2 uses v views and
+    v (p+l) vectors; Alg. 9 uses v views and (v + floor(v/2) - 1)(p+l) vectors; Alg. 7 one view
+    (its two sketches are counted as vectors l + l2 by the caller)."""
+    if algorithm == "subspace":
+        return v, v * width
+    if algorithm == "krylov":
+        return v, (v + v // 2 - 1) * width
+    raise ValueError(algorithm)
+
+
+# ============================================================ error metrics
+
+def rel_frobenius_error(A, Ahat, p):
+    """||A - Ahat||_F / ||A - [[A]]_p||_F - 1."""
+    A = _f64(A)
+    s = np.linalg.svd(A, compute_uv=False)
+    return np.linalg.norm(A - Ahat) / np.sqrt(np.sum(s[p:] ** 2)) - 1.0
+
+
+def rel_spectral_error(A, Ahat, p):
+    """||A - Ahat|| / ||A - [[A]]_p|| - 1."""
+    A = _f64(A)
+    s = np.linalg.svd(A, compute_uv=False)
+    return np.linalg.norm(A - Ahat, 2) / s[p] - 1.0
+
+
+def projector_distance(U, Uo):
+    """||U U^T - Uo Uo^T||_F computed stably as sqrt(2) ||U - Uo (Uo^T U)||_F for U, Uo with
+    orthonormal columns of equal count (SURVEY c-14): sign- and rotation-invariant."""
+    U = _f64(U)
+    Uo = _f64(Uo)
+    return float(np.sqrt(2.0) * np.linalg.norm(U - Uo @ (Uo.T @ U)))
+
+
+def residual_fro(A, U, s, V, panel=4096):
+    """||A - U diag(s) V^T||_F by an explicit pass over A (row panels)."""
+    A = np.asarray(A)
+    U = _f64(U)
+    V = _f64(V)
+    tot = 0.0
+    for r0 in range(0, A.shape[0], panel):
+        r1 = min(A.shape[0], r0 + panel)
+        D = _f64(A[r0:r1]) - (U[r0:r1] * s) @ V.T
+        tot += float(np.sum(D * D))
+    return float(np.sqrt(tot))
+
+
+# ============================================================ theory checks
+
+def half_power_lhs_rhs(A, Qr, q):
+    """Thm A.1: ||A (I - Q_r Q_r^*)||^{2q} <= ||(A^*A)^q (I - Q_r Q_r^*)||.
+    Returns (lhs, rhs)."""
+    A = _f64(A)
+    P = np.eye(A.shape[1]) - Qr @ Qr.T
+    lhs = np.linalg.norm(A @ P, 2) ** (2 * q)
+    AtA = A.T @ A
+    rhs = np.linalg.norm(np.linalg.matrix_power(AtA, q) @ P, 2)
+    return lhs, rhs
+
+
+def thm_bound(sig, p, l, e):
+    """Right-hand side of Thm 3.1 / 4.1 and the even/odd bounds (P:110-118, P:182-190,
+    P:210-243) with exponent e (= 2q+1, 2q, v-1 or v):
+    [ (1 + sqrt(p/(l-1))) sig_{p+1}^e + e_const sqrt(p+l)/l (sum_{j>p} sig_j^{2e})^{1/2} ]^{1/e}."""
+    sig = _f64(sig)
+    t1 = (1.0 + np.sqrt(p / (l - 1.0))) * sig[p] ** e
+    t2 = np.e * np.sqrt(p + l) / l * np.sqrt(np.sum(sig[p:] ** (2 * e)))
+    return (t1 + t2) ** (1.0 / e)

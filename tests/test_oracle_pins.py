@@ -1,0 +1,420 @@
+"""Pins for the CPU oracle (-m "not gpu").
+
+Each test ties the oracle to something other than itself: worked values (tests/golden), closed
+forms, exact identities stated by the paper, brute force at full sampling, the paper's
+inequalities, or an independent route to the same quantity.  Citations are PAPER.md lines (P:).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+from scipy.sparse.linalg import LinearOperator, eigsh
+
+import oracle as O
+import synth as S
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "micro_cases.json")))
+
+
+def proj(U, Uo):
+    return O.projector_distance(U, Uo)
+
+
+def spec_norm_resid(A, Q, side):
+    """|| A - Q Q^T A || (side='c') or || A - A Q Q^T || (side='r') by Lanczos on the Gram op."""
+    if side == "c":
+        R = A - Q @ (Q.T @ A)
+    else:
+        R = A - (A @ Q) @ Q.T
+    n = R.shape[1]
+    op = LinearOperator((n, n), matvec=lambda x: R.T @ (R @ x), dtype=np.float64)
+    w = eigsh(op, k=1, which="LA", tol=1e-10, return_eigenvectors=False)
+    return float(np.sqrt(max(w[0], 0.0)))
+
+
+# ------------------------------------------------------------------ golden micro cases
+
+def test_golden_qr():
+    g = GOLD["qr_3_4"]
+    Q, R = O.qr(np.array(g["M"]))
+    np.testing.assert_allclose(Q, g["Q"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(R, g["R"], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("case", ["svd_perm_diag", "svd_diag_3_1"])
+def test_golden_svd(case):
+    g = GOLD[case]
+    M = np.array(g["M"])
+    for U, s, V in (O.tsvd(M, 2), O.jacobi_svd(M)):
+        np.testing.assert_allclose(s, g["sigma"], rtol=0, atol=1e-15)
+        np.testing.assert_allclose((U * s) @ V.T, M, atol=1e-15)
+        if "U_abs" in g:
+            np.testing.assert_allclose(np.abs(U), g["U_abs"], atol=1e-15)
+            np.testing.assert_allclose(np.abs(V), g["V_abs"], atol=1e-15)
+
+
+def test_golden_chol():
+    g = GOLD["chol_4_2_5"]
+    np.testing.assert_allclose(O.chol_lower(np.array(g["S"])), g["L"], atol=1e-15)
+
+
+def test_golden_diag_full_sampling():
+    g = GOLD["diag_54321_rank2"]
+    A = np.diag(g["d"])
+    Om = S.gaussian((5, g["p"] + g["l"]), 9, S.ROLE_OMEGA)
+    for v in (2, 3, 4):
+        _, s, _ = O.gen_subspace_iteration(A, g["p"], g["l"], v, Om)
+        np.testing.assert_allclose(s, g["sigma"], rtol=1e-13)
+    _, s, _ = O.std_subspace_iteration(A, g["p"], g["l"], 1, Om)
+    np.testing.assert_allclose(s, g["sigma"], rtol=1e-13)
+
+
+# ------------------------------------------------------------------ P3 orthonormality / QR contract
+
+@pytest.mark.parametrize("shape", [(50, 10), (300, 40), (17, 17)])
+def test_qr_contract(shape):
+    M = S.random_gaussian_matrix(*shape, seed=shape[0])
+    Q, R = O.qr(M)
+    assert Q.shape == shape and R.shape == (shape[1], shape[1])
+    np.testing.assert_allclose(Q.T @ Q, np.eye(shape[1]), atol=1e-14)
+    assert np.all(np.tril(R, -1) == 0.0)
+    assert np.all(np.diag(R) >= 0.0)
+    assert np.linalg.norm(Q @ R - M) <= 1e-14 * np.linalg.norm(M)
+
+
+def test_chol_reconstruct():
+    G = S.random_gaussian_matrix(6, 6, seed=3)
+    Sm = G.T @ G + np.eye(6)
+    L = O.chol_lower(Sm)
+    assert np.allclose(np.triu(L, 1), 0)
+    assert np.linalg.norm(L @ L.T - Sm) <= 1e-13 * np.linalg.norm(Sm)
+
+
+def test_jacobi_svd_closed_form():
+    """Jacobi SVD of U diag(d) V^T returns d (known spectrum) and the same subspaces."""
+    d = np.array([7.0, 3.0, 2.5, 1.0, 0.5, 1e-3])
+    A = S.exact_rank_matrix(9, 6, d, seed=1)
+    U, s, V = O.jacobi_svd(A)
+    np.testing.assert_allclose(s, d, rtol=1e-13, atol=1e-14 * d[0])  # A itself carries eps*||A|| rounding
+    X, Y = S.exact_rank_factors(9, 6, 6, seed=1)
+    # the sigma=1e-3 direction moves by ~eps*||A||/sigma_6 ~ 1e-12 under A's own rounding
+    assert proj(U, X) < 1e-11 and proj(V, Y) < 1e-11
+
+
+def test_jacobi_matches_eigensolve():
+    """sigma(M)^2 = eig(M^T M): brute-force symmetric eigensolve (S:75 oracle)."""
+    M = S.random_gaussian_matrix(8, 6, seed=5)
+    _, s, _ = O.jacobi_svd(M)
+    ev = np.sort(np.linalg.eigvalsh(M.T @ M))[::-1]
+    np.testing.assert_allclose(s ** 2, ev, rtol=1e-12)
+    _, s2, _ = O.jacobi_svd(M.T)
+    np.testing.assert_allclose(s, s2, rtol=1e-13)
+
+
+# ------------------------------------------------------------------ P5 brute force on tiny inputs
+
+ALGS = [("subspace", 2), ("subspace", 3), ("subspace", 4), ("subspace", 5),
+        ("krylov", 2), ("krylov", 3), ("krylov", 4), ("krylov", 5)]
+
+
+@pytest.mark.parametrize("shape", [(12, 9), (9, 12), (10, 10)])
+@pytest.mark.parametrize("alg,v", ALGS)
+def test_full_sampling_equals_full_svd(shape, alg, v):
+    """l = min(m,n): the sketch spans the whole (co-)range, so the randomized TSVD equals the
+    exact TSVD, computed here by the oracle's own Jacobi (independent of LAPACK).  Krylov with
+    widths > min(m,n) is skipped (qr needs rows >= cols)."""
+    m, n = shape
+    N = min(m, n)
+    k = 3
+    A = S.random_gaussian_matrix(m, n, seed=m * 100 + n)
+    Om = S.gaussian((n, N), 11, S.ROLE_OMEGA)
+    if alg == "krylov":
+        kw = (v // 2) * N if v % 2 == 0 else ((v - 1) // 2) * N
+        if kw > N:
+            pytest.skip("Krylov basis wider than the space")
+    U, s, V, _ = O.svd_of(A, alg, k, N - k, v=v, Omega=Om)
+    Uj, sj, Vj = O.jacobi_svd(A)
+    np.testing.assert_allclose(s, sj[:k], rtol=1e-12)
+    assert proj(U, Uj[:, :k]) < 1e-11
+    assert proj(V, Vj[:, :k]) < 1e-11
+
+
+def test_single_pass_full_sampling():
+    m, n, k = 12, 10, 3
+    A = S.random_gaussian_matrix(m, n, seed=77)
+    Om = S.gaussian((n, n), 12, S.ROLE_OMEGA)
+    Phi = S.gaussian((m, m), 12, S.ROLE_PHI)
+    U, s, V, _ = O.svd_of(A, "single_pass", k, n - k, Omega=Om, l2=m, Phi=Phi)
+    Uj, sj, Vj = O.jacobi_svd(A)
+    np.testing.assert_allclose(s, sj[:k], rtol=1e-11)
+    assert proj(U, Uj[:, :k]) < 1e-10 and proj(V, Vj[:, :k]) < 1e-10
+
+
+# ------------------------------------------------------------------ P1 exact rank-r recovery
+
+@pytest.mark.parametrize("alg,v", ALGS + [("single_pass", 1)])
+@pytest.mark.parametrize("r_is", ["k", "l"])
+def test_exact_rank_recovery(alg, v, r_is):
+    m, n, k, p = 120, 90, 5, 5
+    l = k + p
+    r = k if r_is == "k" else l
+    sig = np.linspace(3.0, 1.0, r) * np.array([1.0 + 0.1 * i for i in range(r)])[::-1] / 2.0
+    sig = np.sort(sig)[::-1]
+    A = S.exact_rank_matrix(m, n, sig, seed=r)
+    X, Y = S.exact_rank_factors(m, n, r, seed=r)
+    Om = S.gaussian((n, l), 20 + r, S.ROLE_OMEGA)
+    Phi = S.gaussian((m, 2 * l), 20 + r, S.ROLE_PHI)
+    U, s, V, _ = O.svd_of(A, alg, k, p, v=v, Omega=Om, l2=2 * l, Phi=Phi)
+    np.testing.assert_allclose(s, sig[:k], rtol=1e-12)
+    assert proj(U, X[:, :k]) < 1e-11 and proj(V, Y[:, :k]) < 1e-11
+    res = O.residual_fro(A, U, s, V)
+    floor = np.sqrt(np.sum(sig[k:] ** 2))
+    assert abs(res - floor) <= 1e-12 * np.linalg.norm(sig)
+
+
+# ------------------------------------------------------------------ P2 diagonal closed forms
+
+def test_diagonal_structured_omega_exact():
+    """A = diag(d), Omega = I[:, :l]: every sketch is diag(d)[:, :l], every Q = I[:, :l], every
+    R = diag(d_1..d_l): sigma = d[:k] and U = V = I[:, :k] (up to sign) in every algorithm."""
+    n, k, p = 40, 4, 3
+    l = k + p
+    d = S.paper_poly(n, R=1, rho=1.5)[::-1].copy()[::-1]  # strictly decreasing
+    d = np.sort(d)[::-1] * np.linspace(1.0, 0.5, n)
+    A = np.diag(d)
+    Om = np.eye(n)[:, :l]
+    Phi = np.eye(n)[:, :2 * l]
+    E = np.eye(n)[:, :k]
+    for alg, v in ALGS + [("single_pass", 1)]:
+        U, s, V, _ = O.svd_of(A, alg, k, p, v=v, Omega=Om, l2=2 * l, Phi=Phi)
+        np.testing.assert_allclose(s, d[:k], rtol=2e-16, atol=0)
+        np.testing.assert_allclose(np.abs(U), E, atol=1e-15)
+        np.testing.assert_allclose(np.abs(V), E, atol=1e-15)
+
+
+@pytest.mark.parametrize("spec", ["polyfast", "polyslow", "expslow", "expfast"])
+@pytest.mark.parametrize("v", [2, 3, 4])
+def test_eckart_young_floor(spec, v):
+    """||A - U S V^T||_F >= sqrt(sum_{i>p} d_i^2) (optimality of [[A]]_p), on the paper's
+    diagonal test matrices, n = 300, R = 10, p = l = 10 (P:1014 setting)."""
+    n = 300
+    d = {"polyfast": S.paper_poly(n, 10, 2.0), "polyslow": S.paper_poly(n, 10, 1.0),
+         "expslow": S.paper_exp(n, 10, 0.25), "expfast": S.paper_exp(n, 10, 1.0)}[spec]
+    A = np.diag(d)
+    Om = S.gaussian((n, 20), 30, S.ROLE_OMEGA, v)
+    U, s, V, _ = O.svd_of(A, "subspace", 10, 10, v=v, Omega=Om)
+    floor = np.sqrt(np.sum(d[10:] ** 2))
+    assert O.residual_fro(A, U, s, V) >= floor - 1e-12
+    assert np.all(s <= d[:10] + 1e-14)   # Ritz values never exceed the true singular values
+
+
+# ------------------------------------------------------------------ P4 identities and counts
+
+@pytest.mark.parametrize("q", [0, 1, 2])
+def test_alg2_even_equals_alg1(q):
+    """Alg. 2 with v = 2(q+1) IS Alg. 1 with q iterations: bitwise."""
+    cfg = S.CONFIGS["C1"]
+    A = S.make_matrix(cfg)
+    Om = S.gaussian_test_matrix(cfg.n, cfg.l, cfg, S.ROLE_OMEGA)
+    U1, s1, V1 = O.std_subspace_iteration(A, cfg.k, cfg.p, q, Om)
+    U2, s2, V2 = O.gen_subspace_iteration(A, cfg.k, cfg.p, 2 * (q + 1), Om)
+    assert np.array_equal(s1, s2) and np.array_equal(U1, U2) and np.array_equal(V1, V2)
+
+
+@pytest.mark.parametrize("v", [2, 3])
+def test_alg9_equals_alg2_below_4(v):
+    """Alg. 9 'is the same as Alg. 2 for v < 4': bitwise."""
+    cfg = S.CONFIGS["C1"]
+    A = S.make_matrix(cfg)
+    Om = S.gaussian_test_matrix(cfg.n, cfg.l, cfg, S.ROLE_OMEGA)
+    a = O.gen_subspace_iteration(A, cfg.k, cfg.p, v, Om)
+    b = O.gen_block_krylov(A, cfg.k, cfg.p, v, Om)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("v", [2, 3, 4, 5, 6])
+def test_view_and_vector_counts(v):
+    """Alg. 2: v views, v(p+l) vectors; Alg. 9: v views, (v + floor(v/2) - 1)(p+l) vectors."""
+    A = S.random_gaussian_matrix(80, 60, seed=v)
+    w = 6
+    Om = S.gaussian((60, w), 40, S.ROLE_OMEGA)
+    _, _, _, op = O.svd_of(A, "subspace", 3, 3, v=v, Omega=Om)
+    assert (op.views, op.vectors) == O.views_and_vectors("subspace", v, w) == (v, v * w)
+    _, _, _, op = O.svd_of(A, "krylov", 3, 3, v=v, Omega=Om)
+    assert (op.views, op.vectors) == O.views_and_vectors("krylov", v, w) == (v, (v + v // 2 - 1) * w)
+    Phi = S.gaussian((80, 2 * w), 40, S.ROLE_PHI)
+    _, _, _, op = O.svd_of(A, "single_pass", 3, 3, Omega=Om, l2=2 * w, Phi=Phi)
+    assert op.views == 1 and op.vectors == 3 * w
+
+
+@pytest.mark.parametrize("trial", range(20))
+def test_half_power_inequality(trial):
+    """Thm A.1 holds deterministically for ANY orthonormal Q_r and q >= 1."""
+    m, n = 30, 20
+    A = S.random_gaussian_matrix(m, n, seed=500 + trial) * np.linspace(2.0, 0.1, n)
+    Qr = np.linalg.qr(S.random_gaussian_matrix(n, 5, seed=600 + trial))[0]
+    for q in (1, 2, 3):
+        lhs, rhs = O.half_power_lhs_rhs(A, Qr, q)
+        assert lhs <= rhs * (1 + 1e-10)
+
+
+def test_half_power_on_alg_basis():
+    """Thm A.1 with the Q_r Alg. 3 actually produces (v = 2q views)."""
+    A = np.diag(S.paper_poly(200, 10, 1.0))
+    for q in (1, 2):
+        Om = S.gaussian((200, 12), 41, S.ROLE_OMEGA, q)
+        Qr = O.qrqc(A, 6, 6, 2 * q, Om)
+        lhs, rhs = O.half_power_lhs_rhs(A, Qr, q)
+        assert lhs <= rhs * (1 + 1e-10)
+
+
+# ------------------------------------------------------------------ statistical (Thm 3.1/4.1, Fig. 2/5 trends)
+
+def _mean_errors(A, v, trials, p=10, l=10, alg="subspace"):
+    ec, er = [], []
+    n = A.shape[1]
+    for t in range(trials):
+        Om = S.gaussian((n, p + l), 50, S.ROLE_OMEGA, v, t)
+        if alg == "subspace":
+            (_, _, _), (Qc, Qr) = _bases_subspace(A, p, l, v, Om)
+        else:
+            _, (Qc, Qr) = O.gen_block_krylov(A, p, l, v, Om, return_basis=True)
+        ec.append(spec_norm_resid(A, Qc, "c"))
+        er.append(spec_norm_resid(A, Qr, "r"))
+    return float(np.mean(ec)), float(np.mean(er))
+
+
+def _bases_subspace(A, p, l, v, Om):
+    Qr = Om
+    Qc = None
+    for j in range(1, v + 1):
+        if j % 2:
+            Qc = O.qr(A @ Qr)[0]
+        else:
+            Qr = O.qr(A.T @ Qc)[0]
+    return (None, None, None), (Qc, Qr)
+
+
+@pytest.mark.parametrize("name", ["polyslow", "lowrankmed"])
+def test_expected_error_bounds_and_monotone(name):
+    """Means over 20 calls of ||A - Q_c Q_c^* A|| and ||A - A Q_r Q_r^*|| lie below the
+    even/odd-view bounds (Thm 3.1/4.1) and decrease with v (Fig. 2).
+    Paper setting: n = 1000, R = 10, target rank p = 10, oversampling l = 10."""
+    n, p, l = 1000, 10, 10
+    if name == "polyslow":
+        d = S.paper_poly(n, 10, 1.0)
+        A = np.diag(d)
+    else:
+        A = S.paper_lowrank_noise(n, 10, 1e-2)
+        d = np.linalg.svd(A, compute_uv=False)
+    prev = None
+    for v in (2, 3, 4, 5):
+        mc, mr = _mean_errors(A, v, trials=20)
+        ec, er = (v - 1, v) if v % 2 == 0 else (v, v - 1)
+        assert mc <= O.thm_bound(d, p, l, ec)
+        assert mr <= O.thm_bound(d, p, l, er)
+        cur = max(mc, mr)
+        if prev is not None:
+            assert cur <= prev * 1.0001
+        prev = cur
+        # a (p+l)-dimensional basis never beats [[A]]_{p+l}: error >= sigma_{p+l+1}
+        assert mc >= d[p + l] * (1 - 1e-9) and mr >= d[p + l] * (1 - 1e-9)
+
+
+def test_krylov_beats_subspace_at_fixed_views():
+    """'for fixed oversampling and views the block Krylov method is more accurate'."""
+    n = 1000
+    A = np.diag(S.paper_poly(n, 10, 1.0))
+    for v in (4, 5):
+        s_sub = _mean_errors(A, v, 10)
+        s_kry = _mean_errors(A, v, 10, alg="krylov")
+        assert max(s_kry) <= max(s_sub)
+
+
+# ------------------------------------------------------------------ P6 single pass specifics
+
+def test_single_pass_baseline_is_least_squares():
+    """With l_c = l_1, Alg. 7 lines 11-12 compute X = (Omega_c^* Q_c)^dagger Y_r^* (P:595):
+    check against the pseudo-inverse route (independent of the qr-based solve)."""
+    cfg = S.CONFIGS["C1"]
+    A = S.make_matrix(cfg)
+    Om = S.gaussian_test_matrix(cfg.n, cfg.l, cfg, S.ROLE_OMEGA)
+    Phi = S.gaussian_test_matrix(cfg.m, cfg.l2, cfg, S.ROLE_PHI)
+    U, s, V, _ = O.svd_of(A, "single_pass", cfg.k, cfg.p, Omega=Om, l2=cfg.l2, Phi=Phi)
+    Yc, Yr = A @ Om, A.T @ Phi
+    Qc = np.linalg.svd(Yc, full_matrices=False)[0]       # any orthonormal basis of range(Y_c)
+    X = np.linalg.pinv(Phi.T @ Qc) @ Yr.T
+    Ux, sx, Vtx = np.linalg.svd(X, full_matrices=False)
+    np.testing.assert_allclose(s, sx[:cfg.k], rtol=1e-11)
+    assert proj(U, Qc @ Ux[:, :cfg.k]) < 1e-10
+    assert proj(V, Vtx[:cfg.k].T) < 1e-10
+
+
+def test_single_pass_lc_truncation_is_tsvd_of_Yc():
+    """l_c < l_1: Q_c = Q_c Qhat_c equals the p+l_c leading left singular vectors of Y_c."""
+    m, n, p, l1, lc = 150, 120, 6, 6, 2
+    A = S.random_gaussian_matrix(m, n, seed=8) * np.linspace(3, 0.01, n)
+    Om = S.gaussian((n, p + l1), 60, S.ROLE_OMEGA)
+    Yc = A @ Om
+    Qc, Rc = O.qr(Yc)
+    Qh, _, _ = O.tsvd(Rc, p + lc)
+    Uy = np.linalg.svd(Yc, full_matrices=False)[0][:, :p + lc]
+    assert proj(Qc @ Qh, Uy) < 1e-12
+
+
+# ------------------------------------------------------------------ P7 normal mode / orientation
+
+@pytest.mark.parametrize("v", [2, 3, 4])
+def test_normal_mode_full_sampling(v):
+    """Full sampling: V diag(sigma^2) V^T = eig(A^T A) top-k (P:247, P:278 'EVD of J^*J')."""
+    m, n, k = 14, 10, 4
+    A = S.random_gaussian_matrix(m, n, seed=90 + v)
+    Om = S.gaussian((n if v % 2 == 0 else m, n), 70, S.ROLE_OMEGA, v)
+    V, s2 = O.normal_matrix_tevd(A, k, n - k, v, Om)
+    ev, EV = np.linalg.eigh(A.T @ A)
+    ev, EV = ev[::-1], EV[:, ::-1]
+    np.testing.assert_allclose(s2, ev[:k], rtol=1e-12)
+    assert proj(V, EV[:, :k]) < 1e-11
+
+
+def test_recommend_input_table():
+    """P:245-247 and P:897."""
+    g = O
+    assert [g.recommend_input(g.GOAL_NORMAL, v) for v in (2, 3, 4, 5)] == [0, 1, 0, 1]
+    assert [g.recommend_input(g.GOAL_RIGHT, v) for v in (2, 3)] == [0, 1]
+    assert [g.recommend_input(g.GOAL_LEFT, v) for v in (2, 3)] == [1, 0]
+    assert g.recommend_input(g.GOAL_SVD, 3) == 0
+
+
+@pytest.mark.parametrize("alg,v", [("subspace", 2), ("subspace", 3), ("krylov", 4), ("single_pass", 1)])
+def test_transposed_input_returns_A_factors(alg, v):
+    m, n, k, p = 70, 50, 4, 4
+    sig = np.array([5.0, 4.0, 3.0, 2.0])
+    A = S.exact_rank_matrix(m, n, sig, seed=33)
+    X, Y = S.exact_rank_factors(m, n, 4, seed=33)
+    Om = S.gaussian((m, k + p), 80, S.ROLE_OMEGA_M)
+    Phi = S.gaussian((n, 2 * (k + p)), 80, S.ROLE_PHI)
+    U, s, V, _ = O.svd_of(A, alg, k, p, v=v, Omega=Om, l2=2 * (k + p), Phi=Phi, transpose=True)
+    np.testing.assert_allclose(s, sig, rtol=1e-12)
+    assert U.shape == (m, k) and V.shape == (n, k)
+    assert proj(U, X) < 1e-11 and proj(V, Y) < 1e-11
+
+
+def test_argument_errors():
+    A = np.eye(5)
+    with pytest.raises(ValueError):
+        O.gen_subspace_iteration(A, 2, 1, 1, np.eye(5)[:, :3])
+    with pytest.raises(ValueError):
+        O.gen_block_krylov(A, 2, 1, 1, np.eye(5)[:, :3])
+    with pytest.raises(ValueError):
+        O.one_view_tropp(A, 2, 2, 1, 0, np.eye(5)[:, :4], np.eye(5)[:, :3])
+
+
+def test_projector_distance_stable_form():
+    """sqrt(2)||U - Uo Uo^T U||_F equals the explicit ||UU^T - UoUo^T||_F."""
+    U = np.linalg.qr(S.random_gaussian_matrix(30, 4, seed=1))[0]
+    Uo = np.linalg.qr(U + 1e-3 * S.random_gaussian_matrix(30, 4, seed=2))[0]
+    explicit = np.linalg.norm(U @ U.T - Uo @ Uo.T)
+    assert abs(O.projector_distance(U, Uo) - explicit) < 1e-12
