@@ -1,0 +1,176 @@
+/*
+ * rsvd.h — C ABI of the B200 (sm_100a) pass-efficient randomized SVD library (librsvd.so).
+ *
+ * Implements the matrix-view hot path of Bjarkason, "Pass-efficient randomized algorithms for
+ * low-rank matrix approximation using any number of views" (arXiv 1804.07531).  Citations are
+ * PAPER.md line numbers (P:<line>) with the algorithm / section they fall in.
+ *
+ *   rsvd_subspace      Alg. 2, generalized subspace iteration, any v >= 2
+ *   rsvd_block_krylov  Alg. 9, generalized block Krylov, any v >= 2
+ *   rsvd_single_pass   Alg. 7, 1-view Tropp variant with l_c
+ *
+ * plus the primitives they are built from, exported for unit-level parity tests:
+ *   rsvd_view          Y = A X  or  Z = A^T Y        (one matrix view)
+ *   rsvd_view_fused    Y_c = A Omega and Y_r = A^T Phi from one read of A   (P:669 a)+b))
+ *   rsvd_orth          [Q, R] = qr(Y) by CholeskyQR2
+ *   rsvd_core_svd      [U, S, V] = tsvd(M) of a small core by one-sided Jacobi
+ *
+ * NOTATION.  The ABI uses BASELINE.json's letters: k = target rank (paper p), p = oversampling
+ * (paper l), l = k + p = sketch width; l2 = co-range sketch width of the single-pass method
+ * (paper p + l_2); lc in [0, p] = the truncation parameter (paper l_c; lc == p is the Tropp
+ * baseline).
+ *
+ * LAYOUTS.
+ *   A      row-major, m_local x n, row stride lda >= n (elements).
+ *   tall-skinny arrays (Omega, Phi, U, V, X, Y, Q) are COLUMN-major: element (i, j) at
+ *          ptr[j * ld + i], ld >= rows; every test / basis vector is contiguous.
+ *   small square arrays (R, core U/V) are column-major with ld = their row count.
+ * POINTERS.  Every array argument may be device memory or host memory (pageable or pinned); the
+ *   library detects the kind with cudaPointerGetAttributes and stages host data through its own
+ *   device workspace (host<->device copies then happen inside the call).  Device pointers must
+ *   be on the ctx's device.
+ * DTYPE.  All arrays of one call share A's dtype.  RSVD_F64 is fully supported.  RSVD_F32 is
+ *   not implemented in this release and returns RSVD_E_DTYPE.
+ * OWNERSHIP.  The caller owns every array; nothing is retained after return.  The ctx owns its
+ *   workspace (grown on demand, freed by rsvd_destroy) and its CUDA-graph cache.
+ * SYNCHRONISATION.  Calls are synchronous: one stream synchronisation at the end; no host
+ *   round trip between views (the whole algorithm is one CUDA graph launch after the first call
+ *   with a given signature).
+ * MULTI-GPU.  After rsvd_comm_init every algorithm call is a collective over the ranks: A is
+ *   row-sharded (rank r holds rows [row0, row0 + m_local)); U is returned row-sharded like A;
+ *   S and V are replicated and bitwise identical on all ranks.  Gram matrices and the partial
+ *   co-range views A^T Y are summed with NCCL all-reduce.
+ * DETERMINISM.  Bitwise run-to-run reproducible for fixed inputs and rank count, except the
+ *   single-pass Y_c accumulation when the deterministic partial buffers would exceed the memory
+ *   budget (info->nondeterministic = 1; never for the BASELINE configs C1-C3).
+ * ERRORS.  Every function returns an int status (RSVD_OK = 0 or a negative RSVD_E_*); no C++
+ *   exception crosses the ABI.  rsvd_last_error(ctx) gives a one-line detail.  Outputs are
+ *   defined only when the call returns RSVD_OK.
+ */
+#ifndef RSVD_H_
+#define RSVD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rsvd_ctx rsvd_ctx;
+
+enum { RSVD_F32 = 1, RSVD_F64 = 2 };
+enum { RSVD_INPUT_A = 0, RSVD_INPUT_AT = 1 };          /* matrix Alg. 2/9 is applied to */
+enum { RSVD_GOAL_SVD = 0, RSVD_GOAL_LEFT = 1, RSVD_GOAL_RIGHT = 2, RSVD_GOAL_NORMAL = 3 };
+enum {
+  RSVD_OK = 0,
+  RSVD_E_ARG = -1,       /* invalid argument (shape, rank, views, ld, alignment, pointer)   */
+  RSVD_E_DTYPE = -2,     /* unsupported dtype                                                */
+  RSVD_E_CUDA = -3,      /* CUDA runtime / driver failure                                    */
+  RSVD_E_NCCL = -4,      /* NCCL unavailable or failed                                       */
+  RSVD_E_NOMEM = -5,     /* device workspace allocation failed                               */
+  RSVD_E_NUMERIC = -6,   /* numerical failure (Jacobi not converged, singular R-hat in Alg. 7) */
+  RSVD_E_STATE = -7      /* ctx misuse (e.g. comm already initialised)                       */
+};
+/* flags */
+#define RSVD_SQUARED      1u   /* S := sigma^2  (normal-matrix estimate A^T A ~ V S V^T) */
+#define RSVD_NO_GRAPH     2u   /* enqueue kernels directly instead of replaying a CUDA graph    */
+#define RSVD_PROFILE      4u   /* record CUDA events around every view kernel (info->view_*)     */
+#define RSVD_SIM_SHARDS_SHIFT 8 /* debug: bits 8..15 = number of virtual row shards (loopback) */
+
+typedef struct {
+  int32_t dtype;          /* RSVD_F64 (RSVD_F32 reserved)                                */
+  int32_t reserved;
+  int64_t m, n;           /* global shape of A                                            */
+  int64_t m_local, row0;  /* this rank's rows [row0, row0 + m_local); single GPU: m, 0    */
+  int64_t lda;            /* row stride of the local block in elements, >= n              */
+  const void* data;       /* local block, device or host memory, never modified           */
+} rsvd_mat;
+
+typedef struct {
+  int32_t status;               /* return value of the call                                 */
+  int32_t views;                /* views of A used (v; 1 for the single pass)         */
+  int64_t vectors;              /* matrix-vector products (Alg. 2: v l; Alg. 9: (v+floor(v/2)-1) l) */
+  int32_t rank_deficient_cols;  /* columns zeroed by the guarded Cholesky (exact rank < l)   */
+  int32_t jacobi_sweeps;        /* sweeps of the last core SVD                               */
+  int32_t lc_used;              /* l_c of the single pass                                     */
+  int32_t host_staged;          /* 1 if any argument was host memory; 2 if a device A had to be
+                                   copied to a 16-byte-aligned block (TMA needs lda*8 % 16 == 0) */
+  int32_t graph_replayed;       /* 1 if the call replayed a cached CUDA graph                 */
+  int32_t nondeterministic;     /* 1 if atomics were used (see DETERMINISM)                   */
+  int32_t view_launches;        /* view-kernel launches in the call                           */
+  int32_t reserved;
+  double  view_ms;              /* RSVD_PROFILE: summed device time of the view kernels      */
+  double  view_bytes;           /* algorithmic bytes of A streamed by those kernels          */
+  double  view_flops;           /* algorithmic flops of those kernels (2 m n w per view)     */
+  double  total_ms;             /* RSVD_PROFILE: device time of the whole call               */
+} rsvd_info;
+
+/* ---- context ------------------------------------------------------------------------------- */
+int  rsvd_create(rsvd_ctx** ctx, int cuda_device, void* cuda_stream /* NULL: private stream */);
+int  rsvd_destroy(rsvd_ctx* ctx);
+const char* rsvd_strerror(int code);
+const char* rsvd_last_error(const rsvd_ctx* ctx);
+int  rsvd_version(void);                                /* 100 * major + minor               */
+int  rsvd_sm_count(const rsvd_ctx* ctx);
+/* Roofline denominators measured on this device: FP64 DMMA (mma.sync m8n8k4) throughput in
+ * TFLOP/s (register operands, all SMs) and streaming HBM read bandwidth in GB/s (4 GiB buffer,
+ * best of 5).  Allocates 4 GiB temporarily; synchronous. */
+int  rsvd_probe_peaks(rsvd_ctx* ctx, double* dmma_tflops, double* read_gbs);
+/* Orientation rule: returns RSVD_INPUT_A or RSVD_INPUT_AT.
+ * RIGHT / NORMAL: v even -> A, v odd -> A^T;  LEFT: the reverse;  SVD: A.  Pure function. */
+int  rsvd_recommend_input(int goal, int v);
+
+/* ---- multi-GPU (NCCL, loaded at run time from libnccl.so.2) --------------------------------- */
+int  rsvd_get_unique_id(void* id128);                  /* rank 0: fills 128 bytes             */
+int  rsvd_comm_init(rsvd_ctx* ctx, int nranks, int rank, const void* id128);   /* collective */
+int  rsvd_comm_nranks(const rsvd_ctx* ctx);
+
+/* ---- algorithms ----------------------------------------------------------------------------- */
+/* Alg. 2.  k >= 1, p >= 0, l = k + p <= min(m, n), v >= 2.
+ * input == RSVD_INPUT_A : Omega is n x l (replicated on all ranks);
+ * input == RSVD_INPUT_AT: the algorithm runs on A^T and Omega is m_local x l (this rank's rows).
+ * U (m_local x k, ldu >= m_local) and V (n x k, ldv >= n) are A's singular vectors in either
+ * orientation; S (k) descending (sigma, or sigma^2 with RSVD_SQUARED).  U or V may be NULL. */
+int rsvd_subspace(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, int input,
+                  const void* Omega, int64_t ld_omega,
+                  void* U, int64_t ldu, void* S, void* V, int64_t ldv,
+                  unsigned flags, rsvd_info* info);
+
+/* Alg. 9; same arguments.  Additionally the Krylov basis width (v/2) l (v even) or
+ * ((v-1)/2) l (v odd) must not exceed the row count of its side (RSVD_E_ARG). */
+int rsvd_block_krylov(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, int input,
+                      const void* Omega, int64_t ld_omega,
+                      void* U, int64_t ldu, void* S, void* V, int64_t ldv,
+                      unsigned flags, rsvd_info* info);
+
+/* Alg. 7, input = A.  Omega n x (k+p) replicated; Phi m_local x l2 (this rank's rows
+ * of the co-range test matrix, P:667b); l2 >= k + p (P:663 l_2 >= l_1); lc in [0, p] or -1 (= p). */
+int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int lc,
+                     const void* Omega, int64_t ld_omega, const void* Phi, int64_t ld_phi,
+                     void* U, int64_t ldu, void* S, void* V, int64_t ldv,
+                     unsigned flags, rsvd_info* info);
+
+/* ---- primitives (single GPU; for unit tests and the benchmark's kernel timing) -------------- */
+/* trans == 0: Y (m_local x w) = A X with X n x w;  trans == 1: Y (n x w) = A^T X with X m_local x w.
+ * 1 <= w <= 128. */
+int rsvd_view(rsvd_ctx* ctx, const rsvd_mat* A, int trans, const void* X, int64_t ldx, int w,
+              void* Y, int64_t ldy, unsigned flags, rsvd_info* info);
+/* Y_c (m_local x l) = A Omega (Omega n x l) and Y_r (n x l2) = A^T Phi (Phi m_local x l2). */
+int rsvd_view_fused(rsvd_ctx* ctx, const rsvd_mat* A, const void* Omega, int64_t ld_omega, int l,
+                    const void* Phi, int64_t ld_phi, int l2, void* Yc, int64_t ld_yc,
+                    void* Yr, int64_t ld_yr, unsigned flags, rsvd_info* info);
+/* In place: Y (rows x w) <- Q with Q^T Q = I, and R (w x w, column-major, may be NULL) with
+ * Y_in = Q R, diag(R) >= 0.  Columns whose Cholesky pivot falls below the rank guard are set to
+ * zero in Q (and their row of R is zero); their count is info->rank_deficient_cols. */
+int rsvd_orth(rsvd_ctx* ctx, int64_t rows, int w, void* Y, int64_t ldy, void* R, unsigned flags,
+              rsvd_info* info);
+/* M (r x c, column-major, ldm >= r, r >= c): M = U diag(S) V^T with U r x c, S c (descending),
+ * V c x c.  One-sided Jacobi in one CTA; c <= 256, r <= 256. */
+int rsvd_core_svd(rsvd_ctx* ctx, int r, int c, const void* M, int64_t ldm, void* U, void* S, void* V,
+                  unsigned flags, rsvd_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSVD_H_ */

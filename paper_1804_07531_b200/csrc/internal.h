@@ -1,0 +1,94 @@
+// Internal interfaces between the kernel files and the driver (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rsvd.h"
+
+namespace rsvd {
+
+constexpr int kMaxWT = 16;        // view kernels: w <= 128 per launch (wider -> column chunks)
+constexpr int kFusedMaxL = 72;    // fused single-pass kernel: l <= 72 ...
+constexpr int kFusedMaxL2T = 18;  // ... and l2 <= 144
+
+enum { VIEW_AX = 0, VIEW_ATY = 1, VIEW_FUSED = 2 };
+
+struct ViewArgs {
+  const double* A;  // row-major rows x n, lda
+  int64_t rows, n, lda;
+  const double* X;  // AX: X^T (w x n, ldx); ATY: Y^T (w x rows, ldx)
+  int64_t ldx;
+  int w;
+  double* out;      // column-major output (w x out_rows, ldo), slot s at out + s*slot_stride
+  int64_t ldo, slot_stride;
+  int S, KTS;       // reduction split (from plan_view)
+  int grid_cap;     // persistent grid size (SM count)
+};
+
+struct FusedArgs {
+  const double* A;
+  int64_t rows, n, lda;
+  const double* Om;  // Omega^T: l x n, ldom
+  int64_t ldom;
+  int l;
+  const double* Phi; // Phi^T: l2 x rows, ldphi
+  int64_t ldphi;
+  int l2;
+  double* yc;        // Y_c^T partial slots (l x rows, ldyc) per column strip, or one buffer (atomic)
+  int64_t ldyc, yc_slot_stride;
+  int yc_atomic;
+  double* yr;        // Y_r^T partial slots (l2 x n, ldyr) per row split
+  int64_t ldyr, yr_slot_stride;
+  int S, KTS;
+  int grid_cap;
+};
+
+void plan_view(int kind, int64_t rows, int64_t n, int w, int grid_cap, int* S, int* KTS);
+int launch_view_ax(const ViewArgs& a, cudaStream_t st);
+int launch_view_aty(const ViewArgs& a, cudaStream_t st);
+int launch_view_fused(const FusedArgs& a, cudaStream_t st);
+int fused_strips(int64_t n);  // number of 64-column strips of the fused kernel
+
+// ---- small kernels (small_kernels.cu) --------------------------------------------------------
+// device-side status words (one struct in device memory per ctx)
+struct DevStatus {
+  int deficient;        // columns zeroed by the guarded Cholesky
+  int jacobi_sweeps;
+  int jacobi_fail;
+  int numeric_fail;     // e.g. singular R-hat
+};
+
+// out[c][r] = sum_{s<S} in[s][c][r] for c < w, r < rows   (column-major, slot stride)
+int launch_slot_sum(const double* in, int64_t ldi, int64_t slot_stride, int S, int64_t rows, int w, double* out,
+                    int64_t ldo, cudaStream_t st);
+// G partial: G_b (a x b, col-major ld = a) = Xa[rows chunk]^T Xb[rows chunk]; returns #slots used
+int gram_slots(int64_t rows);
+int launch_cross_gram(const double* Xa, int64_t lda_, int a, const double* Xb, int64_t ldb, int b, int64_t rows,
+                      double* slots, int nslots, cudaStream_t st);
+// G = sum of nslots partials (a x b each, contiguous)
+int launch_slots_reduce_small(const double* slots, int nslots, int64_t count, double* G, cudaStream_t st);
+// Guarded Cholesky of the w x w Gram G (col-major): R upper (G = R^T R), Rinv = R^+ on the
+// non-deficient columns, Racc <- R * Racc (if Racc != null, accumulate the product of passes).
+int launch_chol(const double* G, int w, double* R, double* Rinv, double* Racc, DevStatus* status, cudaStream_t st);
+// out (rows x c, col-major) = in (rows x w) * M (w x c, col-major ld = ldm);  mode 0: overwrite,
+// mode 1: out -= in * M.  out must not alias in.
+int launch_ts_gemm(const double* in, int64_t ldi, int64_t rows, int w, const double* M, int64_t ldm, int c,
+                   double* out, int64_t ldo, int mode, cudaStream_t st);
+// One-sided Jacobi SVD of M (r x c col-major, ldm), r >= c, c <= 256, r <= 256:
+// M = Ul diag(S) Vr^T, S descending.  Ul (r x c, ld r), Vr (c x c, ld c).  Scratch >= 2*256*256.
+int launch_jacobi(const double* M, int64_t ldm, int r, int c, double* Ul, double* S, double* Vr, double* scratch,
+                  DevStatus* status, cudaStream_t st);
+// general small GEMM / transposes on device (tiny sizes): C(mxn) = op(A) op(B), col-major
+int launch_small_gemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda_, const double* B,
+                      int64_t ldb, double* C, int64_t ldc, cudaStream_t st);
+// strided 2-D copy of a column-major (rows x cols) block, with optional fill of padding rows
+int launch_copy_cols(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int cols,
+                     cudaStream_t st);
+int launch_fill(double* dst, int64_t count, double v, cudaStream_t st);
+// triangular-system helpers for Alg. 7: out (c x c) = upper-triangular inverse of R (c x c)
+int launch_tri_inv(const double* R, int c, double* Rinv, DevStatus* status, cudaStream_t st);
+// S[i] <- S[i]^2
+int launch_square(double* S, int n, cudaStream_t st);
+
+}  // namespace rsvd

@@ -1,0 +1,1260 @@
+// C-ABI driver of librsvd: context, workspace arena, CUDA-graph cache, NCCL row-sharding and
+// the algorithms of arXiv 1804.07531 expressed as sequences of device kernels.
+//
+//   Alg. 2  generalized subspace iteration
+//   Alg. 9  generalized block Krylov
+//   Alg. 7  1-view (Tropp variant, l_c)
+//
+// Every algorithm is enqueued on the ctx stream with no host round trip; the first call with a
+// given signature is captured into a CUDA graph, later calls replay it.  The workspace is sized
+// by running the same enqueue code in "dry" mode (allocations only, no launches).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace rsvd {
+int launch_chol_ref(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
+                    DevStatus* status, cudaStream_t st);
+int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
+                    double* scratch, DevStatus* status, cudaStream_t st);
+int launch_diag(const double* G, int w, double* d, cudaStream_t st);
+int probe_peaks(int sms, cudaStream_t st, double* dmma_tflops, double* read_gbs);
+}  // namespace rsvd
+
+using namespace rsvd;
+
+// ================================================================ NCCL (dlopen)
+namespace {
+typedef int nccl_res_t;
+typedef void* nccl_comm_t;
+struct nccl_uid_t { char internal[128]; };
+typedef nccl_res_t (*pf_get_uid)(nccl_uid_t*);
+typedef nccl_res_t (*pf_init_rank)(nccl_comm_t*, int, nccl_uid_t, int);
+typedef nccl_res_t (*pf_allreduce)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t);
+typedef nccl_res_t (*pf_destroy)(nccl_comm_t);
+typedef const char* (*pf_errstr)(nccl_res_t);
+struct NcclApi {
+  void* h = nullptr;
+  pf_get_uid get_uid = nullptr;
+  pf_init_rank init_rank = nullptr;
+  pf_allreduce allreduce = nullptr;
+  pf_destroy destroy = nullptr;
+  pf_errstr errstr = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    get_uid = (pf_get_uid)dlsym(h, "ncclGetUniqueId");
+    init_rank = (pf_init_rank)dlsym(h, "ncclCommInitRank");
+    allreduce = (pf_allreduce)dlsym(h, "ncclAllReduce");
+    destroy = (pf_destroy)dlsym(h, "ncclCommDestroy");
+    errstr = (pf_errstr)dlsym(h, "ncclGetErrorString");
+    return get_uid && init_rank && allreduce && destroy;
+  }
+};
+NcclApi g_nccl;
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+}  // namespace
+
+// ================================================================ context
+struct rsvd_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  nccl_comm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  char* arena = nullptr;
+  size_t arena_size = 0;
+  DevStatus* dstat = nullptr;
+  DevStatus* hstat = nullptr;  // pinned
+  std::map<std::string, cudaGraphExec_t> graphs;
+  std::vector<cudaEvent_t> events;
+  std::string err;
+};
+
+namespace {
+
+void set_err(rsvd_ctx* c, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+}
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+enum Side { SIDE_M = 0, SIDE_N = 1 };
+
+struct TS {  // column-major tall-skinny block: w columns of `rows`, leading dim ld
+  double* p = nullptr;
+  int64_t rows = 0, ld = 0;
+  int w = 0;
+  double* col(int j) const { return p + (int64_t)j * ld; }
+};
+
+enum PtrKind { PTR_NULL = 0, PTR_DEVICE = 1, PTR_HOST = 2 };
+
+PtrKind ptr_kind(const void* p, int device) {
+  if (!p) return PTR_NULL;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return PTR_HOST;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return PTR_DEVICE;
+  (void)device;
+  return PTR_HOST;
+}
+
+// ---------------------------------------------------------------- call description
+struct Call {
+  int alg = 0;  // 0 subspace, 1 krylov, 2 single pass, 10 view, 11 fused view, 12 orth, 13 core svd
+  const rsvd_mat* A = nullptr;
+  int k = 0, p = 0, v = 0, input = 0, l2 = 0, lc = 0, trans = 0, w = 0;
+  int64_t rows = 0;  // orth / core
+  int cols = 0;
+  const void* Om = nullptr;
+  int64_t ldom = 0;
+  const void* Phi = nullptr;
+  int64_t ldphi = 0;
+  void* U = nullptr;
+  int64_t ldu = 0;
+  void* S = nullptr;
+  void* V = nullptr;
+  int64_t ldv = 0;
+  void* R = nullptr;
+  unsigned flags = 0;
+  // resolved kinds
+  PtrKind kA = PTR_NULL, kOm = PTR_NULL, kPhi = PTR_NULL, kU = PTR_NULL, kS = PTR_NULL, kV = PTR_NULL,
+          kR = PTR_NULL;
+};
+
+// ---------------------------------------------------------------- executor
+struct Exec {
+  rsvd_ctx* ctx;
+  const Call& call;
+  bool dry;
+  char* base;
+  size_t off = 0, peak = 0;
+  cudaStream_t st;
+  int rc = RSVD_OK;
+  bool profile = false;
+  bool launch_off = false;  // real addresses, record transfers, launch nothing
+  int a_restaged = 0;
+  int nondet = 0;
+  bool live() const { return !dry && !launch_off && rc == RSVD_OK; }
+  std::vector<std::pair<int, int>> ev_pairs;  // indices into ctx->events
+  int ev_used = 0;
+  double view_bytes = 0, view_flops = 0;
+  int view_launches = 0;
+  // device views of the caller's arrays (resolved in prepare)
+  const double* A = nullptr;
+  int64_t lda = 0, m = 0, n = 0;
+  // host-transfer plan (executed outside the graph)
+  struct H2D { void* dst; int64_t ldd; const void* src; int64_t lds; int64_t rows; int64_t cols; };
+  struct D2H { void* dst; int64_t ldd; const void* src; int64_t lds; int64_t rows; int64_t cols; };
+  std::vector<H2D> h2d;
+  std::vector<D2H> d2h;
+
+  Exec(rsvd_ctx* c, const Call& cl, bool d, char* b) : ctx(c), call(cl), dry(d), base(b), st(c->stream) {}
+
+  double* alloc(int64_t n_el) {
+    const size_t bytes = (size_t)round_up(std::max<int64_t>(n_el, 1) * 8, 256);
+    char* p = (dry ? (char*)(uintptr_t)0x100000 : base) + off;
+    off += bytes;
+    peak = std::max(peak, off);
+    return reinterpret_cast<double*>(p);
+  }
+  size_t mark() const { return off; }
+  void release(size_t m_) { off = m_; }
+  void chk(int r) {
+    if (rc == RSVD_OK && r != RSVD_OK) rc = r;
+  }
+  int64_t side_rows(Side s) const { return s == SIDE_M ? m : n; }
+  TS new_ts(Side s, int w) {
+    TS t;
+    t.rows = side_rows(s);
+    t.ld = round_up(std::max<int64_t>(t.rows, 1), 32);
+    t.w = w;
+    t.p = alloc(t.ld * w);
+    return t;
+  }
+  TS slice(const TS& t, int c0, int wc) const {
+    TS s = t;
+    s.p = t.p + (int64_t)c0 * t.ld;
+    s.w = wc;
+    return s;
+  }
+  bool sharded(Side s) const { return s == SIDE_M && ctx->nranks > 1; }
+
+  void allreduce(double* p, int64_t count) {
+    if (!live()) return;
+    nccl_res_t r = g_nccl.allreduce(p, p, (size_t)count, kNcclFloat64, kNcclSum, ctx->comm, st);
+    if (r != 0) {
+      set_err(ctx, "ncclAllReduce failed: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
+      chk(RSVD_E_NCCL);
+    }
+  }
+  void ev_record(int* idx) {
+    if (!live() || !profile) return;
+    if (ev_used >= (int)ctx->events.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ctx->events.push_back(e);
+    }
+    *idx = ev_used++;
+    cudaEventRecord(ctx->events[*idx], st);
+  }
+
+  // ------------------------------------------------------------ matrix views (hot path)
+  // from == SIDE_N: Y (side M) = A X;  from == SIDE_M: Y (side N) = A^T X (+ all-reduce)
+  void view(Side from, const TS& X, const TS& Y) {
+    const int w = X.w;
+    for (int c0 = 0; c0 < w; c0 += kMaxWT * 8) {
+      const int wc = std::min(kMaxWT * 8, w - c0);
+      const size_t mk = mark();
+      ViewArgs a;
+      a.A = A;
+      a.rows = m;
+      a.n = n;
+      a.lda = lda;
+      a.X = X.p + (int64_t)c0 * X.ld;
+      a.ldx = X.ld;
+      a.w = wc;
+      a.grid_cap = ctx->sms;
+      const int kind = (from == SIDE_N) ? VIEW_AX : VIEW_ATY;
+      plan_view(kind, m, n, wc, ctx->sms, &a.S, &a.KTS);
+      double* dst = Y.p + (int64_t)c0 * Y.ld;
+      double* slots = (a.S == 1) ? dst : alloc((int64_t)a.S * Y.ld * wc);
+      a.out = slots;
+      a.ldo = Y.ld;
+      a.slot_stride = (int64_t)Y.ld * wc;
+      view_bytes += (double)m * n * 8.0;
+      view_flops += 2.0 * m * n * wc;
+      ++view_launches;
+      if (live()) {
+        int e0 = -1, e1 = -1;
+        ev_record(&e0);
+        chk(kind == VIEW_AX ? launch_view_ax(a, st) : launch_view_aty(a, st));
+        ev_record(&e1);
+        if (e0 >= 0) ev_pairs.push_back({e0, e1});
+        if (a.S > 1) chk(launch_slot_sum(slots, Y.ld, a.slot_stride, a.S, Y.rows, wc, dst, Y.ld, st));
+      }
+      release(mk);
+    }
+    if (from == SIDE_M && ctx->nranks > 1) allreduce(Y.p, Y.ld * Y.w);
+  }
+
+  // G (a x b, col-major ld a) = Xa^T Xb over the side's rows (+ all-reduce when sharded)
+  void cross(Side s, const TS& Xa, const TS& Xb, double* G) {
+    const size_t mk = mark();
+    const int ns = gram_slots(Xa.rows);
+    double* slots = alloc((int64_t)ns * Xa.w * Xb.w);
+    if (live()) {
+      chk(launch_cross_gram(Xa.p, Xa.ld, Xa.w, Xb.p, Xb.ld, Xb.w, Xa.rows, slots, ns, st));
+      chk(launch_slots_reduce_small(slots, ns, (int64_t)Xa.w * Xb.w, G, st));
+    }
+    release(mk);
+    if (sharded(s)) allreduce(G, (int64_t)Xa.w * Xb.w);
+  }
+
+  // CholeskyQR2 in place: Y <- Q, R_out (w x w) = R2 R1 if requested.  `ref` (w) optional
+  // reference squared column norms for the first pass's rank guard.
+  void orth(Side s, const TS& Y, double* R_out, const double* ref) {
+    const int w = Y.w;
+    const size_t mk = mark();
+    double* G = alloc((int64_t)w * w);
+    double* R1 = alloc((int64_t)w * w);
+    double* R1i = alloc((int64_t)w * w);
+    double* R2 = alloc((int64_t)w * w);
+    double* R2i = alloc((int64_t)w * w);
+    TS T = new_ts(s, w);
+    cross(s, Y, Y, G);
+    if (live()) {
+      chk(launch_chol_ref(G, ref, w, 1e-12, R1, R1i, ctx->dstat, st));
+      chk(launch_ts_gemm(Y.p, Y.ld, Y.rows, w, R1i, w, w, T.p, T.ld, 0, st));
+    }
+    cross(s, T, T, G);
+    if (live()) {
+      chk(launch_chol_ref(G, nullptr, w, 1e-12, R2, R2i, nullptr, st));
+      chk(launch_ts_gemm(T.p, T.ld, T.rows, w, R2i, w, w, Y.p, Y.ld, 0, st));
+      if (R_out) chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R_out, w, st));
+    }
+    release(mk);
+  }
+
+  // block classical Gram-Schmidt, twice, over blocks of width bw, then CholeskyQR2 per block
+  void bcgs2(Side s, const TS& K, int bw) {
+    const int nb = (K.w + bw - 1) / bw;
+    for (int b = 0; b < nb; ++b) {
+      const int c0 = b * bw, wc = std::min(bw, K.w - c0);
+      TS Wb = slice(K, c0, wc);
+      const size_t mk = mark();
+      double* ref = nullptr;
+      if (b > 0) {
+        TS Qp = slice(K, 0, c0);
+        double* G0 = alloc((int64_t)wc * wc);
+        ref = alloc(wc);
+        double* C = alloc((int64_t)c0 * wc);
+        cross(s, Wb, Wb, G0);
+        if (live()) chk(launch_diag(G0, wc, ref, st));
+        for (int pass = 0; pass < 2; ++pass) {
+          cross(s, Qp, Wb, C);
+          if (live()) chk(launch_ts_gemm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1, st));
+        }
+      }
+      orth(s, Wb, nullptr, ref);
+      release(mk);
+    }
+  }
+
+  // out (rows x k, ldo) = Q (rows x w) * Mk (w x k, ld w)
+  void lift(const TS& Q, const double* Mk, int k, double* out, int64_t ldo) {
+    if (live()) chk(launch_ts_gemm(Q.p, Q.ld, Q.rows, Q.w, Mk, Q.w, k, out, ldo, 0, st));
+  }
+
+  void core_svd(const double* M, int w, int trans, double* Ul, double* Sv, double* Vr) {
+    const size_t mk = mark();
+    double* scratch = alloc(2 * 256 * 256);
+    if (live()) chk(launch_jacobi_t(M, w, trans, w, w, Ul, Sv, Vr, scratch, ctx->dstat, st));
+    release(mk);
+  }
+
+  // ------------------------------------------------------------ staging of caller arrays
+  // device TS copy of a caller array (rows x w, column-major, ld_user)
+  TS stage_in(Side s, const void* src, int64_t ld_user, int w, PtrKind kind) {
+    TS t = new_ts(s, w);
+    if (kind == PTR_HOST) {
+      h2d.push_back({t.p, t.ld, src, ld_user, t.rows, w});
+    } else if (live()) {
+      chk(launch_copy_cols(static_cast<const double*>(src), ld_user, t.p, t.ld, t.rows, w, st));
+    }
+    return t;
+  }
+  // where to write a caller output of rows x cols (col-major, ld): direct if device, else staging
+  double* out_ptr(void* user, int64_t ld_user, int64_t rows, int cols, PtrKind kind, int64_t* ld_out) {
+    if (kind == PTR_DEVICE) {
+      *ld_out = ld_user;
+      return static_cast<double*>(user);
+    }
+    const int64_t ld = round_up(std::max<int64_t>(rows, 1), 32);
+    double* p = alloc(ld * cols);
+    *ld_out = ld;
+    if (kind == PTR_HOST) d2h.push_back({user, ld_user, p, ld, rows, cols});
+    return p;
+  }
+};
+
+// ================================================================ algorithms
+// Each takes the resolved Exec; sides: the algorithm's input B = A (input 0) or A^T (input 1).
+// range side of B  (rows of B): side_c;  co-range side (cols of B): side_r.
+
+void write_outputs(Exec& E, Side side_c, Side side_r, const TS& Qc, const TS& Qr, const double* Uh,
+                   const double* Vh, const double* lam, int w, int k) {
+  const Call& c = E.call;
+  // B's U = Qc Uh (side_c), B's V = Qr Vh (side_r); A's U lives on side M, A's V on side N
+  auto emit = [&](Side s, const TS& Q, const double* M) {
+    if (s == SIDE_M) {
+      if (c.kU == PTR_NULL) return;
+      int64_t ld;
+      double* o = E.out_ptr(c.U, c.ldu, Q.rows, k, c.kU, &ld);
+      E.lift(Q, M, k, o, ld);
+    } else {
+      if (c.kV == PTR_NULL) return;
+      int64_t ld;
+      double* o = E.out_ptr(c.V, c.ldv, Q.rows, k, c.kV, &ld);
+      E.lift(Q, M, k, o, ld);
+    }
+  };
+  emit(side_c, Qc, Uh);
+  emit(side_r, Qr, Vh);
+  if (c.kS != PTR_NULL) {
+    int64_t ld;
+    double* so = E.out_ptr(c.S, k, k, 1, c.kS, &ld);
+    if (E.live()) {
+      E.chk(launch_copy_cols(lam, w, so, k, k, 1, E.st));
+      if (c.flags & RSVD_SQUARED) E.chk(launch_square(so, k, E.st));
+    }
+  }
+}
+
+void alg_subspace(Exec& E) {
+  const Call& c = E.call;
+  const int l = c.k + c.p;
+  const Side side_c = c.input == RSVD_INPUT_A ? SIDE_M : SIDE_N;
+  const Side side_r = c.input == RSVD_INPUT_A ? SIDE_N : SIDE_M;
+  TS Qr = E.stage_in(side_r, c.Om, c.ldom, l, c.kOm);   // line 1: Q_r = Omega
+  TS Qc = E.new_ts(side_c, l);
+  double* Rlast = E.alloc((int64_t)l * l);
+  for (int j = 1; j <= c.v; ++j) {                       // lines 2-8
+    if (j % 2 == 1) {
+      E.view(side_r, Qr, Qc);                            // A Q_r
+      E.orth(side_c, Qc, j == c.v ? Rlast : nullptr, nullptr);
+    } else {
+      E.view(side_c, Qc, Qr);                            // A^* Q_c
+      E.orth(side_r, Qr, j == c.v ? Rlast : nullptr, nullptr);
+    }
+  }
+  double* Ul = E.alloc((int64_t)l * l);
+  double* Vr = E.alloc((int64_t)l * l);
+  double* lam = E.alloc(l);
+  E.core_svd(Rlast, l, 0, Ul, lam, Vr);
+  // v even: R_r = Vh Lam Uh^T -> left = Vh, right = Uh;  v odd: R_c = Uh Lam Vh^T
+  if (c.v % 2 == 0)
+    write_outputs(E, side_c, side_r, Qc, Qr, /*Uh=*/Vr, /*Vh=*/Ul, lam, l, c.k);
+  else
+    write_outputs(E, side_c, side_r, Qc, Qr, /*Uh=*/Ul, /*Vh=*/Vr, lam, l, c.k);
+}
+
+void alg_krylov(Exec& E) {
+  const Call& c = E.call;
+  const int l = c.k + c.p, v = c.v;
+  const Side side_c = c.input == RSVD_INPUT_A ? SIDE_M : SIDE_N;
+  const Side side_r = c.input == RSVD_INPUT_A ? SIDE_N : SIDE_M;
+  const bool even = (v % 2 == 0);
+  const int nb = even ? v / 2 : (v - 1) / 2;
+  const int W = nb * l;
+  const Side side_K = even ? side_c : side_r;
+  TS K = E.new_ts(side_K, W);
+  TS Q0 = E.stage_in(side_r, c.Om, c.ldom, l, c.kOm);   // line 1: Q_r^0 = Omega
+  TS tmp_c = E.new_ts(side_c, l), tmp_r = E.new_ts(side_r, l);
+  TS prev = Q0;
+  for (int j = 1; j <= v - 1; ++j) {                    // lines 2-7
+    const bool odd = (j % 2 == 1);
+    const bool in_K = even ? odd : !odd;                 // K_c = odd blocks (v even), K_r = even blocks
+    TS dst;
+    if (in_K) {
+      const int b = even ? (j - 1) / 2 : (j / 2 - 1);
+      dst = E.slice(K, b * l, l);
+    } else {
+      dst = odd ? tmp_c : tmp_r;
+    }
+    E.view(odd ? side_r : side_c, prev, dst);
+    if (j < v - 1) E.orth(odd ? side_c : side_r, dst, nullptr, nullptr);  // last block stays raw
+    prev = dst;
+  }
+  if (v == 1) return;
+  E.bcgs2(side_K, K, l);                                  // qr(K_c) / qr(K_r)  (lines 9 / 14)
+  TS Qo = E.new_ts(even ? side_r : side_c, W);
+  double* Rw = E.alloc((int64_t)W * W);
+  E.view(side_K, K, Qo);                                  // one more view (lines 10 / 15)
+  E.orth(even ? side_r : side_c, Qo, Rw, nullptr);
+  double* Ul = E.alloc((int64_t)W * W);
+  double* Vr = E.alloc((int64_t)W * W);
+  double* lam = E.alloc(W);
+  E.core_svd(Rw, W, 0, Ul, lam, Vr);
+  if (even)  // Q_c = K, Q_r = Qo, R_r = Vh Lam Uh^T
+    write_outputs(E, side_c, side_r, K, Qo, Vr, Ul, lam, W, c.k);
+  else       // Q_r = K, Q_c = Qo, R_c = Uh Lam Vh^T
+    write_outputs(E, side_c, side_r, Qo, K, Ul, Vr, lam, W, c.k);
+}
+
+constexpr double kYcSlotBudget = 4.0e9;  // bytes of deterministic Y_c partial slots
+
+void alg_single_pass(Exec& E) {
+  const Call& c = E.call;
+  const int l = c.k + c.p, l2 = c.l2, lc = c.lc;
+  const int lp = c.k + lc;  // width of Q_c after the optional truncation
+  TS Om = E.stage_in(SIDE_N, c.Om, c.ldom, l, c.kOm);
+  TS Phi = E.stage_in(SIDE_M, c.Phi, c.ldphi, l2, c.kPhi);
+  TS Yc = E.new_ts(SIDE_M, l);
+  TS Yr = E.new_ts(SIDE_N, l2);
+  // ---- line 3: a) Y_c = A Omega  and  b) Y_r = A^* Phi  from one read of A
+  const bool fused_ok = (l <= kFusedMaxL) && ((l2 + 7) / 8 <= kFusedMaxL2T);
+  if (fused_ok) {
+    const size_t mk = E.mark();
+    FusedArgs a;
+    a.A = E.A;
+    a.rows = E.m;
+    a.n = E.n;
+    a.lda = E.lda;
+    a.Om = Om.p;
+    a.ldom = Om.ld;
+    a.l = l;
+    a.Phi = Phi.p;
+    a.ldphi = Phi.ld;
+    a.l2 = l2;
+    a.grid_cap = E.ctx->sms;
+    plan_view(VIEW_FUSED, E.m, E.n, l2, E.ctx->sms, &a.S, &a.KTS);
+    const int nsb = fused_strips(E.n);
+    const double slot_bytes = (double)nsb * Yc.ld * l * 8.0;
+    a.yc_atomic = slot_bytes > kYcSlotBudget ? 1 : 0;
+    E.nondet |= a.yc_atomic;
+    double* ycs = a.yc_atomic ? Yc.p : E.alloc((int64_t)nsb * Yc.ld * l);
+    a.yc = ycs;
+    a.ldyc = Yc.ld;
+    a.yc_slot_stride = (int64_t)Yc.ld * l;
+    double* yrs = (a.S == 1) ? Yr.p : E.alloc((int64_t)a.S * Yr.ld * l2);
+    a.yr = yrs;
+    a.ldyr = Yr.ld;
+    a.yr_slot_stride = (int64_t)Yr.ld * l2;
+    E.view_bytes += (double)E.m * E.n * 8.0;
+    E.view_flops += 2.0 * E.m * E.n * (l + l2);
+    ++E.view_launches;
+    if (E.live()) {
+      if (a.yc_atomic) E.chk(launch_fill(Yc.p, Yc.ld * l, 0.0, E.st));
+      int e0 = -1, e1 = -1;
+      E.ev_record(&e0);
+      E.chk(launch_view_fused(a, E.st));
+      E.ev_record(&e1);
+      if (e0 >= 0) E.ev_pairs.push_back({e0, e1});
+      if (!a.yc_atomic) E.chk(launch_slot_sum(ycs, Yc.ld, a.yc_slot_stride, nsb, Yc.rows, l, Yc.p, Yc.ld, E.st));
+      if (a.S > 1) E.chk(launch_slot_sum(yrs, Yr.ld, a.yr_slot_stride, a.S, Yr.rows, l2, Yr.p, Yr.ld, E.st));
+    }
+    if (E.ctx->nranks > 1) E.allreduce(Yr.p, Yr.ld * l2);
+    E.release(mk);
+  } else {
+    // widths beyond the fused kernel's register budget: two views (documented; info->view_launches = 2)
+    E.view(SIDE_N, Om, Yc);
+    E.view(SIDE_M, Phi, Yr);
+  }
+  // ---- lines 4-10: Q_c (optionally truncated to the top k+l_c left singular vectors of R_c)
+  double* Rc = E.alloc((int64_t)l * l);
+  E.orth(SIDE_M, Yc, Rc, nullptr);
+  TS Qc = Yc;
+  if (lc < c.p) {
+    double* Ul = E.alloc((int64_t)l * l);
+    double* Vr = E.alloc((int64_t)l * l);
+    double* sv = E.alloc(l);
+    E.core_svd(Rc, l, 0, Ul, sv, Vr);
+    TS Q2 = E.new_ts(SIDE_M, lp);
+    if (E.live()) E.chk(launch_ts_gemm(Yc.p, Yc.ld, Yc.rows, l, Ul, l, lp, Q2.p, Q2.ld, 0, E.st));
+    Qc = Q2;
+  }
+  // ---- line 11: [Qh, Rh] = qr(Phi^* Q_c)   (l2 x lp, tiny; replicated)
+  TS C;
+  C.rows = l2;
+  C.ld = round_up(l2, 32);
+  C.w = lp;
+  C.p = E.alloc(C.ld * lp);
+  {
+    double* Cg = E.alloc((int64_t)l2 * lp);
+    E.cross(SIDE_M, Phi, Qc, Cg);
+    if (E.live()) E.chk(launch_copy_cols(Cg, l2, C.p, C.ld, l2, lp, E.st));
+  }
+  // CholeskyQR2 of C, keeping R1^-1 and R2^-1 to form Rh^-1 = R1^-1 R2^-1
+  double* G = E.alloc((int64_t)lp * lp);
+  double* R1 = E.alloc((int64_t)lp * lp);
+  double* R1i = E.alloc((int64_t)lp * lp);
+  double* R2 = E.alloc((int64_t)lp * lp);
+  double* R2i = E.alloc((int64_t)lp * lp);
+  double* Rhi = E.alloc((int64_t)lp * lp);
+  double* T = E.alloc((int64_t)l2 * lp);
+  double* Cq = E.alloc((int64_t)l2 * lp);
+  if (E.live()) {
+    E.chk(launch_small_gemm(1, 0, lp, lp, l2, C.p, C.ld, C.p, C.ld, G, lp, E.st));
+    E.chk(launch_chol_ref(G, nullptr, lp, 1e-12, R1, R1i, E.ctx->dstat, E.st));
+    E.chk(launch_small_gemm(0, 0, l2, lp, lp, C.p, C.ld, R1i, lp, Cq, l2, E.st));
+    E.chk(launch_small_gemm(1, 0, lp, lp, l2, Cq, l2, Cq, l2, G, lp, E.st));
+    E.chk(launch_chol_ref(G, nullptr, lp, 1e-12, R2, R2i, nullptr, E.st));
+    E.chk(launch_small_gemm(0, 0, l2, lp, lp, Cq, l2, R2i, lp, C.p, C.ld, E.st));   // Qh
+    E.chk(launch_small_gemm(0, 0, lp, lp, lp, R1i, lp, R2i, lp, Rhi, lp, E.st));     // Rh^-1
+    // ---- line 12: X = Rh^-1 Qh^* Y_r^*  ->  X^T = Y_r (Qh Rh^-T);  T = Qh Rh^-T  (l2 x lp)
+    E.chk(launch_small_gemm(0, 1, l2, lp, lp, C.p, C.ld, Rhi, lp, T, l2, E.st));
+  }
+  TS Xt = E.new_ts(SIDE_N, lp);
+  if (E.live()) E.chk(launch_ts_gemm(Yr.p, Yr.ld, Yr.rows, l2, T, l2, lp, Xt.p, Xt.ld, 0, E.st));
+  // ---- line 13: tsvd(X, k) via X^T = Qx Rx  ->  X = Rx^T Qx^T,  svd(Rx^T) = Uh Lam Wh^T
+  double* Rx = E.alloc((int64_t)lp * lp);
+  E.orth(SIDE_N, Xt, Rx, nullptr);
+  double* Ul = E.alloc((int64_t)lp * lp);
+  double* Vr = E.alloc((int64_t)lp * lp);
+  double* lam = E.alloc(lp);
+  E.core_svd(Rx, lp, /*trans=*/1, Ul, lam, Vr);
+  // U = Q_c Uh (side M), V = Qx Wh (side N)           (line 14)
+  write_outputs(E, SIDE_M, SIDE_N, Qc, Xt, Ul, Vr, lam, lp, c.k);
+}
+
+// primitives -------------------------------------------------------------------------------
+void prim_view(Exec& E) {
+  const Call& c = E.call;
+  const Side from = c.trans ? SIDE_M : SIDE_N;
+  const Side to = c.trans ? SIDE_N : SIDE_M;
+  TS X = E.stage_in(from, c.Om, c.ldom, c.w, c.kOm);
+  TS Y = E.new_ts(to, c.w);
+  E.view(from, X, Y);
+  int64_t ld;
+  double* o = E.out_ptr(c.U, c.ldu, Y.rows, c.w, c.kU, &ld);
+  if (E.live()) E.chk(launch_copy_cols(Y.p, Y.ld, o, ld, Y.rows, c.w, E.st));
+}
+
+void prim_orth(Exec& E) {
+  const Call& c = E.call;
+  TS Y;
+  Y.rows = c.rows;
+  Y.ld = round_up(std::max<int64_t>(c.rows, 1), 32);
+  Y.w = c.w;
+  Y.p = E.alloc(Y.ld * c.w);
+  if (c.kU == PTR_HOST)
+    E.h2d.push_back({Y.p, Y.ld, c.U, c.ldu, Y.rows, c.w});
+  else if (E.live())
+    E.chk(launch_copy_cols(static_cast<const double*>(c.U), c.ldu, Y.p, Y.ld, Y.rows, c.w, E.st));
+  // orth on a local (unsharded) side of arbitrary length: emulate with m = rows
+  double* R = E.alloc((int64_t)c.w * c.w);
+  const int64_t m_save = E.m;
+  E.m = c.rows;
+  E.orth(SIDE_N, Y, R, nullptr);  // SIDE_N: never all-reduced
+  E.m = m_save;
+  int64_t ld;
+  double* o = E.out_ptr(c.U, c.ldu, Y.rows, c.w, c.kU, &ld);
+  if (E.live()) E.chk(launch_copy_cols(Y.p, Y.ld, o, ld, Y.rows, c.w, E.st));
+  if (c.kR != PTR_NULL) {
+    double* ro = E.out_ptr(c.R, c.w, c.w, c.w, c.kR, &ld);
+    if (E.live()) E.chk(launch_copy_cols(R, c.w, ro, ld, c.w, c.w, E.st));
+  }
+}
+
+void prim_fused(Exec& E) {
+  const Call& c = E.call;
+  const int l = c.w, l2 = c.l2;
+  TS Om = E.stage_in(SIDE_N, c.Om, c.ldom, l, c.kOm);
+  TS Phi = E.stage_in(SIDE_M, c.Phi, c.ldphi, l2, c.kPhi);
+  TS Yc = E.new_ts(SIDE_M, l), Yr = E.new_ts(SIDE_N, l2);
+  if (l > kFusedMaxL || (l2 + 7) / 8 > kFusedMaxL2T) {
+    E.chk(RSVD_E_ARG);
+    return;
+  }
+  FusedArgs a;
+  a.A = E.A;
+  a.rows = E.m;
+  a.n = E.n;
+  a.lda = E.lda;
+  a.Om = Om.p;
+  a.ldom = Om.ld;
+  a.l = l;
+  a.Phi = Phi.p;
+  a.ldphi = Phi.ld;
+  a.l2 = l2;
+  a.grid_cap = E.ctx->sms;
+  plan_view(VIEW_FUSED, E.m, E.n, l2, E.ctx->sms, &a.S, &a.KTS);
+  const int nsb = fused_strips(E.n);
+  a.yc_atomic = ((double)nsb * Yc.ld * l * 8.0 > kYcSlotBudget) ? 1 : 0;
+  E.nondet |= a.yc_atomic;
+  double* ycs = a.yc_atomic ? Yc.p : E.alloc((int64_t)nsb * Yc.ld * l);
+  a.yc = ycs;
+  a.ldyc = Yc.ld;
+  a.yc_slot_stride = (int64_t)Yc.ld * l;
+  double* yrs = (a.S == 1) ? Yr.p : E.alloc((int64_t)a.S * Yr.ld * l2);
+  a.yr = yrs;
+  a.ldyr = Yr.ld;
+  a.yr_slot_stride = (int64_t)Yr.ld * l2;
+  E.view_bytes += (double)E.m * E.n * 8.0;
+  E.view_flops += 2.0 * E.m * E.n * (l + l2);
+  ++E.view_launches;
+  if (E.live()) {
+    if (a.yc_atomic) E.chk(launch_fill(Yc.p, Yc.ld * l, 0.0, E.st));
+    int e0 = -1, e1 = -1;
+    E.ev_record(&e0);
+    E.chk(launch_view_fused(a, E.st));
+    E.ev_record(&e1);
+    if (e0 >= 0) E.ev_pairs.push_back({e0, e1});
+    if (!a.yc_atomic) E.chk(launch_slot_sum(ycs, Yc.ld, a.yc_slot_stride, nsb, Yc.rows, l, Yc.p, Yc.ld, E.st));
+    if (a.S > 1) E.chk(launch_slot_sum(yrs, Yr.ld, a.yr_slot_stride, a.S, Yr.rows, l2, Yr.p, Yr.ld, E.st));
+  }
+  int64_t ld;
+  double* o1 = E.out_ptr(c.U, c.ldu, Yc.rows, l, c.kU, &ld);
+  if (E.live()) E.chk(launch_copy_cols(Yc.p, Yc.ld, o1, ld, Yc.rows, l, E.st));
+  double* o2 = E.out_ptr(c.V, c.ldv, Yr.rows, l2, c.kV, &ld);
+  if (E.live()) E.chk(launch_copy_cols(Yr.p, Yr.ld, o2, ld, Yr.rows, l2, E.st));
+}
+
+void prim_core(Exec& E) {
+  const Call& c = E.call;
+  const int r = (int)c.rows, cc = c.cols;
+  double* M = E.alloc((int64_t)r * cc);
+  if (c.kOm == PTR_HOST)
+    E.h2d.push_back({M, r, c.Om, c.ldom, r, cc});
+  else if (E.live())
+    E.chk(launch_copy_cols(static_cast<const double*>(c.Om), c.ldom, M, r, r, cc, E.st));
+  int64_t ldU, ldV, ldS;
+  double* Uo = E.out_ptr(c.U, r, r, cc, c.kU == PTR_NULL ? PTR_DEVICE : c.kU, &ldU);
+  double* So = E.out_ptr(c.S, cc, cc, 1, c.kS, &ldS);
+  double* Vo = E.out_ptr(c.V, cc, cc, cc, c.kV, &ldV);
+  // jacobi writes Ul with ld r and Vr with ld c: route through arena buffers
+  double* Ul = E.alloc((int64_t)r * cc);
+  double* Vr = E.alloc((int64_t)cc * cc);
+  double* sv = E.alloc(cc);
+  double* scratch = E.alloc(2 * 256 * 256);
+  if (E.live()) {
+    E.chk(launch_jacobi_t(M, r, 0, r, cc, Ul, sv, Vr, scratch, E.ctx->dstat, E.st));
+    if (c.kU != PTR_NULL) E.chk(launch_copy_cols(Ul, r, Uo, ldU, r, cc, E.st));
+    if (c.kS != PTR_NULL) E.chk(launch_copy_cols(sv, cc, So, ldS, cc, 1, E.st));
+    if (c.kV != PTR_NULL) E.chk(launch_copy_cols(Vr, cc, Vo, ldV, cc, cc, E.st));
+  }
+}
+
+void run_alg(Exec& E) {
+  switch (E.call.alg) {
+    case 0: alg_subspace(E); break;
+    case 1: alg_krylov(E); break;
+    case 2: alg_single_pass(E); break;
+    case 10: prim_view(E); break;
+    case 11: prim_fused(E); break;
+    case 12: prim_orth(E); break;
+    case 13: prim_core(E); break;
+    default: E.chk(RSVD_E_ARG);
+  }
+}
+
+std::string call_key(const Call& c, const Exec& E, const rsvd_ctx* ctx) {
+  char buf[1024];
+  snprintf(buf, sizeof buf,
+           "a%d k%d p%d v%d in%d l2%d lc%d t%d w%d r%lld c%d f%u A%p m%lld n%lld lda%lld O%p/%lld/%d P%p/%lld/%d "
+           "U%p/%lld/%d S%p/%d V%p/%lld/%d R%p/%d ar%p nr%d",
+           c.alg, c.k, c.p, c.v, c.input, c.l2, c.lc, c.trans, c.w, (long long)c.rows, c.cols, c.flags,
+           (const void*)E.A, (long long)E.m, (long long)E.n, (long long)E.lda, c.Om, (long long)c.ldom, (int)c.kOm,
+           c.Phi, (long long)c.ldphi, (int)c.kPhi, c.U, (long long)c.ldu, (int)c.kU, c.S, (int)c.kS, c.V,
+           (long long)c.ldv, (int)c.kV, c.R, (int)c.kR, (void*)ctx->arena, ctx->nranks);
+  return std::string(buf);
+}
+
+// Stage A (host memory -> first arena allocation) and bind the executor to the device A.
+void bind_A(Exec& E, const Call& call) {
+  if (!call.A) return;
+  E.m = call.A->m_local;
+  E.n = call.A->n;
+  E.lda = call.A->lda;
+  const bool misaligned = call.kA == PTR_DEVICE &&
+                         ((reinterpret_cast<uintptr_t>(call.A->data) & 15) || ((call.A->lda * 8) & 15));
+  if (call.kA == PTR_HOST || misaligned) {
+    // host A, or a device A whose base / row stride violates TMA's 16-byte rule: copy into an
+    // aligned workspace block (row-major copy: width n doubles, height m rows)
+    E.lda = round_up(call.A->n, 16);
+    double* Ad = E.alloc(E.m * E.lda);
+    E.h2d.push_back({Ad, E.lda, call.A->data, call.A->lda, E.n, E.m});
+    E.A = Ad;
+    E.a_restaged = 1;
+  } else {
+    E.A = static_cast<const double*>(call.A->data);
+  }
+}
+
+int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
+  if (info) memset(info, 0, sizeof(*info));
+  cudaSetDevice(ctx->device);
+  call.kA = call.A ? ptr_kind(call.A->data, ctx->device) : PTR_NULL;
+  call.kOm = ptr_kind(call.Om, ctx->device);
+  call.kPhi = ptr_kind(call.Phi, ctx->device);
+  call.kU = ptr_kind(call.U, ctx->device);
+  call.kS = ptr_kind(call.S, ctx->device);
+  call.kV = ptr_kind(call.V, ctx->device);
+  call.kR = ptr_kind(call.R, ctx->device);
+  const bool profile = (call.flags & RSVD_PROFILE) != 0;
+  // ---- 1. sizing pass (fake base)
+  Exec sz(ctx, call, true, nullptr);
+  bind_A(sz, call);
+  run_alg(sz);
+  if (sz.rc) {
+    set_err(ctx, "invalid configuration (planning failed, code %d)", sz.rc);
+    return sz.rc;
+  }
+  const size_t need = sz.peak + 4096;
+  if (need > ctx->arena_size) {
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+    ctx->graphs.clear();
+    if (ctx->arena) cudaFree(ctx->arena);
+    ctx->arena = nullptr;
+    ctx->arena_size = 0;
+    const size_t bytes = (size_t)round_up((int64_t)(need * 1.25), 1 << 20);
+    if (cudaMalloc(&ctx->arena, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      set_err(ctx, "cudaMalloc of %zu bytes of workspace failed", bytes);
+      return RSVD_E_NOMEM;
+    }
+    ctx->arena_size = bytes;
+  }
+  // ---- 2. enqueue (or record-only) pass at real addresses
+  Exec E(ctx, call, false, ctx->arena);
+  E.profile = profile;
+  bind_A(E, call);
+  cudaStream_t st = ctx->stream;
+  const bool use_graph = !(call.flags & RSVD_NO_GRAPH) && !profile;
+  const std::string key = call_key(call, E, ctx);
+  auto it = use_graph ? ctx->graphs.find(key) : ctx->graphs.end();
+  const bool replay = use_graph && it != ctx->graphs.end();
+
+  auto do_h2d = [&](const std::vector<Exec::H2D>& lst) -> int {
+    for (auto& t : lst)
+      if (cudaMemcpy2DAsync(t.dst, t.ldd * 8, t.src, t.lds * 8, t.rows * 8, t.cols, cudaMemcpyDefault, st) !=
+          cudaSuccess)
+        return RSVD_E_CUDA;
+    return RSVD_OK;
+  };
+  int rc = RSVD_OK;
+  if (use_graph) {
+    cudaGraphExec_t ge = nullptr;
+    if (replay) {
+      E.launch_off = true;  // record transfers only
+      run_alg(E);
+      ge = it->second;
+    } else {
+      cudaGraph_t g;
+      if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        set_err(ctx, "cudaStreamBeginCapture failed");
+        return RSVD_E_CUDA;
+      }
+      cudaMemsetAsync(ctx->dstat, 0, sizeof(DevStatus), st);
+      run_alg(E);
+      cudaError_t ce = cudaStreamEndCapture(st, &g);
+      if (E.rc || ce != cudaSuccess) {
+        cudaGetLastError();
+        if (ce == cudaSuccess) cudaGraphDestroy(g);
+        set_err(ctx, "enqueue failed during capture (rc %d, %s)", E.rc, cudaGetErrorString(ce));
+        return E.rc ? E.rc : RSVD_E_CUDA;
+      }
+      if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphDestroy(g);
+        set_err(ctx, "cudaGraphInstantiate failed");
+        return RSVD_E_CUDA;
+      }
+      cudaGraphDestroy(g);
+      ctx->graphs[key] = ge;
+    }
+    rc = do_h2d(E.h2d);
+    if (rc == RSVD_OK && cudaGraphLaunch(ge, st) != cudaSuccess) rc = RSVD_E_CUDA;
+  } else {
+    // direct enqueue: collect transfers first (launch-free pass), then launch
+    Exec pre(ctx, call, false, ctx->arena);
+    pre.launch_off = true;
+    bind_A(pre, call);
+    run_alg(pre);
+    rc = do_h2d(pre.h2d);
+    if (rc == RSVD_OK) {
+      cudaMemsetAsync(ctx->dstat, 0, sizeof(DevStatus), st);
+      int ev0 = -1, ev1 = -1;
+      E.ev_record(&ev0);
+      run_alg(E);
+      E.ev_record(&ev1);
+      rc = E.rc;
+      if (profile && ev0 >= 0) E.ev_pairs.insert(E.ev_pairs.begin(), {ev0, ev1});
+    }
+  }
+  if (rc == RSVD_OK) {
+    for (auto& t : E.d2h)
+      if (cudaMemcpy2DAsync(t.dst, t.ldd * 8, t.src, t.lds * 8, t.rows * 8, t.cols, cudaMemcpyDefault, st) !=
+          cudaSuccess) {
+        rc = RSVD_E_CUDA;
+        break;
+      }
+  }
+  if (rc == RSVD_OK) cudaMemcpyAsync(ctx->hstat, ctx->dstat, sizeof(DevStatus), cudaMemcpyDefault, st);
+  cudaError_t se = cudaStreamSynchronize(st);
+  if (se != cudaSuccess) {
+    set_err(ctx, "CUDA error: %s", cudaGetErrorString(se));
+    return RSVD_E_CUDA;
+  }
+  if (rc != RSVD_OK) {
+    cudaError_t le = cudaGetLastError();
+    set_err(ctx, "launch failed (rc %d): %s", rc, cudaGetErrorString(le));
+    return rc;
+  }
+  const DevStatus hs = *ctx->hstat;
+  if (info) {
+    info->rank_deficient_cols = hs.deficient;
+    info->jacobi_sweeps = hs.jacobi_sweeps;
+    info->graph_replayed = replay ? 1 : 0;
+    info->host_staged = (call.kA == PTR_HOST || call.kOm == PTR_HOST || call.kPhi == PTR_HOST ||
+                         call.kU == PTR_HOST || call.kV == PTR_HOST || call.kS == PTR_HOST)
+                            ? 1
+                            : 0;
+    if (sz.a_restaged && call.kA == PTR_DEVICE) info->host_staged = 2;
+    info->view_launches = sz.view_launches;
+    info->view_bytes = sz.view_bytes;
+    info->view_flops = sz.view_flops;
+    info->nondeterministic = sz.nondet;
+    if (profile && !E.ev_pairs.empty()) {
+      double vm = 0;
+      for (size_t i = 1; i < E.ev_pairs.size(); ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ctx->events[E.ev_pairs[i].first], ctx->events[E.ev_pairs[i].second]);
+        vm += ms;
+      }
+      float tot = 0;
+      cudaEventElapsedTime(&tot, ctx->events[E.ev_pairs[0].first], ctx->events[E.ev_pairs[0].second]);
+      info->view_ms = vm;
+      info->total_ms = tot;
+    }
+  }
+  if (hs.jacobi_fail) {
+    set_err(ctx, "Jacobi SVD of the core did not converge");
+    if (info) info->status = RSVD_E_NUMERIC;
+    return RSVD_E_NUMERIC;
+  }
+  return RSVD_OK;
+}
+
+int check_mat(rsvd_ctx* ctx, const rsvd_mat* A) {
+  if (!A || !A->data) { set_err(ctx, "A is NULL"); return RSVD_E_ARG; }
+  if (A->dtype == RSVD_F32) { set_err(ctx, "RSVD_F32 is not implemented in this release"); return RSVD_E_DTYPE; }
+  if (A->dtype != RSVD_F64) { set_err(ctx, "unknown dtype %d", A->dtype); return RSVD_E_DTYPE; }
+  if (A->m < 1 || A->n < 1 || A->m_local < 0 || A->row0 < 0 || A->row0 + A->m_local > A->m) {
+    set_err(ctx, "bad shape m=%lld n=%lld m_local=%lld row0=%lld", (long long)A->m, (long long)A->n,
+            (long long)A->m_local, (long long)A->row0);
+    return RSVD_E_ARG;
+  }
+  if (A->lda < A->n) { set_err(ctx, "lda < n"); return RSVD_E_ARG; }
+  if (ctx->nranks == 1 && (A->m_local != A->m || A->row0 != 0)) {
+    set_err(ctx, "single-GPU call needs m_local == m and row0 == 0");
+    return RSVD_E_ARG;
+  }
+  if (A->m_local < 1) { set_err(ctx, "empty shard"); return RSVD_E_ARG; }
+  return RSVD_OK;
+}
+
+int common_checks(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p) {
+  if (!ctx) return RSVD_E_ARG;
+  int r = check_mat(ctx, A);
+  if (r) return r;
+  if (k < 1 || p < 0) { set_err(ctx, "need k >= 1 and p >= 0"); return RSVD_E_ARG; }
+  const int64_t l = (int64_t)k + p;
+  if (l > std::min(A->m, A->n)) { set_err(ctx, "k + p = %lld exceeds min(m, n)", (long long)l); return RSVD_E_ARG; }
+  if (l > 256) { set_err(ctx, "k + p > 256 is not supported"); return RSVD_E_ARG; }
+  return RSVD_OK;
+}
+
+}  // namespace
+
+// ================================================================ exported C ABI
+extern "C" {
+
+int rsvd_version(void) { return 100; }
+
+const char* rsvd_strerror(int code) {
+  switch (code) {
+    case RSVD_OK: return "ok";
+    case RSVD_E_ARG: return "invalid argument";
+    case RSVD_E_DTYPE: return "unsupported dtype";
+    case RSVD_E_CUDA: return "CUDA error";
+    case RSVD_E_NCCL: return "NCCL error";
+    case RSVD_E_NOMEM: return "out of device memory";
+    case RSVD_E_NUMERIC: return "numerical failure";
+    case RSVD_E_STATE: return "invalid state";
+    default: return "unknown error";
+  }
+}
+
+const char* rsvd_last_error(const rsvd_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+int rsvd_recommend_input(int goal, int v) {
+  if (goal == RSVD_GOAL_RIGHT || goal == RSVD_GOAL_NORMAL) return (v % 2 == 0) ? RSVD_INPUT_A : RSVD_INPUT_AT;
+  if (goal == RSVD_GOAL_LEFT) return (v % 2 == 0) ? RSVD_INPUT_AT : RSVD_INPUT_A;
+  return RSVD_INPUT_A;
+}
+
+int rsvd_create(rsvd_ctx** out, int device, void* stream) {
+  if (!out) return RSVD_E_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return RSVD_E_CUDA;
+  }
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10) return RSVD_E_CUDA;  // sm_100a kernels only
+  rsvd_ctx* c = new rsvd_ctx();
+  c->device = device;
+  c->sms = prop.multiProcessorCount;
+  cudaSetDevice(device);
+  if (stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      return RSVD_E_CUDA;
+    }
+    c->own_stream = true;
+  }
+  if (cudaMalloc(&c->dstat, sizeof(DevStatus)) != cudaSuccess ||
+      cudaMallocHost(&c->hstat, sizeof(DevStatus)) != cudaSuccess) {
+    delete c;
+    return RSVD_E_NOMEM;
+  }
+  *out = c;
+  return RSVD_OK;
+}
+
+int rsvd_destroy(rsvd_ctx* c) {
+  if (!c) return RSVD_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto e : c->events) cudaEventDestroy(e);
+  if (c->arena) cudaFree(c->arena);
+  if (c->dstat) cudaFree(c->dstat);
+  if (c->hstat) cudaFreeHost(c->hstat);
+  if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return RSVD_OK;
+}
+
+int rsvd_sm_count(const rsvd_ctx* c) { return c ? c->sms : 0; }
+
+int rsvd_probe_peaks(rsvd_ctx* c, double* dmma_tflops, double* read_gbs) {
+  if (!c || !dmma_tflops || !read_gbs) return RSVD_E_ARG;
+  cudaSetDevice(c->device);
+  return probe_peaks(c->sms, c->stream, dmma_tflops, read_gbs);
+}
+
+int rsvd_get_unique_id(void* id128) {
+  if (!id128) return RSVD_E_ARG;
+  if (!g_nccl.load()) return RSVD_E_NCCL;
+  nccl_uid_t uid;
+  if (g_nccl.get_uid(&uid) != 0) return RSVD_E_NCCL;
+  memcpy(id128, &uid, 128);
+  return RSVD_OK;
+}
+
+int rsvd_comm_init(rsvd_ctx* c, int nranks, int rank, const void* id128) {
+  if (!c || nranks < 1 || rank < 0 || rank >= nranks || !id128) return RSVD_E_ARG;
+  if (c->comm) return RSVD_E_STATE;
+  if (nranks == 1) return RSVD_OK;
+  if (!g_nccl.load()) {
+    set_err(c, "libnccl.so.2 not loadable");
+    return RSVD_E_NCCL;
+  }
+  cudaSetDevice(c->device);
+  nccl_uid_t uid;
+  memcpy(&uid, id128, 128);
+  nccl_comm_t comm = nullptr;
+  nccl_res_t r = g_nccl.init_rank(&comm, nranks, uid, rank);
+  if (r != 0) {
+    set_err(c, "ncclCommInitRank failed: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
+    return RSVD_E_NCCL;
+  }
+  c->comm = comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  c->graphs.clear();
+  return RSVD_OK;
+}
+
+int rsvd_comm_nranks(const rsvd_ctx* c) { return c ? c->nranks : 0; }
+
+static int algo_entry(int alg, rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, int input, const void* Omega,
+                      int64_t ld_omega, void* U, int64_t ldu, void* S, void* V, int64_t ldv, unsigned flags,
+                      rsvd_info* info) {
+  int r = common_checks(ctx, A, k, p);
+  if (r == RSVD_OK) {
+    const int l = k + p;
+    if (v < 2) { set_err(ctx, "v >= 2 required (P:142, P:903); use rsvd_single_pass for v = 1"); r = RSVD_E_ARG; }
+    else if (input != RSVD_INPUT_A && input != RSVD_INPUT_AT) { set_err(ctx, "bad input"); r = RSVD_E_ARG; }
+    else if (!Omega) { set_err(ctx, "Omega is NULL"); r = RSVD_E_ARG; }
+    else {
+      const int64_t om_rows = (input == RSVD_INPUT_A) ? A->n : A->m_local;
+      if (ld_omega < om_rows) { set_err(ctx, "ld_omega < rows of Omega"); r = RSVD_E_ARG; }
+      if (U && ldu < A->m_local) { set_err(ctx, "ldu < m_local"); r = RSVD_E_ARG; }
+      if (V && ldv < A->n) { set_err(ctx, "ldv < n"); r = RSVD_E_ARG; }
+      if (input == RSVD_INPUT_AT && ctx->nranks > 1 && alg == 1) {
+        // fine: sharded side handled by the same code path
+      }
+      if (alg == 1 && r == RSVD_OK) {
+        const int nb = (v % 2 == 0) ? v / 2 : (v - 1) / 2;
+        const int64_t W = (int64_t)nb * l;
+        const int64_t side_rows_c = (input == RSVD_INPUT_A) ? A->m : A->n;
+        const int64_t side_rows_r = (input == RSVD_INPUT_A) ? A->n : A->m;
+        const int64_t krows = (v % 2 == 0) ? side_rows_c : side_rows_r;
+        if (W > krows || W > 160) {
+          set_err(ctx, "Krylov basis width %lld exceeds its side (%lld rows) or 160", (long long)W,
+                  (long long)krows);
+          r = RSVD_E_ARG;
+        }
+      }
+    }
+  }
+  if (r != RSVD_OK) {
+    if (info) { memset(info, 0, sizeof(*info)); info->status = r; }
+    return r;
+  }
+  Call c;
+  c.alg = alg;
+  c.A = A;
+  c.k = k;
+  c.p = p;
+  c.v = v;
+  c.input = input;
+  c.Om = Omega;
+  c.ldom = ld_omega;
+  c.U = U;
+  c.ldu = ldu;
+  c.S = S;
+  c.V = V;
+  c.ldv = ldv;
+  c.flags = flags;
+  r = execute(ctx, c, info);
+  if (info) {
+    info->status = r;
+    info->views = v;
+    const int l = k + p;
+    info->vectors = (alg == 0) ? (int64_t)v * l : (int64_t)(v + v / 2 - 1) * l;
+  }
+  return r;
+}
+
+int rsvd_subspace(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, int input, const void* Omega,
+                  int64_t ld_omega, void* U, int64_t ldu, void* S, void* V, int64_t ldv, unsigned flags,
+                  rsvd_info* info) {
+  return algo_entry(0, ctx, A, k, p, v, input, Omega, ld_omega, U, ldu, S, V, ldv, flags, info);
+}
+
+int rsvd_block_krylov(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, int input, const void* Omega,
+                      int64_t ld_omega, void* U, int64_t ldu, void* S, void* V, int64_t ldv, unsigned flags,
+                      rsvd_info* info) {
+  return algo_entry(1, ctx, A, k, p, v, input, Omega, ld_omega, U, ldu, S, V, ldv, flags, info);
+}
+
+int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int lc, const void* Omega,
+                     int64_t ld_omega, const void* Phi, int64_t ld_phi, void* U, int64_t ldu, void* S, void* V,
+                     int64_t ldv, unsigned flags, rsvd_info* info) {
+  int r = common_checks(ctx, A, k, p);
+  if (lc == -1) lc = p;
+  if (r == RSVD_OK) {
+    if (l2 < k + p) { set_err(ctx, "l2 >= k + p required (P:663)"); r = RSVD_E_ARG; }
+    else if (l2 > std::min<int64_t>(A->m, 256)) { set_err(ctx, "l2 exceeds min(m, 256)"); r = RSVD_E_ARG; }
+    else if (lc < 0 || lc > p) { set_err(ctx, "lc must be in [0, p] (P:663)"); r = RSVD_E_ARG; }
+    else if (!Omega || !Phi) { set_err(ctx, "Omega/Phi NULL"); r = RSVD_E_ARG; }
+    else if (ld_omega < A->n || ld_phi < A->m_local) { set_err(ctx, "ld_omega/ld_phi too small"); r = RSVD_E_ARG; }
+    else if ((U && ldu < A->m_local) || (V && ldv < A->n)) { set_err(ctx, "ldu/ldv too small"); r = RSVD_E_ARG; }
+  }
+  if (r != RSVD_OK) {
+    if (info) { memset(info, 0, sizeof(*info)); info->status = r; }
+    return r;
+  }
+  Call c;
+  c.alg = 2;
+  c.A = A;
+  c.k = k;
+  c.p = p;
+  c.l2 = l2;
+  c.lc = lc;
+  c.Om = Omega;
+  c.ldom = ld_omega;
+  c.Phi = Phi;
+  c.ldphi = ld_phi;
+  c.U = U;
+  c.ldu = ldu;
+  c.S = S;
+  c.V = V;
+  c.ldv = ldv;
+  c.flags = flags;
+  r = execute(ctx, c, info);
+  if (info) {
+    info->status = r;
+    info->views = 1;
+    info->vectors = (int64_t)(k + p) + l2;
+    info->lc_used = lc;
+  }
+  return r;
+}
+
+int rsvd_view(rsvd_ctx* ctx, const rsvd_mat* A, int trans, const void* X, int64_t ldx, int w, void* Y, int64_t ldy,
+              unsigned flags, rsvd_info* info) {
+  if (!ctx) return RSVD_E_ARG;
+  int r = check_mat(ctx, A);
+  if (r == RSVD_OK) {
+    const int64_t xr = trans ? A->m_local : A->n, yr = trans ? A->n : A->m_local;
+    if (w < 1 || w > 256 || !X || !Y || ldx < xr || ldy < yr) { set_err(ctx, "bad view arguments"); r = RSVD_E_ARG; }
+  }
+  if (r) return r;
+  Call c;
+  c.alg = 10;
+  c.A = A;
+  c.trans = trans ? 1 : 0;
+  c.w = w;
+  c.Om = X;
+  c.ldom = ldx;
+  c.U = Y;
+  c.ldu = ldy;
+  c.flags = flags;
+  return execute(ctx, c, info);
+}
+
+int rsvd_view_fused(rsvd_ctx* ctx, const rsvd_mat* A, const void* Omega, int64_t ld_omega, int l, const void* Phi,
+                    int64_t ld_phi, int l2, void* Yc, int64_t ld_yc, void* Yr, int64_t ld_yr, unsigned flags,
+                    rsvd_info* info) {
+  if (!ctx) return RSVD_E_ARG;
+  int r = check_mat(ctx, A);
+  if (r == RSVD_OK) {
+    if (l < 1 || l > kFusedMaxL || l2 < 1 || (l2 + 7) / 8 > kFusedMaxL2T || !Omega || !Phi || !Yc || !Yr ||
+        ld_omega < A->n || ld_phi < A->m_local || ld_yc < A->m_local || ld_yr < A->n) {
+      set_err(ctx, "bad fused-view arguments (l <= %d, l2 <= %d)", kFusedMaxL, kFusedMaxL2T * 8);
+      r = RSVD_E_ARG;
+    }
+  }
+  if (r) return r;
+  Call c;
+  c.alg = 11;
+  c.A = A;
+  c.w = l;
+  c.l2 = l2;
+  c.Om = Omega;
+  c.ldom = ld_omega;
+  c.Phi = Phi;
+  c.ldphi = ld_phi;
+  c.U = Yc;
+  c.ldu = ld_yc;
+  c.V = Yr;
+  c.ldv = ld_yr;
+  c.flags = flags;
+  return execute(ctx, c, info);
+}
+
+int rsvd_orth(rsvd_ctx* ctx, int64_t rows, int w, void* Y, int64_t ldy, void* R, unsigned flags, rsvd_info* info) {
+  if (!ctx) return RSVD_E_ARG;
+  if (rows < 1 || w < 1 || w > 160 || w > rows || !Y || ldy < rows) {
+    set_err(ctx, "bad orth arguments (1 <= w <= min(rows, 160))");
+    return RSVD_E_ARG;
+  }
+  Call c;
+  c.alg = 12;
+  c.rows = rows;
+  c.w = w;
+  c.U = Y;
+  c.ldu = ldy;
+  c.R = R;
+  c.flags = flags;
+  return execute(ctx, c, info);
+}
+
+int rsvd_core_svd(rsvd_ctx* ctx, int r, int cc, const void* M, int64_t ldm, void* U, void* S, void* V,
+                  unsigned flags, rsvd_info* info) {
+  if (!ctx) return RSVD_E_ARG;
+  if (cc < 1 || r < cc || r > 256 || !M || ldm < r) {
+    set_err(ctx, "bad core-svd arguments (1 <= c <= r <= 256)");
+    return RSVD_E_ARG;
+  }
+  Call c;
+  c.alg = 13;
+  c.rows = r;
+  c.cols = cc;
+  c.Om = M;
+  c.ldom = ldm;
+  c.U = U;
+  c.S = S;
+  c.V = V;
+  c.flags = flags;
+  return execute(ctx, c, info);
+}
+
+}  // extern "C"

@@ -1,0 +1,549 @@
+// Kernels that run between the matrix views (PAPER.md P:69 qr/chol, P:67 tsvd, P:159 lift):
+//   slot sums (deterministic split-K reduction), Gram / cross products, guarded Cholesky with
+//   pseudo-inverse of R (CholeskyQR2 building block), tall-skinny x small GEMM, one-sided
+//   Jacobi SVD of the small core.  All fp64.
+#include "common.cuh"
+#include "internal.h"
+
+#include <algorithm>
+
+namespace rsvd {
+
+// ------------------------------------------------------------------ slot sum
+__global__ void k_slot_sum(const double* __restrict__ in, int64_t ldi, int64_t slot_stride, int S, int64_t rows, int w,
+                           double* __restrict__ out, int64_t ldo) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (r >= rows || c >= w) return;
+  const double* p = in + (int64_t)c * ldi + r;
+  double s = p[0];
+  for (int k = 1; k < S; ++k) s += p[(int64_t)k * slot_stride];
+  out[(int64_t)c * ldo + r] = s;
+}
+
+int launch_slot_sum(const double* in, int64_t ldi, int64_t slot_stride, int S, int64_t rows, int w, double* out,
+                    int64_t ldo, cudaStream_t st) {
+  if (rows <= 0 || w <= 0) return RSVD_OK;
+  dim3 grid((unsigned)((rows + 255) / 256), (unsigned)w);
+  k_slot_sum<<<grid, 256, 0, st>>>(in, ldi, slot_stride, S, rows, w, out, ldo);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+// ------------------------------------------------------------------ cross Gram  G = Xa^T Xb
+// grid.x = row slots, grid.y = 64x64 output blocks (bi, bj).  256 threads, 4x4 register tile.
+constexpr int kGR = 32;  // rows per smem tile
+__global__ void __launch_bounds__(256) k_cross_gram(const double* __restrict__ Xa, int64_t lda_, int a,
+                                                    const double* __restrict__ Xb, int64_t ldb, int b, int64_t rows,
+                                                    int64_t rows_per_slot, double* __restrict__ slots, int nbj) {
+  __shared__ double sa[kGR][64 + 2];
+  __shared__ double sb[kGR][64 + 2];
+  const int slot = blockIdx.x;
+  const int bi = blockIdx.y / nbj, bj = blockIdx.y % nbj;
+  const int i0 = bi * 64, j0 = bj * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t r0 = (int64_t)slot * rows_per_slot;
+  const int64_t r1 = min(rows, r0 + rows_per_slot);
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int64_t rr = r0; rr < r1; rr += kGR) {
+    // load: 64 columns x kGR rows of each operand (coalesced along rows)
+    for (int e = threadIdx.x; e < 64 * kGR; e += 256) {
+      const int col = e / kGR, row = e % kGR;
+      const int64_t r = rr + row;
+      const bool okr = r < r1;
+      sa[row][col] = (okr && i0 + col < a) ? Xa[(int64_t)(i0 + col) * lda_ + r] : 0.0;
+      sb[row][col] = (okr && j0 + col < b) ? Xb[(int64_t)(j0 + col) * ldb + r] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int row = 0; row < kGR; ++row) {
+      double va[4], vb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) va[i] = sa[row][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) vb[j] = sb[row][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(va[i], vb[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  double* out = slots + (int64_t)slot * a * b;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gi = i0 + ty + 16 * i, gj = j0 + tx + 16 * j;
+      if (gi < a && gj < b) out[(int64_t)gj * a + gi] = acc[i][j];
+    }
+}
+
+int gram_slots(int64_t rows) {
+  int64_t s = rows / 1024;
+  if (s < 1) s = 1;
+  if (s > 128) s = 128;
+  return (int)s;
+}
+
+int launch_cross_gram(const double* Xa, int64_t lda_, int a, const double* Xb, int64_t ldb, int b, int64_t rows,
+                      double* slots, int nslots, cudaStream_t st) {
+  const int nbi = (a + 63) / 64, nbj = (b + 63) / 64;
+  const int64_t rps = (rows + nslots - 1) / nslots;
+  dim3 grid((unsigned)nslots, (unsigned)(nbi * nbj));
+  k_cross_gram<<<grid, 256, 0, st>>>(Xa, lda_, a, Xb, ldb, b, rows, rps, slots, nbj);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+__global__ void k_slots_reduce_small(const double* __restrict__ slots, int nslots, int64_t count, double* __restrict__ G) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double s = slots[i];
+  for (int k = 1; k < nslots; ++k) s += slots[(int64_t)k * count + i];
+  G[i] = s;
+}
+
+int launch_slots_reduce_small(const double* slots, int nslots, int64_t count, double* G, cudaStream_t st) {
+  k_slots_reduce_small<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(slots, nslots, count, G);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+// ------------------------------------------------------------------ guarded Cholesky
+// G = R^T R (R upper).  Pivot j is "deficient" when d_j <= tol * ref_j with ref_j the reference
+// squared norm of column j (G_jj itself, or the pre-projection norm for block Gram-Schmidt) —
+// then row j of R is zero and column j of Rinv is zero (the column drops out of Q).
+// Rinv is the upper-triangular inverse restricted to the kept columns.
+constexpr int kCholMaxW = 160;
+__global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, const double* __restrict__ ref, int w,
+                                               double tol, double* __restrict__ R, double* __restrict__ Rinv,
+                                               DevStatus* status) {
+  extern __shared__ double S[];  // w*w (col-major), then deficient flags
+  int* defi = reinterpret_cast<int*>(S + w * w);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < w * w; e += nt) S[e] = G[e];
+  __syncthreads();
+  for (int j = 0; j < w; ++j) {
+    const double d = S[j * w + j];
+    const double rf = ref ? ref[j] : G[j * w + j];
+    const bool def = !(d > tol * rf) || !(rf > 0.0);
+    const double rjj = def ? 0.0 : sqrt(d);
+    __syncthreads();  // everyone has read S(j,j)
+    if (tid == 0) {
+      S[j * w + j] = rjj;
+      defi[j] = def ? 1 : 0;
+    }
+    // row j of R: R(j,i) = S(j,i) / rjj, i > j  (S(j,i) at S[i*w + j])
+    for (int i = j + 1 + tid; i < w; i += nt) S[i * w + j] = def ? 0.0 : S[i * w + j] / rjj;
+    __syncthreads();
+    // trailing update of the upper triangle: S(i,k) -= R(j,i) R(j,k), j < i <= k
+    const int m = w - j - 1;
+    if (!def && m > 0) {
+      const int tot = m * m;
+      for (int e = tid; e < tot; e += nt) {
+        const int ii = e % m, kk = e / m;
+        if (ii <= kk) {
+          const int i = j + 1 + ii, k = j + 1 + kk;
+          S[k * w + i] -= S[i * w + j] * S[k * w + j];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // write R (upper, zero below)
+  for (int e = tid; e < w * w; e += nt) {
+    const int i = e % w, k = e / w;
+    R[e] = (i <= k) ? S[k * w + i] : 0.0;
+  }
+  // Rinv: column j solves R x = e_j on the kept columns
+  for (int j = tid; j < w; j += nt) {
+    double* x = Rinv + (int64_t)j * w;
+    for (int i = 0; i < w; ++i) x[i] = 0.0;
+    if (!defi[j]) {
+      x[j] = 1.0 / S[j * w + j];
+      for (int i = j - 1; i >= 0; --i) {
+        if (defi[i]) continue;
+        double s = 0.0;
+        for (int k = i + 1; k <= j; ++k) s = fma(S[k * w + i], x[k], s);
+        x[i] = -s / S[i * w + i];
+      }
+    }
+  }
+  if (tid == 0 && status) {
+    int cnt = 0;
+    for (int j = 0; j < w; ++j) cnt += defi[j];
+    if (cnt) atomicAdd(&status->deficient, cnt);
+  }
+}
+
+int launch_chol_ref(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
+                    DevStatus* status, cudaStream_t st) {
+  if (w < 1 || w > kCholMaxW) return RSVD_E_ARG;
+  const size_t smem = (size_t)w * w * 8 + (size_t)w * 4 + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholMaxW * kCholMaxW * 8 + kCholMaxW * 4 + 16);
+    attr = true;
+  }
+  k_chol<<<1, 1024, smem, st>>>(G, ref, w, tol, R, Rinv, status);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+int launch_chol(const double* G, int w, double* R, double* Rinv, double* /*Racc*/, DevStatus* status,
+                cudaStream_t st) {
+  return launch_chol_ref(G, nullptr, w, 1e-12, R, Rinv, status, st);
+}
+
+// ------------------------------------------------------------------ tall-skinny x small GEMM
+// out(rows x c) (=|-=) in(rows x w) M(w x c).  One thread per row, 16 output columns per CTA.
+constexpr int kTsCC = 16;
+__global__ void __launch_bounds__(128) k_ts_gemm(const double* __restrict__ in, int64_t ldi, int64_t rows, int w,
+                                                 const double* __restrict__ M, int64_t ldm, int c,
+                                                 double* __restrict__ out, int64_t ldo, int mode) {
+  extern __shared__ double Ms[];  // w x kTsCC (row-major by k)
+  const int c0 = blockIdx.y * kTsCC;
+  for (int e = threadIdx.x; e < w * kTsCC; e += blockDim.x) {
+    const int k = e / kTsCC, cc = e % kTsCC;
+    Ms[e] = (c0 + cc < c) ? M[(int64_t)(c0 + cc) * ldm + k] : 0.0;
+  }
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double acc[kTsCC];
+#pragma unroll
+  for (int i = 0; i < kTsCC; ++i) acc[i] = 0.0;
+  for (int k = 0; k < w; ++k) {
+    const double x = in[(int64_t)k * ldi + r];
+    const double2* mrow = reinterpret_cast<const double2*>(Ms + k * kTsCC);
+#pragma unroll
+    for (int i = 0; i < kTsCC / 2; ++i) {
+      const double2 mv = mrow[i];
+      acc[2 * i] = fma(x, mv.x, acc[2 * i]);
+      acc[2 * i + 1] = fma(x, mv.y, acc[2 * i + 1]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kTsCC; ++i) {
+    if (c0 + i < c) {
+      double* o = out + (int64_t)(c0 + i) * ldo + r;
+      *o = mode ? (*o - acc[i]) : acc[i];
+    }
+  }
+}
+
+int launch_ts_gemm(const double* in, int64_t ldi, int64_t rows, int w, const double* M, int64_t ldm, int c,
+                   double* out, int64_t ldo, int mode, cudaStream_t st) {
+  if (rows <= 0 || c <= 0) return RSVD_OK;
+  if (w > 1024) return RSVD_E_ARG;
+  dim3 grid((unsigned)((rows + 127) / 128), (unsigned)((c + kTsCC - 1) / kTsCC));
+  const size_t smem = (size_t)w * kTsCC * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ts_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * kTsCC * 8);
+    attr = true;
+  }
+  k_ts_gemm<<<grid, 128, smem, st>>>(in, ldi, rows, w, M, ldm, c, out, ldo, mode);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+// ------------------------------------------------------------------ one-sided Jacobi SVD
+// Hestenes: W = M J with plane rotations on column pairs (parallel round-robin ordering, one
+// warp per pair) until every pair satisfies |w_p . w_q| <= tol sqrt(|w_p|^2 |w_q|^2).
+// M = (W S^-1) S J^T  ->  left vectors W_j / s_j, right vectors J, values s_j = |W_j|.
+constexpr int kJacThreads = 512;
+__global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict__ M, int64_t ldm, int trans, int r,
+                                                        int c, double* __restrict__ Ul, double* __restrict__ Sv,
+                                                        double* __restrict__ Vr, double* __restrict__ gW,
+                                                        double* __restrict__ gJ, int w_in_smem, int j_in_smem,
+                                                        double tol, int max_sweeps, DevStatus* status) {
+  extern __shared__ double sm[];
+  const int ce = c + (c & 1);  // even number of columns (pad with a zero column)
+  double* W = w_in_smem ? sm : gW;
+  double* J = j_in_smem ? (sm + (w_in_smem ? (int64_t)r * ce : 0)) : gJ;
+  __shared__ int rotated;
+  __shared__ double sval[256];
+  __shared__ int srank[256];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
+  for (int e = tid; e < r * ce; e += nt) {
+    const int i = e % r, j = e / r;
+    double v = 0.0;
+    if (j < c) v = trans ? M[(int64_t)i * ldm + j] : M[(int64_t)j * ldm + i];
+    W[(int64_t)j * r + i] = v;
+  }
+  for (int e = tid; e < ce * ce; e += nt) J[e] = ((e % ce) == (e / ce)) ? 1.0 : 0.0;
+  __syncthreads();
+  int sweep = 0;
+  bool converged = false;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < ce - 1; ++round) {
+      for (int pi = warp; pi < ce / 2; pi += nwarp) {
+        int p, q;
+        if (pi == 0) {
+          p = round;
+          q = ce - 1;
+        } else {
+          p = (round + pi) % (ce - 1);
+          q = (round - pi + (ce - 1)) % (ce - 1);
+        }
+        if (p > q) { const int tt = p; p = q; q = tt; }
+        double* wp = W + (int64_t)p * r;
+        double* wq = W + (int64_t)q * r;
+        double a = 0.0, b = 0.0, cc = 0.0;
+        for (int i = lane; i < r; i += 32) {
+          const double x = wp[i], y = wq[i];
+          a = fma(x, x, a);
+          b = fma(y, y, b);
+          cc = fma(x, y, cc);
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        cc = warp_sum(cc);
+        if (cc != 0.0 && fabs(cc) > tol * sqrt(a * b)) {
+          const double zeta = (b - a) / (2.0 * cc);
+          const double t = (zeta != 0.0) ? copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta)) : 1.0;
+          const double cs = 1.0 / sqrt(1.0 + t * t);
+          const double sn = cs * t;
+          for (int i = lane; i < r; i += 32) {
+            const double x = wp[i], y = wq[i];
+            wp[i] = cs * x - sn * y;
+            wq[i] = sn * x + cs * y;
+          }
+          double* jp = J + (int64_t)p * ce;
+          double* jq = J + (int64_t)q * ce;
+          for (int i = lane; i < ce; i += 32) {
+            const double x = jp[i], y = jq[i];
+            jp[i] = cs * x - sn * y;
+            jq[i] = sn * x + cs * y;
+          }
+          if (lane == 0) rotated = 1;
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+    }
+    if (!rotated) {
+      converged = true;
+      ++sweep;
+      break;
+    }
+  }
+  // singular values and descending ranks (ties broken by index)
+  for (int j = warp; j < ce; j += nwarp) {
+    const double* wj = W + (int64_t)j * r;
+    double s = 0.0;
+    for (int i = lane; i < r; i += 32) s = fma(wj[i], wj[i], s);
+    s = warp_sum(s);
+    if (lane == 0) sval[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = tid; j < ce; j += nt) {
+    const double sj = sval[j];
+    int rk = 0;
+    for (int i = 0; i < ce; ++i) {
+      const double si = sval[i];
+      rk += (si > sj) || (si == sj && i < j);
+    }
+    srank[j] = rk;
+  }
+  __syncthreads();
+  for (int e = tid; e < r * ce; e += nt) {
+    const int i = e % r, j = e / r;
+    const int rk = srank[j];
+    if (rk < c) {
+      const double sj = sval[j];
+      Ul[(int64_t)rk * r + i] = sj > 0.0 ? W[(int64_t)j * r + i] / sj : 0.0;
+    }
+  }
+  for (int e = tid; e < ce * ce; e += nt) {
+    const int i = e % ce, j = e / ce;
+    const int rk = srank[j];
+    if (rk < c && i < c) Vr[(int64_t)rk * c + i] = J[(int64_t)j * ce + i];
+  }
+  for (int j = tid; j < ce; j += nt)
+    if (srank[j] < c) Sv[srank[j]] = sval[j];
+  if (tid == 0 && status) {
+    status->jacobi_sweeps = sweep;
+    if (!converged) atomicAdd(&status->jacobi_fail, 1);
+  }
+}
+
+int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
+                    double* scratch, DevStatus* status, cudaStream_t st) {
+  if (c < 1 || c > 256 || r < c || r > 256) return RSVD_E_ARG;
+  const int ce = c + (c & 1);
+  const size_t wbytes = (size_t)r * ce * 8, jbytes = (size_t)ce * ce * 8;
+  const size_t budget = 200 * 1024;
+  int w_in = wbytes <= budget ? 1 : 0;
+  int j_in = (w_in ? wbytes + jbytes : jbytes) <= budget ? 1 : 0;
+  const size_t smem = (w_in ? wbytes : 0) + (j_in ? jbytes : 0);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
+    attr = true;
+  }
+  const double tol = 2.220446049250313e-16 * (double)c;
+  k_jacobi<<<1, kJacThreads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, scratch + 256 * 256, w_in, j_in, tol,
+                                         60, status);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+int launch_jacobi(const double* M, int64_t ldm, int r, int c, double* Ul, double* S, double* Vr, double* scratch,
+                  DevStatus* status, cudaStream_t st) {
+  return launch_jacobi_t(M, ldm, 0, r, c, Ul, S, Vr, scratch, status, st);
+}
+
+// ------------------------------------------------------------------ small dense helpers
+__global__ void k_small_gemm(int ta, int tb, int m, int n, int k, const double* __restrict__ A, int64_t lda_,
+                             const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i >= m || j >= n) return;
+  double s = 0.0;
+  for (int p = 0; p < k; ++p) {
+    const double a = ta ? A[(int64_t)i * lda_ + p] : A[(int64_t)p * lda_ + i];
+    const double b = tb ? B[(int64_t)p * ldb + j] : B[(int64_t)j * ldb + p];
+    s = fma(a, b, s);
+  }
+  C[(int64_t)j * ldc + i] = s;
+}
+
+int launch_small_gemm(int ta, int tb, int m, int n, int k, const double* A, int64_t lda_, const double* B,
+                      int64_t ldb, double* C, int64_t ldc, cudaStream_t st) {
+  dim3 grid((unsigned)((m + 127) / 128), (unsigned)n);
+  k_small_gemm<<<grid, 128, 0, st>>>(ta, tb, m, n, k, A, lda_, B, ldb, C, ldc);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+__global__ void k_copy_cols(const double* __restrict__ src, int64_t lds, double* __restrict__ dst, int64_t ldd,
+                            int64_t rows) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (r < rows) dst[(int64_t)c * ldd + r] = src[(int64_t)c * lds + r];
+}
+
+int launch_copy_cols(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int cols,
+                     cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return RSVD_OK;
+  dim3 grid((unsigned)((rows + 255) / 256), (unsigned)cols);
+  k_copy_cols<<<grid, 256, 0, st>>>(src, lds, dst, ldd, rows);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+__global__ void k_fill(double* dst, int64_t n, double v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = v;
+}
+
+int launch_fill(double* dst, int64_t count, double v, cudaStream_t st) {
+  if (count <= 0) return RSVD_OK;
+  k_fill<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(dst, count, v);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+__global__ void k_square(double* S, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) S[i] = S[i] * S[i];
+}
+
+int launch_square(double* S, int n, cudaStream_t st) {
+  k_square<<<(n + 127) / 128, 128, 0, st>>>(S, n);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+// diag of a (w x w) matrix -> vector
+__global__ void k_diag(const double* G, int w, double* d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < w) d[i] = G[(int64_t)i * w + i];
+}
+
+int launch_diag(const double* G, int w, double* d, cudaStream_t st) {
+  k_diag<<<(w + 127) / 128, 128, 0, st>>>(G, w, d);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+}  // namespace rsvd
+
+// ------------------------------------------------------------------ peak probes (roofline denominators)
+namespace rsvd {
+// FP64 DMMA issue-rate probe: 8 independent accumulator chains per warp, operands in registers.
+__global__ void __launch_bounds__(256) k_probe_dmma(double* sink, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma(c[i][0], c[i][1], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.0) sink[threadIdx.x] = s;
+}
+
+// streaming read probe: 128-bit loads, grid-stride, sum into a sink
+__global__ void __launch_bounds__(512) k_probe_read(const double2* __restrict__ p, int64_t n2, double* sink) {
+  double acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n2; i += 4 * stride) {
+    const double2 v0 = __ldcs(p + i), v1 = __ldcs(p + i + stride), v2 = __ldcs(p + i + 2 * stride),
+                  v3 = __ldcs(p + i + 3 * stride);
+    acc += v0.x + v0.y + v1.x + v1.y + v2.x + v2.y + v3.x + v3.y;
+  }
+  for (; i < n2; i += stride) {
+    const double2 v = __ldcs(p + i);
+    acc += v.x + v.y;
+  }
+  if (acc == 12345.0) sink[0] = acc;
+}
+
+int probe_peaks(int sms, cudaStream_t st, double* dmma_tflops, double* read_gbs) {
+  double* sink = nullptr;
+  cudaMalloc(&sink, 4096);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 20000;
+  const int blocks = sms * 4;
+  k_probe_dmma<<<blocks, 256, 0, st>>>(sink, 100);  // warm-up
+  cudaEventRecord(e0, st);
+  k_probe_dmma<<<blocks, 256, 0, st>>>(sink, iters);
+  cudaEventRecord(e1, st);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double flops = 2.0 * 256.0 * 8.0 * iters * (blocks * 256 / 32);
+  *dmma_tflops = flops / (ms * 1e-3) / 1e12;
+  // read probe over 4 GiB
+  const size_t bytes = (size_t)4 << 30;
+  void* buf = nullptr;
+  *read_gbs = 0;
+  if (cudaMalloc(&buf, bytes) == cudaSuccess) {
+    cudaMemsetAsync(buf, 0, bytes, st);
+    const int64_t n2 = (int64_t)(bytes / 16);
+    k_probe_read<<<sms * 4, 512, 0, st>>>((const double2*)buf, n2, sink);
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0, st);
+      k_probe_read<<<sms * 4, 512, 0, st>>>((const double2*)buf, n2, sink);
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      best = ms < best ? ms : best;
+    }
+    *read_gbs = (double)bytes / (best * 1e-3) / 1e9;
+    cudaFree(buf);
+  } else {
+    cudaGetLastError();
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  return cudaGetLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+}  // namespace rsvd

@@ -1,0 +1,270 @@
+"""Thin ctypes binding of librsvd.so (include/rsvd.h).  Argument marshalling only: every step
+of the randomized-SVD path runs in the library's CUDA kernels.  There is no CPU fallback — if
+the shared library cannot be loaded, every entry point raises.
+
+Tensors: A is a row-major (m, n) float64 tensor (CUDA or CPU/pinned).  Tall-skinny arguments are
+(rows, w) tensors; they are passed column-major (each column contiguous) — a tensor with
+stride (1, ld) is passed as is, anything else is copied to that layout first.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librsvd.so")
+
+RSVD_F32, RSVD_F64 = 1, 2
+RSVD_INPUT_A, RSVD_INPUT_AT = 0, 1
+RSVD_GOAL_SVD, RSVD_GOAL_LEFT, RSVD_GOAL_RIGHT, RSVD_GOAL_NORMAL = 0, 1, 2, 3
+RSVD_SQUARED, RSVD_NO_GRAPH, RSVD_PROFILE = 1, 2, 4
+ERR = {0: "RSVD_OK", -1: "RSVD_E_ARG", -2: "RSVD_E_DTYPE", -3: "RSVD_E_CUDA", -4: "RSVD_E_NCCL",
+       -5: "RSVD_E_NOMEM", -6: "RSVD_E_NUMERIC", -7: "RSVD_E_STATE"}
+
+EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_strerror", "rsvd_last_error", "rsvd_version", "rsvd_sm_count",
+           "rsvd_recommend_input", "rsvd_probe_peaks", "rsvd_get_unique_id", "rsvd_comm_init", "rsvd_comm_nranks", "rsvd_subspace",
+           "rsvd_block_krylov", "rsvd_single_pass", "rsvd_view", "rsvd_view_fused", "rsvd_orth", "rsvd_core_svd"]
+
+
+class RsvdMat(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int32), ("reserved", ctypes.c_int32), ("m", ctypes.c_int64),
+                ("n", ctypes.c_int64), ("m_local", ctypes.c_int64), ("row0", ctypes.c_int64),
+                ("lda", ctypes.c_int64), ("data", ctypes.c_void_p)]
+
+
+class RsvdInfo(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("views", ctypes.c_int32), ("vectors", ctypes.c_int64),
+                ("rank_deficient_cols", ctypes.c_int32), ("jacobi_sweeps", ctypes.c_int32),
+                ("lc_used", ctypes.c_int32), ("host_staged", ctypes.c_int32), ("graph_replayed", ctypes.c_int32),
+                ("nondeterministic", ctypes.c_int32), ("view_launches", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("view_ms", ctypes.c_double), ("view_bytes", ctypes.c_double),
+                ("view_flops", ctypes.c_double), ("total_ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"}
+
+
+class RsvdError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERR.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load librsvd.so (fail loudly if it is missing: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `python -m paper_1804_07531_b200.build`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, u32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint
+    pinfo = ctypes.POINTER(RsvdInfo)
+    pmat = ctypes.POINTER(RsvdMat)
+    L.rsvd_create.argtypes = [ctypes.POINTER(vp), i32, vp]
+    L.rsvd_destroy.argtypes = [vp]
+    L.rsvd_strerror.argtypes = [i32]
+    L.rsvd_strerror.restype = ctypes.c_char_p
+    L.rsvd_last_error.argtypes = [vp]
+    L.rsvd_last_error.restype = ctypes.c_char_p
+    L.rsvd_sm_count.argtypes = [vp]
+    L.rsvd_recommend_input.argtypes = [i32, i32]
+    L.rsvd_get_unique_id.argtypes = [vp]
+    L.rsvd_probe_peaks.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    L.rsvd_comm_init.argtypes = [vp, i32, i32, vp]
+    L.rsvd_comm_nranks.argtypes = [vp]
+    alg = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
+    L.rsvd_subspace.argtypes = alg
+    L.rsvd_block_krylov.argtypes = alg
+    L.rsvd_single_pass.argtypes = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
+    L.rsvd_view.argtypes = [vp, pmat, i32, vp, i64, i32, vp, i64, u32, pinfo]
+    L.rsvd_view_fused.argtypes = [vp, pmat, vp, i64, i32, vp, i64, i32, vp, i64, vp, i64, u32, pinfo]
+    L.rsvd_orth.argtypes = [vp, i64, i32, vp, i64, vp, u32, pinfo]
+    L.rsvd_core_svd.argtypes = [vp, i32, i32, vp, i64, vp, vp, vp, u32, pinfo]
+    _lib = L
+    return L
+
+
+def recommend_input(goal: int, v: int) -> int:
+    return lib().rsvd_recommend_input(goal, v)
+
+
+def get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = lib().rsvd_get_unique_id(buf)
+    if rc:
+        raise RsvdError(rc, "rsvd_get_unique_id")
+    return buf.raw
+
+
+def _colmajor(t: torch.Tensor) -> torch.Tensor:
+    """(rows, w) tensor in column-major layout (stride (1, ld))."""
+    if t.dim() == 1:
+        t = t[:, None]
+    if t.stride(0) == 1 and (t.shape[1] == 1 or t.stride(1) >= t.shape[0]):
+        return t
+    return t.t().contiguous().t()
+
+
+def _ld(t: torch.Tensor) -> int:
+    return t.stride(1) if t.shape[1] > 1 else max(t.shape[0], 1)
+
+
+def _new_colmajor(rows, cols, like: torch.Tensor, pin=False):
+    if like.is_cuda:
+        return torch.empty((cols, rows), dtype=like.dtype, device=like.device).t()
+    return torch.empty((cols, rows), dtype=like.dtype, pin_memory=pin).t()
+
+
+class Context:
+    """One rsvd_ctx bound to a CUDA device and (by default) torch's current stream."""
+
+    def __init__(self, device: int | None = None, stream: torch.cuda.Stream | None = None):
+        L = lib()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = ctypes.c_void_p()
+        rc = L.rsvd_create(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream))
+        if rc:
+            raise RsvdError(rc, "rsvd_create")
+        self._h = h
+        self.nranks = 1
+        self.rank = 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().rsvd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def sm_count(self) -> int:
+        return lib().rsvd_sm_count(self._h)
+
+    def probe_peaks(self):
+        """(FP64 DMMA TFLOP/s, HBM read GB/s) measured on this device."""
+        t, g = ctypes.c_double(), ctypes.c_double()
+        self._check(lib().rsvd_probe_peaks(self._h, ctypes.byref(t), ctypes.byref(g)), "rsvd_probe_peaks")
+        return t.value, g.value
+
+    def _check(self, rc, what):
+        if rc:
+            raise RsvdError(rc, f"{what}: {lib().rsvd_last_error(self._h).decode()}")
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        """Collective: all ranks pass the same 128-byte id (rank 0's get_unique_id())."""
+        buf = ctypes.create_string_buffer(uid, 128)
+        self._check(lib().rsvd_comm_init(self._h, nranks, rank, buf), "rsvd_comm_init")
+        self.nranks, self.rank = nranks, rank
+
+    # ------------------------------------------------------------------ helpers
+    @staticmethod
+    def mat(A: torch.Tensor, m: int | None = None, row0: int = 0) -> RsvdMat:
+        if A.dtype != torch.float64:
+            dt = RSVD_F32 if A.dtype == torch.float32 else 0
+        else:
+            dt = RSVD_F64
+        if A.stride(1) != 1:
+            raise ValueError("A must be row-major (stride(1) == 1)")
+        ml, n = A.shape
+        return RsvdMat(dt, 0, m if m is not None else ml, n, ml, row0, A.stride(0), A.data_ptr())
+
+    def _out_like(self, A, rows, cols, host_out):
+        if host_out or not A.is_cuda:
+            return _new_colmajor(rows, cols, A.cpu() if A.is_cuda else A, pin=True)
+        return _new_colmajor(rows, cols, A)
+
+    # ------------------------------------------------------------------ algorithms
+    def _alg(self, fn, name, A, k, p, v, Omega, input=RSVD_INPUT_A, flags=0, m=None, row0=0,
+             want_u=True, want_v=True, host_out=False):
+        Om = _colmajor(Omega)
+        M = self.mat(A, m, row0)
+        U = self._out_like(A, A.shape[0], k, host_out) if want_u else None
+        V = self._out_like(A, A.shape[1], k, host_out) if want_v else None
+        S = (torch.empty(k, dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
+             else torch.empty(k, dtype=A.dtype, device=A.device))
+        info = RsvdInfo()
+        rc = fn(self._h, ctypes.byref(M), k, p, v, input, Om.data_ptr(), _ld(Om),
+                U.data_ptr() if U is not None else None, _ld(U) if U is not None else 0, S.data_ptr(),
+                V.data_ptr() if V is not None else None, _ld(V) if V is not None else 0, flags, ctypes.byref(info))
+        self._check(rc, name)
+        return U, S, V, info
+
+    def subspace(self, A, k, p, v, Omega, input=RSVD_INPUT_A, flags=0, **kw):
+        """Alg. 2.  Returns (U, S, V, info) of A."""
+        return self._alg(lib().rsvd_subspace, "rsvd_subspace", A, k, p, v, Omega, input, flags, **kw)
+
+    def block_krylov(self, A, k, p, v, Omega, input=RSVD_INPUT_A, flags=0, **kw):
+        """Alg. 9."""
+        return self._alg(lib().rsvd_block_krylov, "rsvd_block_krylov", A, k, p, v, Omega, input, flags, **kw)
+
+    def single_pass(self, A, k, p, l2, Omega, Phi, lc=-1, flags=0, m=None, row0=0, host_out=False):
+        """Alg. 7.  lc = -1 -> lc = p (Tropp baseline)."""
+        Om, Ph = _colmajor(Omega), _colmajor(Phi)
+        M = self.mat(A, m, row0)
+        U = self._out_like(A, A.shape[0], k, host_out)
+        V = self._out_like(A, A.shape[1], k, host_out)
+        S = (torch.empty(k, dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
+             else torch.empty(k, dtype=A.dtype, device=A.device))
+        info = RsvdInfo()
+        rc = lib().rsvd_single_pass(self._h, ctypes.byref(M), k, p, l2, lc, Om.data_ptr(), _ld(Om), Ph.data_ptr(),
+                                    _ld(Ph), U.data_ptr(), _ld(U), S.data_ptr(), V.data_ptr(), _ld(V), flags,
+                                    ctypes.byref(info))
+        self._check(rc, "rsvd_single_pass")
+        return U, S, V, info
+
+    # ------------------------------------------------------------------ primitives
+    def view(self, A, X, trans=False, flags=0):
+        X = _colmajor(X)
+        M = self.mat(A)
+        rows = A.shape[1] if trans else A.shape[0]
+        Y = _new_colmajor(rows, X.shape[1], A) if A.is_cuda else _new_colmajor(rows, X.shape[1], A, pin=True)
+        info = RsvdInfo()
+        self._check(lib().rsvd_view(self._h, ctypes.byref(M), int(trans), X.data_ptr(), _ld(X), X.shape[1],
+                                    Y.data_ptr(), _ld(Y), flags, ctypes.byref(info)), "rsvd_view")
+        return Y, info
+
+    def view_fused(self, A, Omega, Phi, flags=0):
+        Om, Ph = _colmajor(Omega), _colmajor(Phi)
+        M = self.mat(A)
+        Yc = _new_colmajor(A.shape[0], Om.shape[1], A)
+        Yr = _new_colmajor(A.shape[1], Ph.shape[1], A)
+        info = RsvdInfo()
+        self._check(lib().rsvd_view_fused(self._h, ctypes.byref(M), Om.data_ptr(), _ld(Om), Om.shape[1],
+                                          Ph.data_ptr(), _ld(Ph), Ph.shape[1], Yc.data_ptr(), _ld(Yc),
+                                          Yr.data_ptr(), _ld(Yr), flags, ctypes.byref(info)), "rsvd_view_fused")
+        return Yc, Yr, info
+
+    def orth(self, Y, flags=0):
+        """CholeskyQR2 (returns a new Q and R; the input is not modified)."""
+        Q = _colmajor(Y).clone() if _colmajor(Y).data_ptr() == Y.data_ptr() else _colmajor(Y)
+        Q = Q.t().contiguous().t()
+        w = Q.shape[1]
+        R = torch.empty((w, w), dtype=Q.dtype, device=Q.device).t()
+        info = RsvdInfo()
+        self._check(lib().rsvd_orth(self._h, Q.shape[0], w, Q.data_ptr(), _ld(Q), R.data_ptr(), flags,
+                                    ctypes.byref(info)), "rsvd_orth")
+        return Q, R, info
+
+    def core_svd(self, Mx, flags=0):
+        Mx = _colmajor(Mx)
+        r, c = Mx.shape
+        U = torch.empty((c, r), dtype=Mx.dtype, device=Mx.device).t()
+        S = torch.empty(c, dtype=Mx.dtype, device=Mx.device)
+        V = torch.empty((c, c), dtype=Mx.dtype, device=Mx.device).t()
+        info = RsvdInfo()
+        self._check(lib().rsvd_core_svd(self._h, r, c, Mx.data_ptr(), _ld(Mx), U.data_ptr(), S.data_ptr(),
+                                        V.data_ptr(), flags, ctypes.byref(info)), "rsvd_core_svd")
+        return U, S, V, info
