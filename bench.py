@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark of the pass-efficient randomized SVD hot path on B200 (BASELINE.json metric
+"A-view HBM GB/s (fraction of roofline) and rank-k SVD time per view budget").
+
+A STEP is one pass of the whole hot path over one synthetic matrix:
+    rsvd_subspace (Alg. 2, v=3)  +  rsvd_block_krylov (Alg. 9, v=4)  +  rsvd_single_pass (Alg. 7)
+= 3 + 4 + 1 = 8 views of A.  Workload at N=1: BASELINE.json configs[1] = C2 (fp64 4000x4000,
+k=20, p=10, l2=60).  At N GPUs (weak scaling) every rank holds a C2-sized row block of an
+(N*4000) x 4000 matrix with the same spectrum and the step is ONE distributed SVD (NCCL all-reduce
+of the Gram matrices and of the co-range views).
+
+value = A-view bytes of all ranks / step time (GB/s); L2 is flushed (256 MiB write) before every
+timed step, outside the timed events.  `e2e` = same metric through the C ABI with pinned HOST
+buffers (A, Omega, Phi in; U, S, V out) — the host<->device copies are inside the timed region.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C2]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth as S  # noqa: E402
+
+STEP_PLAN = [("subspace", 3), ("krylov", 4), ("single_pass", 1)]
+METRIC = "A-view HBM GB/s (fraction of roofline) and rank-k SVD time per view budget"
+
+
+def step_views():
+    return sum(v for _, v in STEP_PLAN)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU oracle baseline (reference arm)
+def run_oracle_step(A, cfg, Om, Phi):
+    import oracle as O
+
+    for alg, v in STEP_PLAN:
+        O.svd_of(A, alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi)
+
+
+def oracle_baseline(cfg, steps=1, budget_s=30.0):
+    """Time the oracle, as it stands, on this host's cores on the same workload (C2 step)."""
+    A = S.make_matrix(cfg)
+    Om = S.gaussian_test_matrix(cfg.n, cfg.l, cfg, S.ROLE_OMEGA)
+    Phi = S.gaussian_test_matrix(cfg.m, cfg.l2, cfg, S.ROLE_PHI)
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        run_oracle_step(A, cfg, Om, Phi)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget_s:
+            break
+    step_s = statistics.median(times)
+    bytes_step = step_views() * cfg.m * cfg.n * cfg.itemsize
+    cores = len(os.sched_getaffinity(0))
+    return {"value": bytes_step / step_s / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "sample": f"{len(times)} full step(s) of {cfg.name} ({'+'.join(f'{a}(v={v})' for a, v in STEP_PLAN)}), "
+                      f"NumPy/OpenBLAS fp64, median step {step_s:.3f} s",
+            "step_s": step_s}
+
+
+def reference_main(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = S.CONFIGS[args.config]
+    steps = max(1, min(args.steps, 3))
+    base = oracle_baseline(cfg, steps=steps + args.warmup * 0, budget_s=120.0)
+    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": 0, "ms_per_step": base["step_s"] * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: fp64 {cfg.m}x{cfg.n} Haar-spectrum matrix, k={cfg.k}, p={cfg.p}, "
+                                   f"l2={cfg.l2}; step = subspace v=3 + block Krylov v=4 + single pass (8 views)"},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_main(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1804_07531_b200 import rsvd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = S.CONFIGS[args.config]
+    ctx = rsvd.Context(local)
+    if world > 1:
+        obj = [rsvd.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.comm_init(world, rank, obj[0])
+
+    # ---- inputs: rank r holds rows [r*m, (r+1)*m) of A_global = [U_1;..;U_N] diag(sigma) V^T / sqrt(N)
+    m, n = cfg.m, cfg.n
+    A = S.make_matrix_torch(cfg, dev, m, n, seed_offset=rank)
+    if world > 1:
+        A.mul_(1.0 / np.sqrt(world))
+    Om = S.gaussian_test_matrix_torch(n, cfg.l, cfg, S.ROLE_OMEGA, dev)          # replicated
+    Phi = S.gaussian_test_matrix_torch(m, cfg.l2, cfg, S.ROLE_PHI, dev, seed_offset=rank)
+    M_glob, row0 = m * world, m * rank
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)     # 256 MiB > L2 (126 MB)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(flags=0, Ax=A, Omx=Om, Phix=Phi, host_out=False):
+        infos = []
+        for alg, v in STEP_PLAN:
+            if alg == "subspace":
+                r = ctx.subspace(Ax, cfg.k, cfg.p, v, Omx, flags=flags, m=M_glob, row0=row0, host_out=host_out)
+            elif alg == "krylov":
+                r = ctx.block_krylov(Ax, cfg.k, cfg.p, v, Omx, flags=flags, m=M_glob, row0=row0, host_out=host_out)
+            else:
+                r = ctx.single_pass(Ax, cfg.k, cfg.p, cfg.l2, Omx, Phix, flags=flags, m=M_glob, row0=row0,
+                                    host_out=host_out)
+            infos.append(r[3])
+        return infos
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up (also captures the CUDA graphs)
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+
+    # ---- timed region: device events per step, L2 flushed before each step (outside the events)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            infos = step()
+            evs[i][1].record(stream)
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = max_over_ranks(sum(step_ms))
+    ms_per_step = total_ms / args.steps
+    bytes_step_rank = step_views() * m * n * 8
+    value = world * bytes_step_rank * args.steps / (total_ms * 1e-3) / 1e9
+    launches_per_step = sum(inf.kernel_launches for inf in infos)
+
+    # ---- per-algorithm SVD time (graph replay, device events, L2 flushed)
+    alg_ms = {}
+    for idx, (alg, v) in enumerate(STEP_PLAN):
+        ts = []
+        for _ in range(max(3, args.steps // 2)):
+            flush.zero_()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            if alg == "subspace":
+                ctx.subspace(A, cfg.k, cfg.p, v, Om, m=M_glob, row0=row0)
+            elif alg == "krylov":
+                ctx.block_krylov(A, cfg.k, cfg.p, v, Om, m=M_glob, row0=row0)
+            else:
+                ctx.single_pass(A, cfg.k, cfg.p, cfg.l2, Om, Phi, m=M_glob, row0=row0)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ts.append(e0.elapsed_time(e1))
+        alg_ms[f"{alg}_v{v}"] = max_over_ranks(statistics.median(ts))
+
+    # ---- view-kernel durations (RSVD_PROFILE: events around every view kernel, same stream)
+    vms, vfl, vby, vcount, tot = 0.0, 0.0, 0.0, 0, 0.0
+    for _ in range(args.profile_steps):
+        flush.zero_()
+        barrier()
+        for inf in step(flags=rsvd.RSVD_PROFILE):
+            vms += inf.view_ms
+            vfl += inf.view_flops
+            vby += inf.view_bytes
+            vcount += inf.view_launches
+            tot += inf.total_ms
+    peaks = {}
+    try:
+        t_dmma, g_read = ctx.probe_peaks()
+        peaks = {"dmma_fp64_tflops": t_dmma, "hbm_read_gbs": g_read}
+    except Exception as e:  # pragma: no cover
+        peaks = {"error": str(e)}
+    achieved_tf = vfl / (vms * 1e-3) / 1e12 if vms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(cfg.name)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": "view kernels (k_view_ax / k_view_aty / k_view_fused), FP64 DMMA",
+                "achieved": achieved_tf, "peak": peaks.get("dmma_fp64_tflops"), "unit": "TFLOP/s",
+                "frac": (achieved_tf / peaks["dmma_fp64_tflops"]) if achieved_tf and peaks.get("dmma_fp64_tflops") else None,
+                "traffic": traffic,
+                "peak_source": "measured on this GPU by rsvd_probe_peaks (FP64 DMMA m8n8k4, all SMs); "
+                               "nominal-ratio alternative 1652.7 TF bf16 x 40/2250 = 29.4 TF",
+                "view_share_of_step": (vms / tot) if tot > 0 else None,
+                "hbm_gbs_during_views": (vby / (vms * 1e-3) / 1e9) if vms > 0 else None,
+                "hbm_read_peak_gbs": peaks.get("hbm_read_gbs"),
+                "avg_view_ms": vms / max(vcount, 1)}
+
+    # ---- e2e: pinned host buffers through the C ABI, copies inside the timed region
+    Ah = A.cpu().pin_memory()
+    Omh = Om.t().contiguous().cpu().pin_memory().t()
+    Phih = Phi.t().contiguous().cpu().pin_memory().t()
+    for _ in range(2):
+        step(Ax=Ah, Omx=Omh, Phix=Phih)
+    barrier()
+    e2e_ms = []
+    for _ in range(args.e2e_steps):
+        flush.zero_()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(Ax=Ah, Omx=Omh, Phix=Phih)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e_step = max_over_ranks(statistics.median(e2e_ms))
+    h2d = 3 * m * n * 8 + 3 * n * cfg.l * 8 + m * cfg.l2 * 8
+    d2h = 3 * (m + n + 1) * cfg.k * 8
+    e2e = {"value": world * bytes_step_rank / (e2e_step * 1e-3) / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step}
+
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: fp64 {m * world}x{n} (row block {m}x{n} per GPU), Haar factors, "
+                                   f"sigma_i=1 (i<=20) then 10^(-0.25(i-20)); k={cfg.k}, p={cfg.p}, l2={cfg.l2}; "
+                                   "step = subspace v=3 + block Krylov v=4 + single pass (8 views of A)",
+                       "l2_flush": "256 MiB write before every timed step (outside the events)",
+                       "parallelism": f"row-sharded A over {world} GPU(s), NCCL all-reduce" if world > 1 else "1 GPU"},
+            "views_per_s": world * step_views() * args.steps / (total_ms * 1e-3) / world,
+            "svd_ms": alg_ms, "roofline": roofline, "peaks_measured": peaks, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base = oracle_baseline(cfg, steps=1, budget_s=30.0)
+        line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

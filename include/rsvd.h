@@ -99,7 +99,8 @@ typedef struct {
   int32_t graph_replayed;       /* 1 if the call replayed a cached CUDA graph                 */
   int32_t nondeterministic;     /* 1 if atomics were used (see DETERMINISM)                   */
   int32_t view_launches;        /* view-kernel launches in the call                           */
-  int32_t reserved;
+  int32_t kernel_launches;      /* all librsvd kernels launched by the call (CUDA-graph kernel
+                                   nodes; 0 with RSVD_NO_GRAPH / RSVD_PROFILE)                  */
   double  view_ms;              /* RSVD_PROFILE: summed device time of the view kernels      */
   double  view_bytes;           /* algorithmic bytes of A streamed by those kernels          */
   double  view_flops;           /* algorithmic flops of those kernels (2 m n w per view)     */

@@ -23,7 +23,7 @@
 
 namespace rsvd {
 int launch_chol_ref(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
-                    DevStatus* status, cudaStream_t st);
+                    DevStatus* status, cudaStream_t st, double shift_coef = 0.0);
 int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
                     double* scratch, DevStatus* status, cudaStream_t st);
 int launch_diag(const double* G, int w, double* d, cudaStream_t st);
@@ -82,6 +82,7 @@ struct rsvd_ctx {
   DevStatus* dstat = nullptr;
   DevStatus* hstat = nullptr;  // pinned
   std::map<std::string, cudaGraphExec_t> graphs;
+  std::map<std::string, int> graph_kernels;  // kernel nodes per cached graph
   std::vector<cudaEvent_t> events;
   std::string err;
 };
@@ -276,7 +277,10 @@ struct Exec {
 
   // CholeskyQR2 in place: Y <- Q, R_out (w x w) = R2 R1 if requested.  `ref` (w) optional
   // reference squared column norms for the first pass's rank guard.
-  void orth(Side s, const TS& Y, double* R_out, const double* ref) {
+  // With `shifted`, a first shifted-Cholesky pass (G + sI, s = 11 (rows w + w(w+1)) u ||Y||_F^2)
+  // makes any Y with kappa(Y) < 1/u well enough conditioned for the two CholeskyQR passes
+  // (shifted CholeskyQR3, Fukaya et al. 2020); used for the projected Krylov blocks.
+  void orth(Side s, const TS& Y, double* R_out, const double* ref, bool shifted = false) {
     const int w = Y.w;
     const size_t mk = mark();
     double* G = alloc((int64_t)w * w);
@@ -285,6 +289,19 @@ struct Exec {
     double* R2 = alloc((int64_t)w * w);
     double* R2i = alloc((int64_t)w * w);
     TS T = new_ts(s, w);
+    if (shifted) {
+      double* R0 = alloc((int64_t)w * w);
+      double* R0i = alloc((int64_t)w * w);
+      const double rows_all = (double)(s == SIDE_M ? m * ctx->nranks : Y.rows);
+      const double coef = 11.0 * (rows_all * w + (double)w * (w + 1)) * 1.1102230246251565e-16;
+      cross(s, Y, Y, G);
+      if (live()) {
+        chk(launch_chol_ref(G, nullptr, w, 0.0, R0, R0i, nullptr, st, coef));
+        chk(launch_ts_gemm(Y.p, Y.ld, Y.rows, w, R0i, w, w, T.p, T.ld, 0, st));
+        chk(launch_copy_cols(T.p, T.ld, Y.p, Y.ld, Y.rows, w, st));
+      }
+      if (R_out) set_err(ctx, "internal: shifted orth does not return R");
+    }
     cross(s, Y, Y, G);
     if (live()) {
       chk(launch_chol_ref(G, ref, w, 1e-12, R1, R1i, ctx->dstat, st));
@@ -306,20 +323,19 @@ struct Exec {
       const int c0 = b * bw, wc = std::min(bw, K.w - c0);
       TS Wb = slice(K, c0, wc);
       const size_t mk = mark();
-      double* ref = nullptr;
       if (b > 0) {
+        // BCGS2 (Barlow & Smoktunowicz): project, normalise (shifted CholeskyQR: the projected
+        // remainder of a raw Krylov block can be tiny and nearly rank deficient), project again
+        // (removes the components the normalisation amplified), then CholeskyQR2.
         TS Qp = slice(K, 0, c0);
-        double* G0 = alloc((int64_t)wc * wc);
-        ref = alloc(wc);
         double* C = alloc((int64_t)c0 * wc);
-        cross(s, Wb, Wb, G0);
-        if (live()) chk(launch_diag(G0, wc, ref, st));
-        for (int pass = 0; pass < 2; ++pass) {
-          cross(s, Qp, Wb, C);
-          if (live()) chk(launch_ts_gemm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1, st));
-        }
+        cross(s, Qp, Wb, C);
+        if (live()) chk(launch_ts_gemm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1, st));
+        orth(s, Wb, nullptr, nullptr, /*shifted=*/true);
+        cross(s, Qp, Wb, C);
+        if (live()) chk(launch_ts_gemm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1, st));
       }
-      orth(s, Wb, nullptr, ref);
+      orth(s, Wb, nullptr, nullptr);
       release(mk);
     }
   }
@@ -338,25 +354,21 @@ struct Exec {
 
   // ------------------------------------------------------------ staging of caller arrays
   // device TS copy of a caller array (rows x w, column-major, ld_user)
+  // (host or device) caller arrays are copied in by cudaMemcpy2DAsync before the graph launch,
+  // and outputs are copied out after it, so the captured graph never references caller memory
+  // other than A: one graph serves every call with the same A, shapes and flags.
   TS stage_in(Side s, const void* src, int64_t ld_user, int w, PtrKind kind) {
+    (void)kind;
     TS t = new_ts(s, w);
-    if (kind == PTR_HOST) {
-      h2d.push_back({t.p, t.ld, src, ld_user, t.rows, w});
-    } else if (live()) {
-      chk(launch_copy_cols(static_cast<const double*>(src), ld_user, t.p, t.ld, t.rows, w, st));
-    }
+    h2d.push_back({t.p, t.ld, src, ld_user, t.rows, w});
     return t;
   }
   // where to write a caller output of rows x cols (col-major, ld): direct if device, else staging
   double* out_ptr(void* user, int64_t ld_user, int64_t rows, int cols, PtrKind kind, int64_t* ld_out) {
-    if (kind == PTR_DEVICE) {
-      *ld_out = ld_user;
-      return static_cast<double*>(user);
-    }
     const int64_t ld = round_up(std::max<int64_t>(rows, 1), 32);
     double* p = alloc(ld * cols);
     *ld_out = ld;
-    if (kind == PTR_HOST) d2h.push_back({user, ld_user, p, ld, rows, cols});
+    if (kind != PTR_NULL && user) d2h.push_back({user, ld_user, p, ld, rows, cols});
     return p;
   }
 };
@@ -601,16 +613,13 @@ void prim_orth(Exec& E) {
   Y.ld = round_up(std::max<int64_t>(c.rows, 1), 32);
   Y.w = c.w;
   Y.p = E.alloc(Y.ld * c.w);
-  if (c.kU == PTR_HOST)
-    E.h2d.push_back({Y.p, Y.ld, c.U, c.ldu, Y.rows, c.w});
-  else if (E.live())
-    E.chk(launch_copy_cols(static_cast<const double*>(c.U), c.ldu, Y.p, Y.ld, Y.rows, c.w, E.st));
+  E.h2d.push_back({Y.p, Y.ld, c.U, c.ldu, Y.rows, c.w});
   // orth on a local (unsharded) side of arbitrary length: emulate with m = rows
   double* R = E.alloc((int64_t)c.w * c.w);
-  const int64_t m_save = E.m;
-  E.m = c.rows;
+  const int64_t n_save = E.n;
+  E.n = c.rows;
   E.orth(SIDE_N, Y, R, nullptr);  // SIDE_N: never all-reduced
-  E.m = m_save;
+  E.n = n_save;
   int64_t ld;
   double* o = E.out_ptr(c.U, c.ldu, Y.rows, c.w, c.kU, &ld);
   if (E.live()) E.chk(launch_copy_cols(Y.p, Y.ld, o, ld, Y.rows, c.w, E.st));
@@ -678,10 +687,7 @@ void prim_core(Exec& E) {
   const Call& c = E.call;
   const int r = (int)c.rows, cc = c.cols;
   double* M = E.alloc((int64_t)r * cc);
-  if (c.kOm == PTR_HOST)
-    E.h2d.push_back({M, r, c.Om, c.ldom, r, cc});
-  else if (E.live())
-    E.chk(launch_copy_cols(static_cast<const double*>(c.Om), c.ldom, M, r, r, cc, E.st));
+  E.h2d.push_back({M, r, c.Om, c.ldom, r, cc});
   int64_t ldU, ldV, ldS;
   double* Uo = E.out_ptr(c.U, r, r, cc, c.kU == PTR_NULL ? PTR_DEVICE : c.kU, &ldU);
   double* So = E.out_ptr(c.S, cc, cc, 1, c.kS, &ldS);
@@ -714,13 +720,10 @@ void run_alg(Exec& E) {
 
 std::string call_key(const Call& c, const Exec& E, const rsvd_ctx* ctx) {
   char buf[1024];
-  snprintf(buf, sizeof buf,
-           "a%d k%d p%d v%d in%d l2%d lc%d t%d w%d r%lld c%d f%u A%p m%lld n%lld lda%lld O%p/%lld/%d P%p/%lld/%d "
-           "U%p/%lld/%d S%p/%d V%p/%lld/%d R%p/%d ar%p nr%d",
+  snprintf(buf, sizeof buf, "a%d k%d p%d v%d in%d l2%d lc%d t%d w%d r%lld c%d f%u A%p m%lld n%lld lda%lld U%d S%d V%d R%d ar%p nr%d",
            c.alg, c.k, c.p, c.v, c.input, c.l2, c.lc, c.trans, c.w, (long long)c.rows, c.cols, c.flags,
-           (const void*)E.A, (long long)E.m, (long long)E.n, (long long)E.lda, c.Om, (long long)c.ldom, (int)c.kOm,
-           c.Phi, (long long)c.ldphi, (int)c.kPhi, c.U, (long long)c.ldu, (int)c.kU, c.S, (int)c.kS, c.V,
-           (long long)c.ldv, (int)c.kV, c.R, (int)c.kR, (void*)ctx->arena, ctx->nranks);
+           (const void*)E.A, (long long)E.m, (long long)E.n, (long long)E.lda, c.kU != PTR_NULL, c.kS != PTR_NULL,
+           c.kV != PTR_NULL, c.kR != PTR_NULL, (void*)ctx->arena, ctx->nranks);
   return std::string(buf);
 }
 
@@ -769,6 +772,7 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
     cudaStreamSynchronize(ctx->stream);
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
     ctx->graphs.clear();
+    ctx->graph_kernels.clear();
     if (ctx->arena) cudaFree(ctx->arena);
     ctx->arena = nullptr;
     ctx->arena_size = 0;
@@ -819,6 +823,18 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
         if (ce == cudaSuccess) cudaGraphDestroy(g);
         set_err(ctx, "enqueue failed during capture (rc %d, %s)", E.rc, cudaGetErrorString(ce));
         return E.rc ? E.rc : RSVD_E_CUDA;
+      }
+      {
+        size_t nn = 0;
+        cudaGraphGetNodes(g, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) cudaGraphGetNodes(g, nodes.data(), &nn);
+        int kn = 0;
+        for (auto nd : nodes) {
+          cudaGraphNodeType ty;
+          if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++kn;
+        }
+        ctx->graph_kernels[key] = kn;
       }
       if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) {
         cudaGetLastError();
@@ -878,6 +894,7 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
                             : 0;
     if (sz.a_restaged && call.kA == PTR_DEVICE) info->host_staged = 2;
     info->view_launches = sz.view_launches;
+    if (use_graph) info->kernel_launches = ctx->graph_kernels[key];
     info->view_bytes = sz.view_bytes;
     info->view_flops = sz.view_flops;
     info->nondeterministic = sz.nondet;

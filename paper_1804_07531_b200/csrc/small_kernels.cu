@@ -118,16 +118,27 @@ int launch_slots_reduce_small(const double* slots, int nslots, int64_t count, do
 // Rinv is the upper-triangular inverse restricted to the kept columns.
 constexpr int kCholMaxW = 160;
 __global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, const double* __restrict__ ref, int w,
-                                               double tol, double* __restrict__ R, double* __restrict__ Rinv,
-                                               DevStatus* status) {
+                                               double tol, double shift_coef, double* __restrict__ R,
+                                               double* __restrict__ Rinv, DevStatus* status) {
   extern __shared__ double S[];  // w*w (col-major), then deficient flags
   int* defi = reinterpret_cast<int*>(S + w * w);
+  __shared__ double s_shift;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int e = tid; e < w * w; e += nt) S[e] = G[e];
+  if (tid == 0) {
+    // shifted CholeskyQR (Fukaya et al.): G + s I, s = shift_coef * ||Y||_F^2 >= shift_coef ||Y||_2^2
+    double tr = 0.0;
+    for (int j = 0; j < w; ++j) tr += G[j * w + j];
+    s_shift = shift_coef * tr;
+  }
   __syncthreads();
+  if (shift_coef > 0.0) {
+    for (int j = tid; j < w; j += nt) S[j * w + j] += s_shift;
+    __syncthreads();
+  }
   for (int j = 0; j < w; ++j) {
     const double d = S[j * w + j];
-    const double rf = ref ? ref[j] : G[j * w + j];
+    const double rf = ref ? ref[j] : (G[j * w + j] + s_shift * (shift_coef > 0.0));
     const bool def = !(d > tol * rf) || !(rf > 0.0);
     const double rjj = def ? 0.0 : sqrt(d);
     __syncthreads();  // everyone has read S(j,j)
@@ -179,7 +190,7 @@ __global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, con
 }
 
 int launch_chol_ref(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
-                    DevStatus* status, cudaStream_t st) {
+                    DevStatus* status, cudaStream_t st, double shift_coef) {
   if (w < 1 || w > kCholMaxW) return RSVD_E_ARG;
   const size_t smem = (size_t)w * w * 8 + (size_t)w * 4 + 16;
   static bool attr = false;
@@ -187,13 +198,13 @@ int launch_chol_ref(const double* G, const double* ref, int w, double tol, doubl
     cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholMaxW * kCholMaxW * 8 + kCholMaxW * 4 + 16);
     attr = true;
   }
-  k_chol<<<1, 1024, smem, st>>>(G, ref, w, tol, R, Rinv, status);
+  k_chol<<<1, 1024, smem, st>>>(G, ref, w, tol, shift_coef, R, Rinv, status);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
 int launch_chol(const double* G, int w, double* R, double* Rinv, double* /*Racc*/, DevStatus* status,
                 cudaStream_t st) {
-  return launch_chol_ref(G, nullptr, w, 1e-12, R, Rinv, status, st);
+  return launch_chol_ref(G, nullptr, w, 1e-12, R, Rinv, status, st, 0.0);
 }
 
 // ------------------------------------------------------------------ tall-skinny x small GEMM

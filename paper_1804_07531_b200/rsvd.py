@@ -39,7 +39,7 @@ class RsvdInfo(ctypes.Structure):
                 ("rank_deficient_cols", ctypes.c_int32), ("jacobi_sweeps", ctypes.c_int32),
                 ("lc_used", ctypes.c_int32), ("host_staged", ctypes.c_int32), ("graph_replayed", ctypes.c_int32),
                 ("nondeterministic", ctypes.c_int32), ("view_launches", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("view_ms", ctypes.c_double), ("view_bytes", ctypes.c_double),
+                ("kernel_launches", ctypes.c_int32), ("view_ms", ctypes.c_double), ("view_bytes", ctypes.c_double),
                 ("view_flops", ctypes.c_double), ("total_ms", ctypes.c_double)]
 
     def as_dict(self):
