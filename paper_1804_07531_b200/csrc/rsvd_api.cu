@@ -28,6 +28,10 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
                     double* scratch, DevStatus* status, cudaStream_t st);
 int launch_diag(const double* G, int w, double* d, cudaStream_t st);
 int probe_peaks(int sms, cudaStream_t st, double* dmma_tflops, double* read_gbs);
+int cholqr_pass_ctas(int64_t rows);
+int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo, int64_t rows, int w,
+                       const double* Rin, double* slots, unsigned* counter, double tol, double shift_coef, double* R,
+                       double* Rinv, DevStatus* status, cudaStream_t st);
 }  // namespace rsvd
 
 using namespace rsvd;
@@ -81,6 +85,7 @@ struct rsvd_ctx {
   size_t arena_size = 0;
   DevStatus* dstat = nullptr;
   DevStatus* hstat = nullptr;  // pinned
+  unsigned* counter = nullptr; // arrival counter of the last-CTA finisher kernels (self-resetting)
   std::map<std::string, cudaGraphExec_t> graphs;
   std::map<std::string, int> graph_kernels;  // kernel nodes per cached graph
   std::vector<cudaEvent_t> events;
@@ -282,6 +287,10 @@ struct Exec {
   // (shifted CholeskyQR3, Fukaya et al. 2020); used for the projected Krylov blocks.
   void orth(Side s, const TS& Y, double* R_out, const double* ref, bool shifted = false) {
     const int w = Y.w;
+    if (w <= 64 && !sharded(s) && ref == nullptr) {
+      orth_fused(s, Y, R_out, shifted);
+      return;
+    }
     const size_t mk = mark();
     double* G = alloc((int64_t)w * w);
     double* R1 = alloc((int64_t)w * w);
@@ -312,6 +321,45 @@ struct Exec {
       chk(launch_chol_ref(G, nullptr, w, 1e-12, R2, R2i, nullptr, st));
       chk(launch_ts_gemm(T.p, T.ld, T.rows, w, R2i, w, w, Y.p, Y.ld, 0, st));
       if (R_out) chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R_out, w, st));
+    }
+    release(mk);
+  }
+
+  // CholeskyQR2 (or shifted CholeskyQR3) for w <= 64 on an unsharded side: every pass is one
+  // launch of k_cholqr_pass (apply previous R^-1, Gram, last-CTA Cholesky + inverse).
+  void orth_fused(Side s, const TS& Y, double* R_out, bool shifted) {
+    (void)s;
+    const int w = Y.w;
+    const size_t mk = mark();
+    const int G = cholqr_pass_ctas(Y.rows);
+    double* slots = alloc((int64_t)G * w * w);
+    double* R0 = alloc((int64_t)w * w);
+    double* R0i = alloc((int64_t)w * w);
+    double* R1 = alloc((int64_t)w * w);
+    double* R1i = alloc((int64_t)w * w);
+    double* R2 = alloc((int64_t)w * w);
+    double* R2i = alloc((int64_t)w * w);
+    TS T = new_ts(s, w);
+    if (live()) {
+      const double coef = 11.0 * ((double)Y.rows * w + (double)w * (w + 1)) * 1.1102230246251565e-16;
+      if (!shifted) {
+        chk(launch_cholqr_pass(Y.p, Y.ld, nullptr, 0, Y.rows, w, nullptr, slots, ctx->counter, 1e-12, 0.0, R1, R1i,
+                               ctx->dstat, st));
+        chk(launch_cholqr_pass(Y.p, Y.ld, T.p, T.ld, Y.rows, w, R1i, slots, ctx->counter, 1e-12, 0.0, R2, R2i,
+                               nullptr, st));
+        chk(launch_ts_gemm(T.p, T.ld, T.rows, w, R2i, w, w, Y.p, Y.ld, 0, st));
+        if (R_out) chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R_out, w, st));
+      } else {
+        chk(launch_cholqr_pass(Y.p, Y.ld, nullptr, 0, Y.rows, w, nullptr, slots, ctx->counter, 0.0, coef, R0, R0i,
+                               nullptr, st));
+        chk(launch_cholqr_pass(Y.p, Y.ld, T.p, T.ld, Y.rows, w, R0i, slots, ctx->counter, 1e-12, 0.0, R1, R1i,
+                               ctx->dstat, st));
+        chk(launch_cholqr_pass(T.p, T.ld, Y.p, Y.ld, Y.rows, w, R1i, slots, ctx->counter, 1e-12, 0.0, R2, R2i,
+                               nullptr, st));
+        chk(launch_ts_gemm(Y.p, Y.ld, Y.rows, w, R2i, w, w, T.p, T.ld, 0, st));
+        chk(launch_copy_cols(T.p, T.ld, Y.p, Y.ld, Y.rows, w, st));
+        if (R_out) chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R_out, w, st));  // R0 not folded in
+      }
     }
     release(mk);
   }
@@ -426,7 +474,7 @@ void alg_subspace(Exec& E) {
   double* Ul = E.alloc((int64_t)l * l);
   double* Vr = E.alloc((int64_t)l * l);
   double* lam = E.alloc(l);
-  E.core_svd(Rlast, l, 0, Ul, lam, Vr);
+  E.core_svd(Rlast, l, 1, Vr, lam, Ul);  // Jacobi on R^T: left(R^T) = right(R)
   // v even: R_r = Vh Lam Uh^T -> left = Vh, right = Uh;  v odd: R_c = Uh Lam Vh^T
   if (c.v % 2 == 0)
     write_outputs(E, side_c, side_r, Qc, Qr, /*Uh=*/Vr, /*Vh=*/Ul, lam, l, c.k);
@@ -470,7 +518,7 @@ void alg_krylov(Exec& E) {
   double* Ul = E.alloc((int64_t)W * W);
   double* Vr = E.alloc((int64_t)W * W);
   double* lam = E.alloc(W);
-  E.core_svd(Rw, W, 0, Ul, lam, Vr);
+  E.core_svd(Rw, W, 1, Vr, lam, Ul);
   if (even)  // Q_c = K, Q_r = Qo, R_r = Vh Lam Uh^T
     write_outputs(E, side_c, side_r, K, Qo, Vr, Ul, lam, W, c.k);
   else       // Q_r = K, Q_c = Qo, R_c = Uh Lam Vh^T
@@ -544,7 +592,7 @@ void alg_single_pass(Exec& E) {
     double* Ul = E.alloc((int64_t)l * l);
     double* Vr = E.alloc((int64_t)l * l);
     double* sv = E.alloc(l);
-    E.core_svd(Rc, l, 0, Ul, sv, Vr);
+    E.core_svd(Rc, l, 1, Vr, sv, Ul);
     TS Q2 = E.new_ts(SIDE_M, lp);
     if (E.live()) E.chk(launch_ts_gemm(Yc.p, Yc.ld, Yc.rows, l, Ul, l, lp, Q2.p, Q2.ld, 0, E.st));
     Qc = Q2;
@@ -588,7 +636,7 @@ void alg_single_pass(Exec& E) {
   double* Ul = E.alloc((int64_t)lp * lp);
   double* Vr = E.alloc((int64_t)lp * lp);
   double* lam = E.alloc(lp);
-  E.core_svd(Rx, lp, /*trans=*/1, Ul, lam, Vr);
+  E.core_svd(Rx, lp, /*trans=*/0, Vr, lam, Ul);  // svd(Rx^T) from Jacobi on Rx
   // U = Q_c Uh (side M), V = Qx Wh (side N)           (line 14)
   write_outputs(E, SIDE_M, SIDE_N, Qc, Xt, Ul, Vr, lam, lp, c.k);
 }
@@ -816,6 +864,7 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
         return RSVD_E_CUDA;
       }
       cudaMemsetAsync(ctx->dstat, 0, sizeof(DevStatus), st);
+      cudaMemsetAsync(ctx->counter, 0, 256, st);
       run_alg(E);
       cudaError_t ce = cudaStreamEndCapture(st, &g);
       if (E.rc || ce != cudaSuccess) {
@@ -1001,7 +1050,8 @@ int rsvd_create(rsvd_ctx** out, int device, void* stream) {
     }
     c->own_stream = true;
   }
-  if (cudaMalloc(&c->dstat, sizeof(DevStatus)) != cudaSuccess ||
+  if (cudaMalloc(&c->counter, 256) != cudaSuccess || cudaMemset(c->counter, 0, 256) != cudaSuccess ||
+      cudaMalloc(&c->dstat, sizeof(DevStatus)) != cudaSuccess ||
       cudaMallocHost(&c->hstat, sizeof(DevStatus)) != cudaSuccess) {
     delete c;
     return RSVD_E_NOMEM;
@@ -1018,6 +1068,7 @@ int rsvd_destroy(rsvd_ctx* c) {
   for (auto e : c->events) cudaEventDestroy(e);
   if (c->arena) cudaFree(c->arena);
   if (c->dstat) cudaFree(c->dstat);
+  if (c->counter) cudaFree(c->counter);
   if (c->hstat) cudaFreeHost(c->hstat);
   if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
   if (c->own_stream) cudaStreamDestroy(c->stream);

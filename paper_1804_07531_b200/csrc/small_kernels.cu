@@ -83,9 +83,9 @@ __global__ void __launch_bounds__(256) k_cross_gram(const double* __restrict__ X
 }
 
 int gram_slots(int64_t rows) {
-  int64_t s = rows / 1024;
+  int64_t s = (rows + 255) / 256;
   if (s < 1) s = 1;
-  if (s > 128) s = 128;
+  if (s > 148) s = 148;
   return (int)s;
 }
 
@@ -168,19 +168,28 @@ __global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, con
     const int i = e % w, k = e / w;
     R[e] = (i <= k) ? S[k * w + i] : 0.0;
   }
-  // Rinv: column j solves R x = e_j on the kept columns
-  for (int j = tid; j < w; j += nt) {
-    double* x = Rinv + (int64_t)j * w;
-    for (int i = 0; i < w; ++i) x[i] = 0.0;
-    if (!defi[j]) {
-      x[j] = 1.0 / S[j * w + j];
-      for (int i = j - 1; i >= 0; --i) {
-        if (defi[i]) continue;
+  __syncthreads();
+  // R^-1 in place, row by row from the bottom: X(i,j) = -(sum_{k=i+1..j} R(i,k) X(k,j)) / R(i,i)
+  for (int i = w - 1; i >= 0; --i) {
+    double xv[1];
+    const int j = tid;
+    xv[0] = 0.0;
+    if (j < w && !defi[i] && j >= i) {
+      if (j == i) {
+        xv[0] = 1.0 / S[i * w + i];
+      } else {
         double s = 0.0;
-        for (int k = i + 1; k <= j; ++k) s = fma(S[k * w + i], x[k], s);
-        x[i] = -s / S[i * w + i];
+        for (int k = i + 1; k <= j; ++k) s = fma(S[k * w + i], S[j * w + k], s);
+        xv[0] = -s / S[i * w + i];
       }
     }
+    __syncthreads();
+    if (j < w && j >= i) S[j * w + i] = xv[0];
+    __syncthreads();
+  }
+  for (int e = tid; e < w * w; e += nt) {
+    const int i = e % w, k = e / w;
+    Rinv[e] = (i <= k) ? S[k * w + i] : 0.0;
   }
   if (tid == 0 && status) {
     int cnt = 0;
@@ -263,7 +272,7 @@ int launch_ts_gemm(const double* in, int64_t ldi, int64_t rows, int w, const dou
 // Hestenes: W = M J with plane rotations on column pairs (parallel round-robin ordering, one
 // warp per pair) until every pair satisfies |w_p . w_q| <= tol sqrt(|w_p|^2 |w_q|^2).
 // M = (W S^-1) S J^T  ->  left vectors W_j / s_j, right vectors J, values s_j = |W_j|.
-constexpr int kJacThreads = 512;
+constexpr int kJacThreads = 1024;
 __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict__ M, int64_t ldm, int trans, int r,
                                                         int c, double* __restrict__ Ul, double* __restrict__ Sv,
                                                         double* __restrict__ Vr, double* __restrict__ gW,
@@ -310,13 +319,18 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
           b = fma(y, y, b);
           cc = fma(x, y, cc);
         }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        cc = warp_sum(cc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          cc += __shfl_xor_sync(0xffffffffu, cc, o);
+        }
         if (cc != 0.0 && fabs(cc) > tol * sqrt(a * b)) {
-          const double zeta = (b - a) / (2.0 * cc);
-          const double t = (zeta != 0.0) ? copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta)) : 1.0;
-          const double cs = 1.0 / sqrt(1.0 + t * t);
+          // t = tan(theta), the smaller root of t^2 + 2 zeta t - 1 = 0, zeta = (b - a) / (2 c):
+          // t = sign(d) e / (|d| + sqrt(d^2 + e^2)) with d = b - a, e = 2c
+          const double d = b - a, e = 2.0 * cc;
+          const double t = copysign(1.0, d) * e / (fabs(d) + sqrt(fma(d, d, e * e)));
+          const double cs = rsqrt(fma(t, t, 1.0));
           const double sn = cs * t;
           for (int i = lane; i < r; i += 32) {
             const double x = wp[i], y = wq[i];
@@ -396,7 +410,7 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
     cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
     attr = true;
   }
-  const double tol = 2.220446049250313e-16 * (double)c;
+  const double tol = 2.220446049250313e-16 * sqrt((double)r);  // LAPACK dgesvj's CTOL
   k_jacobi<<<1, kJacThreads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, scratch + 256 * 256, w_in, j_in, tol,
                                          60, status);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
@@ -557,4 +571,196 @@ int probe_peaks(int sms, cudaStream_t st, double* dmma_tflops, double* read_gbs)
   cudaFree(sink);
   return cudaGetLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
+}  // namespace rsvd
+
+// =====================================================================================
+// Fused CholeskyQR pass for w <= 64 (one launch):
+//   [apply]  Y_out = Y_in * Rin        (if Rin != null; Rin = R^-1 of the previous pass)
+//   [gram]   partial G = Y_out^T Y_out over this CTA's rows  -> slot[blockIdx.x]
+//   [finish] the last CTA to arrive sums the slots in fixed order, factors
+//            G (+ shift I) = R^T R with the rank guard, and writes R and R^-1.
+// Deterministic: every slot is summed in index order by one thread per entry.
+// =====================================================================================
+namespace rsvd {
+
+constexpr int kFW = 64;          // max width of the fused path
+constexpr int kFRows = 16;       // rows per smem tile (static smem < 48 KB)
+
+template <int WQ>                // WQ = ceil(w/16): thread (ty,tx) owns G[ty+16a][tx+16b], a,b < WQ
+__global__ void __launch_bounds__(256) k_cholqr_pass(const double* __restrict__ Yin, int64_t ldi,
+                                                     double* __restrict__ Yout, int64_t ldo, int64_t rows, int w,
+                                                     int64_t rows_per_cta, const double* __restrict__ Rin,
+                                                     double* __restrict__ slots, unsigned* counter, double tol,
+                                                     double shift_coef, double* __restrict__ Rout,
+                                                     double* __restrict__ Rinv_out, DevStatus* status) {
+  __shared__ double tile[kFRows][kFW + 1];
+  __shared__ double big[kFW * kFW];       // Rin during the apply phase; G / R / R^-1 in the finisher
+  __shared__ double row_tmp[kFW];
+  __shared__ int defi[kFW];
+  __shared__ unsigned ticket;
+  __shared__ double s_shift;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const bool apply = Rin != nullptr;
+  if (apply)
+    for (int e = tid; e < w * w; e += 256) big[e] = Rin[e];  // col-major: big[k*w + j] = Rin(j,k)
+  double acc[WQ][WQ];
+#pragma unroll
+  for (int a = 0; a < WQ; ++a)
+#pragma unroll
+    for (int b = 0; b < WQ; ++b) acc[a][b] = 0.0;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(rows, r0 + rows_per_cta);
+  __syncthreads();
+  for (int64_t rr = r0; rr < r1; rr += kFRows) {
+    const int nr = (int)min((int64_t)kFRows, r1 - rr);
+    // load Y_in tile (coalesced along rows)
+    for (int e = tid; e < kFRows * w; e += 256) {
+      const int c = e / kFRows, i = e % kFRows;
+      tile[i][c] = (i < nr) ? Yin[(int64_t)c * ldi + rr + i] : 0.0;
+    }
+    __syncthreads();
+    if (apply) {
+      // out(i, c) = sum_j tile(i, j) Rin(j, c), Rin upper triangular -> j <= c
+      double o[kFRows * kFW / 256 + 1];
+      int cnt = 0;
+      for (int e = tid; e < kFRows * w; e += 256, ++cnt) {
+        const int c = e / kFRows, i = e % kFRows;
+        double s = 0.0;
+        for (int j = 0; j <= c; ++j) s = fma(tile[i][j], big[c * w + j], s);
+        o[cnt] = s;
+      }
+      __syncthreads();
+      cnt = 0;
+      for (int e = tid; e < kFRows * w; e += 256, ++cnt) {
+        const int c = e / kFRows, i = e % kFRows;
+        tile[i][c] = (i < nr) ? o[cnt] : 0.0;
+        if (i < nr) Yout[(int64_t)c * ldo + rr + i] = o[cnt];
+      }
+      __syncthreads();
+    }
+#pragma unroll 4
+    for (int i = 0; i < kFRows; ++i) {
+      double va[WQ], vb[WQ];
+#pragma unroll
+      for (int a = 0; a < WQ; ++a) va[a] = (ty + 16 * a < w) ? tile[i][ty + 16 * a] : 0.0;
+#pragma unroll
+      for (int b = 0; b < WQ; ++b) vb[b] = (tx + 16 * b < w) ? tile[i][tx + 16 * b] : 0.0;
+#pragma unroll
+      for (int a = 0; a < WQ; ++a)
+#pragma unroll
+        for (int b = 0; b < WQ; ++b) acc[a][b] = fma(va[a], vb[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+  double* slot = slots + (int64_t)blockIdx.x * w * w;
+#pragma unroll
+  for (int a = 0; a < WQ; ++a)
+#pragma unroll
+    for (int b = 0; b < WQ; ++b) {
+      const int i = ty + 16 * a, j = tx + 16 * b;
+      if (i < w && j < w) slot[j * w + i] = acc[a][b];
+    }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) ticket = atomicAdd(counter, 1u);
+  __syncthreads();
+  if (ticket != gridDim.x - 1) return;
+  // ---------------- finisher (last CTA)
+  __threadfence();
+  const int G = gridDim.x;
+  for (int e = tid; e < w * w; e += 256) {
+    double s = 0.0;
+    for (int k = 0; k < G; ++k) s += __ldcg(&slots[(int64_t)k * w * w + e]);
+    big[e] = s;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double tr = 0.0;
+    for (int j = 0; j < w; ++j) tr += big[j * w + j];
+    s_shift = shift_coef * tr;
+    *counter = 0u;  // ready for the next pass
+  }
+  __syncthreads();
+  for (int j = tid; j < w; j += 256) row_tmp[j] = big[j * w + j] + s_shift;  // reference diag
+  if (shift_coef > 0.0)
+    for (int j = tid; j < w; j += 256) big[j * w + j] += s_shift;
+  __syncthreads();
+  // right-looking upper Cholesky in place: big(j, i) (i >= j) becomes R(j, i)
+  for (int j = 0; j < w; ++j) {
+    const double d = big[j * w + j];
+    const double rf = row_tmp[j];
+    const bool def = !(d > tol * rf) || !(rf > 0.0);
+    const double rjj = def ? 0.0 : sqrt(d);
+    const double inv = def ? 0.0 : 1.0 / rjj;
+    __syncthreads();
+    if (tid == 0) {
+      big[j * w + j] = rjj;
+      defi[j] = def;
+    }
+    for (int i = j + 1 + tid; i < w; i += 256) big[i * w + j] *= inv;
+    __syncthreads();
+    const int m = w - j - 1;
+    if (!def)
+      for (int e = tid; e < m * m; e += 256) {
+        const int ii = e % m, kk = e / m;
+        if (ii <= kk) big[(j + 1 + kk) * w + (j + 1 + ii)] -= big[(j + 1 + ii) * w + j] * big[(j + 1 + kk) * w + j];
+      }
+    __syncthreads();
+  }
+  for (int e = tid; e < w * w; e += 256) {
+    const int i = e % w, k = e / w;
+    Rout[e] = (i <= k) ? big[k * w + i] : 0.0;
+  }
+  __syncthreads();
+  // R^-1 in place, row by row from the bottom: X(i,j) = -(sum_{k=i+1..j} R(i,k) X(k,j)) / R(i,i)
+  for (int i = w - 1; i >= 0; --i) {
+    double xv = 0.0;
+    const int j = tid;
+    if (j < w && !defi[i] && j >= i) {
+      if (j == i) {
+        xv = 1.0 / big[i * w + i];
+      } else {
+        double s = 0.0;
+        for (int k = i + 1; k <= j; ++k) s = fma(big[k * w + i], big[j * w + k], s);  // R(i,k) X(k,j)
+        xv = -s / big[i * w + i];
+      }
+    }
+    __syncthreads();
+    if (j < w && j >= i) big[j * w + i] = xv;  // row i of X replaces row i of R (upper part)
+    __syncthreads();
+  }
+  for (int e = tid; e < w * w; e += 256) {
+    const int i = e % w, k = e / w;
+    Rinv_out[e] = (i <= k) ? big[k * w + i] : 0.0;
+  }
+  if (tid == 0 && status) {
+    int cnt = 0;
+    for (int j = 0; j < w; ++j) cnt += defi[j];
+    if (cnt) atomicAdd(&status->deficient, cnt);
+  }
+}
+
+int cholqr_pass_ctas(int64_t rows) {
+  int64_t g = (rows + 127) / 128;
+  if (g > 148) g = 148;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo, int64_t rows, int w,
+                       const double* Rin, double* slots, unsigned* counter, double tol, double shift_coef, double* R,
+                       double* Rinv, DevStatus* status, cudaStream_t st) {
+  if (w < 1 || w > kFW) return RSVD_E_ARG;
+  const int G = cholqr_pass_ctas(rows);
+  const int64_t rpc = (rows + G - 1) / G;
+  const int WQ = (w + 15) / 16;
+  switch (WQ) {
+    case 1: k_cholqr_pass<1><<<G, 256, 0, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
+    case 2: k_cholqr_pass<2><<<G, 256, 0, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
+    case 3: k_cholqr_pass<3><<<G, 256, 0, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
+    default: k_cholqr_pass<4><<<G, 256, 0, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
 }  // namespace rsvd
