@@ -396,9 +396,13 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
   }
 }
 
+int launch_jacobi_small(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
+                        DevStatus* status, cudaStream_t st);
+
 int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
                     double* scratch, DevStatus* status, cudaStream_t st) {
   if (c < 1 || c > 256 || r < c || r > 256) return RSVD_E_ARG;
+  if (r <= 64) return launch_jacobi_small(M, ldm, trans, r, c, Ul, S, Vr, status, st);
   const int ce = c + (c & 1);
   const size_t wbytes = (size_t)r * ce * 8, jbytes = (size_t)ce * ce * 8;
   const size_t budget = 200 * 1024;
@@ -584,7 +588,114 @@ int probe_peaks(int sms, cudaStream_t st, double* dmma_tflops, double* read_gbs)
 namespace rsvd {
 
 constexpr int kFW = 64;          // max width of the fused path
-constexpr int kFRows = 16;       // rows per smem tile (static smem < 48 KB)
+constexpr int kFRows = 32;       // rows per smem tile
+constexpr int kFLd = kFW + 1;    // padded tile row
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Upper Cholesky G = R^T R and R^-1 by warp 0 alone, columns held in registers: lane owns
+// columns lane and lane+32 (NC = 1 or 2 halves); big (col-major w x w, big[k*w+i] = (i,k)) holds G
+// on entry.  `ref` = reference diagonal for the rank guard.  All loops have compile-time bounds
+// so the column arrays stay in registers.
+template <int NC>
+__device__ void warp_chol_inv(double* big, int w, const double* ref, double tol, int* defi, double* Rout,
+                              double* Rinv_out, DevStatus* status) {
+  const int lane = threadIdx.x & 31;
+  double col[NC][32 * NC];
+#pragma unroll
+  for (int h = 0; h < NC; ++h) {
+    const int k = lane + 32 * h;
+#pragma unroll
+    for (int i = 0; i < 32 * NC; ++i) col[h][i] = (k < w && i <= k) ? big[k * w + i] : 0.0;
+  }
+  int mydef = 0;
+  // ---- Cholesky, right-looking: step j scales row j and updates rows i > j of each column
+#pragma unroll
+  for (int j = 0; j < 32 * NC; ++j) {
+    if (j < w) {
+      const int hj = j >> 5, lj = j & 31;
+      const double d = __shfl_sync(0xffffffffu, col[hj][j], lj);
+      const bool def = !(d > tol * ref[j]) || !(ref[j] > 0.0);
+      const double rjj = def ? 0.0 : sqrt(d);
+      const double inv = def ? 0.0 : 1.0 / rjj;
+      if (lane == 0) defi[j] = def;
+#pragma unroll
+      for (int h = 0; h < NC; ++h) {
+        const int k = lane + 32 * h;
+        if (k == j) col[h][j] = rjj;
+        else if (k > j) col[h][j] *= inv;   // R(j, k)
+      }
+      if (!def) {
+#pragma unroll
+        for (int i = j + 1; i < 32 * NC; ++i) {
+          const double rji = __shfl_sync(0xffffffffu, col[i >> 5][j], i & 31);   // R(j, i) from lane i
+#pragma unroll
+          for (int h = 0; h < NC; ++h) {
+            const int k = lane + 32 * h;
+            if (k >= i) col[h][i] -= rji * col[h][j];
+          }
+        }
+      }
+    }
+  }
+  // ---- R out (col-major), and R into smem for the inverse's broadcast reads
+#pragma unroll
+  for (int h = 0; h < NC; ++h) {
+    const int k = lane + 32 * h;
+    if (k < w) {
+#pragma unroll
+      for (int i = 0; i < 32 * NC; ++i)
+        if (i < w) {
+          const double v = (i <= k) ? col[h][i] : 0.0;
+          Rout[k * w + i] = v;
+          big[k * w + i] = v;
+        }
+    }
+  }
+  __syncwarp();
+  // ---- X = R^-1 (upper), rows from the bottom; lane owns columns of X in registers (reuse col)
+#pragma unroll
+  for (int h = 0; h < NC; ++h)
+#pragma unroll
+    for (int i = 0; i < 32 * NC; ++i) col[h][i] = 0.0;
+#pragma unroll
+  for (int i = 32 * NC - 1; i >= 0; --i) {
+    if (i < w) {
+      const double rii = big[i * w + i];
+      const bool di = defi[i];
+      const double inv = di ? 0.0 : 1.0 / rii;
+#pragma unroll
+      for (int h = 0; h < NC; ++h) {
+        const int j = lane + 32 * h;
+        double sacc = 0.0;
+#pragma unroll
+        for (int k = i + 1; k < 32 * NC; ++k)
+          if (k < w && k <= j) sacc = fma(big[k * w + i], col[h][k], sacc);   // R(i,k) X(k,j)
+        if (j < w && j >= i) col[h][i] = (j == i) ? inv : -sacc * inv;
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < NC; ++h) {
+    const int k = lane + 32 * h;
+    if (k < w) {
+#pragma unroll
+      for (int i = 0; i < 32 * NC; ++i)
+        if (i < w) Rinv_out[k * w + i] = (i <= k) ? col[h][i] : 0.0;
+    }
+  }
+  (void)mydef;
+  if (lane == 0 && status) {
+    int cnt = 0;
+    for (int j = 0; j < w; ++j) cnt += defi[j];
+    if (cnt) atomicAdd(&status->deficient, cnt);
+  }
+}
 
 template <int WQ>                // WQ = ceil(w/16): thread (ty,tx) owns G[ty+16a][tx+16b], a,b < WQ
 __global__ void __launch_bounds__(256) k_cholqr_pass(const double* __restrict__ Yin, int64_t ldi,
@@ -593,16 +704,16 @@ __global__ void __launch_bounds__(256) k_cholqr_pass(const double* __restrict__ 
                                                      double* __restrict__ slots, unsigned* counter, double tol,
                                                      double shift_coef, double* __restrict__ Rout,
                                                      double* __restrict__ Rinv_out, DevStatus* status) {
-  __shared__ double tile[kFRows][kFW + 1];
-  __shared__ double big[kFW * kFW];       // Rin during the apply phase; G / R / R^-1 in the finisher
-  __shared__ double row_tmp[kFW];
+  extern __shared__ double cq_dyn[];
+  double* tiles = cq_dyn;                       // 2 x kFRows x kFLd
+  double* big = cq_dyn + 2 * kFRows * kFLd;     // w x w
+  __shared__ double refd[kFW];
   __shared__ int defi[kFW];
   __shared__ unsigned ticket;
-  __shared__ double s_shift;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const bool apply = Rin != nullptr;
   if (apply)
-    for (int e = tid; e < w * w; e += 256) big[e] = Rin[e];  // col-major: big[k*w + j] = Rin(j,k)
+    for (int e = tid; e < w * w; e += 256) big[e] = Rin[e];
   double acc[WQ][WQ];
 #pragma unroll
   for (int a = 0; a < WQ; ++a)
@@ -610,31 +721,45 @@ __global__ void __launch_bounds__(256) k_cholqr_pass(const double* __restrict__ 
     for (int b = 0; b < WQ; ++b) acc[a][b] = 0.0;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
   const int64_t r1 = min(rows, r0 + rows_per_cta);
-  __syncthreads();
-  for (int64_t rr = r0; rr < r1; rr += kFRows) {
-    const int nr = (int)min((int64_t)kFRows, r1 - rr);
-    // load Y_in tile (coalesced along rows)
+  const int ntiles = (int)((r1 - r0 + kFRows - 1) / kFRows);
+  auto issue = [&](int t) {
+    double* dst = tiles + (t & 1) * kFRows * kFLd;
+    const int64_t rr = r0 + (int64_t)t * kFRows;
     for (int e = tid; e < kFRows * w; e += 256) {
       const int c = e / kFRows, i = e % kFRows;
-      tile[i][c] = (i < nr) ? Yin[(int64_t)c * ldi + rr + i] : 0.0;
+      if (rr + i < r1) cp_async8(dst + i * kFLd + c, Yin + (int64_t)c * ldi + rr + i);
+      else dst[i * kFLd + c] = 0.0;
+    }
+    cp_async_commit();
+  };
+  if (ntiles > 0) issue(0);
+  for (int t = 0; t < ntiles; ++t) {
+    if (t + 1 < ntiles) {
+      issue(t + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    double* tile = tiles + (t & 1) * kFRows * kFLd;
+    const int64_t rr = r0 + (int64_t)t * kFRows;
     if (apply) {
-      // out(i, c) = sum_j tile(i, j) Rin(j, c), Rin upper triangular -> j <= c
-      double o[kFRows * kFW / 256 + 1];
+      // out(i, c) = sum_{j <= c} tile(i, j) Rin(j, c)   (Rin upper triangular)
+      double o[kFRows * kFW / 256];
       int cnt = 0;
       for (int e = tid; e < kFRows * w; e += 256, ++cnt) {
         const int c = e / kFRows, i = e % kFRows;
-        double s = 0.0;
-        for (int j = 0; j <= c; ++j) s = fma(tile[i][j], big[c * w + j], s);
-        o[cnt] = s;
+        double sacc = 0.0;
+        for (int j = 0; j <= c; ++j) sacc = fma(tile[i * kFLd + j], big[c * w + j], sacc);
+        o[cnt] = sacc;
       }
       __syncthreads();
       cnt = 0;
       for (int e = tid; e < kFRows * w; e += 256, ++cnt) {
         const int c = e / kFRows, i = e % kFRows;
-        tile[i][c] = (i < nr) ? o[cnt] : 0.0;
-        if (i < nr) Yout[(int64_t)c * ldo + rr + i] = o[cnt];
+        const bool ok = rr + i < r1;
+        tile[i * kFLd + c] = ok ? o[cnt] : 0.0;
+        if (ok) Yout[(int64_t)c * ldo + rr + i] = o[cnt];
       }
       __syncthreads();
     }
@@ -642,9 +767,9 @@ __global__ void __launch_bounds__(256) k_cholqr_pass(const double* __restrict__ 
     for (int i = 0; i < kFRows; ++i) {
       double va[WQ], vb[WQ];
 #pragma unroll
-      for (int a = 0; a < WQ; ++a) va[a] = (ty + 16 * a < w) ? tile[i][ty + 16 * a] : 0.0;
+      for (int a = 0; a < WQ; ++a) va[a] = tile[i * kFLd + ty + 16 * a];
 #pragma unroll
-      for (int b = 0; b < WQ; ++b) vb[b] = (tx + 16 * b < w) ? tile[i][tx + 16 * b] : 0.0;
+      for (int b = 0; b < WQ; ++b) vb[b] = tile[i * kFLd + tx + 16 * b];
 #pragma unroll
       for (int a = 0; a < WQ; ++a)
 #pragma unroll
@@ -665,83 +790,53 @@ __global__ void __launch_bounds__(256) k_cholqr_pass(const double* __restrict__ 
   if (tid == 0) ticket = atomicAdd(counter, 1u);
   __syncthreads();
   if (ticket != gridDim.x - 1) return;
-  // ---------------- finisher (last CTA)
+  // ---------------- finisher (last CTA): fixed-order slot sum, then warp 0 factors
   __threadfence();
   const int G = gridDim.x;
-  for (int e = tid; e < w * w; e += 256) {
-    double s = 0.0;
-    for (int k = 0; k < G; ++k) s += __ldcg(&slots[(int64_t)k * w * w + e]);
-    big[e] = s;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double tr = 0.0;
-    for (int j = 0; j < w; ++j) tr += big[j * w + j];
-    s_shift = shift_coef * tr;
-    *counter = 0u;  // ready for the next pass
-  }
-  __syncthreads();
-  for (int j = tid; j < w; j += 256) row_tmp[j] = big[j * w + j] + s_shift;  // reference diag
-  if (shift_coef > 0.0)
-    for (int j = tid; j < w; j += 256) big[j * w + j] += s_shift;
-  __syncthreads();
-  // right-looking upper Cholesky in place: big(j, i) (i >= j) becomes R(j, i)
-  for (int j = 0; j < w; ++j) {
-    const double d = big[j * w + j];
-    const double rf = row_tmp[j];
-    const bool def = !(d > tol * rf) || !(rf > 0.0);
-    const double rjj = def ? 0.0 : sqrt(d);
-    const double inv = def ? 0.0 : 1.0 / rjj;
-    __syncthreads();
-    if (tid == 0) {
-      big[j * w + j] = rjj;
-      defi[j] = def;
-    }
-    for (int i = j + 1 + tid; i < w; i += 256) big[i * w + j] *= inv;
-    __syncthreads();
-    const int m = w - j - 1;
-    if (!def)
-      for (int e = tid; e < m * m; e += 256) {
-        const int ii = e % m, kk = e / m;
-        if (ii <= kk) big[(j + 1 + kk) * w + (j + 1 + ii)] -= big[(j + 1 + ii) * w + j] * big[(j + 1 + kk) * w + j];
-      }
-    __syncthreads();
-  }
-  for (int e = tid; e < w * w; e += 256) {
-    const int i = e % w, k = e / w;
-    Rout[e] = (i <= k) ? big[k * w + i] : 0.0;
-  }
-  __syncthreads();
-  // R^-1 in place, row by row from the bottom: X(i,j) = -(sum_{k=i+1..j} R(i,k) X(k,j)) / R(i,i)
-  for (int i = w - 1; i >= 0; --i) {
-    double xv = 0.0;
-    const int j = tid;
-    if (j < w && !defi[i] && j >= i) {
-      if (j == i) {
-        xv = 1.0 / big[i * w + i];
-      } else {
-        double s = 0.0;
-        for (int k = i + 1; k <= j; ++k) s = fma(big[k * w + i], big[j * w + k], s);  // R(i,k) X(k,j)
-        xv = -s / big[i * w + i];
+  for (int e0 = tid; e0 < w * w; e0 += 512) {
+    // two entries at a time, eight slots per batch: 16 independent loads in flight
+    const int e1 = e0 + 256;
+    double a[8], b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = b[u] = 0.0;
+    int k = 0;
+    for (; k + 8 <= G; k += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a[u] += __ldcg(&slots[(int64_t)(k + u) * w * w + e0]);
+        if (e1 < w * w) b[u] += __ldcg(&slots[(int64_t)(k + u) * w * w + e1]);
       }
     }
-    __syncthreads();
-    if (j < w && j >= i) big[j * w + i] = xv;  // row i of X replaces row i of R (upper part)
-    __syncthreads();
+    for (; k < G; ++k) {
+      a[0] += __ldcg(&slots[(int64_t)k * w * w + e0]);
+      if (e1 < w * w) b[0] += __ldcg(&slots[(int64_t)k * w * w + e1]);
+    }
+    big[e0] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    if (e1 < w * w) big[e1] = ((b[0] + b[1]) + (b[2] + b[3])) + ((b[4] + b[5]) + (b[6] + b[7]));
   }
-  for (int e = tid; e < w * w; e += 256) {
-    const int i = e % w, k = e / w;
-    Rinv_out[e] = (i <= k) ? big[k * w + i] : 0.0;
+  __syncthreads();
+  if (tid >= 32) return;
+  double tr = 0.0;
+  for (int j = tid; j < w; j += 32) tr += big[j * w + j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+  const double shift = shift_coef * tr;
+  for (int j = tid; j < w; j += 32) {
+    refd[j] = big[j * w + j] + shift;
+    big[j * w + j] += shift;
   }
-  if (tid == 0 && status) {
-    int cnt = 0;
-    for (int j = 0; j < w; ++j) cnt += defi[j];
-    if (cnt) atomicAdd(&status->deficient, cnt);
-  }
+  if (tid == 0) *counter = 0u;
+  __syncwarp();
+  if (WQ <= 2)
+    warp_chol_inv<1>(big, w, refd, tol, defi, Rout, Rinv_out, status);
+  else
+    warp_chol_inv<2>(big, w, refd, tol, defi, Rout, Rinv_out, status);
 }
 
+int cholqr_smem_bytes(int w) { return (2 * kFRows * kFLd + w * w) * 8; }
+
 int cholqr_pass_ctas(int64_t rows) {
-  int64_t g = (rows + 127) / 128;
+  int64_t g = (rows + 255) / 256;
   if (g > 148) g = 148;
   if (g < 1) g = 1;
   return (int)g;
@@ -754,12 +849,204 @@ int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo
   const int G = cholqr_pass_ctas(rows);
   const int64_t rpc = (rows + G - 1) / G;
   const int WQ = (w + 15) / 16;
-  switch (WQ) {
-    case 1: k_cholqr_pass<1><<<G, 256, 0, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
-    case 2: k_cholqr_pass<2><<<G, 256, 0, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
-    case 3: k_cholqr_pass<3><<<G, 256, 0, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
-    default: k_cholqr_pass<4><<<G, 256, 0, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
+  const int smem = cholqr_smem_bytes(w);
+  static bool attr = false;
+  if (!attr) {
+    const int mx = cholqr_smem_bytes(kFW);
+    cudaFuncSetAttribute(k_cholqr_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_cholqr_pass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_cholqr_pass<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_cholqr_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    attr = true;
   }
+  switch (WQ) {
+    case 1: k_cholqr_pass<1><<<G, 256, smem, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
+    case 2: k_cholqr_pass<2><<<G, 256, smem, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
+    case 3: k_cholqr_pass<3><<<G, 256, smem, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
+    default: k_cholqr_pass<4><<<G, 256, smem, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+}  // namespace rsvd
+
+// =====================================================================================
+// One-sided Jacobi for small cores (r <= 64 rows, c <= 64 columns): W and J live in shared
+// memory, one warp per column pair, round-robin pair table precomputed, rows-per-lane fixed at
+// compile time.  The rotation angle t is computed in fp32 from the fp64 ratio (any t gives an
+// exactly orthogonal rotation because cs = rsqrt(1 + t^2) and sn = cs t are formed in fp64; an
+// approximate angle only leaves a ~1e-7 fraction of the off-diagonal, which the next sweep removes).
+// =====================================================================================
+namespace rsvd {
+
+template <int RW>  // rows per lane (r <= 32 RW)
+__global__ void __launch_bounds__(1024) k_jacobi_small(const double* __restrict__ M, int64_t ldm, int trans, int r,
+                                                       int c, double* __restrict__ Ul, double* __restrict__ Sv,
+                                                       double* __restrict__ Vr, double tol, int max_sweeps,
+                                                       DevStatus* status) {
+  constexpr int RS = 32 * RW;          // padded rows of W
+  extern __shared__ double jac_dyn[];
+  double* W = jac_dyn;                 // 64 x RS
+  double* J = jac_dyn + 64 * RS;       // 64 x 64
+  __shared__ unsigned short pairs[63 * 32];
+  __shared__ double sval[64];
+  __shared__ int srank[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+  const int ce = c + (c & 1);
+  const int npairs = ce >> 1;
+  for (int e = tid; e < 64 * RS; e += nt) {
+    const int i = e % RS, j = e / RS;
+    double v = 0.0;
+    if (i < r && j < c) v = trans ? M[(int64_t)i * ldm + j] : M[(int64_t)j * ldm + i];
+    W[e] = v;
+  }
+  for (int e = tid; e < 64 * 64; e += nt) J[e] = ((e & 63) == (e >> 6)) ? 1.0 : 0.0;
+  for (int e = tid; e < (ce - 1) * npairs; e += nt) {
+    const int round = e / npairs, pi = e % npairs;
+    int p, q;
+    if (pi == 0) { p = round; q = ce - 1; }
+    else { p = (round + pi) % (ce - 1); q = (round - pi + (ce - 1)) % (ce - 1); }
+    if (p > q) { const int t = p; p = q; q = t; }
+    pairs[round * 32 + pi] = (unsigned short)(p | (q << 8));
+  }
+  __syncthreads();
+  const double tol2 = tol * tol;
+  int sweep = 0;
+  bool converged = false;
+  // J rotations lag one round behind W's: they touch only J (never read by the W updates), the
+  // lag keeps per-column order (a column's round-r update finishes before the round-r+1 barrier),
+  // and it takes the J work off the round's critical path (it overlaps the next reductions).
+  int pj_p = 0, pj_q = 0, pj_on = 0;
+  double pj_cs = 1.0, pj_sn = 0.0;
+  auto apply_pending_J = [&]() {
+    if (pj_on) {
+      double* jp = J + pj_p * 64;
+      double* jq = J + pj_q * 64;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double u = jp[lane + 32 * k], v = jq[lane + 32 * k];
+        jp[lane + 32 * k] = pj_cs * u - pj_sn * v;
+        jq[lane + 32 * k] = pj_sn * u + pj_cs * v;
+      }
+      pj_on = 0;
+    }
+  };
+  for (; sweep < max_sweeps; ++sweep) {
+    int rotated = 0;
+    for (int round = 0; round < ce - 1; ++round) {
+      if (warp < npairs) {
+        const unsigned pq = pairs[round * 32 + warp];
+        const int p = pq & 255, q = pq >> 8;
+        double* wp = W + p * RS;
+        double* wq = W + q * RS;
+        double x[RW], y[RW];
+        double a = 0.0, b = 0.0, cc = 0.0;
+#pragma unroll
+        for (int t = 0; t < RW; ++t) {
+          x[t] = wp[lane + 32 * t];
+          y[t] = wq[lane + 32 * t];
+          a = fma(x[t], x[t], a);
+          b = fma(y[t], y[t], b);
+          cc = fma(x[t], y[t], cc);
+        }
+        apply_pending_J();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          cc += __shfl_xor_sync(0xffffffffu, cc, o);
+        }
+        if (cc * cc > tol2 * (a * b) && cc != 0.0) {
+          rotated = 1;
+          const double d = b - a, e2 = 2.0 * cc;
+          double t;
+          if (fabs(d) < 1e-300 * fabs(e2) || d == 0.0) {
+            t = copysign(1.0, e2);
+          } else {
+            const double rho = e2 / fabs(d);                 // tan(2 theta), sign folded below
+            const float rf = (float)rho;
+            float tf = fabsf(rf) > 1e18f ? copysignf(1.0f, rf) : rf / (1.0f + sqrtf(fmaf(rf, rf, 1.0f)));
+            t = copysign(1.0, d) * (double)tf;
+          }
+          const double cs = rsqrt(fma(t, t, 1.0));
+          const double sn = cs * t;
+#pragma unroll
+          for (int k = 0; k < RW; ++k) {
+            wp[lane + 32 * k] = cs * x[k] - sn * y[k];
+            wq[lane + 32 * k] = sn * x[k] + cs * y[k];
+          }
+          pj_p = p; pj_q = q; pj_cs = cs; pj_sn = sn; pj_on = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!__syncthreads_or(rotated)) {
+      converged = true;
+      ++sweep;
+      break;
+    }
+  }
+  if (warp < npairs) apply_pending_J();
+  __syncthreads();
+  for (int j = warp; j < ce; j += (nt >> 5)) {
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < RW; ++t) {
+      const double v = W[j * RS + lane + 32 * t];
+      s = fma(v, v, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sval[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = tid; j < ce; j += nt) {
+    const double sj = sval[j];
+    int rk = 0;
+    for (int i = 0; i < ce; ++i) {
+      const double si = sval[i];
+      rk += (si > sj) || (si == sj && i < j);
+    }
+    srank[j] = rk;
+  }
+  __syncthreads();
+  for (int e = tid; e < r * ce; e += nt) {
+    const int i = e % r, j = e / r;
+    const int rk = srank[j];
+    if (rk < c) {
+      const double sj = sval[j];
+      Ul[(int64_t)rk * r + i] = sj > 0.0 ? W[j * RS + i] / sj : 0.0;
+    }
+  }
+  for (int e = tid; e < c * ce; e += nt) {
+    const int i = e % c, j = e / c;
+    const int rk = srank[j];
+    if (rk < c) Vr[(int64_t)rk * c + i] = J[j * 64 + i];
+  }
+  for (int j = tid; j < ce; j += nt)
+    if (srank[j] < c) Sv[srank[j]] = sval[j];
+  if (tid == 0 && status) {
+    status->jacobi_sweeps = sweep;
+    if (!converged) atomicAdd(&status->jacobi_fail, 1);
+  }
+}
+
+int launch_jacobi_small(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
+                        DevStatus* status, cudaStream_t st) {
+  if (c < 1 || c > 64 || r < c || r > 64) return RSVD_E_ARG;
+  const int ce = c + (c & 1);
+  const int threads = 32 * std::max(1, ce / 2);
+  const double tol = 2.220446049250313e-16 * sqrt((double)r);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_jacobi_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 32 + 64 * 64) * 8);
+    cudaFuncSetAttribute(k_jacobi_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 64 + 64 * 64) * 8);
+    attr = true;
+  }
+  if (r <= 32)
+    k_jacobi_small<1><<<1, threads, (64 * 32 + 64 * 64) * 8, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
+  else
+    k_jacobi_small<2><<<1, threads, (64 * 64 + 64 * 64) * 8, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
