@@ -90,6 +90,26 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // quarter-warp {g=2i, g=2i+1} touches smem rows {i, i+4} whose swizzled chunks are disjoint.
 __device__ __forceinline__ int perm8(int g) { return ((g & 1) << 2) | (g >> 1); }
 
+// 1/sqrt(x) for x > 0 in fp64 without the IEEE div/sqrt subroutines: fp32 seed (scaled into
+// range by a power of two) + two Newton steps (relative error ~1e-16).
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  const int e = ilogb(x) & ~1;                 // even exponent so sqrt scales exactly
+  const double xs = ldexp(x, -e);              // xs in [1, 4)
+  double y = (double)rsqrtf((float)xs);
+  y = y * fma(-0.5 * xs, y * y, 1.5);
+  y = y * fma(-0.5 * xs, y * y, 1.5);
+  return ldexp(y, -e / 2);
+}
+// 1/x in fp64: fp32 seed of the scaled value + two Newton steps
+__device__ __forceinline__ double fast_rcp(double x) {
+  const int e = ilogb(x);
+  const double xs = ldexp(x, -e);              // |xs| in [1, 2)
+  double y = (double)(1.0f / (float)xs);
+  y = y * fma(-xs, y, 2.0);
+  y = y * fma(-xs, y, 2.0);
+  return ldexp(y, -e);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

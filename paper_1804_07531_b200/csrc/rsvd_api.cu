@@ -30,8 +30,8 @@ int launch_diag(const double* G, int w, double* d, cudaStream_t st);
 int probe_peaks(int sms, cudaStream_t st, double* dmma_tflops, double* read_gbs);
 int cholqr_pass_ctas(int64_t rows);
 int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo, int64_t rows, int w,
-                       const double* Rin, double* slots, unsigned* counter, double tol, double shift_coef, double* R,
-                       double* Rinv, DevStatus* status, cudaStream_t st);
+                       const double* Rin, double* slots, unsigned* counter, double tol, double shift_coef,
+                       int second_pass, double* R, double* Rinv, DevStatus* status, cudaStream_t st);
 }  // namespace rsvd
 
 using namespace rsvd;
@@ -343,18 +343,18 @@ struct Exec {
     if (live()) {
       const double coef = 11.0 * ((double)Y.rows * w + (double)w * (w + 1)) * 1.1102230246251565e-16;
       if (!shifted) {
-        chk(launch_cholqr_pass(Y.p, Y.ld, nullptr, 0, Y.rows, w, nullptr, slots, ctx->counter, 1e-12, 0.0, R1, R1i,
-                               ctx->dstat, st));
-        chk(launch_cholqr_pass(Y.p, Y.ld, T.p, T.ld, Y.rows, w, R1i, slots, ctx->counter, 1e-12, 0.0, R2, R2i,
+        chk(launch_cholqr_pass(Y.p, Y.ld, nullptr, 0, Y.rows, w, nullptr, slots, ctx->counter, 1e-12, 0.0, 0, R1,
+                               R1i, ctx->dstat, st));
+        chk(launch_cholqr_pass(Y.p, Y.ld, T.p, T.ld, Y.rows, w, R1i, slots, ctx->counter, 1e-12, 0.0, 1, R2, R2i,
                                nullptr, st));
         chk(launch_ts_gemm(T.p, T.ld, T.rows, w, R2i, w, w, Y.p, Y.ld, 0, st));
         if (R_out) chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R_out, w, st));
       } else {
-        chk(launch_cholqr_pass(Y.p, Y.ld, nullptr, 0, Y.rows, w, nullptr, slots, ctx->counter, 0.0, coef, R0, R0i,
-                               nullptr, st));
-        chk(launch_cholqr_pass(Y.p, Y.ld, T.p, T.ld, Y.rows, w, R0i, slots, ctx->counter, 1e-12, 0.0, R1, R1i,
+        chk(launch_cholqr_pass(Y.p, Y.ld, nullptr, 0, Y.rows, w, nullptr, slots, ctx->counter, 0.0, coef, 0, R0,
+                               R0i, nullptr, st));
+        chk(launch_cholqr_pass(Y.p, Y.ld, T.p, T.ld, Y.rows, w, R0i, slots, ctx->counter, 1e-12, 0.0, 0, R1, R1i,
                                ctx->dstat, st));
-        chk(launch_cholqr_pass(T.p, T.ld, Y.p, Y.ld, Y.rows, w, R1i, slots, ctx->counter, 1e-12, 0.0, R2, R2i,
+        chk(launch_cholqr_pass(T.p, T.ld, Y.p, Y.ld, Y.rows, w, R1i, slots, ctx->counter, 1e-12, 0.0, 1, R2, R2i,
                                nullptr, st));
         chk(launch_ts_gemm(Y.p, Y.ld, Y.rows, w, R2i, w, w, T.p, T.ld, 0, st));
         chk(launch_copy_cols(T.p, T.ld, Y.p, Y.ld, Y.rows, w, st));

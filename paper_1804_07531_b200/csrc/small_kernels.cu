@@ -587,6 +587,23 @@ int probe_peaks(int sms, cudaStream_t st, double* dmma_tflops, double* read_gbs)
 // =====================================================================================
 namespace rsvd {
 
+#ifdef RSVD_PHASE_TIMING
+__device__ unsigned long long g_phase[16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PHASE(i) do { if (threadIdx.x == 0) g_phase[i] = gtimer(); } while (0)
+#define CYC(i) do { if (threadIdx.x == 0) g_phase[i] = clock64(); } while (0)
+#define PHASE_MAX(i) do { if (threadIdx.x == 0) atomicMax(&g_phase[i], gtimer()); } while (0)
+#define PHASE_MIN(i) do { if (threadIdx.x == 0) atomicMin(&g_phase[i], gtimer()); } while (0)
+#else
+#define PHASE(i) do {} while (0)
+#define CYC(i) do {} while (0)
+#define PHASE_MAX(i) do {} while (0)
+#define PHASE_MIN(i) do {} while (0)
+#endif
 constexpr int kFW = 64;          // max width of the fused path
 constexpr int kFRows = 32;       // rows per smem tile
 constexpr int kFLd = kFW + 1;    // padded tile row
@@ -598,242 +615,302 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Upper Cholesky G = R^T R and R^-1 by warp 0 alone, columns held in registers: lane owns
-// columns lane and lane+32 (NC = 1 or 2 halves); big (col-major w x w, big[k*w+i] = (i,k)) holds G
-// on entry.  `ref` = reference diagonal for the rank guard.  All loops have compile-time bounds
-// so the column arrays stay in registers.
-template <int NC>
-__device__ void warp_chol_inv(double* big, int w, const double* ref, double tol, int* defi, double* Rout,
-                              double* Rinv_out, DevStatus* status) {
-  const int lane = threadIdx.x & 31;
-  double col[NC][32 * NC];
+// ---------------------------------------------------------------------------------------
+// CTA-wide guarded Cholesky (upper, G = R^T R) + inverse for w <= 64, in shared memory.
+//   S  (col-major, ld w): G on entry (diagonal already shifted), R on exit (upper part)
+//   X  (col-major, ld w): scratch, R^-1 on exit
+// One barrier per pivot: every thread recomputes the pivot's 1/sqrt; the trailing update uses
+// the unscaled row (S(i,k) -= S(j,i) S(j,k) / d_j); rows are scaled at the end.
+// ---------------------------------------------------------------------------------------
+__device__ void cta_chol_inv(double* S, double* X, int w, const double* ref, double tol, int* defi,
+                             double* invd, double* Rout, double* Rinv_out, DevStatus* status) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 thread grid over (row i, column k)
+  CYC(8);
+  for (int j = 0; j < w; ++j) {
+    const double d = S[j * w + j];
+    const bool def = !(d > tol * ref[j]) || !(ref[j] > 0.0);
+    const double inv = def ? 0.0 : rsqrt(d);
+    if (tid == 0) { defi[j] = def; invd[j] = inv; }
+    if (!def) {
+      const double inv2 = inv * inv;
 #pragma unroll
-  for (int h = 0; h < NC; ++h) {
-    const int k = lane + 32 * h;
+      for (int a = 0; a < 4; ++a) {
+        const int i = ty + 16 * a;
+        if (i > j && i < w) {
+          const double sji = S[i * w + j] * inv2;
 #pragma unroll
-    for (int i = 0; i < 32 * NC; ++i) col[h][i] = (k < w && i <= k) ? big[k * w + i] : 0.0;
-  }
-  int mydef = 0;
-  // ---- Cholesky, right-looking: step j scales row j and updates rows i > j of each column
-#pragma unroll
-  for (int j = 0; j < 32 * NC; ++j) {
-    if (j < w) {
-      const int hj = j >> 5, lj = j & 31;
-      const double d = __shfl_sync(0xffffffffu, col[hj][j], lj);
-      const bool def = !(d > tol * ref[j]) || !(ref[j] > 0.0);
-      const double rjj = def ? 0.0 : sqrt(d);
-      const double inv = def ? 0.0 : 1.0 / rjj;
-      if (lane == 0) defi[j] = def;
-#pragma unroll
-      for (int h = 0; h < NC; ++h) {
-        const int k = lane + 32 * h;
-        if (k == j) col[h][j] = rjj;
-        else if (k > j) col[h][j] *= inv;   // R(j, k)
-      }
-      if (!def) {
-#pragma unroll
-        for (int i = j + 1; i < 32 * NC; ++i) {
-          const double rji = __shfl_sync(0xffffffffu, col[i >> 5][j], i & 31);   // R(j, i) from lane i
-#pragma unroll
-          for (int h = 0; h < NC; ++h) {
-            const int k = lane + 32 * h;
-            if (k >= i) col[h][i] -= rji * col[h][j];
+          for (int b = 0; b < 4; ++b) {
+            const int k = tx + 16 * b;
+            if (k >= i && k < w) S[k * w + i] = fma(-sji, S[k * w + j], S[k * w + i]);
           }
         }
       }
     }
+    __syncthreads();
   }
-  // ---- R out (col-major), and R into smem for the inverse's broadcast reads
+  CYC(9);
+  // scale rows: R(j,k) = S(j,k) / sqrt(d_j) (k >= j); zero below the diagonal and deficient rows
 #pragma unroll
-  for (int h = 0; h < NC; ++h) {
-    const int k = lane + 32 * h;
-    if (k < w) {
-#pragma unroll
-      for (int i = 0; i < 32 * NC; ++i)
-        if (i < w) {
-          const double v = (i <= k) ? col[h][i] : 0.0;
-          Rout[k * w + i] = v;
-          big[k * w + i] = v;
-        }
-    }
-  }
-  __syncwarp();
-  // ---- X = R^-1 (upper), rows from the bottom; lane owns columns of X in registers (reuse col)
-#pragma unroll
-  for (int h = 0; h < NC; ++h)
-#pragma unroll
-    for (int i = 0; i < 32 * NC; ++i) col[h][i] = 0.0;
-#pragma unroll
-  for (int i = 32 * NC - 1; i >= 0; --i) {
+  for (int a = 0; a < 4; ++a) {
+    const int i = ty + 16 * a;
     if (i < w) {
-      const double rii = big[i * w + i];
-      const bool di = defi[i];
-      const double inv = di ? 0.0 : 1.0 / rii;
+      const double sc = defi[i] ? 0.0 : invd[i];
 #pragma unroll
-      for (int h = 0; h < NC; ++h) {
-        const int j = lane + 32 * h;
-        double sacc = 0.0;
-#pragma unroll
-        for (int k = i + 1; k < 32 * NC; ++k)
-          if (k < w && k <= j) sacc = fma(big[k * w + i], col[h][k], sacc);   // R(i,k) X(k,j)
-        if (j < w && j >= i) col[h][i] = (j == i) ? inv : -sacc * inv;
+      for (int b = 0; b < 4; ++b) {
+        const int k = tx + 16 * b;
+        if (k < w) {
+          const double v = (i <= k) ? S[k * w + i] * sc : 0.0;
+          S[k * w + i] = v;
+          Rout[k * w + i] = v;
+        }
       }
     }
   }
-#pragma unroll
-  for (int h = 0; h < NC; ++h) {
-    const int k = lane + 32 * h;
-    if (k < w) {
-#pragma unroll
-      for (int i = 0; i < 32 * NC; ++i)
-        if (i < w) Rinv_out[k * w + i] = (i <= k) ? col[h][i] : 0.0;
+  __syncthreads();
+  CYC(10);
+  // X = R^-1 row by row from the bottom: X(i,i) = 1/R(i,i), X(i,j) = -(sum_k R(i,k) X(k,j)) / R(i,i)
+  for (int i = w - 1; i >= 0; --i) {
+    const double rinv = defi[i] ? 0.0 : 1.0 / S[i * w + i];
+    for (int j = tid; j < w; j += nt) {
+      double v = 0.0;
+      if (j == i) {
+        v = rinv;
+      } else if (j > i && rinv != 0.0) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int k = i + 1;
+        for (; k + 3 <= j; k += 4) {
+          s0 = fma(S[k * w + i], X[j * w + k], s0);
+          s1 = fma(S[(k + 1) * w + i], X[j * w + k + 1], s1);
+          s2 = fma(S[(k + 2) * w + i], X[j * w + k + 2], s2);
+          s3 = fma(S[(k + 3) * w + i], X[j * w + k + 3], s3);
+        }
+        for (; k <= j; ++k) s0 = fma(S[k * w + i], X[j * w + k], s0);
+        v = -((s0 + s1) + (s2 + s3)) * rinv;
+      }
+      X[j * w + i] = v;
     }
+    __syncthreads();
   }
-  (void)mydef;
-  if (lane == 0 && status) {
+  CYC(11);
+  for (int e = tid; e < w * w; e += nt) Rinv_out[e] = X[e];
+  if (tid == 0 && status) {
     int cnt = 0;
     for (int j = 0; j < w; ++j) cnt += defi[j];
     if (cnt) atomicAdd(&status->deficient, cnt);
   }
 }
 
-template <int WQ>                // WQ = ceil(w/16): thread (ty,tx) owns G[ty+16a][tx+16b], a,b < WQ
+// smem row stride for a w-wide tile: >= 8*ceil(w/8), == 4 (mod 16) so that the m8n8k4 fragment
+// loads (8 rows x 4 consecutive columns, or 4 rows x 8 consecutive columns) are conflict free
+__host__ __device__ inline int cq_ld(int w) {
+  const int wp = (w + 7) / 8 * 8;
+  return wp + ((4 - wp % 16) + 16) % 16;
+}
+constexpr int kChunkBytes = 64 * 1024;   // staged row chunk (and its output buffer)
+__host__ __device__ inline int cholqr_chunk_rows(int w) {
+  int r = kChunkBytes / (cq_ld(w) * 8);
+  r -= r % 8;
+  return r < 8 ? 8 : r;
+}
+
+// One CholeskyQR pass over rows split among CTAs (each CTA a contiguous chunk):
+//   [apply]  O = T * Rin  (T = staged rows of Yin; Rin = R^-1 of the previous pass)  -> Yout
+//   [gram]   partial G = O^T O (upper 8x8 tiles by FP64 DMMA)  -> slot[blockIdx.x]
+//   [finish] last CTA: fixed-order slot sum, then either the first-order closed form (second
+//            pass with |G - I| <= 1e-8) or the guarded Cholesky + inverse.
 __global__ void __launch_bounds__(256) k_cholqr_pass(const double* __restrict__ Yin, int64_t ldi,
                                                      double* __restrict__ Yout, int64_t ldo, int64_t rows, int w,
                                                      int64_t rows_per_cta, const double* __restrict__ Rin,
                                                      double* __restrict__ slots, unsigned* counter, double tol,
-                                                     double shift_coef, double* __restrict__ Rout,
+                                                     double shift_coef, int second_pass, double* __restrict__ Rout,
                                                      double* __restrict__ Rinv_out, DevStatus* status) {
   extern __shared__ double cq_dyn[];
-  double* tiles = cq_dyn;                       // 2 x kFRows x kFLd
-  double* big = cq_dyn + 2 * kFRows * kFLd;     // w x w
-  __shared__ double refd[kFW];
+  const int ld = cq_ld(w);
+  const int WP = (w + 7) / 8 * 8;
+  const int NT = WP / 8;                         // 8-wide tiles per side
+  const int CR = cholqr_chunk_rows(w);
+  double* T = cq_dyn;                            // CR x ld   (staged input rows)
+  double* O = T + CR * ld;                       // CR x ld   (applied rows)
+  double* Rs = O + CR * ld;                      // WP x ld   (Rin^T: Rs[n*ld + k] = Rin(k, n))
+  __shared__ double refd[kFW], invd[kFW];
   __shared__ int defi[kFW];
   __shared__ unsigned ticket;
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  __shared__ int fastpath;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  PHASE_MIN(0);
   const bool apply = Rin != nullptr;
   if (apply)
-    for (int e = tid; e < w * w; e += 256) big[e] = Rin[e];
-  double acc[WQ][WQ];
+    for (int n = 0; n < WP; ++n)
+      for (int k = tid; k < ld; k += 256) Rs[n * ld + k] = (n < w && k < w && k <= n) ? Rin[n * w + k] : 0.0;
+  // this warp's upper-triangle Gram tiles (bi <= bj): tile index q = warp, warp+8, ...
+  const int ntiles = NT * (NT + 1) / 2;
+  double gacc[5][2];
 #pragma unroll
-  for (int a = 0; a < WQ; ++a)
+  for (int u = 0; u < 5; ++u) gacc[u][0] = gacc[u][1] = 0.0;
+  int tbi[5], tbj[5];
 #pragma unroll
-    for (int b = 0; b < WQ; ++b) acc[a][b] = 0.0;
+  for (int u = 0; u < 5; ++u) {
+    int q = warp + 8 * u, bi = 0;
+    while (q >= NT - bi && bi < NT) { q -= NT - bi; ++bi; }
+    tbi[u] = bi;
+    tbj[u] = bi + q;
+  }
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
   const int64_t r1 = min(rows, r0 + rows_per_cta);
-  const int ntiles = (int)((r1 - r0 + kFRows - 1) / kFRows);
-  auto issue = [&](int t) {
-    double* dst = tiles + (t & 1) * kFRows * kFLd;
-    const int64_t rr = r0 + (int64_t)t * kFRows;
-    for (int e = tid; e < kFRows * w; e += 256) {
-      const int c = e / kFRows, i = e % kFRows;
-      if (rr + i < r1) cp_async8(dst + i * kFLd + c, Yin + (int64_t)c * ldi + rr + i);
-      else dst[i * kFLd + c] = 0.0;
+  for (int64_t rr = r0; rr < r1; rr += CR) {
+    const int nr = (int)min((int64_t)CR, r1 - rr);
+    const int nr8 = (nr + 7) & ~7;
+    for (int c = 0; c < WP; ++c) {
+      const double* src = Yin + (int64_t)c * ldi + rr;
+      for (int i = tid; i < nr8; i += 256) {
+        if (i < nr && c < w) cp_async8(T + i * ld + c, src + i);
+        else T[i * ld + c] = 0.0;
+      }
     }
     cp_async_commit();
-  };
-  if (ntiles > 0) issue(0);
-  for (int t = 0; t < ntiles; ++t) {
-    if (t + 1 < ntiles) {
-      issue(t + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<0>();
     __syncthreads();
-    double* tile = tiles + (t & 1) * kFRows * kFLd;
-    const int64_t rr = r0 + (int64_t)t * kFRows;
+    const double* Gsrc = T;
     if (apply) {
-      // out(i, c) = sum_{j <= c} tile(i, j) Rin(j, c)   (Rin upper triangular)
-      double o[kFRows * kFW / 256];
-      int cnt = 0;
-      for (int e = tid; e < kFRows * w; e += 256, ++cnt) {
-        const int c = e / kFRows, i = e % kFRows;
-        double sacc = 0.0;
-        for (int j = 0; j <= c; ++j) sacc = fma(tile[i * kFLd + j], big[c * w + j], sacc);
-        o[cnt] = sacc;
+      // O = T Rin: warp takes 8-row m-tiles; all n-tiles per m-tile; K = WP
+      for (int mt = warp; mt < nr8 / 8; mt += 8) {
+        double oc[8][2];
+#pragma unroll
+        for (int n = 0; n < 8; ++n) oc[n][0] = oc[n][1] = 0.0;
+        for (int k0 = 0; k0 < WP; k0 += 4) {
+          const double a = T[(mt * 8 + g) * ld + k0 + t4];
+#pragma unroll
+          for (int n = 0; n < 8; ++n)
+            if (n < NT) dmma(oc[n][0], oc[n][1], a, Rs[(n * 8 + g) * ld + k0 + t4]);
+        }
+#pragma unroll
+        for (int n = 0; n < 8; ++n)
+          if (n < NT) {
+            const int row = mt * 8 + g, c0 = n * 8 + 2 * t4;
+            *reinterpret_cast<double2*>(O + row * ld + c0) = make_double2(oc[n][0], oc[n][1]);
+            if (row < nr) {
+              if (c0 < w) Yout[(int64_t)c0 * ldo + rr + row] = oc[n][0];
+              if (c0 + 1 < w) Yout[(int64_t)(c0 + 1) * ldo + rr + row] = oc[n][1];
+            }
+          }
       }
       __syncthreads();
-      cnt = 0;
-      for (int e = tid; e < kFRows * w; e += 256, ++cnt) {
-        const int c = e / kFRows, i = e % kFRows;
-        const bool ok = rr + i < r1;
-        tile[i * kFLd + c] = ok ? o[cnt] : 0.0;
-        if (ok) Yout[(int64_t)c * ldo + rr + i] = o[cnt];
-      }
-      __syncthreads();
+      Gsrc = O;
     }
-#pragma unroll 4
-    for (int i = 0; i < kFRows; ++i) {
-      double va[WQ], vb[WQ];
+    // Gram tiles: G(bi, bj) += Src[:, bi-block]^T Src[:, bj-block]  (K = rows)
+    for (int k0 = 0; k0 < nr8; k0 += 4) {
 #pragma unroll
-      for (int a = 0; a < WQ; ++a) va[a] = tile[i * kFLd + ty + 16 * a];
-#pragma unroll
-      for (int b = 0; b < WQ; ++b) vb[b] = tile[i * kFLd + tx + 16 * b];
-#pragma unroll
-      for (int a = 0; a < WQ; ++a)
-#pragma unroll
-        for (int b = 0; b < WQ; ++b) acc[a][b] = fma(va[a], vb[b], acc[a][b]);
+      for (int u = 0; u < 5; ++u) {
+        if (warp + 8 * u < ntiles) {
+          const double a = Gsrc[(k0 + t4) * ld + tbi[u] * 8 + g];
+          const double b = Gsrc[(k0 + t4) * ld + tbj[u] * 8 + g];
+          dmma(gacc[u][0], gacc[u][1], a, b);
+        }
+      }
     }
     __syncthreads();
   }
   double* slot = slots + (int64_t)blockIdx.x * w * w;
 #pragma unroll
-  for (int a = 0; a < WQ; ++a)
+  for (int u = 0; u < 5; ++u) {
+    if (warp + 8 * u < ntiles) {
+      const int i = tbi[u] * 8 + g;
 #pragma unroll
-    for (int b = 0; b < WQ; ++b) {
-      const int i = ty + 16 * a, j = tx + 16 * b;
-      if (i < w && j < w) slot[j * w + i] = acc[a][b];
+      for (int h = 0; h < 2; ++h) {
+        const int j = tbj[u] * 8 + 2 * t4 + h;
+        if (i < w && j < w) {
+          slot[j * w + i] = gacc[u][h];
+          slot[i * w + j] = gacc[u][h];
+        }
+      }
     }
+  }
   __threadfence();
   __syncthreads();
+  PHASE_MAX(1);
   if (tid == 0) ticket = atomicAdd(counter, 1u);
   __syncthreads();
   if (ticket != gridDim.x - 1) return;
-  // ---------------- finisher (last CTA): fixed-order slot sum, then warp 0 factors
+  // ---------------- finisher (last CTA): fixed-order slot sum into S (reuses T)
   __threadfence();
-  const int G = gridDim.x;
+  PHASE(2);
+  double* S = T;
+  double* X = O;
+  const int Gn = gridDim.x;
   for (int e0 = tid; e0 < w * w; e0 += 512) {
-    // two entries at a time, eight slots per batch: 16 independent loads in flight
     const int e1 = e0 + 256;
     double a[8], b[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) a[u] = b[u] = 0.0;
     int k = 0;
-    for (; k + 8 <= G; k += 8) {
+    for (; k + 8 <= Gn; k += 8) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         a[u] += __ldcg(&slots[(int64_t)(k + u) * w * w + e0]);
         if (e1 < w * w) b[u] += __ldcg(&slots[(int64_t)(k + u) * w * w + e1]);
       }
     }
-    for (; k < G; ++k) {
+    for (; k < Gn; ++k) {
       a[0] += __ldcg(&slots[(int64_t)k * w * w + e0]);
       if (e1 < w * w) b[0] += __ldcg(&slots[(int64_t)k * w * w + e1]);
     }
-    big[e0] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-    if (e1 < w * w) big[e1] = ((b[0] + b[1]) + (b[2] + b[3])) + ((b[4] + b[5]) + (b[6] + b[7]));
+    S[e0] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    if (e1 < w * w) S[e1] = ((b[0] + b[1]) + (b[2] + b[3])) + ((b[4] + b[5]) + (b[6] + b[7]));
+  }
+  if (tid == 0) { *counter = 0u; fastpath = second_pass; }
+  __syncthreads();
+  PHASE(3);
+  if (second_pass) {
+    // G = Q1^T Q1 = I + E (CholeskyQR's second pass).  With max|E| <= 1e-8 the first-order
+    // factor R2 = I + triu(E,1) + diag(E)/2 and R2^-1 = I - triu(E,1) - diag(E)/2 are exact to
+    // O(|E|^2) <= 1e-16.  Columns zeroed by the first pass (G_jj == 0) stay zero.
+    for (int k = 0; k < w; ++k)
+      for (int i = tid; i < w; i += 256) {
+        if (S[i * w + i] == 0.0 || S[k * w + k] == 0.0) continue;
+        const double E = S[k * w + i] - (i == k ? 1.0 : 0.0);
+        if (!(fabs(E) <= 1e-8)) fastpath = 0;
+      }
+    __syncthreads();
+    if (fastpath) {
+      int cnt = 0;
+      for (int k = 0; k < w; ++k)
+        for (int i = tid; i < w; i += 256) {
+          const int e = k * w + i;
+          const bool dz = S[i * w + i] == 0.0 || S[k * w + k] == 0.0;
+          double r = 0.0, ri = 0.0;
+          if (!dz && i <= k) {
+            const double E = S[e] - (i == k ? 1.0 : 0.0);
+            r = (i == k) ? 1.0 + 0.5 * E : E;
+            ri = (i == k) ? 1.0 - 0.5 * E : -E;
+          }
+          Rout[e] = r;
+          Rinv_out[e] = ri;
+          if (i == k && dz) ++cnt;
+        }
+      if (cnt && status) atomicAdd(&status->deficient, cnt);
+      PHASE(4);
+      return;
+    }
+  }
+  if (tid < 32) {
+    double tr = 0.0;
+    for (int j = tid; j < w; j += 32) tr += S[j * w + j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    const double shift = shift_coef * tr;
+    for (int j = tid; j < w; j += 32) {
+      refd[j] = S[j * w + j] + shift;
+      S[j * w + j] += shift;
+    }
   }
   __syncthreads();
-  if (tid >= 32) return;
-  double tr = 0.0;
-  for (int j = tid; j < w; j += 32) tr += big[j * w + j];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
-  const double shift = shift_coef * tr;
-  for (int j = tid; j < w; j += 32) {
-    refd[j] = big[j * w + j] + shift;
-    big[j * w + j] += shift;
-  }
-  if (tid == 0) *counter = 0u;
-  __syncwarp();
-  if (WQ <= 2)
-    warp_chol_inv<1>(big, w, refd, tol, defi, Rout, Rinv_out, status);
-  else
-    warp_chol_inv<2>(big, w, refd, tol, defi, Rout, Rinv_out, status);
+  cta_chol_inv(S, X, w, refd, tol, defi, invd, Rout, Rinv_out, status);
+  PHASE(4);
 }
 
-int cholqr_smem_bytes(int w) { return (2 * kFRows * kFLd + w * w) * 8; }
+int cholqr_smem_bytes(int w) { return (2 * cholqr_chunk_rows(w) * cq_ld(w) + ((w + 7) / 8 * 8) * cq_ld(w)) * 8; }
 
 int cholqr_pass_ctas(int64_t rows) {
   int64_t g = (rows + 255) / 256;
@@ -843,28 +920,19 @@ int cholqr_pass_ctas(int64_t rows) {
 }
 
 int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo, int64_t rows, int w,
-                       const double* Rin, double* slots, unsigned* counter, double tol, double shift_coef, double* R,
-                       double* Rinv, DevStatus* status, cudaStream_t st) {
+                       const double* Rin, double* slots, unsigned* counter, double tol, double shift_coef,
+                       int second_pass, double* R, double* Rinv, DevStatus* status, cudaStream_t st) {
   if (w < 1 || w > kFW) return RSVD_E_ARG;
   const int G = cholqr_pass_ctas(rows);
   const int64_t rpc = (rows + G - 1) / G;
-  const int WQ = (w + 15) / 16;
   const int smem = cholqr_smem_bytes(w);
   static bool attr = false;
   if (!attr) {
-    const int mx = cholqr_smem_bytes(kFW);
-    cudaFuncSetAttribute(k_cholqr_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_cholqr_pass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_cholqr_pass<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(k_cholqr_pass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_cholqr_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  switch (WQ) {
-    case 1: k_cholqr_pass<1><<<G, 256, smem, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
-    case 2: k_cholqr_pass<2><<<G, 256, smem, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
-    case 3: k_cholqr_pass<3><<<G, 256, smem, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
-    default: k_cholqr_pass<4><<<G, 256, smem, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef, R, Rinv, status); break;
-  }
+  k_cholqr_pass<<<G, 256, smem, st>>>(Yin, ldi, Yout, ldo, rows, w, rpc, Rin, slots, counter, tol, shift_coef,
+                                      second_pass, R, Rinv, status);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
@@ -879,19 +947,21 @@ int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo
 // =====================================================================================
 namespace rsvd {
 
-template <int RW>  // rows per lane (r <= 32 RW)
-__global__ void __launch_bounds__(1024) k_jacobi_small(const double* __restrict__ M, int64_t ldm, int trans, int r,
-                                                       int c, double* __restrict__ Ul, double* __restrict__ Sv,
-                                                       double* __restrict__ Vr, double tol, int max_sweeps,
-                                                       DevStatus* status) {
-  constexpr int RS = 32 * RW;          // padded rows of W
+template <int RW>  // rows per lane, r <= 8 RW; a column pair is handled by 8 lanes (4 pairs per warp)
+__global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__ M, int64_t ldm, int trans, int r,
+                                                      int c, double* __restrict__ Ul, double* __restrict__ Sv,
+                                                      double* __restrict__ Vr, double tol, int max_sweeps,
+                                                      DevStatus* status) {
+  constexpr int RS = 8 * RW;           // padded rows of W (stride of a column)
   extern __shared__ double jac_dyn[];
   double* W = jac_dyn;                 // 64 x RS
   double* J = jac_dyn + 64 * RS;       // 64 x 64
   __shared__ unsigned short pairs[63 * 32];
   __shared__ double sval[64];
   __shared__ int srank[64];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int grp = tid >> 3, sl = tid & 7;          // pair group and its sub-lane
+  const unsigned gmask = 0xffu << (tid & 24);      // the 8 lanes of this group
   const int ce = c + (c & 1);
   const int npairs = ce >> 1;
   for (int e = tid; e < 64 * RS; e += nt) {
@@ -913,29 +983,26 @@ __global__ void __launch_bounds__(1024) k_jacobi_small(const double* __restrict_
   const double tol2 = tol * tol;
   int sweep = 0;
   bool converged = false;
-  // J rotations lag one round behind W's: they touch only J (never read by the W updates), the
-  // lag keeps per-column order (a column's round-r update finishes before the round-r+1 barrier),
-  // and it takes the J work off the round's critical path (it overlaps the next reductions).
+  // J rotations lag one round (they touch only J; per-column order is kept by the barrier)
   int pj_p = 0, pj_q = 0, pj_on = 0;
   double pj_cs = 1.0, pj_sn = 0.0;
-  auto apply_pending_J = [&]() {
-    if (pj_on) {
-      double* jp = J + pj_p * 64;
-      double* jq = J + pj_q * 64;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const double u = jp[lane + 32 * k], v = jq[lane + 32 * k];
-        jp[lane + 32 * k] = pj_cs * u - pj_sn * v;
-        jq[lane + 32 * k] = pj_sn * u + pj_cs * v;
-      }
-      pj_on = 0;
-    }
-  };
+#define RSVD_APPLY_PENDING_J()                                   \
+  if (pj_on) {                                                   \
+    double* jp = J + pj_p * 64;                                  \
+    double* jq = J + pj_q * 64;                                  \
+    _Pragma("unroll") for (int k = 0; k < 8; ++k) {              \
+      const double u = jp[sl + 8 * k], v = jq[sl + 8 * k];       \
+      jp[sl + 8 * k] = pj_cs * u - pj_sn * v;                    \
+      jq[sl + 8 * k] = pj_sn * u + pj_cs * v;                    \
+    }                                                            \
+    pj_on = 0;                                                   \
+  }
+  const bool active = grp < npairs;
   for (; sweep < max_sweeps; ++sweep) {
     int rotated = 0;
     for (int round = 0; round < ce - 1; ++round) {
-      if (warp < npairs) {
-        const unsigned pq = pairs[round * 32 + warp];
+      if (active) {
+        const unsigned pq = pairs[round * 32 + grp];
         const int p = pq & 255, q = pq >> 8;
         double* wp = W + p * RS;
         double* wq = W + q * RS;
@@ -943,37 +1010,41 @@ __global__ void __launch_bounds__(1024) k_jacobi_small(const double* __restrict_
         double a = 0.0, b = 0.0, cc = 0.0;
 #pragma unroll
         for (int t = 0; t < RW; ++t) {
-          x[t] = wp[lane + 32 * t];
-          y[t] = wq[lane + 32 * t];
+          x[t] = wp[sl + 8 * t];
+          y[t] = wq[sl + 8 * t];
           a = fma(x[t], x[t], a);
           b = fma(y[t], y[t], b);
           cc = fma(x[t], y[t], cc);
         }
-        apply_pending_J();
+        RSVD_APPLY_PENDING_J();
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          a += __shfl_xor_sync(0xffffffffu, a, o);
-          b += __shfl_xor_sync(0xffffffffu, b, o);
-          cc += __shfl_xor_sync(0xffffffffu, cc, o);
+        for (int o = 4; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(gmask, a, o, 8);
+          b += __shfl_xor_sync(gmask, b, o, 8);
+          cc += __shfl_xor_sync(gmask, cc, o, 8);
         }
         if (cc * cc > tol2 * (a * b) && cc != 0.0) {
           rotated = 1;
           const double d = b - a, e2 = 2.0 * cc;
           double t;
-          if (fabs(d) < 1e-300 * fabs(e2) || d == 0.0) {
+          const double ad = fabs(d), ae = fabs(e2);
+          if (ad > 1e-30 && ad < 1e30 && ae > 1e-30 && ae < 1e30) {
+            // tan(theta) from fp32 (any t gives an exactly orthogonal rotation below)
+            const float rf = (float)e2 / (float)ad;
+            const float tf = rf / (1.0f + sqrtf(fmaf(rf, rf, 1.0f)));
+            t = copysign(1.0, d) * (double)tf;
+          } else if (d == 0.0) {
             t = copysign(1.0, e2);
           } else {
-            const double rho = e2 / fabs(d);                 // tan(2 theta), sign folded below
-            const float rf = (float)rho;
-            float tf = fabsf(rf) > 1e18f ? copysignf(1.0f, rf) : rf / (1.0f + sqrtf(fmaf(rf, rf, 1.0f)));
-            t = copysign(1.0, d) * (double)tf;
+            const double rho = e2 / ad;
+            t = copysign(1.0, d) * rho / (1.0 + sqrt(fma(rho, rho, 1.0)));
           }
           const double cs = rsqrt(fma(t, t, 1.0));
           const double sn = cs * t;
 #pragma unroll
           for (int k = 0; k < RW; ++k) {
-            wp[lane + 32 * k] = cs * x[k] - sn * y[k];
-            wq[lane + 32 * k] = sn * x[k] + cs * y[k];
+            wp[sl + 8 * k] = cs * x[k] - sn * y[k];
+            wq[sl + 8 * k] = sn * x[k] + cs * y[k];
           }
           pj_p = p; pj_q = q; pj_cs = cs; pj_sn = sn; pj_on = 1;
         }
@@ -986,18 +1057,18 @@ __global__ void __launch_bounds__(1024) k_jacobi_small(const double* __restrict_
       break;
     }
   }
-  if (warp < npairs) apply_pending_J();
+  if (active) { RSVD_APPLY_PENDING_J(); }
   __syncthreads();
-  for (int j = warp; j < ce; j += (nt >> 5)) {
-    double s = 0.0;
+  for (int j = grp; j < ce; j += (nt >> 3)) {
+    double sacc = 0.0;
 #pragma unroll
     for (int t = 0; t < RW; ++t) {
-      const double v = W[j * RS + lane + 32 * t];
-      s = fma(v, v, s);
+      const double v = W[j * RS + sl + 8 * t];
+      sacc = fma(v, v, sacc);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) sval[j] = sqrt(s);
+    for (int o = 4; o > 0; o >>= 1) sacc += __shfl_xor_sync(gmask, sacc, o, 8);
+    if (sl == 0) sval[j] = sqrt(sacc);
   }
   __syncthreads();
   for (int j = tid; j < ce; j += nt) {
@@ -1035,19 +1106,30 @@ int launch_jacobi_small(const double* M, int64_t ldm, int trans, int r, int c, d
                         DevStatus* status, cudaStream_t st) {
   if (c < 1 || c > 64 || r < c || r > 64) return RSVD_E_ARG;
   const int ce = c + (c & 1);
-  const int threads = 32 * std::max(1, ce / 2);
+  const int threads = ((8 * std::max(1, ce / 2)) + 31) / 32 * 32;
   const double tol = 2.220446049250313e-16 * sqrt((double)r);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_jacobi_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 32 + 64 * 64) * 8);
-    cudaFuncSetAttribute(k_jacobi_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 64 + 64 * 64) * 8);
+    cudaFuncSetAttribute(k_jacobi_small<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 32 + 64 * 64) * 8);
+    cudaFuncSetAttribute(k_jacobi_small<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 64 + 64 * 64) * 8);
     attr = true;
   }
   if (r <= 32)
-    k_jacobi_small<1><<<1, threads, (64 * 32 + 64 * 64) * 8, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
+    k_jacobi_small<4><<<1, threads, (64 * 32 + 64 * 64) * 8, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
   else
-    k_jacobi_small<2><<<1, threads, (64 * 64 + 64 * 64) * 8, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
+    k_jacobi_small<8><<<1, threads, (64 * 64 + 64 * 64) * 8, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
 }  // namespace rsvd
+
+#ifdef RSVD_PHASE_TIMING
+namespace rsvd {
+void read_phases(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 16); }
+void reset_phases() {
+  unsigned long long init[16];
+  for (int i = 0; i < 16; ++i) init[i] = (i == 0) ? ~0ull : 0ull;
+  cudaMemcpyToSymbol(g_phase, init, sizeof(init));
+}
+}  // namespace rsvd
+#endif
