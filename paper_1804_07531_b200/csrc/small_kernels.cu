@@ -624,29 +624,44 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // ---------------------------------------------------------------------------------------
 __device__ void cta_chol_inv(double* S, double* X, int w, const double* ref, double tol, int* defi,
                              double* invd, double* Rout, double* Rinv_out, DevStatus* status) {
+  // S, X: col-major with odd leading dimension lw (bank-conflict-free column walks)
+  const int lw = w | 1;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 thread grid over (row i, column k)
   CYC(8);
   for (int j = 0; j < w; ++j) {
-    const double d = S[j * w + j];
+    // issue every shared load of this step before the pivot math: the stores below cannot alias
+    // them (they touch rows/columns > j only), so nothing serialises behind the rsqrt.
+    const double d = S[j * lw + j];
+    double sji[4], sjk[4], tg[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = ty + 16 * a;
+      sji[a] = (i > j && i < w) ? S[i * lw + j] : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int k = tx + 16 * b;
+      sjk[b] = (k > j && k < w) ? S[k * lw + j] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = ty + 16 * a, k = tx + 16 * b;
+        tg[a][b] = (i > j && k >= i && k < w) ? S[k * lw + i] : 0.0;
+      }
     const bool def = !(d > tol * ref[j]) || !(ref[j] > 0.0);
     const double inv = def ? 0.0 : rsqrt(d);
     if (tid == 0) { defi[j] = def; invd[j] = inv; }
-    if (!def) {
-      const double inv2 = inv * inv;
+    const double inv2 = inv * inv;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int i = ty + 16 * a;
-        if (i > j && i < w) {
-          const double sji = S[i * w + j] * inv2;
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int k = tx + 16 * b;
-            if (k >= i && k < w) S[k * w + i] = fma(-sji, S[k * w + j], S[k * w + i]);
-          }
-        }
+      for (int b = 0; b < 4; ++b) {
+        const int i = ty + 16 * a, k = tx + 16 * b;
+        if (!def && i > j && k >= i && k < w) S[k * lw + i] = fma(-sji[a] * inv2, sjk[b], tg[a][b]);
       }
-    }
     __syncthreads();
   }
   CYC(9);
@@ -660,8 +675,8 @@ __device__ void cta_chol_inv(double* S, double* X, int w, const double* ref, dou
       for (int b = 0; b < 4; ++b) {
         const int k = tx + 16 * b;
         if (k < w) {
-          const double v = (i <= k) ? S[k * w + i] * sc : 0.0;
-          S[k * w + i] = v;
+          const double v = (i <= k) ? S[k * lw + i] * sc : 0.0;
+          S[k * lw + i] = v;
           Rout[k * w + i] = v;
         }
       }
@@ -669,34 +684,42 @@ __device__ void cta_chol_inv(double* S, double* X, int w, const double* ref, dou
   }
   __syncthreads();
   CYC(10);
-  // X = R^-1 row by row from the bottom: X(i,i) = 1/R(i,i), X(i,j) = -(sum_k R(i,k) X(k,j)) / R(i,i)
+  // X = R^-1 row by row from the bottom: X(i,i) = 1/R(i,i), X(i,j) = -(sum_k R(i,k) X(k,j)) / R(i,i).
+  // Four threads share a column j (k split four ways, shuffle-combined) so each chain is short.
+  const int j = tid >> 2, part = tid & 3;
+  // 1/R(i,i) = 1/sqrt(d_i) * ... : R(i,i) = d_i * invd_i, so 1/R(i,i) = 1 / (d_i invd_i); computed
+  // for all i at once (off the row loop's critical path), stored in the ref slot no longer needed
+  double* rinvs = const_cast<double*>(ref);
+  for (int i = tid; i < w; i += nt) rinvs[i] = defi[i] ? 0.0 : 1.0 / S[i * lw + i];
+  __syncthreads();
   for (int i = w - 1; i >= 0; --i) {
-    const double rinv = defi[i] ? 0.0 : 1.0 / S[i * w + i];
-    for (int j = tid; j < w; j += nt) {
-      double v = 0.0;
-      if (j == i) {
-        v = rinv;
-      } else if (j > i && rinv != 0.0) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int k = i + 1;
-        for (; k + 3 <= j; k += 4) {
-          s0 = fma(S[k * w + i], X[j * w + k], s0);
-          s1 = fma(S[(k + 1) * w + i], X[j * w + k + 1], s1);
-          s2 = fma(S[(k + 2) * w + i], X[j * w + k + 2], s2);
-          s3 = fma(S[(k + 3) * w + i], X[j * w + k + 3], s3);
-        }
-        for (; k <= j; ++k) s0 = fma(S[k * w + i], X[j * w + k], s0);
-        v = -((s0 + s1) + (s2 + s3)) * rinv;
+    const double rinv = rinvs[i];
+    double sacc = 0.0;
+    if (j < w && j > i && rinv != 0.0) {
+      const double* srow = S + i;          // R(i,k) at srow[k * lw]
+      const double* xcol = X + j * lw;     // X(k,j) at xcol[k]
+      double s0 = 0.0, s1 = 0.0;
+      int k = i + 1 + part;
+      for (; k + 4 <= j; k += 8) {
+        s0 = fma(srow[k * lw], xcol[k], s0);
+        s1 = fma(srow[(k + 4) * lw], xcol[k + 4], s1);
       }
-      X[j * w + i] = v;
+      for (; k <= j; k += 4) s0 = fma(srow[k * lw], xcol[k], s0);
+      sacc = s0 + s1;
     }
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+    if (j < w && part == 0) X[j * lw + i] = (j == i) ? rinv : (j > i ? -sacc * rinv : 0.0);
     __syncthreads();
   }
   CYC(11);
-  for (int e = tid; e < w * w; e += nt) Rinv_out[e] = X[e];
+  for (int e = tid; e < w * w; e += nt) {
+    const int i = e % w, k = e / w;
+    Rinv_out[e] = X[k * lw + i];
+  }
   if (tid == 0 && status) {
     int cnt = 0;
-    for (int j = 0; j < w; ++j) cnt += defi[j];
+    for (int jj = 0; jj < w; ++jj) cnt += defi[jj];
     if (cnt) atomicAdd(&status->deficient, cnt);
   }
 }
@@ -894,15 +917,24 @@ __global__ void __launch_bounds__(256) k_cholqr_pass(const double* __restrict__ 
       return;
     }
   }
+  // re-layout S to the odd leading dimension used by cta_chol_inv (X as scratch)
+  const int lw = w | 1;
+  for (int e = tid; e < w * w; e += 256) X[e] = S[e];
+  __syncthreads();
+  for (int e = tid; e < w * w; e += 256) {
+    const int i = e % w, k = e / w;
+    S[k * lw + i] = X[e];
+  }
+  __syncthreads();
   if (tid < 32) {
     double tr = 0.0;
-    for (int j = tid; j < w; j += 32) tr += S[j * w + j];
+    for (int j = tid; j < w; j += 32) tr += S[j * lw + j];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
     const double shift = shift_coef * tr;
     for (int j = tid; j < w; j += 32) {
-      refd[j] = S[j * w + j] + shift;
-      S[j * w + j] += shift;
+      refd[j] = S[j * lw + j] + shift;
+      S[j * lw + j] += shift;
     }
   }
   __syncthreads();
