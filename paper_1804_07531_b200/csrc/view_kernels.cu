@@ -25,6 +25,10 @@ constexpr int kThreads = (kNW + 1) * 32;
 constexpr int kBK = 32;            // reduction-dimension elements per pipeline stage
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kNG = 4;             // n-tiles per B-fragment group
+// k-loop unroll by width: narrow tiles have registers to spare, so unrolling lets the next
+// step's fragment loads overlap the current DMMAs; wide tiles stay rolled (register budget 168)
+template <int WT>
+struct KUnroll { static constexpr int v = WT <= 4 ? 4 : (WT <= 6 ? 2 : 1); };
 
 // =====================================================================================
 // Y = A X     (M = rows of A, K = n, N = w)
@@ -105,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&full[stage], phase);
       const uint8_t* As = smem + stage * C::STAGE;
       const uint8_t* Xs = As + C::A_STAGE;
-#pragma unroll 1
+#pragma unroll (KUnroll<WT>::v)
       for (int kk = 0; kk < 4; ++kk) {   // 4 x 8 k per stage; thread t owns k = 8kk + {2t, 2t+1}
         const int box = kk >> 1;
         const uint32_t q = ((kk & 1) << 2) + t;
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&full[stage], phase);
       const uint8_t* As = smem + stage * C::STAGE;
       const uint8_t* Ys = As + C::A_STAGE;
-#pragma unroll 1
+#pragma unroll (KUnroll<WT>::v)
       for (int kk = 0; kk < 4; ++kk) {
         const int r0 = kk * 8 + 2 * t;     // rows of A (the reduction index) this thread feeds
         const int boxy = kk >> 1;

@@ -1,0 +1,231 @@
+"""Multi-rank (N > 1) host logic on CPU: world_size-2 gloo process groups on 127.0.0.1.
+
+* shard planning, unique-id broadcast and max-over-ranks timing (paper_1804_07531_b200.sharding);
+* the library's row-sharded schedule (include/rsvd.h MULTI-GPU) emulated in NumPy
+  with gloo all-reduces: A X local, A^T Y and every Gram / cross product of a row-sharded block
+  all-reduced, column-side blocks replicated.  Each rank runs Alg. 2 / 9 / 7 on its row block;
+  the gathered result must equal the single-process oracle (the schedule is exact algebra, so the
+  same 1e-10 / 1e-9 tolerances as GPU parity apply).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+import synth as S
+from paper_1804_07531_b200.sharding import broadcast_uid, max_over_ranks, shard_rows, weak_scaled
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+# ------------------------------------------------------------------ pure shard planning
+@pytest.mark.parametrize("m,world,align", [(4000, 2, 1), (4001, 2, 1), (50000, 8, 128), (9, 8, 1), (1037, 3, 32)])
+def test_shard_rows_tile_in_rank_order(m, world, align):
+    shards = [shard_rows(m, world, r, align) for r in range(world)]
+    assert shards[0].row0 == 0
+    for a, b in zip(shards, shards[1:]):
+        assert a.row0 + a.m_local == b.row0
+    assert shards[-1].row0 + shards[-1].m_local == m
+    assert all(s.m_local >= 1 for s in shards)
+    assert max(s.m_local for s in shards) - min(s.m_local for s in shards) <= 2 * align  # one chunk + ragged tail
+
+
+def test_weak_scaled():
+    sh = [weak_scaled(4000, 4, r) for r in range(4)]
+    assert [s.row0 for s in sh] == [0, 4000, 8000, 12000] and all(s.m == 16000 for s in sh)
+
+
+def test_shard_rows_errors():
+    with pytest.raises(ValueError):
+        shard_rows(3, 4, 0)
+    with pytest.raises(ValueError):
+        shard_rows(10, 2, 2)
+
+
+# ------------------------------------------------------------------ the sharded schedule (emulated)
+class ShardedOps:
+    """Row-sharded executor mirroring librsvd's Exec: side M (rows of A) is sharded, side N is
+    replicated.  All reductions go through dist.all_reduce (sum)."""
+
+    def __init__(self, A_local):
+        self.A = A_local
+
+    @staticmethod
+    def allreduce(x):
+        t = torch.from_numpy(np.ascontiguousarray(x))
+        dist.all_reduce(t)
+        return t.numpy()
+
+    def view(self, from_side, X):             # from N: A X (local, side M); from M: A^T X (all-reduced)
+        return self.A @ X if from_side == "N" else self.allreduce(self.A.T @ X)
+
+    def cross(self, side, Xa, Xb):
+        G = Xa.T @ Xb
+        return self.allreduce(G) if side == "M" else G
+
+    def orth(self, side, Y, shifted=False):
+        """CholeskyQR2 (shifted CholeskyQR3 if `shifted`) with the Gram all-reduced on the sharded
+        side; R replicated.  Mirrors Exec::orth / orth_fused."""
+        R = np.eye(Y.shape[1])
+        if shifted:
+            rows = self.allreduce(np.array([float(Y.shape[0])]))[0] if side == "M" else Y.shape[0]
+            G = self.cross(side, Y, Y)
+            w = Y.shape[1]
+            G = G + 11.0 * (rows * w + w * (w + 1)) * 1.1102230246251565e-16 * np.trace(G) * np.eye(w)
+            L = np.linalg.cholesky(G)
+            Y = np.linalg.solve(L, Y.T).T
+        for _ in range(2):
+            G = self.cross(side, Y, Y)
+            L = np.linalg.cholesky(G)
+            Y = np.linalg.solve(L, Y.T).T      # Y L^-T
+            R = L.T @ R
+        return Y, R
+
+
+def _alg2_sharded(ops, k, p, v, Om):
+    Qr = Om.copy()
+    Qc = Rc = Rr = None
+    for j in range(1, v + 1):
+        if j % 2:
+            Qc, Rc = ops.orth("M", ops.view("N", Qr))
+        else:
+            Qr, Rr = ops.orth("N", ops.view("M", Qc))
+    if v % 2 == 0:
+        Vw, lam, Uwt = np.linalg.svd(Rr)
+        return Qc @ Uwt.T[:, :k], lam[:k], Qr @ Vw[:, :k]
+    Uw, lam, Vwt = np.linalg.svd(Rc)
+    return Qc @ Uw[:, :k], lam[:k], Qr @ Vwt.T[:, :k]
+
+
+def _alg9_sharded(ops, k, p, v, Om):
+    l = Om.shape[1]
+    blocks, prev = [], Om
+    for j in range(1, v):
+        B = ops.view("N", prev) if j % 2 else ops.view("M", prev)
+        side = "M" if j % 2 else "N"
+        if j < v - 1:
+            B, _ = ops.orth(side, B)
+        if (v % 2 == 0 and j % 2 == 1) or (v % 2 == 1 and j % 2 == 0):
+            blocks.append(B)
+        prev = B
+    side_K = "M" if v % 2 == 0 else "N"
+    Q = None
+    for B in blocks:                            # BCGS2 with all-reduced cross products
+        W = B
+        if Q is not None:
+            W = W - Q @ ops.cross(side_K, Q, W)
+            W, _ = ops.orth(side_K, W, shifted=True)
+            W = W - Q @ ops.cross(side_K, Q, W)
+        W, _ = ops.orth(side_K, W)
+        Q = W if Q is None else np.hstack([Q, W])
+    if v % 2 == 0:
+        Qr, Rr = ops.orth("N", ops.view("M", Q))
+        Vw, lam, Uwt = np.linalg.svd(Rr)
+        return Q @ Uwt.T[:, :k], lam[:k], Qr @ Vw[:, :k]
+    Qc, Rc = ops.orth("M", ops.view("N", Q))
+    Uw, lam, Vwt = np.linalg.svd(Rc)
+    return Qc @ Uw[:, :k], lam[:k], Q @ Vwt.T[:, :k]
+
+
+def _alg7_sharded(ops, k, p, Om, Phi_local):
+    Yc = ops.view("N", Om)                      # local
+    Yr = ops.view("M", Phi_local)               # all-reduced (fused kernel's Y_r partial)
+    Qc, _ = ops.orth("M", Yc)
+    C = ops.cross("M", Phi_local, Qc)           # Phi^T Q_c, all-reduced
+    Qh, Rh = np.linalg.qr(C)
+    X = np.linalg.solve(Rh, Qh.T @ Yr.T)
+    Uw, lam, Vwt = np.linalg.svd(X, full_matrices=False)
+    return Qc @ Uw[:, :k], lam[:k], Vwt[:k].T
+
+
+CASES = [("subspace", "C1", 2, None, None), ("subspace", "C1", 3, None, None),
+         ("subspace", "C2", 4, 1200, 900), ("krylov", "C1", 4, None, None),
+         ("krylov", "C2", 5, 1200, 900), ("single_pass", "C1", 1, None, None),
+         ("single_pass", "C3", 1, 1500, 700)]
+
+
+def _one_case(rank, world, case):
+    alg, name, v, mm, nn = case
+    cfg = S.CONFIGS[name]
+    A = S.make_matrix(cfg, mm, nn)
+    Om = S.gaussian_test_matrix(A.shape[1], cfg.l, cfg, S.ROLE_OMEGA)
+    Phi = S.gaussian_test_matrix(A.shape[0], cfg.l2, cfg, S.ROLE_PHI)
+    sh = shard_rows(A.shape[0], world, rank)
+    ops = ShardedOps(A[sh.row0:sh.row0 + sh.m_local])
+    if alg == "subspace":
+        U, s, V = _alg2_sharded(ops, cfg.k, cfg.p, v, Om)
+    elif alg == "krylov":
+        U, s, V = _alg9_sharded(ops, cfg.k, cfg.p, v, Om)
+    else:
+        U, s, V = _alg7_sharded(ops, cfg.k, cfg.p, Om, Phi[sh.row0:sh.row0 + sh.m_local])
+    parts = [None] * world
+    dist.all_gather_object(parts, U)
+    res = {}
+    if rank == 0:
+        Ug = np.vstack(parts)
+        Uo, so, Vo, _ = O.svd_of(A, alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi)
+        res["sig"] = float(np.max(np.abs(s - so) / so))
+        res["pu"] = O.projector_distance(Ug, Uo)
+        res["pv"] = O.projector_distance(V, Vo)
+    sv = [None] * world                         # replicated outputs: bitwise identical on all ranks
+    dist.all_gather_object(sv, (s.tobytes(), V.tobytes()))
+    res["replicated_equal"] = all(x == sv[0] for x in sv)
+    return res
+
+
+def _worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        uid = os.urandom(128) if rank == 0 else None
+        got = broadcast_uid(uid, rank)
+        t = torch.tensor(list(got), dtype=torch.float64)
+        lst = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(lst, t)
+        res["uid_equal"] = all(torch.equal(lst[0], x) for x in lst)
+        res["max"] = max_over_ranks(float(rank + 1) * 1.5)
+        res["cases"] = [_one_case(rank, world, c) for c in CASES]
+        out_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.fixture(scope="module")
+def gloo_results():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    return res
+
+
+def test_gloo_uid_broadcast_and_max(gloo_results):
+    assert gloo_results[0]["uid_equal"] and gloo_results[1]["uid_equal"]
+    assert gloo_results[0]["max"] == gloo_results[1]["max"] == 3.0
+
+
+@pytest.mark.parametrize("idx", range(len(CASES)), ids=[f"{c[0]}-{c[1]}-v{c[2]}" for c in CASES])
+def test_row_sharded_schedule_matches_oracle(gloo_results, idx):
+    r0 = gloo_results[0]["cases"][idx]
+    assert r0["sig"] <= 1e-10 and r0["pu"] <= 1e-9 and r0["pv"] <= 1e-9, r0
+    assert r0["replicated_equal"] and gloo_results[1]["cases"][idx]["replicated_equal"]
