@@ -43,7 +43,7 @@ def step_views():
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
@@ -159,6 +159,7 @@ def main():
     import torch.distributed as dist
 
     from paper_1804_07531_b200 import rsvd
+    from paper_1804_07531_b200.sharding import broadcast_uid, max_over_ranks as _mor, weak_scaled
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -170,9 +171,8 @@ def main():
     cfg = S.CONFIGS[args.config]
     ctx = rsvd.Context(local)
     if world > 1:
-        obj = [rsvd.get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctx.comm_init(world, rank, obj[0])
+        uid = broadcast_uid(rsvd.get_unique_id() if rank == 0 else None, rank)
+        ctx.comm_init(world, rank, uid)
 
     # ---- inputs: rank r holds rows [r*m, (r+1)*m) of A_global = [U_1;..;U_N] diag(sigma) V^T / sqrt(N)
     m, n = cfg.m, cfg.n
@@ -181,7 +181,8 @@ def main():
         A.mul_(1.0 / np.sqrt(world))
     Om = S.gaussian_test_matrix_torch(n, cfg.l, cfg, S.ROLE_OMEGA, dev)          # replicated
     Phi = S.gaussian_test_matrix_torch(m, cfg.l2, cfg, S.ROLE_PHI, dev, seed_offset=rank)
-    M_glob, row0 = m * world, m * rank
+    shard = weak_scaled(m, world, rank)
+    M_glob, row0 = shard.m, shard.row0
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)     # 256 MiB > L2 (126 MB)
     stream = torch.cuda.current_stream(dev)
 
@@ -205,11 +206,7 @@ def main():
         torch.cuda.synchronize(dev)
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return _mor(x, device=dev)
 
     # ---- warm-up (also captures the CUDA graphs)
     for _ in range(max(3, args.warmup)):
@@ -219,6 +216,12 @@ def main():
     # ---- timed region: device events per step, L2 flushed before each step (outside the events)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
+        # keep the GPU busy (untimed steps) while nvidia-smi starts sampling, so that the samples
+        # bracket the timed region under load
+        t_busy = time.perf_counter()
+        while time.perf_counter() - t_busy < 1.0:
+            step()
+            torch.cuda.synchronize(dev)
         barrier()
         for i in range(args.steps):
             flush.zero_()
@@ -226,6 +229,10 @@ def main():
             infos = step()
             evs[i][1].record(stream)
         barrier()
+        t_busy = time.perf_counter()
+        while time.perf_counter() - t_busy < 0.4:      # a few more samples under load
+            step()
+            torch.cuda.synchronize(dev)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = max_over_ranks(sum(step_ms))
     ms_per_step = total_ms / args.steps
