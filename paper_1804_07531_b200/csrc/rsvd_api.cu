@@ -25,7 +25,7 @@ namespace rsvd {
 int launch_chol_ref(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
                     DevStatus* status, cudaStream_t st, double shift_coef = 0.0);
 int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
-                    double* scratch, DevStatus* status, cudaStream_t st);
+                    double* scratch, DevStatus* status, cudaStream_t st, int want_j);
 int launch_diag(const double* G, int w, double* d, cudaStream_t st);
 int probe_peaks(int sms, cudaStream_t st, double* dmma_tflops, double* read_gbs);
 int cholqr_pass_ctas(int64_t rows);
@@ -396,7 +396,7 @@ struct Exec {
   void core_svd(const double* M, int w, int trans, double* Ul, double* Sv, double* Vr) {
     const size_t mk = mark();
     double* scratch = alloc(2 * 256 * 256);
-    if (live()) chk(launch_jacobi_t(M, w, trans, w, w, Ul, Sv, Vr, scratch, ctx->dstat, st));
+    if (live()) chk(launch_jacobi_t(M, w, trans, w, w, Ul, Sv, Vr, scratch, ctx->dstat, st, /*want_j=*/0));
     release(mk);
   }
 
@@ -746,7 +746,7 @@ void prim_core(Exec& E) {
   double* sv = E.alloc(cc);
   double* scratch = E.alloc(2 * 256 * 256);
   if (E.live()) {
-    E.chk(launch_jacobi_t(M, r, 0, r, cc, Ul, sv, Vr, scratch, E.ctx->dstat, E.st));
+    E.chk(launch_jacobi_t(M, r, 0, r, cc, Ul, sv, Vr, scratch, E.ctx->dstat, E.st, /*want_j=*/1));
     if (c.kU != PTR_NULL) E.chk(launch_copy_cols(Ul, r, Uo, ldU, r, cc, E.st));
     if (c.kS != PTR_NULL) E.chk(launch_copy_cols(sv, cc, So, ldS, cc, 1, E.st));
     if (c.kV != PTR_NULL) E.chk(launch_copy_cols(Vr, cc, Vo, ldV, cc, cc, E.st));

@@ -397,12 +397,13 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
 }
 
 int launch_jacobi_small(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
-                        DevStatus* status, cudaStream_t st);
+                        DevStatus* status, cudaStream_t st, int want_j);
 
+// want_j = 0: right vectors formed as B^T U S^-1 at the end (leading triplets only accurate)
 int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
-                    double* scratch, DevStatus* status, cudaStream_t st) {
+                    double* scratch, DevStatus* status, cudaStream_t st, int want_j) {
   if (c < 1 || c > 256 || r < c || r > 256) return RSVD_E_ARG;
-  if (r <= 64) return launch_jacobi_small(M, ldm, trans, r, c, Ul, S, Vr, status, st);
+  if (r <= 64) return launch_jacobi_small(M, ldm, trans, r, c, Ul, S, Vr, status, st, want_j);
   const int ce = c + (c & 1);
   const size_t wbytes = (size_t)r * ce * 8, jbytes = (size_t)ce * ce * 8;
   const size_t budget = 200 * 1024;
@@ -422,7 +423,7 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
 
 int launch_jacobi(const double* M, int64_t ldm, int r, int c, double* Ul, double* S, double* Vr, double* scratch,
                   DevStatus* status, cudaStream_t st) {
-  return launch_jacobi_t(M, ldm, 0, r, c, Ul, S, Vr, scratch, status, st);
+  return launch_jacobi_t(M, ldm, 0, r, c, Ul, S, Vr, scratch, status, st, 1);
 }
 
 // ------------------------------------------------------------------ small dense helpers
@@ -979,12 +980,14 @@ int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo
 // =====================================================================================
 namespace rsvd {
 
-template <int RW>  // rows per lane, r <= 8 RW; a column pair is handled by 8 lanes (4 pairs per warp)
+// LPP lanes per column pair (2, 4 or 8), RW rows per lane (r <= LPP * RW).  With LPP = 2 and
+// c <= 32 all pairs of a round fit in one warp: rounds synchronise with __syncwarp only.
+template <int LPP, int RW>
 __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__ M, int64_t ldm, int trans, int r,
                                                       int c, double* __restrict__ Ul, double* __restrict__ Sv,
                                                       double* __restrict__ Vr, double tol, int max_sweeps,
-                                                      DevStatus* status) {
-  constexpr int RS = 8 * RW;           // padded rows of W (stride of a column)
+                                                      int want_j, DevStatus* status) {
+  constexpr int RS = LPP * RW;         // padded rows of W (stride of a column)
   extern __shared__ double jac_dyn[];
   double* W = jac_dyn;                 // 64 x RS
   double* J = jac_dyn + 64 * RS;       // 64 x 64
@@ -992,8 +995,8 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
   __shared__ double sval[64];
   __shared__ int srank[64];
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int grp = tid >> 3, sl = tid & 7;          // pair group and its sub-lane
-  const unsigned gmask = 0xffu << (tid & 24);      // the 8 lanes of this group
+  const int grp = tid / LPP, sl = tid % LPP;       // pair group and its sub-lane
+  const unsigned gmask = (LPP == 32 ? 0xffffffffu : ((1u << LPP) - 1u)) << (tid & 31 & ~(LPP - 1));
   const int ce = c + (c & 1);
   const int npairs = ce >> 1;
   for (int e = tid; e < 64 * RS; e += nt) {
@@ -1022,10 +1025,10 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
   if (pj_on) {                                                   \
     double* jp = J + pj_p * 64;                                  \
     double* jq = J + pj_q * 64;                                  \
-    _Pragma("unroll") for (int k = 0; k < 8; ++k) {              \
-      const double u = jp[sl + 8 * k], v = jq[sl + 8 * k];       \
-      jp[sl + 8 * k] = pj_cs * u - pj_sn * v;                    \
-      jq[sl + 8 * k] = pj_sn * u + pj_cs * v;                    \
+    for (int k = sl; k < ce; k += LPP) {                         \
+      const double u = jp[k], v = jq[k];                         \
+      jp[k] = pj_cs * u - pj_sn * v;                             \
+      jq[k] = pj_sn * u + pj_cs * v;                             \
     }                                                            \
     pj_on = 0;                                                   \
   }
@@ -1039,21 +1042,30 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
         double* wp = W + p * RS;
         double* wq = W + q * RS;
         double x[RW], y[RW];
-        double a = 0.0, b = 0.0, cc = 0.0;
+        double a0 = 0.0, b0 = 0.0, c0 = 0.0, a1 = 0.0, b1 = 0.0, c1 = 0.0;
 #pragma unroll
         for (int t = 0; t < RW; ++t) {
-          x[t] = wp[sl + 8 * t];
-          y[t] = wq[sl + 8 * t];
-          a = fma(x[t], x[t], a);
-          b = fma(y[t], y[t], b);
-          cc = fma(x[t], y[t], cc);
+          x[t] = wp[sl + LPP * t];
+          y[t] = wq[sl + LPP * t];
         }
+#pragma unroll
+        for (int t = 0; t < RW; t += 2) {
+          a0 = fma(x[t], x[t], a0);
+          b0 = fma(y[t], y[t], b0);
+          c0 = fma(x[t], y[t], c0);
+          if (t + 1 < RW) {
+            a1 = fma(x[t + 1], x[t + 1], a1);
+            b1 = fma(y[t + 1], y[t + 1], b1);
+            c1 = fma(x[t + 1], y[t + 1], c1);
+          }
+        }
+        double a = a0 + a1, b = b0 + b1, cc = c0 + c1;
         RSVD_APPLY_PENDING_J();
 #pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-          a += __shfl_xor_sync(gmask, a, o, 8);
-          b += __shfl_xor_sync(gmask, b, o, 8);
-          cc += __shfl_xor_sync(gmask, cc, o, 8);
+        for (int o = LPP / 2; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(gmask, a, o, LPP);
+          b += __shfl_xor_sync(gmask, b, o, LPP);
+          cc += __shfl_xor_sync(gmask, cc, o, LPP);
         }
         if (cc * cc > tol2 * (a * b) && cc != 0.0) {
           rotated = 1;
@@ -1075,13 +1087,13 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
           const double sn = cs * t;
 #pragma unroll
           for (int k = 0; k < RW; ++k) {
-            wp[sl + 8 * k] = cs * x[k] - sn * y[k];
-            wq[sl + 8 * k] = sn * x[k] + cs * y[k];
+            wp[sl + LPP * k] = cs * x[k] - sn * y[k];
+            wq[sl + LPP * k] = sn * x[k] + cs * y[k];
           }
-          pj_p = p; pj_q = q; pj_cs = cs; pj_sn = sn; pj_on = 1;
+          pj_p = p; pj_q = q; pj_cs = cs; pj_sn = sn; pj_on = want_j;
         }
       }
-      __syncthreads();
+      if (nt <= 32) __syncwarp(); else __syncthreads();
     }
     if (!__syncthreads_or(rotated)) {
       converged = true;
@@ -1091,15 +1103,15 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
   }
   if (active) { RSVD_APPLY_PENDING_J(); }
   __syncthreads();
-  for (int j = grp; j < ce; j += (nt >> 3)) {
+  for (int j = grp; j < ce; j += (nt / LPP)) {
     double sacc = 0.0;
 #pragma unroll
     for (int t = 0; t < RW; ++t) {
-      const double v = W[j * RS + sl + 8 * t];
+      const double v = W[j * RS + sl + LPP * t];
       sacc = fma(v, v, sacc);
     }
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1) sacc += __shfl_xor_sync(gmask, sacc, o, 8);
+    for (int o = LPP / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(gmask, sacc, o, LPP);
     if (sl == 0) sval[j] = sqrt(sacc);
   }
   __syncthreads();
@@ -1121,10 +1133,30 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
       Ul[(int64_t)rk * r + i] = sj > 0.0 ? W[j * RS + i] / sj : 0.0;
     }
   }
-  for (int e = tid; e < c * ce; e += nt) {
-    const int i = e % c, j = e / c;
-    const int rk = srank[j];
-    if (rk < c) Vr[(int64_t)rk * c + i] = J[j * 64 + i];
+  if (want_j) {
+    for (int e = tid; e < c * ce; e += nt) {
+      const int i = e % c, j = e / c;
+      const int rk = srank[j];
+      if (rk < c) Vr[(int64_t)rk * c + i] = J[j * 64 + i];
+    }
+  } else {
+    // right vectors from the left ones: B = W J^T with W = U S  ->  J = B^T U S^-1 (B = the
+    // input as seen by the sweep).  Accurate to ~u sigma_1 / sigma_j, i.e. for the leading
+    // triplets the algorithms use (the rsvd_core_svd primitive accumulates J instead).
+    for (int e = tid; e < c * ce; e += nt) {
+      const int a = e % c, j = e / c;       // row a of the right vector of column j
+      const int rk = srank[j];
+      if (rk < c) {
+        const double sj = sval[j];
+        double sacc = 0.0;
+        if (sj > 0.0)
+          for (int i = 0; i < r; ++i) {
+            const double bia = trans ? M[(int64_t)i * ldm + a] : M[(int64_t)a * ldm + i];
+            sacc = fma(bia, W[j * RS + i], sacc);
+          }
+        Vr[(int64_t)rk * c + a] = sj > 0.0 ? sacc / (sj * sj) : 0.0;
+      }
+    }
   }
   for (int j = tid; j < ce; j += nt)
     if (srank[j] < c) Sv[srank[j]] = sval[j];
@@ -1135,21 +1167,24 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
 }
 
 int launch_jacobi_small(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
-                        DevStatus* status, cudaStream_t st) {
+                        DevStatus* status, cudaStream_t st, int want_j) {
   if (c < 1 || c > 64 || r < c || r > 64) return RSVD_E_ARG;
   const int ce = c + (c & 1);
-  const int threads = ((8 * std::max(1, ce / 2)) + 31) / 32 * 32;
   const double tol = 2.220446049250313e-16 * sqrt((double)r);
+  const int smem = (64 * 64 + 64 * 64) * 8;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_jacobi_small<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 32 + 64 * 64) * 8);
-    cudaFuncSetAttribute(k_jacobi_small<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (64 * 64 + 64 * 64) * 8);
+    cudaFuncSetAttribute(k_jacobi_small<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_jacobi_small<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
+  // 8 lanes per column pair (a single warp per round was measured 2.8x slower: too little
+  // latency hiding); r <= 32 -> 4 rows per lane, r <= 64 -> 8
+  const int threads = ((8 * (ce / 2)) + 31) / 32 * 32;
   if (r <= 32)
-    k_jacobi_small<4><<<1, threads, (64 * 32 + 64 * 64) * 8, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
+    k_jacobi_small<8, 4><<<1, threads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, want_j, status);
   else
-    k_jacobi_small<8><<<1, threads, (64 * 64 + 64 * 64) * 8, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
+    k_jacobi_small<8, 8><<<1, threads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, want_j, status);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 

@@ -9,7 +9,7 @@ int launch_cholqr_pass(const double*, int64_t, double*, int64_t, int64_t, int, c
 int cholqr_pass_ctas(int64_t rows);
 void read_phases(unsigned long long* out);
 void reset_phases();
-int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr, double* scratch, DevStatus* status, cudaStream_t st);
+int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr, double* scratch, DevStatus* status, cudaStream_t st, int want_j);
 }
 using namespace rsvd;
 int main(int argc, char** argv) {
@@ -51,9 +51,9 @@ int main(int argc, char** argv) {
   double *M, *U, *S, *V, *scr; cudaMalloc(&M, w * w * 8); cudaMalloc(&U, w * w * 8); cudaMalloc(&S, w * 8); cudaMalloc(&V, w * w * 8); cudaMalloc(&scr, 2 * 256 * 256 * 8);
   cudaMemcpy(M, m.data(), w * w * 8, cudaMemcpyHostToDevice);
   for (int t = 0; t < 2; ++t) {
-    for (int it = 0; it < 2; ++it) launch_jacobi_t(M, w, t, w, w, U, S, V, scr, st, s);
+    for (int it = 0; it < 2; ++it) launch_jacobi_t(M, w, t, w, w, U, S, V, scr, st, s, 0);
     cudaEventRecord(e0, s);
-    for (int it = 0; it < 10; ++it) launch_jacobi_t(M, w, t, w, w, U, S, V, scr, st, s);
+    for (int it = 0; it < 10; ++it) launch_jacobi_t(M, w, t, w, w, U, S, V, scr, st, s, 0);
     cudaEventRecord(e1, s); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     DevStatus hs; cudaMemcpy(&hs, st, sizeof hs, cudaMemcpyDeviceToHost);
