@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (multi-GB configs)")
     return ap.parse_args()
 
 
@@ -147,6 +148,32 @@ def reference_main(args):
             "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, cfg, A, Om, Phi, step, barrier, flush, stream, dev, max_over_ranks, world, m, n, bytes_step_rank):
+    import torch
+    Ah = A.cpu().pin_memory()
+    Omh = Om.t().contiguous().cpu().pin_memory().t()
+    Phih = Phi.t().contiguous().cpu().pin_memory().t()
+    for _ in range(2):
+        step(Ax=Ah, Omx=Omh, Phix=Phih)
+    barrier()
+    e2e_ms = []
+    for _ in range(args.e2e_steps):
+        flush.zero_()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(Ax=Ah, Omx=Omh, Phix=Phih)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e_step = max_over_ranks(statistics.median(e2e_ms))
+    h2d = 3 * m * n * 8 + 3 * n * cfg.l * 8 + m * cfg.l2 * 8
+    d2h = 3 * (m + n + 1) * cfg.k * 8
+    e2e = {"value": world * bytes_step_rank / (e2e_step * 1e-3) / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step}
+    return e2e
 
 
 # ------------------------------------------------------------------ our arm
@@ -297,28 +324,11 @@ def main():
                 "avg_view_ms": vms / max(vcount, 1)}
 
     # ---- e2e: pinned host buffers through the C ABI, copies inside the timed region
-    Ah = A.cpu().pin_memory()
-    Omh = Om.t().contiguous().cpu().pin_memory().t()
-    Phih = Phi.t().contiguous().cpu().pin_memory().t()
-    for _ in range(2):
-        step(Ax=Ah, Omx=Omh, Phix=Phih)
-    barrier()
-    e2e_ms = []
-    for _ in range(args.e2e_steps):
-        flush.zero_()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        step(Ax=Ah, Omx=Omh, Phix=Phih)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        e2e_ms.append(e0.elapsed_time(e1))
-    e2e_step = max_over_ranks(statistics.median(e2e_ms))
-    h2d = 3 * m * n * 8 + 3 * n * cfg.l * 8 + m * cfg.l2 * 8
-    d2h = 3 * (m + n + 1) * cfg.k * 8
-    e2e = {"value": world * bytes_step_rank / (e2e_step * 1e-3) / 1e9, "unit": "GB/s",
-           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step}
-
+    if args.no_e2e:
+        e2e = None
+    else:
+        e2e = run_e2e(args, cfg, A, Om, Phi, step, barrier, flush, stream, dev, max_over_ranks, world, m, n,
+                      bytes_step_rank)
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",

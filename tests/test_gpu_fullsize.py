@@ -12,7 +12,10 @@ it): properties that hold at any size, checked by the oracle on sampled rows cop
   * sigma_i(A) interlacing: the randomized sigma never exceeds the construction's
     (sigma_i + noise bound), and the top singular values match the construction
     sigma_i = i^-1.5 to the noise level 1e-8 (||G|| <~ sqrt(m) + sqrt(n));
-  * the normal-matrix mode returns S^2 of the same triplets.
+  * the normal-matrix mode returns S^2 of the same triplets;
+  * the single pass (its core is a least-squares estimate, not a projection): orthonormal
+    factors and leading values near the construction; its parity with the oracle is checked on
+    the same recipe and widths at 5000 x 20000 (test_c4_recipe_scaled_vs_oracle).
 """
 import numpy as np
 import pytest
@@ -100,8 +103,14 @@ def _check_c4_triplets(cfg, A, U, s, V, exact_av):
     assert np.all(np.diff(s) <= 0)
     sig = S.sigma_c4(cfg.rank)[:k]
     noise = cfg.noise * (np.sqrt(cfg.m) + np.sqrt(cfg.n)) * 1.1
-    assert np.all(s <= sig + noise)                         # Ritz values never exceed sigma_i(A)
-    np.testing.assert_allclose(s[:20], sig[:20], rtol=0, atol=noise + 1e-12 * sig[0])
+    if exact_av:
+        # projection methods: Ritz values never exceed sigma_i(A), top ones at the noise level
+        assert np.all(s <= sig + noise)
+        np.testing.assert_allclose(s[:20], sig[:20], rtol=0, atol=noise + 1e-12 * sig[0])
+    else:
+        # the single pass's core is a least-squares estimate, not a projection of A:
+        # no interlacing; its leading values are still accurate to the 1-view error level
+        np.testing.assert_allclose(s[:10], sig[:10], rtol=1e-2)
     rows = [0, 1, 4999, 25000, cfg.m - 1]
     Ar = _sampled_rows(A, rows)                             # oracle-side fp64 dot products
     AV = Ar @ V
@@ -125,8 +134,35 @@ def test_c4_krylov_v3_full_size(ctx, c4):
 def test_c4_single_pass_full_size(ctx, c4):
     cfg, A, Om, _, Phi = c4
     U, s, V, info = ctx.single_pass(A, cfg.k, cfg.p, cfg.l2, Om, Phi)
-    U, s, V = U, s, V
+    assert info.views == 1
     _check_c4_triplets(cfg, A, U, s, V, exact_av=False)
+
+
+@pytest.mark.parametrize("alg,v,inp", [("single_pass", 1, 0), ("krylov", 3, 0), ("subspace", 3, 1)])
+def test_c4_recipe_scaled_vs_oracle(ctx, alg, v, inp):
+    """C4's recipe and widths (k=100, p=20, l2=240: the single pass takes the two-view path for
+    l > 72) at 5000 x 20000, element-wise against the oracle."""
+    from paper_1804_07531_b200 import rsvd
+
+    cfg = S.CONFIGS["C4"]
+    A = S.make_matrix(cfg, 5000, 20000)
+    Om = S.gaussian_test_matrix(A.shape[0] if inp else A.shape[1], cfg.l, cfg,
+                                S.ROLE_OMEGA_M if inp else S.ROLE_OMEGA)
+    Phi = S.gaussian_test_matrix(A.shape[0], cfg.l2, cfg, S.ROLE_PHI)
+    Ad = torch.from_numpy(A).cuda()
+    if alg == "single_pass":
+        U, s, V, info = ctx.single_pass(Ad, cfg.k, cfg.p, cfg.l2, colmajor_dev(Om), colmajor_dev(Phi))
+        assert info.view_launches >= 2      # Y_c (w=120) + Y_r (w=240 in two 128-wide chunks)
+    elif alg == "krylov":
+        U, s, V, info = ctx.block_krylov(Ad, cfg.k, cfg.p, v, colmajor_dev(Om))
+    else:
+        U, s, V, info = ctx.subspace(Ad, cfg.k, cfg.p, v, colmajor_dev(Om), input=inp, flags=rsvd.RSVD_SQUARED)
+        s = s.sqrt()
+    Uo, so, Vo, _ = O.svd_of(A, alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi, transpose=bool(inp))
+    U, s, V = host(U), host(s), host(V)
+    assert np.max(np.abs(s - so) / so) <= 1e-10
+    assert O.projector_distance(U, Uo) <= 1e-9
+    assert O.projector_distance(V, Vo) <= 1e-9
 
 
 def test_c4_normal_mode_full_size(ctx, c4):
