@@ -44,6 +44,32 @@ struct FusedArgs {
   int grid_cap;
 };
 
+// fp32 A (view_tf32.cu): tcgen05 kind::tf32 views with the 3xTF32 split of both operands
+constexpr int kMaxW32 = 512;      // widths per launch (wider -> column chunks)
+struct ViewArgs32 {
+  int kind;           // VIEW_AX or VIEW_ATY
+  const float* A;     // row-major rows x n, lda (lda * 4 a multiple of 16 bytes)
+  int64_t rows, n, lda;
+  const float* Xhi;   // pre-split skinny operand, column-major [K x w] with ld ldx (K = n or rows)
+  const float* Xlo;
+  int64_t ldx;
+  int w;
+  double* out;        // fp64 partial slots, column-major (out_rows x w, ldo), slot s at out + s*slot_stride
+  int64_t ldo, slot_stride;
+  int S, KTS;
+  int grid_cap;
+};
+void plan_view_tf32(int kind, int64_t rows, int64_t n, int w, int grid_cap, int* S, int* KTS);
+int launch_view_tf32(const ViewArgs32& a, cudaStream_t st);
+// X (fp64 col-major rows x w, ld) -> tf32-rounded hi / lo parts (fp32 col-major, ld32)
+int launch_split_tf32(const double* X, int64_t ld, int64_t rows, int w, float* hi, float* lo, int64_t ld32,
+                      cudaStream_t st);
+// dtype conversions of column-major blocks (rows x cols)
+int launch_f32_to_f64(const float* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int cols,
+                      cudaStream_t st);
+int launch_f64_to_f32(const double* src, int64_t lds, float* dst, int64_t ldd, int64_t rows, int cols,
+                      cudaStream_t st);
+
 void plan_view(int kind, int64_t rows, int64_t n, int w, int grid_cap, int* S, int* KTS);
 int launch_view_ax(const ViewArgs& a, cudaStream_t st);
 int launch_view_aty(const ViewArgs& a, cudaStream_t st);

@@ -171,12 +171,23 @@ struct Exec {
   int view_launches = 0;
   // device views of the caller's arrays (resolved in prepare)
   const double* A = nullptr;
+  const float* A32 = nullptr;   // dtype == RSVD_F32: A itself (every internal block stays fp64)
+  int dtype = RSVD_F64;
   int64_t lda = 0, m = 0, n = 0;
-  // host-transfer plan (executed outside the graph)
-  struct H2D { void* dst; int64_t ldd; const void* src; int64_t lds; int64_t rows; int64_t cols; };
-  struct D2H { void* dst; int64_t ldd; const void* src; int64_t lds; int64_t rows; int64_t cols; };
+  // host-transfer plan (executed outside the graph); esz = element bytes (8, or 4 for fp32)
+  struct H2D { void* dst; int64_t ldd; const void* src; int64_t lds; int64_t rows; int64_t cols; int esz = 8; };
+  struct D2H { void* dst; int64_t ldd; const void* src; int64_t lds; int64_t rows; int64_t cols; int esz = 8; };
   std::vector<H2D> h2d;
   std::vector<D2H> d2h;
+  // fp32 outputs: fp64 result block -> fp32 staging block, converted at the end of the algorithm
+  struct Narrow { const double* src; int64_t lds; float* dst; int64_t ldd; int64_t rows; int cols; };
+  std::vector<Narrow> narrow;
+  float* alloc_f(int64_t n_el) { return reinterpret_cast<float*>(alloc((n_el + 1) / 2)); }
+  void flush_outputs() {
+    for (auto& t : narrow)
+      if (live()) chk(launch_f64_to_f32(t.src, t.lds, t.dst, t.ldd, t.rows, t.cols, st));
+    narrow.clear();
+  }
 
   Exec(rsvd_ctx* c, const Call& cl, bool d, char* b) : ctx(c), call(cl), dry(d), base(b), st(c->stream) {}
 
@@ -231,6 +242,10 @@ struct Exec {
   // ------------------------------------------------------------ matrix views (hot path)
   // from == SIDE_N: Y (side M) = A X;  from == SIDE_M: Y (side N) = A^T X (+ all-reduce)
   void view(Side from, const TS& X, const TS& Y) {
+    if (dtype == RSVD_F32) {
+      view32(from, X, Y);
+      return;
+    }
     const int w = X.w;
     for (int c0 = 0; c0 < w; c0 += kMaxWT * 8) {
       const int wc = std::min(kMaxWT * 8, w - c0);
@@ -258,6 +273,48 @@ struct Exec {
         int e0 = -1, e1 = -1;
         ev_record(&e0);
         chk(kind == VIEW_AX ? launch_view_ax(a, st) : launch_view_aty(a, st));
+        ev_record(&e1);
+        if (e0 >= 0) ev_pairs.push_back({e0, e1});
+        if (a.S > 1) chk(launch_slot_sum(slots, Y.ld, a.slot_stride, a.S, Y.rows, wc, dst, Y.ld, st));
+      }
+      release(mk);
+    }
+    if (from == SIDE_M && ctx->nranks > 1) allreduce(Y.p, Y.ld * Y.w);
+  }
+
+  // fp32 A: split X into tf32 hi / lo parts, tcgen05 3xTF32 view into fp64 partial slots
+  void view32(Side from, const TS& X, const TS& Y) {
+    const int w = X.w;
+    for (int c0 = 0; c0 < w; c0 += kMaxW32) {
+      const int wc = std::min(kMaxW32, w - c0);
+      const size_t mk = mark();
+      ViewArgs32 a;
+      a.kind = (from == SIDE_N) ? VIEW_AX : VIEW_ATY;
+      a.A = A32;
+      a.rows = m;
+      a.n = n;
+      a.lda = lda;
+      float* xh = alloc_f(X.ld * wc);
+      float* xl = alloc_f(X.ld * wc);
+      a.Xhi = xh;
+      a.Xlo = xl;
+      a.ldx = X.ld;
+      a.w = wc;
+      a.grid_cap = ctx->sms;
+      plan_view_tf32(a.kind, m, n, wc, ctx->sms, &a.S, &a.KTS);
+      double* dst = Y.p + (int64_t)c0 * Y.ld;
+      double* slots = (a.S == 1) ? dst : alloc((int64_t)a.S * Y.ld * wc);
+      a.out = slots;
+      a.ldo = Y.ld;
+      a.slot_stride = (int64_t)Y.ld * wc;
+      view_bytes += (double)m * n * 4.0;
+      view_flops += 2.0 * m * n * wc;
+      ++view_launches;
+      if (live()) {
+        chk(launch_split_tf32(X.p + (int64_t)c0 * X.ld, X.ld, X.rows, wc, xh, xl, X.ld, st));
+        int e0 = -1, e1 = -1;
+        ev_record(&e0);
+        chk(launch_view_tf32(a, st));
         ev_record(&e1);
         if (e0 >= 0) ev_pairs.push_back({e0, e1});
         if (a.S > 1) chk(launch_slot_sum(slots, Y.ld, a.slot_stride, a.S, Y.rows, wc, dst, Y.ld, st));
@@ -408,7 +465,13 @@ struct Exec {
   TS stage_in(Side s, const void* src, int64_t ld_user, int w, PtrKind kind) {
     (void)kind;
     TS t = new_ts(s, w);
-    h2d.push_back({t.p, t.ld, src, ld_user, t.rows, w});
+    if (dtype == RSVD_F32) {
+      float* f = alloc_f(t.ld * w);
+      h2d.push_back({f, t.ld, src, ld_user, t.rows, w, 4});
+      if (live()) chk(launch_f32_to_f64(f, t.ld, t.p, t.ld, t.rows, w, st));
+    } else {
+      h2d.push_back({t.p, t.ld, src, ld_user, t.rows, w});
+    }
     return t;
   }
   // where to write a caller output of rows x cols (col-major, ld): direct if device, else staging
@@ -416,7 +479,15 @@ struct Exec {
     const int64_t ld = round_up(std::max<int64_t>(rows, 1), 32);
     double* p = alloc(ld * cols);
     *ld_out = ld;
-    if (kind != PTR_NULL && user) d2h.push_back({user, ld_user, p, ld, rows, cols});
+    if (kind != PTR_NULL && user) {
+      if (dtype == RSVD_F32) {
+        float* f = alloc_f(ld * cols);
+        narrow.push_back({p, ld, f, ld, rows, cols});
+        d2h.push_back({user, ld_user, f, ld, rows, cols, 4});
+      } else {
+        d2h.push_back({user, ld_user, p, ld, rows, cols});
+      }
+    }
     return p;
   }
 };
@@ -536,7 +607,7 @@ void alg_single_pass(Exec& E) {
   TS Yc = E.new_ts(SIDE_M, l);
   TS Yr = E.new_ts(SIDE_N, l2);
   // ---- line 3: a) Y_c = A Omega  and  b) Y_r = A^* Phi  from one read of A
-  const bool fused_ok = (l <= kFusedMaxL) && ((l2 + 7) / 8 <= kFusedMaxL2T);
+  const bool fused_ok = (E.dtype == RSVD_F64) && (l <= kFusedMaxL) && ((l2 + 7) / 8 <= kFusedMaxL2T);
   if (fused_ok) {
     const size_t mk = E.mark();
     FusedArgs a;
@@ -680,6 +751,10 @@ void prim_orth(Exec& E) {
 void prim_fused(Exec& E) {
   const Call& c = E.call;
   const int l = c.w, l2 = c.l2;
+  if (E.dtype != RSVD_F64) {  // the fused fp32 sketch is not built: Alg. 7 runs it as two views
+    E.chk(RSVD_E_DTYPE);
+    return;
+  }
   TS Om = E.stage_in(SIDE_N, c.Om, c.ldom, l, c.kOm);
   TS Phi = E.stage_in(SIDE_M, c.Phi, c.ldphi, l2, c.kPhi);
   TS Yc = E.new_ts(SIDE_M, l), Yr = E.new_ts(SIDE_N, l2);
@@ -764,6 +839,7 @@ void run_alg(Exec& E) {
     case 13: prim_core(E); break;
     default: E.chk(RSVD_E_ARG);
   }
+  E.flush_outputs();
 }
 
 std::string call_key(const Call& c, const Exec& E, const rsvd_ctx* ctx) {
@@ -781,18 +857,24 @@ void bind_A(Exec& E, const Call& call) {
   E.m = call.A->m_local;
   E.n = call.A->n;
   E.lda = call.A->lda;
+  E.dtype = call.A->dtype;
+  const int esz = E.dtype == RSVD_F32 ? 4 : 8;
   const bool misaligned = call.kA == PTR_DEVICE &&
-                         ((reinterpret_cast<uintptr_t>(call.A->data) & 15) || ((call.A->lda * 8) & 15));
+                         ((reinterpret_cast<uintptr_t>(call.A->data) & 15) || ((call.A->lda * esz) & 15));
   if (call.kA == PTR_HOST || misaligned) {
     // host A, or a device A whose base / row stride violates TMA's 16-byte rule: copy into an
-    // aligned workspace block (row-major copy: width n doubles, height m rows)
-    E.lda = round_up(call.A->n, 16);
-    double* Ad = E.alloc(E.m * E.lda);
-    E.h2d.push_back({Ad, E.lda, call.A->data, call.A->lda, E.n, E.m});
-    E.A = Ad;
+    // aligned workspace block (row-major copy: width n elements, height m rows)
+    E.lda = round_up(call.A->n, 32);
+    void* Ad = E.alloc(E.m * E.lda * esz / 8);
+    E.h2d.push_back({Ad, E.lda, call.A->data, call.A->lda, E.n, E.m, esz});
+    E.A = static_cast<const double*>(Ad);
     E.a_restaged = 1;
   } else {
     E.A = static_cast<const double*>(call.A->data);
+  }
+  if (E.dtype == RSVD_F32) {
+    E.A32 = reinterpret_cast<const float*>(E.A);
+    E.A = nullptr;
   }
 }
 
@@ -844,8 +926,8 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
 
   auto do_h2d = [&](const std::vector<Exec::H2D>& lst) -> int {
     for (auto& t : lst)
-      if (cudaMemcpy2DAsync(t.dst, t.ldd * 8, t.src, t.lds * 8, t.rows * 8, t.cols, cudaMemcpyDefault, st) !=
-          cudaSuccess)
+      if (cudaMemcpy2DAsync(t.dst, t.ldd * t.esz, t.src, t.lds * t.esz, t.rows * t.esz, t.cols, cudaMemcpyDefault,
+                            st) != cudaSuccess)
         return RSVD_E_CUDA;
     return RSVD_OK;
   };
@@ -915,8 +997,8 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
   }
   if (rc == RSVD_OK) {
     for (auto& t : E.d2h)
-      if (cudaMemcpy2DAsync(t.dst, t.ldd * 8, t.src, t.lds * 8, t.rows * 8, t.cols, cudaMemcpyDefault, st) !=
-          cudaSuccess) {
+      if (cudaMemcpy2DAsync(t.dst, t.ldd * t.esz, t.src, t.lds * t.esz, t.rows * t.esz, t.cols, cudaMemcpyDefault,
+                            st) != cudaSuccess) {
         rc = RSVD_E_CUDA;
         break;
       }
@@ -970,8 +1052,7 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
 
 int check_mat(rsvd_ctx* ctx, const rsvd_mat* A) {
   if (!A || !A->data) { set_err(ctx, "A is NULL"); return RSVD_E_ARG; }
-  if (A->dtype == RSVD_F32) { set_err(ctx, "RSVD_F32 is not implemented in this release"); return RSVD_E_DTYPE; }
-  if (A->dtype != RSVD_F64) { set_err(ctx, "unknown dtype %d", A->dtype); return RSVD_E_DTYPE; }
+  if (A->dtype != RSVD_F64 && A->dtype != RSVD_F32) { set_err(ctx, "unknown dtype %d", A->dtype); return RSVD_E_DTYPE; }
   if (A->m < 1 || A->n < 1 || A->m_local < 0 || A->row0 < 0 || A->row0 + A->m_local > A->m) {
     set_err(ctx, "bad shape m=%lld n=%lld m_local=%lld row0=%lld", (long long)A->m, (long long)A->n,
             (long long)A->m_local, (long long)A->row0);
@@ -1242,7 +1323,7 @@ int rsvd_view(rsvd_ctx* ctx, const rsvd_mat* A, int trans, const void* X, int64_
   int r = check_mat(ctx, A);
   if (r == RSVD_OK) {
     const int64_t xr = trans ? A->m_local : A->n, yr = trans ? A->n : A->m_local;
-    if (w < 1 || w > 256 || !X || !Y || ldx < xr || ldy < yr) { set_err(ctx, "bad view arguments"); r = RSVD_E_ARG; }
+    if (w < 1 || w > 1024 || !X || !Y || ldx < xr || ldy < yr) { set_err(ctx, "bad view arguments"); r = RSVD_E_ARG; }
   }
   if (r) return r;
   Call c;

@@ -296,5 +296,5 @@ def test_argument_errors(ctx):
     with pytest.raises(rsvd.RsvdError):
         ctx.single_pass(A, 5, 5, 8, Om, colmajor_dev(np.zeros((50, 8))))  # l2 < l
     with pytest.raises(rsvd.RsvdError) as e:
-        ctx.subspace(dev(np.zeros((50, 40), dtype=np.float32)), 5, 5, 2, colmajor_dev(np.zeros((40, 10), np.float32)))
-    assert e.value.code == -2
+        ctx.subspace(dev(np.zeros((50, 40), dtype=np.float16)), 5, 5, 2, colmajor_dev(np.zeros((40, 10), np.float16)))
+    assert e.value.code == -2  # only fp64 and fp32 are defined
