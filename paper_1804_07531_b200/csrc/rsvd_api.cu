@@ -452,7 +452,7 @@ struct Exec {
 
   void core_svd(const double* M, int w, int trans, double* Ul, double* Sv, double* Vr) {
     const size_t mk = mark();
-    double* scratch = alloc(2 * 256 * 256);
+    double* scratch = alloc(2 * 512 * 512);
     if (live()) chk(launch_jacobi_t(M, w, trans, w, w, Ul, Sv, Vr, scratch, ctx->dstat, st, /*want_j=*/0));
     release(mk);
   }
@@ -819,7 +819,7 @@ void prim_core(Exec& E) {
   double* Ul = E.alloc((int64_t)r * cc);
   double* Vr = E.alloc((int64_t)cc * cc);
   double* sv = E.alloc(cc);
-  double* scratch = E.alloc(2 * 256 * 256);
+  double* scratch = E.alloc(2 * 512 * 512);
   if (E.live()) {
     E.chk(launch_jacobi_t(M, r, 0, r, cc, Ul, sv, Vr, scratch, E.ctx->dstat, E.st, /*want_j=*/1));
     if (c.kU != PTR_NULL) E.chk(launch_copy_cols(Ul, r, Uo, ldU, r, cc, E.st));
@@ -1074,7 +1074,7 @@ int common_checks(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p) {
   if (k < 1 || p < 0) { set_err(ctx, "need k >= 1 and p >= 0"); return RSVD_E_ARG; }
   const int64_t l = (int64_t)k + p;
   if (l > std::min(A->m, A->n)) { set_err(ctx, "k + p = %lld exceeds min(m, n)", (long long)l); return RSVD_E_ARG; }
-  if (l > 256) { set_err(ctx, "k + p > 256 is not supported"); return RSVD_E_ARG; }
+  if (l > 512) { set_err(ctx, "k + p > 512 is not supported"); return RSVD_E_ARG; }
   return RSVD_OK;
 }
 
@@ -1224,8 +1224,8 @@ static int algo_entry(int alg, rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, i
         const int64_t side_rows_c = (input == RSVD_INPUT_A) ? A->m : A->n;
         const int64_t side_rows_r = (input == RSVD_INPUT_A) ? A->n : A->m;
         const int64_t krows = (v % 2 == 0) ? side_rows_c : side_rows_r;
-        if (W > krows || W > 160) {
-          set_err(ctx, "Krylov basis width %lld exceeds its side (%lld rows) or 160", (long long)W,
+        if (W > krows || W > 512) {
+          set_err(ctx, "Krylov basis width %lld exceeds its side (%lld rows) or 512", (long long)W,
                   (long long)krows);
           r = RSVD_E_ARG;
         }
@@ -1280,7 +1280,7 @@ int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int
   if (lc == -1) lc = p;
   if (r == RSVD_OK) {
     if (l2 < k + p) { set_err(ctx, "l2 >= k + p required (P:663)"); r = RSVD_E_ARG; }
-    else if (l2 > std::min<int64_t>(A->m, 256)) { set_err(ctx, "l2 exceeds min(m, 256)"); r = RSVD_E_ARG; }
+    else if (l2 > std::min<int64_t>(A->m, 512)) { set_err(ctx, "l2 exceeds min(m, 512)"); r = RSVD_E_ARG; }
     else if (lc < 0 || lc > p) { set_err(ctx, "lc must be in [0, p] (P:663)"); r = RSVD_E_ARG; }
     else if (!Omega || !Phi) { set_err(ctx, "Omega/Phi NULL"); r = RSVD_E_ARG; }
     else if (ld_omega < A->n || ld_phi < A->m_local) { set_err(ctx, "ld_omega/ld_phi too small"); r = RSVD_E_ARG; }
@@ -1371,8 +1371,8 @@ int rsvd_view_fused(rsvd_ctx* ctx, const rsvd_mat* A, const void* Omega, int64_t
 
 int rsvd_orth(rsvd_ctx* ctx, int64_t rows, int w, void* Y, int64_t ldy, void* R, unsigned flags, rsvd_info* info) {
   if (!ctx) return RSVD_E_ARG;
-  if (rows < 1 || w < 1 || w > 160 || w > rows || !Y || ldy < rows) {
-    set_err(ctx, "bad orth arguments (1 <= w <= min(rows, 160))");
+  if (rows < 1 || w < 1 || w > 512 || w > rows || !Y || ldy < rows) {
+    set_err(ctx, "bad orth arguments (1 <= w <= min(rows, 512))");
     return RSVD_E_ARG;
   }
   Call c;
@@ -1389,8 +1389,8 @@ int rsvd_orth(rsvd_ctx* ctx, int64_t rows, int w, void* Y, int64_t ldy, void* R,
 int rsvd_core_svd(rsvd_ctx* ctx, int r, int cc, const void* M, int64_t ldm, void* U, void* S, void* V,
                   unsigned flags, rsvd_info* info) {
   if (!ctx) return RSVD_E_ARG;
-  if (cc < 1 || r < cc || r > 256 || !M || ldm < r) {
-    set_err(ctx, "bad core-svd arguments (1 <= c <= r <= 256)");
+  if (cc < 1 || r < cc || r > 512 || !M || ldm < r) {
+    set_err(ctx, "bad core-svd arguments (1 <= c <= r <= 512)");
     return RSVD_E_ARG;
   }
   Call c;

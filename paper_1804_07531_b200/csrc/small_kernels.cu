@@ -198,9 +198,13 @@ __global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, con
   }
 }
 
+int launch_chol_big(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
+                    DevStatus* status, cudaStream_t st, double shift_coef);
+
 int launch_chol_ref(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
                     DevStatus* status, cudaStream_t st, double shift_coef) {
-  if (w < 1 || w > kCholMaxW) return RSVD_E_ARG;
+  if (w > kCholMaxW) return launch_chol_big(G, ref, w, tol, R, Rinv, status, st, shift_coef);
+  if (w < 1) return RSVD_E_ARG;
   const size_t smem = (size_t)w * w * 8 + (size_t)w * 4 + 16;
   static bool attr = false;
   if (!attr) {
@@ -273,18 +277,19 @@ int launch_ts_gemm(const double* in, int64_t ldi, int64_t rows, int w, const dou
 // warp per pair) until every pair satisfies |w_p . w_q| <= tol sqrt(|w_p|^2 |w_q|^2).
 // M = (W S^-1) S J^T  ->  left vectors W_j / s_j, right vectors J, values s_j = |W_j|.
 constexpr int kJacThreads = 1024;
+constexpr int kJacMaxC = 512;
 __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict__ M, int64_t ldm, int trans, int r,
                                                         int c, double* __restrict__ Ul, double* __restrict__ Sv,
                                                         double* __restrict__ Vr, double* __restrict__ gW,
                                                         double* __restrict__ gJ, int w_in_smem, int j_in_smem,
-                                                        double tol, int max_sweeps, DevStatus* status) {
+                                                        double tol, int max_sweeps, int want_j, DevStatus* status) {
   extern __shared__ double sm[];
   const int ce = c + (c & 1);  // even number of columns (pad with a zero column)
   double* W = w_in_smem ? sm : gW;
   double* J = j_in_smem ? (sm + (w_in_smem ? (int64_t)r * ce : 0)) : gJ;
   __shared__ int rotated;
-  __shared__ double sval[256];
-  __shared__ int srank[256];
+  __shared__ double sval[kJacMaxC];
+  __shared__ int srank[kJacMaxC];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
   for (int e = tid; e < r * ce; e += nt) {
     const int i = e % r, j = e / r;
@@ -292,7 +297,8 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
     if (j < c) v = trans ? M[(int64_t)i * ldm + j] : M[(int64_t)j * ldm + i];
     W[(int64_t)j * r + i] = v;
   }
-  for (int e = tid; e < ce * ce; e += nt) J[e] = ((e % ce) == (e / ce)) ? 1.0 : 0.0;
+  if (want_j)
+    for (int e = tid; e < ce * ce; e += nt) J[e] = ((e % ce) == (e / ce)) ? 1.0 : 0.0;
   __syncthreads();
   int sweep = 0;
   bool converged = false;
@@ -337,12 +343,14 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
             wp[i] = cs * x - sn * y;
             wq[i] = sn * x + cs * y;
           }
-          double* jp = J + (int64_t)p * ce;
-          double* jq = J + (int64_t)q * ce;
-          for (int i = lane; i < ce; i += 32) {
-            const double x = jp[i], y = jq[i];
-            jp[i] = cs * x - sn * y;
-            jq[i] = sn * x + cs * y;
+          if (want_j) {
+            double* jp = J + (int64_t)p * ce;
+            double* jq = J + (int64_t)q * ce;
+            for (int i = lane; i < ce; i += 32) {
+              const double x = jp[i], y = jq[i];
+              jp[i] = cs * x - sn * y;
+              jq[i] = sn * x + cs * y;
+            }
           }
           if (lane == 0) rotated = 1;
         }
@@ -383,10 +391,28 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
       Ul[(int64_t)rk * r + i] = sj > 0.0 ? W[(int64_t)j * r + i] / sj : 0.0;
     }
   }
-  for (int e = tid; e < ce * ce; e += nt) {
-    const int i = e % ce, j = e / ce;
-    const int rk = srank[j];
-    if (rk < c && i < c) Vr[(int64_t)rk * c + i] = J[(int64_t)j * ce + i];
+  if (want_j) {
+    for (int e = tid; e < ce * ce; e += nt) {
+      const int i = e % ce, j = e / ce;
+      const int rk = srank[j];
+      if (rk < c && i < c) Vr[(int64_t)rk * c + i] = J[(int64_t)j * ce + i];
+    }
+  } else {
+    // right vectors from the left ones (B = W J^T, W = U S -> J = B^T U S^-1), as in k_jacobi_small
+    for (int e = tid; e < c * ce; e += nt) {
+      const int a = e % c, j = e / c;
+      const int rk = srank[j];
+      if (rk < c) {
+        const double sj = sval[j];
+        double sacc = 0.0;
+        if (sj > 0.0)
+          for (int i = 0; i < r; ++i) {
+            const double bia = trans ? M[(int64_t)i * ldm + a] : M[(int64_t)a * ldm + i];
+            sacc = fma(bia, W[(int64_t)j * r + i], sacc);
+          }
+        Vr[(int64_t)rk * c + a] = sj > 0.0 ? sacc / (sj * sj) : 0.0;
+      }
+    }
   }
   for (int j = tid; j < ce; j += nt)
     if (srank[j] < c) Sv[srank[j]] = sval[j];
@@ -402,10 +428,10 @@ int launch_jacobi_small(const double* M, int64_t ldm, int trans, int r, int c, d
 // want_j = 0: right vectors formed as B^T U S^-1 at the end (leading triplets only accurate)
 int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
                     double* scratch, DevStatus* status, cudaStream_t st, int want_j) {
-  if (c < 1 || c > 256 || r < c || r > 256) return RSVD_E_ARG;
+  if (c < 1 || c > kJacMaxC || r < c || r > kJacMaxC) return RSVD_E_ARG;
   if (r <= 64) return launch_jacobi_small(M, ldm, trans, r, c, Ul, S, Vr, status, st, want_j);
   const int ce = c + (c & 1);
-  const size_t wbytes = (size_t)r * ce * 8, jbytes = (size_t)ce * ce * 8;
+  const size_t wbytes = (size_t)r * ce * 8, jbytes = want_j ? (size_t)ce * ce * 8 : 0;
   const size_t budget = 200 * 1024;
   int w_in = wbytes <= budget ? 1 : 0;
   int j_in = (w_in ? wbytes + jbytes : jbytes) <= budget ? 1 : 0;
@@ -416,8 +442,8 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
     attr = true;
   }
   const double tol = 2.220446049250313e-16 * sqrt((double)r);  // LAPACK dgesvj's CTOL
-  k_jacobi<<<1, kJacThreads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, scratch + 256 * 256, w_in, j_in, tol,
-                                         60, status);
+  k_jacobi<<<1, kJacThreads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, scratch + kJacMaxC * kJacMaxC,
+                                         w_in, j_in, tol, 60, want_j, status);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 

@@ -116,6 +116,19 @@ def test_f32_algorithms_vs_oracle(ctx, alg, v, k, p):
     check32(U, s, V, Uo, so, Vo, A64)
 
 
+@pytest.mark.parametrize("alg,v", [("subspace", 2), ("subspace", 3), ("krylov", 3), ("krylov", 4)])
+def test_f32_c5_widths_vs_oracle(ctx, alg, v):
+    """C5's own k = 200, p = 50 (l = 250; Krylov v = 4 -> basis width 500) on a scaled C5 matrix."""
+    cfg, A = c5_scaled(2600, 2400)
+    k, p = cfg.k, cfg.p
+    Om = S.gaussian_test_matrix(A.shape[1], k + p, cfg, S.ROLE_OMEGA)
+    fn = ctx.subspace if alg == "subspace" else ctx.block_krylov
+    U, s, V, info = fn(dev(A), k, p, v, colmajor_dev(Om))
+    A64 = A.astype(np.float64)
+    Uo, so, Vo, _ = O.svd_of(A64, alg, k, p, v=v, Omega=Om.astype(np.float64))
+    check32(U, s, V, Uo, so, Vo, A64)
+
+
 def test_f32_host_arguments(ctx):
     """Host fp32 A / Omega and host outputs through the same ABI call."""
     cfg, A = c5_scaled(1500, 1200)

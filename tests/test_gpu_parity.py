@@ -89,7 +89,8 @@ def test_fused_view_bit_exact(ctx, shape, l, l2):
 
 # ------------------------------------------------------------------ orth and core SVD
 
-@pytest.mark.parametrize("rows,w", [(4000, 30), (1037, 20), (200000, 8), (777, 128), (5000, 160), (40, 40)])
+@pytest.mark.parametrize("rows,w", [(4000, 30), (1037, 20), (200000, 8), (777, 128), (5000, 160), (40, 40),
+                                    (3000, 200), (5000, 250), (2000, 500)])
 def test_orth_cholqr2(ctx, rows, w):
     Y = S.random_gaussian_matrix(rows, w, seed=rows + w) * np.logspace(0, -3, w)
     Q, R, info = ctx.orth(colmajor_dev(Y))
@@ -102,9 +103,10 @@ def test_orth_cholqr2(ctx, rows, w):
     assert info.rank_deficient_cols == 0
 
 
-def test_orth_rank_deficient(ctx):
+@pytest.mark.parametrize("w,r", [(24, 17), (250, 201)])
+def test_orth_rank_deficient(ctx, w, r):
     """Exactly rank-r input: the guarded Cholesky zeroes l - r columns; the kept Q spans range(Y)."""
-    rows, w, r = 3000, 24, 17
+    rows = 3000
     X, _ = S.exact_rank_factors(rows, w, r, seed=4)
     Y = X @ S.random_gaussian_matrix(r, w, seed=5)
     Q, R, info = ctx.orth(colmajor_dev(Y))
@@ -119,7 +121,7 @@ def test_orth_rank_deficient(ctx):
     assert np.linalg.norm(X - Qk @ (Qk.T @ X)) < 1e-10
 
 
-@pytest.mark.parametrize("w", [2, 3, 20, 30, 64, 70, 120, 140, 160])
+@pytest.mark.parametrize("w", [2, 3, 20, 30, 64, 70, 120, 140, 160, 200, 250, 301, 500])
 def test_core_svd_jacobi(ctx, w):
     Mx = np.triu(S.random_gaussian_matrix(w, w, seed=w)) * np.logspace(0, -4, w)[None, :]
     U, s, V, info = ctx.core_svd(colmajor_dev(Mx))
@@ -128,7 +130,7 @@ def test_core_svd_jacobi(ctx, w):
     np.testing.assert_allclose(s, so, rtol=1e-12, atol=1e-15 * so[0])
     assert np.linalg.norm((U * s) @ V.T - Mx) <= 1e-13 * np.linalg.norm(Mx)
     np.testing.assert_allclose(V.T @ V, np.eye(w), atol=1e-13)
-    assert 1 <= info.jacobi_sweeps < 30
+    assert 1 <= info.jacobi_sweeps < (30 if w <= 256 else 50)  # random graded triu, no QR preconditioning
 
 
 def test_core_svd_golden(ctx):
