@@ -76,6 +76,7 @@ enum {
 #define RSVD_SQUARED      1u   /* S := sigma^2  (normal-matrix estimate A^T A ~ V S V^T) */
 #define RSVD_NO_GRAPH     2u   /* enqueue kernels directly instead of replaying a CUDA graph    */
 #define RSVD_PROFILE      4u   /* record CUDA events around every view kernel (info->view_*)     */
+#define RSVD_CORE_NO_J    16u  /* rsvd_core_svd: V = M^T U S^-1 instead of accumulated rotations  */
 #define RSVD_SIM_SHARDS_SHIFT 8 /* debug: bits 8..15 = number of virtual row shards (loopback) */
 
 typedef struct {

@@ -1,0 +1,423 @@
+// CholeskyQR2 (and shifted CholeskyQR3) of a tall-skinny block in ONE launch on a thread-block
+// cluster: the qr of PAPER.md P:69, applied to the m x l and n x l blocks at P:149/151 (Alg. 2),
+// P:671 (Alg. 7) and P:910-922 (Alg. 9 Krylov blocks).  For blocks that fit in the cluster's
+// shared memory (w <= 64, rows x w x 8 <= ~3.4 MB: every C1/C2 block), it replaces the chain
+// pass / pass / apply kernels whose serial finishers dominated the small configurations.
+//
+//   each CTA: its row chunk of Y resident in shared memory for the whole call
+//   per pass:  [apply R_prev^-1 in place]  Gram partial (FP64 DMMA)  -> cluster barrier
+//              CTA 0: fixed-order DSMEM sum of the partials, guarded Cholesky G = R^T R and
+//              R^-1 (thread j owns column j, in registers)          -> cluster barrier
+//              every CTA copies R^-1 from CTA 0's shared memory (DSMEM)
+//   end:       apply the last R^-1, write Q over Y; R_out = R_2 R_1
+// Same numerics as the pass kernels (small_kernels.cu): rank guard d_j <= tol * ref_j zeroes
+// row j of R and column j of R^-1; the second pass takes the first-order closed form when
+// |G - I| <= 1e-8.  The kernel is compiled per padded width W (multiple of 8): the padding
+// columns of Y are zero and the padding block of G is set to the identity, so they factor
+// trivially, never count as deficient and never mix with the real columns.
+// Deterministic (fixed summation orders).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace rsvd {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kCluster = 16;
+constexpr int kSmemMax = 220 * 1024;
+
+// smem row stride for a W-wide tile: == 4 (mod 16) -> conflict-free m8n8k4 fragment loads
+__host__ __device__ constexpr int oc_ld(int W) { return W + ((4 - W % 16) + 16) % 16; }
+// fixed smem (doubles): Ri (W x ld), G (W x W), broadcast / pivot scratch
+__host__ __device__ constexpr int oc_fixed(int W) { return W * oc_ld(W) + W * W + 4 * 64; }
+__host__ __device__ constexpr int oc_rows_max(int W) {
+  return ((kSmemMax / 8 - oc_fixed(W)) / oc_ld(W)) / 8 * 8;
+}
+
+enum { PASS_SHIFT = 0, PASS_GUARD = 1, PASS_SECOND = 2 };
+
+#ifdef RSVD_ORTH_TIMING
+__device__ long long g_orth_t[32];
+#define OT(i) do { if (threadIdx.x == 0 && cg::this_cluster().block_rank() == 0) g_orth_t[i] = clock64(); } while (0)
+#else
+#define OT(i) do {} while (0)
+#endif
+
+// The factorisation runs with every thread of the CTA in uniform control flow (threads
+// j >= W only take part in the synchronisation): a warp that enters warp-synchronous code in a
+// diverged state executes every shuffle on the slow divergent path (measured ~100x slower).
+template <int W>
+__device__ __forceinline__ void csync() {
+  if (W <= 32) __syncwarp(); else asm volatile("bar.sync 1, 64;" ::: "memory");
+}
+// warps that run the factorisation (they do nothing else on CTA 0, so they enter it converged)
+template <int W>
+__host__ __device__ constexpr int chol_warps() { return W <= 32 ? 1 : 2; }
+
+// Guarded Cholesky of the W x W matrix G (smem, col-major, padding block = I), thread j owning
+// column j.  The column lives in registers as a shift register: before pivot p, c[i] holds the
+// updated entry G~(p + i, j), so every register index is a compile-time constant while the
+// pivot loop itself stays a compact runtime loop (straight-line code executed once is dominated
+// by instruction-cache misses).  R(p, j) goes to shared memory (G is overwritten: its upper
+// triangle becomes R), then thread j back-substitutes column j of R^-1 into Ri.
+// Writes R (global, col-major w x w, the real block).  Returns the deficient real columns.
+template <int W>
+__device__ int chol_inv_cols(double* G, int w, double shift, double tol, double* R, double* Ri, int ld, double* bc) {
+  const int j = threadIdx.x;  // column; threads j >= W only take part in the barriers
+  const bool act = j < W;
+  double* rrow = bc;          // R(p, .) broadcast, 2W slots (the upper W stay 0)
+  double* invd = bc + 128;    // 1 / R(p, p), 0 for a deficient pivot
+  double c[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) c[i] = act ? G[j * W + i] : 0.0;
+  const double sj = (j < w) ? shift : 0.0;
+  if (j < 2 * W && j >= W) rrow[j] = 0.0;
+  double refj = 0.0;
+#pragma unroll
+  for (int i = 0; i < W; ++i)
+    if (i == j) refj = c[i] + sj;  // G_jj + shift: the rank-guard reference
+  csync<W>();                      // everyone has read G before it is overwritten with R
+  int ndef = 0;
+  OT(25);
+  // rrow has 2W slots so that rrow[p + i] (i < W) never needs clamping; pivot values are
+  // broadcast through shared memory (immediate-offset loads, no shuffles)
+  for (int p = 0; p < W; ++p) {
+    if (j == p) {
+      c[0] += sj;
+      bc[192] = c[0];
+      bc[193] = refj;
+    }
+    csync<W>();
+    const double d = bc[192], rf = bc[193];
+    const bool def = !(d > tol * rf) || !(rf > 0.0);
+    ndef += (def && p < w) ? 1 : 0;
+    const double inv = def ? 0.0 : rsqrt(d);
+    const double rpj = (j > p) ? c[0] * inv : ((j == p) ? d * inv : 0.0);
+    if (act && j >= p) G[j * W + p] = def ? 0.0 : rpj;  // R(p, j)
+    if (j == p) invd[p] = inv;
+    if (act) rrow[j] = rpj;
+    csync<W>();
+    const double* rp = rrow + p;
+#pragma unroll
+    for (int i = 1; i < W; ++i) c[i - 1] = def ? c[i] : fma(-rp[i], rpj, c[i]);
+    c[W - 1] = 0.0;
+    csync<W>();
+  }
+  csync<W>();
+  OT(26);
+  // R (global, real block; lower part zero)
+  if (act)
+    for (int i = 0; i < W; ++i)
+      if (i < w && j < w) R[j * w + i] = (i <= j) ? G[j * W + i] : 0.0;
+  // X = R^-1, column j in Ri: x_j = 1/R_jj, x_i = -(sum_{i<k<=j} R(i,k) x_k) / R_ii, 0 for i > j
+  if (act) {
+    double* xj = Ri + j * ld;
+    for (int i = W - 1; i > j; --i) xj[i] = 0.0;
+    xj[j] = invd[j];
+    for (int i = j - 1; i >= 0; --i) {
+      double s0 = 0.0, s1 = 0.0;
+      int k = i + 1;
+      for (; k + 1 <= j; k += 2) {
+        s0 = fma(G[k * W + i], xj[k], s0);
+        s1 = fma(G[(k + 1) * W + i], xj[k + 1], s1);
+      }
+      if (k <= j) s0 = fma(G[k * W + i], xj[k], s0);
+      xj[i] = -(s0 + s1) * invd[i];
+    }
+  }
+  OT(27);
+  return ndef;
+}
+
+// O = Yc Ri for this warp's 8-row tiles (mt = warp, warp + 8, ...), up to 4 tiles at once
+// (4 * W/8 independent DMMA chains).  In place (out == nullptr) or to global column-major out.
+template <int W>
+__device__ __forceinline__ void apply_rinv(double* Yc, const double* Ri, int rpc, int warp, int g, int t4,
+                                           double* out, int64_t ldo, int nr, int w) {
+  constexpr int NT = W / 8, ld = oc_ld(W);
+  const int nmt = rpc / 8;
+  for (int mt0 = warp; mt0 < nmt; mt0 += 32) {
+    double oc[4][NT][2];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) oc[m][n][0] = oc[m][n][1] = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < W; k0 += 4) {
+      double b[NT];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) b[n] = Ri[(n * 8 + g) * ld + k0 + t4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int mt = mt0 + 8 * m;
+        if (mt < nmt) {
+          const double a = Yc[(mt * 8 + g) * ld + k0 + t4];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) dmma(oc[m][n][0], oc[m][n][1], a, b[n]);
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int mt = mt0 + 8 * m;
+      if (mt >= nmt) continue;
+      const int row = mt * 8 + g;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        const int c0 = n * 8 + 2 * t4;
+        if (out == nullptr) {
+          *reinterpret_cast<double2*>(Yc + row * ld + c0) = make_double2(oc[m][n][0], oc[m][n][1]);
+        } else if (row < nr) {
+          if (c0 < w) out[(int64_t)c0 * ldo + row] = oc[m][n][0];
+          if (c0 + 1 < w) out[(int64_t)(c0 + 1) * ldo + row] = oc[m][n][1];
+        }
+      }
+    }
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_orth_cluster(double* __restrict__ Y, int64_t ldy, int64_t rows, int w, int rpc, int shifted, double shift_coef,
+                   double* __restrict__ Rout, double* __restrict__ Rw /* 2 w*w global scratch */,
+                   DevStatus* status) {
+  constexpr int NT = W / 8, NTILES = NT * (NT + 1) / 2;
+  constexpr int ld = oc_ld(W);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int crank = (int)cluster.block_rank();
+  extern __shared__ double osm[];
+  double* Ri = osm;                 // W x ld  (R^-1, col-major: Ri[n*ld + k] = R^-1(k, n))
+  double* G = Ri + W * ld;          // W x W   (Gram partial, col-major; on CTA 0 the reduced G)
+  double* bc = G + W * W;           // 4*64    scratch of the factorisation
+  double* Yc = bc + 4 * 64;         // rpc x ld (this CTA's rows, row-major)
+  __shared__ int fast;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t r0 = (int64_t)crank * rpc;
+  const int nr = (int)max((int64_t)0, min((int64_t)rpc, rows - r0));
+  OT(0);
+  // ---- load this CTA's rows (W/8 x 8 independent loads in flight per thread)
+  for (int i = tid; i < rpc; i += kThreads) {
+#pragma unroll
+    for (int c0 = 0; c0 < W; c0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = (c0 + u < w && i < nr) ? Y[(int64_t)(c0 + u) * ldy + r0 + i] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) Yc[i * ld + c0 + u] = v[u];
+    }
+  }
+  __syncthreads();
+  OT(1);
+  const int npass = shifted ? 3 : 2;
+  double* R1 = Rw;             // R of the guard pass (global scratch, w x w)
+  double* Rc = Rw + w * w;     // R of the current pass
+  for (int ps = 0; ps < npass; ++ps) {
+    const int kind = shifted ? ps : ps + 1;  // PASS_SHIFT / PASS_GUARD / PASS_SECOND
+    if (ps > 0) {
+      apply_rinv<W>(Yc, Ri, rpc, warp, g, t4, nullptr, 0, 0, 0);
+      __syncthreads();
+    }
+    // ---- Gram partial: warp q owns upper 8x8 tiles q, q+8, ... over all rows, with 4 chains
+    //      per tile (k-steps interleaved), summed in a fixed order: no cross-warp reduction
+    {
+      constexpr int TPW = (NTILES + 7) / 8;  // tiles per warp (max)
+      int tbi[TPW], tbj[TPW];
+#pragma unroll
+      for (int q = 0; q < TPW; ++q) {
+        int u = warp + 8 * q, bi = 0;
+        if (u >= NTILES) u = NTILES - 1;
+        while (u >= NT - bi) { u -= NT - bi; ++bi; }
+        tbi[q] = bi;
+        tbj[q] = bi + u;
+      }
+      double ga[TPW][4][2];
+#pragma unroll
+      for (int q = 0; q < TPW; ++q)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) ga[q][r][0] = ga[q][r][1] = 0.0;
+      for (int k0 = 0; k0 < rpc; k0 += 16) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int kr = k0 + 4 * r + t4;
+          if (k0 + 4 * r < rpc) {
+#pragma unroll
+            for (int q = 0; q < TPW; ++q)
+              if (warp + 8 * q < NTILES)
+                dmma(ga[q][r][0], ga[q][r][1], Yc[kr * ld + tbi[q] * 8 + g], Yc[kr * ld + tbj[q] * 8 + g]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < TPW; ++q)
+        if (warp + 8 * q < NTILES) {
+          const int i = tbi[q] * 8 + g;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int jj = tbj[q] * 8 + 2 * t4 + h;
+            if (tbi[q] < tbj[q] || i <= jj)
+              G[jj * W + i] = (ga[q][0][h] + ga[q][1][h]) + (ga[q][2][h] + ga[q][3][h]);
+          }
+        }
+      __syncthreads();
+    }
+    OT(2 + 6 * ps);
+    cluster.sync();
+    OT(3 + 6 * ps);
+    if (crank == 0) {
+      // bookkeeping warps (>= CW): fixed-order DSMEM sum of the cluster's upper-triangle
+      // partials, identity padding, mirror, second-pass test; factorisation warps (< CW) wait
+      constexpr int CW = chol_warps<W>();
+      const int bt = tid - 32 * CW, nbt = kThreads - 32 * CW;
+      if (warp >= CW) {
+        for (int e = bt; e < W * W; e += nbt) {
+          const int i = e % W, jj = e / W;
+          if (i <= jj) {
+            double v[kCluster];
+#pragma unroll
+            for (int k = 0; k < kCluster; ++k) v[k] = (k < C) ? cluster.map_shared_rank(G, k)[e] : 0.0;
+            double sum = v[0];
+#pragma unroll
+            for (int k = 1; k < kCluster; ++k) sum += v[k];
+            if (jj >= w) sum = (i == jj) ? 1.0 : 0.0;
+            G[e] = sum;
+          }
+        }
+        if (bt == 0) fast = (kind == PASS_SECOND) ? 1 : 0;
+      }
+      __syncthreads();
+      if (warp >= CW)
+        for (int e = bt; e < W * W; e += nbt) {
+          const int i = e % W, jj = e / W;
+          if (i > jj) G[e] = G[i * W + jj];
+        }
+      __syncthreads();
+      OT(4 + 6 * ps);
+      if (kind == PASS_SECOND) {
+        if (warp >= CW)
+          for (int e = bt; e < W * W; e += nbt) {
+            const int i = e % W, k = e / W;
+            if (G[i * W + i] != 0.0 && G[k * W + k] != 0.0) {
+              const double E = G[e] - (i == k ? 1.0 : 0.0);
+              if (!(fabs(E) <= 1e-8)) fast = 0;
+            }
+          }
+        __syncthreads();
+      }
+      if (fast) {
+        if (warp >= CW)
+          for (int e = bt; e < W * W; e += nbt) {
+            const int i = e % W, k = e / W;
+            const bool dz = G[i * W + i] == 0.0 || G[k * W + k] == 0.0;
+            double r = 0.0, ri = 0.0;
+            if (!dz && i <= k) {
+              const double E = G[e] - (i == k ? 1.0 : 0.0);
+              r = (i == k) ? 1.0 + 0.5 * E : E;
+              ri = (i == k) ? 1.0 - 0.5 * E : -E;
+            }
+            if (i < w && k < w) Rc[k * w + i] = r;
+            Ri[k * ld + i] = ri;
+          }
+      } else if (warp < CW) {
+        double shift = 0.0;
+        if (kind == PASS_SHIFT) {
+          double tr = 0.0;
+          for (int jj = 0; jj < w; ++jj) tr += G[jj * W + jj];
+          shift = shift_coef * tr;
+        }
+        const double tol = (kind == PASS_SHIFT) ? 0.0 : 1e-12;
+        double* Rdst = (kind == PASS_GUARD) ? R1 : Rc;
+        const int cnt = chol_inv_cols<W>(G, w, shift, tol, Rdst, Ri, ld, bc);
+        if (tid == 0 && kind == PASS_GUARD && cnt && status) atomicAdd(&status->deficient, cnt);
+      }
+      __syncthreads();
+      OT(5 + 6 * ps);
+    }
+    cluster.sync();
+    OT(6 + 6 * ps);
+    if (crank != 0) {
+      const double* src = cluster.map_shared_rank(Ri, 0);
+      for (int e = tid; e < W * ld; e += kThreads) Ri[e] = src[e];
+    }
+    __syncthreads();
+  }
+  OT(20);
+  // ---- final apply, write Q over Y
+  apply_rinv<W>(Yc, Ri, rpc, warp, g, t4, Y + r0, ldy, nr, w);
+  // R_out = R_2 R_1 (upper triangular product), CTA 0
+  if (Rout && crank == 0) {
+    for (int e = tid; e < w * w; e += kThreads) {
+      const int i = e % w, k = e / w;
+      double s = 0.0;
+      for (int q = i; q <= k; ++q) s = fma(Rc[q * w + i], R1[k * w + q], s);
+      Rout[e] = (i <= k) ? s : 0.0;
+    }
+  }
+  OT(21);
+  // keep every CTA's shared memory alive until the DSMEM reads of CTA 0's Ri are done
+  cluster.sync();
+  OT(22);
+}
+
+template <int W>
+int launch_w(double* Y, int64_t ldy, int64_t rows, int w, int shifted, double shift_coef, double* Rout, double* Rw,
+             DevStatus* status, cudaStream_t st) {
+  int rpc = (int)((rows + kCluster - 1) / kCluster);
+  rpc = (rpc + 7) / 8 * 8;
+  if (rpc > oc_rows_max(W)) return RSVD_E_ARG;
+  const size_t smem = (size_t)(oc_fixed(W) + rpc * oc_ld(W)) * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_orth_cluster<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+    cudaFuncSetAttribute(k_orth_cluster<W>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kCluster);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kCluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_orth_cluster<W>, Y, ldy, rows, w, rpc, shifted, shift_coef, Rout, Rw,
+                                     status);
+  return e == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+}  // namespace
+
+// true if the block fits the one-launch cluster path
+bool orth_cluster_fits(int64_t rows, int w) {
+  if (w < 1 || w > 64) return false;
+  static constexpr int rmax[8] = {oc_rows_max(8),  oc_rows_max(16), oc_rows_max(24), oc_rows_max(32),
+                                  oc_rows_max(40), oc_rows_max(48), oc_rows_max(56), oc_rows_max(64)};
+  return rows <= (int64_t)kCluster * rmax[(w + 7) / 8 - 1];
+}
+
+int launch_orth_cluster(double* Y, int64_t ldy, int64_t rows, int w, int shifted, double shift_coef, double* Rout,
+                        double* Rw, DevStatus* status, cudaStream_t st) {
+  if (!orth_cluster_fits(rows, w)) return RSVD_E_ARG;
+  switch ((w + 7) / 8) {
+    case 1: return launch_w<8>(Y, ldy, rows, w, shifted, shift_coef, Rout, Rw, status, st);
+    case 2: return launch_w<16>(Y, ldy, rows, w, shifted, shift_coef, Rout, Rw, status, st);
+    case 3: return launch_w<24>(Y, ldy, rows, w, shifted, shift_coef, Rout, Rw, status, st);
+    case 4: return launch_w<32>(Y, ldy, rows, w, shifted, shift_coef, Rout, Rw, status, st);
+    case 5: return launch_w<40>(Y, ldy, rows, w, shifted, shift_coef, Rout, Rw, status, st);
+    case 6: return launch_w<48>(Y, ldy, rows, w, shifted, shift_coef, Rout, Rw, status, st);
+    case 7: return launch_w<56>(Y, ldy, rows, w, shifted, shift_coef, Rout, Rw, status, st);
+    default: return launch_w<64>(Y, ldy, rows, w, shifted, shift_coef, Rout, Rw, status, st);
+  }
+}
+
+}  // namespace rsvd

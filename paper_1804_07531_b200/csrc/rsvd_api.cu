@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -29,6 +30,9 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
 int launch_diag(const double* G, int w, double* d, cudaStream_t st);
 int probe_peaks(int sms, cudaStream_t st, double* dmma_tflops, double* read_gbs);
 int cholqr_pass_ctas(int64_t rows);
+bool orth_cluster_fits(int64_t rows, int w);
+int launch_orth_cluster(double* Y, int64_t ldy, int64_t rows, int w, int shifted, double shift_coef, double* Rout,
+                        double* Rw, DevStatus* status, cudaStream_t st);
 int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo, int64_t rows, int w,
                        const double* Rin, double* slots, unsigned* counter, double tol, double shift_coef,
                        int second_pass, double* R, double* Rinv, DevStatus* status, cudaStream_t st);
@@ -104,6 +108,12 @@ void set_err(rsvd_ctx* c, const char* fmt, ...) {
 }
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// debug / A-B switches read once from the environment (e.g. RSVD_NO_ORTH_CLUSTER=1)
+bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] && v[0] != '0';
+}
 
 enum Side { SIDE_M = 0, SIDE_N = 1 };
 
@@ -388,6 +398,14 @@ struct Exec {
     (void)s;
     const int w = Y.w;
     const size_t mk = mark();
+    if (orth_cluster_fits(Y.rows, w) && !getenv_flag("RSVD_NO_ORTH_CLUSTER")) {
+      // the whole CholeskyQR2 / shifted CholeskyQR3 in one cluster launch (Y resident in smem)
+      double* Rw = alloc(2 * (int64_t)w * w);
+      const double coef = 11.0 * ((double)Y.rows * w + (double)w * (w + 1)) * 1.1102230246251565e-16;
+      if (live()) chk(launch_orth_cluster(Y.p, Y.ld, Y.rows, w, shifted ? 1 : 0, coef, R_out, Rw, ctx->dstat, st));
+      release(mk);
+      return;
+    }
     const int G = cholqr_pass_ctas(Y.rows);
     double* slots = alloc((int64_t)G * w * w);
     double* R0 = alloc((int64_t)w * w);
@@ -452,7 +470,7 @@ struct Exec {
 
   void core_svd(const double* M, int w, int trans, double* Ul, double* Sv, double* Vr) {
     const size_t mk = mark();
-    double* scratch = alloc(2 * 512 * 512);
+    double* scratch = alloc(2 * 512 * 512 + 4096);
     if (live()) chk(launch_jacobi_t(M, w, trans, w, w, Ul, Sv, Vr, scratch, ctx->dstat, st, /*want_j=*/0));
     release(mk);
   }
@@ -819,9 +837,10 @@ void prim_core(Exec& E) {
   double* Ul = E.alloc((int64_t)r * cc);
   double* Vr = E.alloc((int64_t)cc * cc);
   double* sv = E.alloc(cc);
-  double* scratch = E.alloc(2 * 512 * 512);
+  double* scratch = E.alloc(2 * 512 * 512 + 4096);
   if (E.live()) {
-    E.chk(launch_jacobi_t(M, r, 0, r, cc, Ul, sv, Vr, scratch, E.ctx->dstat, E.st, /*want_j=*/1));
+    E.chk(launch_jacobi_t(M, r, 0, r, cc, Ul, sv, Vr, scratch, E.ctx->dstat, E.st,
+                           (c.flags & RSVD_CORE_NO_J) ? 0 : 1));
     if (c.kU != PTR_NULL) E.chk(launch_copy_cols(Ul, r, Uo, ldU, r, cc, E.st));
     if (c.kS != PTR_NULL) E.chk(launch_copy_cols(sv, cc, So, ldS, cc, 1, E.st));
     if (c.kV != PTR_NULL) E.chk(launch_copy_cols(Vr, cc, Vo, ldV, cc, cc, E.st));

@@ -424,12 +424,15 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
 
 int launch_jacobi_small(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
                         DevStatus* status, cudaStream_t st, int want_j);
+int launch_jacobi_cluster(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
+                          double* scratch, DevStatus* status, cudaStream_t st, int want_j);
 
 // want_j = 0: right vectors formed as B^T U S^-1 at the end (leading triplets only accurate)
 int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
                     double* scratch, DevStatus* status, cudaStream_t st, int want_j) {
   if (c < 1 || c > kJacMaxC || r < c || r > kJacMaxC) return RSVD_E_ARG;
   if (r <= 64) return launch_jacobi_small(M, ldm, trans, r, c, Ul, S, Vr, status, st, want_j);
+  if (c > 128) return launch_jacobi_cluster(M, ldm, trans, r, c, Ul, S, Vr, scratch, status, st, want_j);
   const int ce = c + (c & 1);
   const size_t wbytes = (size_t)r * ce * 8, jbytes = want_j ? (size_t)ce * ce * 8 : 0;
   const size_t budget = 200 * 1024;

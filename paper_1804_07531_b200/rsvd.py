@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "librsvd.so")
 RSVD_F32, RSVD_F64 = 1, 2
 RSVD_INPUT_A, RSVD_INPUT_AT = 0, 1
 RSVD_GOAL_SVD, RSVD_GOAL_LEFT, RSVD_GOAL_RIGHT, RSVD_GOAL_NORMAL = 0, 1, 2, 3
-RSVD_SQUARED, RSVD_NO_GRAPH, RSVD_PROFILE = 1, 2, 4
+RSVD_SQUARED, RSVD_NO_GRAPH, RSVD_PROFILE, RSVD_CORE_NO_J = 1, 2, 4, 16
 ERR = {0: "RSVD_OK", -1: "RSVD_E_ARG", -2: "RSVD_E_DTYPE", -3: "RSVD_E_CUDA", -4: "RSVD_E_NCCL",
        -5: "RSVD_E_NOMEM", -6: "RSVD_E_NUMERIC", -7: "RSVD_E_STATE"}
 
