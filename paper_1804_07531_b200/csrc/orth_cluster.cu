@@ -109,24 +109,13 @@ __device__ int chol_inv_cols(double* G, int w, double shift, double tol, double*
   }
   csync<W>();
   OT(26);
-  // R (global, real block; lower part zero)
-  if (act)
-    for (int i = 0; i < W; ++i)
-      if (i < w && j < w) R[j * w + i] = (i <= j) ? G[j * W + i] : 0.0;
-  // X = R^-1, column j in Ri: x_j = 1/R_jj, x_i = -(sum_{i<k<=j} R(i,k) x_k) / R_ii, 0 for i > j
+  // R (global, real block; lower part zero) and, for the row solves, R row-major with
+  // 1 / R_jj on the diagonal (0 for a deficient pivot) in Ri
   if (act) {
-    double* xj = Ri + j * ld;
-    for (int i = W - 1; i > j; --i) xj[i] = 0.0;
-    xj[j] = invd[j];
-    for (int i = j - 1; i >= 0; --i) {
-      double s0 = 0.0, s1 = 0.0;
-      int k = i + 1;
-      for (; k + 1 <= j; k += 2) {
-        s0 = fma(G[k * W + i], xj[k], s0);
-        s1 = fma(G[(k + 1) * W + i], xj[k + 1], s1);
-      }
-      if (k <= j) s0 = fma(G[k * W + i], xj[k], s0);
-      xj[i] = -(s0 + s1) * invd[i];
+    for (int i = 0; i < W; ++i) {
+      const double r = (i <= j) ? G[j * W + i] : 0.0;
+      if (i < w && j < w) R[j * w + i] = r;
+      Ri[i * ld + j] = (i == j) ? invd[j] : r;
     }
   }
   OT(27);
@@ -181,6 +170,76 @@ __device__ __forceinline__ void apply_rinv(double* Yc, const double* Ri, int rpc
   }
 }
 
+// Gram partial G (upper triangle, col-major W x W) = Yc^T Yc over this CTA's rpc rows: warp q
+// owns upper 8x8 tiles q, q+8, ... over all rows, with 4 DMMA chains per tile (k-steps
+// interleaved) summed in a fixed order: no cross-warp reduction.
+// Yc <- Yc R^-1 by forward substitution, one thread per row (q R = y): Rm is R row-major
+// (Rm[i*ld + k] = R(i, k)) with 1/R_jj on the diagonal.  The row lives in registers as a shift
+// register (y[0] = the entry being solved), so the column loop stays compact.  Reads past
+// row W-1 of Rm land in G (the next buffer): those values multiply padding entries only.
+template <int W>
+__device__ __forceinline__ void solve_rows(double* Yc, const double* Rm, int rpc, int tid) {
+  constexpr int ld = oc_ld(W);
+  for (int r = tid; r < rpc; r += kThreads) {
+    double* yr = Yc + r * ld;
+    double y[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) y[i] = yr[i];
+    for (int j = 0; j < W; ++j) {
+      const double* rj = Rm + j * ld + j;  // R(j, j + i) at rj[i]
+      const double q = y[0] * rj[0];
+      yr[j] = q;
+#pragma unroll
+      for (int i = 1; i < W; ++i) y[i - 1] = fma(-q, rj[i], y[i]);
+      y[W - 1] = 0.0;
+    }
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void gram_tiles(const double* Yc, int rpc, double* G, int warp, int g, int t4) {
+  constexpr int NT = W / 8, NTILES = NT * (NT + 1) / 2, ld = oc_ld(W);
+  constexpr int TPW = (NTILES + 7) / 8;  // tiles per warp (max)
+  int tbi[TPW], tbj[TPW];
+#pragma unroll
+  for (int q = 0; q < TPW; ++q) {
+    int u = warp + 8 * q, bi = 0;
+    if (u >= NTILES) u = NTILES - 1;
+    while (u >= NT - bi) { u -= NT - bi; ++bi; }
+    tbi[q] = bi;
+    tbj[q] = bi + u;
+  }
+  double ga[TPW][4][2];
+#pragma unroll
+  for (int q = 0; q < TPW; ++q)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) ga[q][r][0] = ga[q][r][1] = 0.0;
+  for (int k0 = 0; k0 < rpc; k0 += 16) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int kr = k0 + 4 * r + t4;
+      if (k0 + 4 * r < rpc) {
+#pragma unroll
+        for (int q = 0; q < TPW; ++q)
+          if (warp + 8 * q < NTILES)
+            dmma(ga[q][r][0], ga[q][r][1], Yc[kr * ld + tbi[q] * 8 + g], Yc[kr * ld + tbj[q] * 8 + g]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < TPW; ++q)
+    if (warp + 8 * q < NTILES) {
+      const int i = tbi[q] * 8 + g;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int jj = tbj[q] * 8 + 2 * t4 + h;
+        if (tbi[q] < tbj[q] || i <= jj)
+          G[jj * W + i] = (ga[q][0][h] + ga[q][1][h]) + (ga[q][2][h] + ga[q][3][h]);
+      }
+    }
+  __syncthreads();
+}
+
 template <int W>
 __global__ void __launch_bounds__(kThreads, 1)
     k_orth_cluster(double* __restrict__ Y, int64_t ldy, int64_t rows, int w, int rpc, int shifted, double shift_coef,
@@ -197,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* bc = G + W * W;           // 4*64    scratch of the factorisation
   double* Yc = bc + 4 * 64;         // rpc x ld (this CTA's rows, row-major)
   __shared__ int fast;
+  __shared__ int mode;   // how Ri is to be applied: 0 = explicit R^-1 (DMMA), 1 = R (row solve)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t r0 = (int64_t)crank * rpc;
@@ -221,52 +281,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int ps = 0; ps < npass; ++ps) {
     const int kind = shifted ? ps : ps + 1;  // PASS_SHIFT / PASS_GUARD / PASS_SECOND
     if (ps > 0) {
-      apply_rinv<W>(Yc, Ri, rpc, warp, g, t4, nullptr, 0, 0, 0);
+      if (mode) solve_rows<W>(Yc, Ri, rpc, tid);
+      else apply_rinv<W>(Yc, Ri, rpc, warp, g, t4, nullptr, 0, 0, 0);
       __syncthreads();
     }
-    // ---- Gram partial: warp q owns upper 8x8 tiles q, q+8, ... over all rows, with 4 chains
-    //      per tile (k-steps interleaved), summed in a fixed order: no cross-warp reduction
-    {
-      constexpr int TPW = (NTILES + 7) / 8;  // tiles per warp (max)
-      int tbi[TPW], tbj[TPW];
-#pragma unroll
-      for (int q = 0; q < TPW; ++q) {
-        int u = warp + 8 * q, bi = 0;
-        if (u >= NTILES) u = NTILES - 1;
-        while (u >= NT - bi) { u -= NT - bi; ++bi; }
-        tbi[q] = bi;
-        tbj[q] = bi + u;
-      }
-      double ga[TPW][4][2];
-#pragma unroll
-      for (int q = 0; q < TPW; ++q)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) ga[q][r][0] = ga[q][r][1] = 0.0;
-      for (int k0 = 0; k0 < rpc; k0 += 16) {
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int kr = k0 + 4 * r + t4;
-          if (k0 + 4 * r < rpc) {
-#pragma unroll
-            for (int q = 0; q < TPW; ++q)
-              if (warp + 8 * q < NTILES)
-                dmma(ga[q][r][0], ga[q][r][1], Yc[kr * ld + tbi[q] * 8 + g], Yc[kr * ld + tbj[q] * 8 + g]);
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < TPW; ++q)
-        if (warp + 8 * q < NTILES) {
-          const int i = tbi[q] * 8 + g;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int jj = tbj[q] * 8 + 2 * t4 + h;
-            if (tbi[q] < tbj[q] || i <= jj)
-              G[jj * W + i] = (ga[q][0][h] + ga[q][1][h]) + (ga[q][2][h] + ga[q][3][h]);
-          }
-        }
-      __syncthreads();
-    }
+    gram_tiles<W>(Yc, rpc, G, warp, g, t4);
     OT(2 + 6 * ps);
     cluster.sync();
     OT(3 + 6 * ps);
@@ -289,7 +308,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             G[e] = sum;
           }
         }
-        if (bt == 0) fast = (kind == PASS_SECOND) ? 1 : 0;
+        if (bt == 0) {
+          fast = (kind == PASS_SECOND) ? 1 : 0;
+          mode = (kind == PASS_SECOND) ? 0 : 1;
+        }
       }
       __syncthreads();
       if (warp >= CW)
@@ -334,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const double tol = (kind == PASS_SHIFT) ? 0.0 : 1e-12;
         double* Rdst = (kind == PASS_GUARD) ? R1 : Rc;
         const int cnt = chol_inv_cols<W>(G, w, shift, tol, Rdst, Ri, ld, bc);
+        if (tid == 0) mode = 1;
         if (tid == 0 && kind == PASS_GUARD && cnt && status) atomicAdd(&status->deficient, cnt);
       }
       __syncthreads();
@@ -344,19 +367,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (crank != 0) {
       const double* src = cluster.map_shared_rank(Ri, 0);
       for (int e = tid; e < W * ld; e += kThreads) Ri[e] = src[e];
+      if (tid == 0) mode = *cluster.map_shared_rank(&mode, 0);
     }
     __syncthreads();
   }
   OT(20);
   // ---- final apply, write Q over Y
-  apply_rinv<W>(Yc, Ri, rpc, warp, g, t4, Y + r0, ldy, nr, w);
+  if (mode) {
+    solve_rows<W>(Yc, Ri, rpc, tid);
+    __syncthreads();
+    for (int i = tid; i < nr; i += kThreads)
+      for (int c = 0; c < w; ++c) Y[(int64_t)c * ldy + r0 + i] = Yc[i * ld + c];
+  } else {
+    apply_rinv<W>(Yc, Ri, rpc, warp, g, t4, Y + r0, ldy, nr, w);
+  }
   // R_out = R_2 R_1 (upper triangular product), CTA 0
   if (Rout && crank == 0) {
+    // stage R_2 in shared memory (G is free on CTA 0 now), R_1 is read from global (L1/L2)
+    __syncthreads();
+    const double* R1s = R1;
+    for (int e = tid; e < w * w; e += kThreads) G[e] = Rc[e];
+    __syncthreads();
     for (int e = tid; e < w * w; e += kThreads) {
       const int i = e % w, k = e / w;
-      double s = 0.0;
-      for (int q = i; q <= k; ++q) s = fma(Rc[q * w + i], R1[k * w + q], s);
-      Rout[e] = (i <= k) ? s : 0.0;
+      double sa[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int q = i; q <= k; ++q) sa[q & 3] = fma(G[q * w + i], R1s[k * w + q], sa[q & 3]);
+      Rout[e] = (i <= k) ? (sa[0] + sa[1]) + (sa[2] + sa[3]) : 0.0;
     }
   }
   OT(21);

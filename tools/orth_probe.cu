@@ -5,7 +5,9 @@
 #include <vector>
 using namespace rsvd;
 int chol_alone_main();
+int gram_alone_main();
 int main(int argc, char** argv) {
+  if (argc > 4) return gram_alone_main();
   if (argc > 3) return chol_alone_main();
   const int rows = argc > 1 ? atoi(argv[1]) : 4000, w = argc > 2 ? atoi(argv[2]) : 30;
   const int ld = (rows + 31) / 32 * 32;
@@ -54,6 +56,36 @@ int chol_alone_main() {
     k_chol_alone<32><<<1, 256>>>(G, 30, R, t); long long ht; cudaMemcpy(&ht, t, 8, cudaMemcpyDeviceToHost);
     long long tt[32]; cudaMemcpyFromSymbol(tt, g_orth_t, sizeof(tt));
     printf("standalone chol+inv W=32: %lld cycles (pivots %lld, R out %lld, inverse %lld)\n", ht, tt[26]-tt[25], 0LL, tt[27]-tt[26]);
+  }
+  return 0;
+}
+namespace rsvd { namespace {
+template <int W>
+__global__ void k_gram_alone(int rpc, long long* t, double* out) {
+  extern __shared__ double sm[];
+  double* G = sm;
+  double* Yc = sm + W * W;
+  constexpr int ld = oc_ld(W);
+  for (int e = threadIdx.x; e < rpc * ld; e += blockDim.x) Yc[e] = 1e-3 * (e % 97);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  long long t0 = clock64();
+  gram_tiles<W>(Yc, rpc, G, warp, lane >> 2, lane & 3);
+  long long t1 = clock64();
+  apply_rinv<W>(Yc, G, rpc, warp, lane >> 2, lane & 3, nullptr, 0, 0, 0);
+  __syncthreads();
+  long long t2 = clock64();
+  if (threadIdx.x == 0) { t[0] = t1 - t0; t[1] = t2 - t1; out[0] = G[5] + Yc[7]; }
+}
+} }
+int gram_alone_main() {
+  long long* t; double* o; cudaMalloc(&t, 16); cudaMalloc(&o, 8);
+  const int rpc = 256;
+  size_t smem = (32 * 32 + rpc * oc_ld(32)) * 8;
+  cudaFuncSetAttribute(k_gram_alone<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+  for (int rep = 0; rep < 3; ++rep) {
+    k_gram_alone<32><<<1, 256, smem>>>(rpc, t, o); long long ht[2]; cudaMemcpy(ht, t, 16, cudaMemcpyDeviceToHost);
+    printf("standalone W=32 rpc=256: gram %lld cycles, apply %lld cycles (%s)\n", ht[0], ht[1], cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
