@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (multi-GB configs)")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the C5 fp32 (tcgen05) view measurement")
     return ap.parse_args()
 
 
@@ -174,6 +175,52 @@ def run_e2e(args, cfg, A, Om, Phi, step, barrier, flush, stream, dev, max_over_r
     e2e = {"value": world * bytes_step_rank / (e2e_step * 1e-3) / 1e9, "unit": "GB/s",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step}
     return e2e
+
+
+def c5_secondary(ctx, dev, reps=3):
+    """C5-shaped fp32 views (tcgen05 kind::tf32, 3xTF32) on a 100000 x 100000 fp32 A (40 GB),
+    w = l = 250: device time of the view kernels (RSVD_PROFILE events), roofline against the
+    tf32 tensor peak (measured bf16 burst x nominal tf32/bf16 ratio) at 3x the flops."""
+    import torch
+    from paper_1804_07531_b200 import rsvd
+
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    bf16 = peaks.get("bf16_tflops", 1590.0)
+    tf32_peak = bf16 * 1.1 / 2.25
+    m = n = 100000
+    w = 250
+    A = torch.empty(m, n, dtype=torch.float32, device=dev)
+    for r0 in range(0, m, 8192):
+        A[r0:r0 + 8192].normal_()
+    out = {"workload": "C5 fp32 100000x100000, views A*X and A^T*Y at w = k+p = 250",
+           "tf32_peak_tflops": tf32_peak,
+           "tf32_peak_source": f"MEASURED_PEAKS bf16 burst {bf16:.1f} TF x nominal tf32/bf16 1.1/2.25"}
+    for trans in (0, 1):
+        X = torch.randn(w, m if trans else n, dtype=torch.float32, device=dev).t()
+        ctx.view(A, X, trans=bool(trans), flags=rsvd.RSVD_PROFILE)
+        ts = []
+        for _ in range(reps):
+            _, info = ctx.view(A, X, trans=bool(trans), flags=rsvd.RSVD_PROFILE)
+            ts.append(info.view_ms)
+        t = statistics.median(ts)
+        fl = 2.0 * m * n * w
+        out["aty" if trans else "ax"] = {"ms": t, "tflops_3xtf32": 3 * fl / t / 1e9,
+                                         "frac_tensor": 3 * fl / t / 1e9 / tf32_peak,
+                                         "hbm_gbs": m * n * 4 / t / 1e6}
+        del X
+    Om = torch.randn(250, n, dtype=torch.float32, device=dev).t()
+    ctx.subspace(A, 200, 50, 2, Om)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ctx.subspace(A, 200, 50, 2, Om)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    out["subspace_v2_k200_p50_ms"] = e0.elapsed_time(e1)
+    del A
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------------------ our arm
@@ -340,6 +387,8 @@ def main():
             "views_per_s": world * step_views() * args.steps / (total_ms * 1e-3) / world,
             "svd_ms": alg_ms, "roofline": roofline, "peaks_measured": peaks, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_secondary:
+        line["secondary_c5_fp32"] = c5_secondary(ctx, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         base = oracle_baseline(cfg, steps=1, budget_s=30.0)
         line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}

@@ -154,8 +154,28 @@ int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int
                      unsigned flags, rsvd_info* info);
 
 /* ---- primitives (single GPU; for unit tests and the benchmark's kernel timing) -------------- */
+/* ---------------------------------------------------------------------------------------------
+ * Normal-matrix estimates A^T A ~ V diag(S) V^T (S = eigenvalues, descending), v >= 2 views.
+ *
+ * rsvd_nystrom   Alg. 4, modified prolonged (Nystrom) TEVD.  Q_r = orth(Omega) (v = 2),
+ *                QrQc(A, v-2) (v even) or QrQc(A^T, v-2) (v odd) (Alg. 3); then
+ *                Y_r = A^T (A Q_r), nu = 2.2e-16 ||Y_r||_2, Y_r += nu Q_r, B = Q_r^T Y_r,
+ *                C_L = chol((B + B^T)/2), F = C_L^-1 Y_r^T, [~, Lam, V] = tsvd(F, k),
+ *                S = max(Lam^2 - nu, 0).  Algebraically equal to rsvd_subspace with
+ *                RSVD_SQUARED in the recommended orientation.
+ *                Omega: n x (k+p) for even v, m_local x (k+p) for odd v (column-major).
+ * rsvd_pinched   Alg. 5, modified pinched TEVD: Q_r = QrQc(A^T, v-1) (v even) or
+ *                QrQc(A, v-1) (v odd), B_c = A Q_r, [S, V^] = tevd(B_c^T B_c, k), V = Q_r V^.
+ *                Omega: m_local x (k+p) for even v, n x (k+p) for odd v.
+ * S: k values (A's dtype), V: n x k (ldv >= n), either may be NULL.  Errors as rsvd_subspace.
+ * ------------------------------------------------------------------------------------------- */
+int rsvd_nystrom(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, const void* Omega, int64_t ld_omega, void* S,
+                 void* V, int64_t ldv, unsigned flags, rsvd_info* info);
+int rsvd_pinched(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, const void* Omega, int64_t ld_omega, void* S,
+                 void* V, int64_t ldv, unsigned flags, rsvd_info* info);
+
 /* trans == 0: Y (m_local x w) = A X with X n x w;  trans == 1: Y (n x w) = A^T X with X m_local x w.
- * 1 <= w <= 128. */
+ * 1 <= w <= 1024 (wider views run as column chunks of 128 (fp64) / 512 (fp32) columns). */
 int rsvd_view(rsvd_ctx* ctx, const rsvd_mat* A, int trans, const void* X, int64_t ldx, int w,
               void* Y, int64_t ldy, unsigned flags, rsvd_info* info);
 /* Y_c (m_local x l) = A Omega (Omega n x l) and Y_r (n x l2) = A^T Phi (Phi m_local x l2). */

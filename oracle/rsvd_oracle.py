@@ -33,7 +33,7 @@ import numpy as np
 __all__ = [
     "qr", "orth", "tsvd", "chol_lower", "jacobi_svd",
     "std_subspace_iteration", "gen_subspace_iteration", "qrqc", "one_view_tropp",
-    "gen_block_krylov", "normal_matrix_tevd", "recommend_input", "svd_of",
+    "gen_block_krylov", "normal_matrix_tevd", "nystrom_tevd", "pinched_tevd", "recommend_input", "svd_of",
     "views_and_vectors", "rel_frobenius_error", "rel_spectral_error", "projector_distance",
     "residual_fro", "half_power_lhs_rhs", "thm_bound",
     "GOAL_SVD", "GOAL_LEFT", "GOAL_RIGHT", "GOAL_NORMAL",
@@ -325,6 +325,55 @@ def normal_matrix_tevd(A, k, p, v, Omega, algorithm="subspace", transpose=None):
         transpose = bool(recommend_input(GOAL_NORMAL, v))
     _, s, V, _ = svd_of(A, algorithm, k, p, v=v, Omega=Omega, transpose=transpose)
     return V, s * s
+
+
+# ============================================================ Algorithms 4 and 5
+
+def nystrom_tevd(A, p, l, v, Omega):
+    """Alg. 4 — modified prolonged (Nystrom) TEVD of the normal matrix J^* J, v >= 2 views
+    (P:274-297).  J = A.  Omega replaces line 2's / Alg. 3's randn: n_c x (p+l) for even v
+    (Q_r built from J), n_r x (p+l) for odd v (Q_r built from J^*, line 6).
+    Returns (V_p, Lambda_p^2) with J^* J ~ V_p diag(Lambda_p^2) V_p^*.
+
+    Readings: ||Y_r|| in line 9 is the spectral norm; tsvd(F, p) of the wide
+    F (line 13) is the exact rank-p truncated SVD."""
+    if v < 2:
+        raise ValueError("Alg. 4 needs v >= 2 (P:277)")
+    J = _f64(A)
+    if v == 2:                                    # lines 1-2
+        Qr = orth(_f64(Omega))
+    elif v % 2 == 0:                              # lines 3-4: QrQc(J, p, l, v-2) -> Q_r
+        Qr = qrqc(J, p, l, v - 2, Omega)
+    else:                                         # lines 5-6: QrQc(J^*, p, l, v-2) -> its Q_c
+        Qr = qrqc(J, p, l, v - 2, Omega, transpose=True)
+    Yr = J.T @ (J @ Qr)                           # line 8 (two views)
+    nu = 2.2e-16 * np.linalg.norm(Yr, 2)          # line 9
+    Yr = Yr + nu * Qr                             # line 10
+    B = Qr.T @ Yr                                 # line 11
+    CL = chol_lower((B + B.T) / 2.0)              # line 12
+    F = np.linalg.solve(CL, Yr.T)                 # line 13: F = C_L^-1 Y_r^*
+    _, lam_hat, Vp = tsvd(F, p)                   # line 14
+    lam2 = lam_hat ** 2 - nu                      # line 15
+    lam2[lam2 < 0] = 0.0
+    return Vp, lam2
+
+
+def pinched_tevd(A, p, l, v, Omega):
+    """Alg. 5 — modified pinched TEVD of J^* J, v >= 2 views.  J = A.
+    Omega: n_r x (p+l) for even v (Q_r = QrQc(J^*, v-1), line 2), n_c x (p+l) for odd v
+    (Q_r = QrQc(J, v-1), line 4).  Returns (V_p, Lambda_p^2)."""
+    if v < 2:
+        raise ValueError("Alg. 5 needs v >= 2")
+    J = _f64(A)
+    if v % 2 == 0:
+        Qr = qrqc(J, p, l, v - 1, Omega, transpose=True)   # odd v-1 on J^*: its Q_c
+    else:
+        Qr = qrqc(J, p, l, v - 1, Omega)                   # even v-1 on J: Q_r
+    Bc = J @ Qr                                            # line 6 (one view)
+    evals, evecs = np.linalg.eigh(Bc.T @ Bc)               # line 7: tevd, descending
+    order = np.argsort(evals)[::-1][:p]
+    lam2 = np.maximum(evals[order], 0.0)
+    return Qr @ evecs[:, order], lam2                      # line 8
 
 
 def views_and_vectors(algorithm, v, width):

@@ -116,5 +116,12 @@ int launch_fill(double* dst, int64_t count, double v, cudaStream_t st);
 int launch_tri_inv(const double* R, int c, double* Rinv, DevStatus* status, cudaStream_t st);
 // S[i] <- S[i]^2
 int launch_square(double* S, int n, cudaStream_t st);
+// Nystrom (Alg. 4) helpers: nu = 2.2e-16 ||Y_r||_2 from the Gram of Y_r (power iteration);
+// Y += nu Q; S = (B + B^T)/2; lam2 = max(lam^2 - nu, 0)
+int launch_nys_nu(const double* G, int w, double* out, cudaStream_t st);
+int launch_axpy_dev(double* Y, int64_t ldy, const double* Q, int64_t ldq, int64_t rows, int w, const double* nu,
+                    cudaStream_t st);
+int launch_symmetrize(const double* B, int w, double* S, cudaStream_t st);
+int launch_nys_eig(const double* lam, int k, const double* nu, double* lam2, cudaStream_t st);
 
 }  // namespace rsvd

@@ -730,6 +730,129 @@ void alg_single_pass(Exec& E) {
   write_outputs(E, SIDE_M, SIDE_N, Qc, Xt, Ul, Vr, lam, lp, c.k);
 }
 
+// Alg. 3 QrQc on B = A (tr = false) or B = A^T (tr = true), v >= 0 views, starting
+// from the staged test matrix Q (on B's co-range side).  Returns the final basis: Q_r of B
+// (B's co-range side, in Q) for even v, Q_c of B (B's range side, new block) for odd v.
+TS qrqc(Exec& E, bool tr, TS Q, int v, int l) {
+  const Side side_c = tr ? SIDE_N : SIDE_M;
+  const Side side_r = tr ? SIDE_M : SIDE_N;
+  TS Qc = E.new_ts(side_c, l);
+  for (int j = 1; j <= v; ++j) {
+    if (j % 2 == 1) {
+      E.view(side_r, Q, Qc);                 // B Q_r
+      E.orth(side_c, Qc, nullptr, nullptr);
+    } else {
+      E.view(side_c, Qc, Q);                 // B^* Q_c
+      E.orth(side_r, Q, nullptr, nullptr);
+    }
+  }
+  return (v % 2 == 0) ? Q : Qc;
+}
+
+// tsvd(F, k) of the wide F = Ft^T (l x n) and its right vectors / values:
+// Ft = Q_f R_f (CholeskyQR2) -> F = R_f^T Q_f^T; Jacobi on R_f: R_f = Lf S Rf^T
+// -> F = Rf S (Q_f Lf)^T: right vectors Q_f Lf, values S.  Writes V (n x k) and S (k).
+void tsvd_wide_right(Exec& E, const TS& Ft, int l, int k, double* lam_out, TS* Qf_out, double** Lf_out) {
+  double* Rf = E.alloc((int64_t)l * l);
+  E.orth(SIDE_N, Ft, Rf, nullptr);
+  double* Lf = E.alloc((int64_t)l * l);
+  double* Rr = E.alloc((int64_t)l * l);
+  E.core_svd(Rf, l, /*trans=*/0, Lf, lam_out, Rr);
+  *Qf_out = Ft;
+  *Lf_out = Lf;
+  (void)k;
+}
+
+// emit V = Q W[:, :k] (side N) and S = lam2 (k) to the caller
+void write_normal_outputs(Exec& E, const TS& Q, const double* W, const double* lam2, int k) {
+  const Call& c = E.call;
+  if (c.kV != PTR_NULL) {
+    int64_t ld;
+    double* o = E.out_ptr(c.V, c.ldv, Q.rows, k, c.kV, &ld);
+    E.lift(Q, W, k, o, ld);
+  }
+  if (c.kS != PTR_NULL) {
+    int64_t ld;
+    double* so = E.out_ptr(c.S, k, k, 1, c.kS, &ld);
+    if (E.live()) E.chk(launch_copy_cols(lam2, k, so, k, k, 1, E.st));
+  }
+}
+
+// Alg. 4: modified prolonged (Nystrom) TEVD of the normal matrix A^T A with v views
+void alg_nystrom(Exec& E) {
+  const Call& c = E.call;
+  const int l = c.k + c.p, v = c.v;
+  // lines 1-7: Q_r (side N) from orth(Omega) (v = 2), QrQc(A, v-2) (even), QrQc(A^T, v-2) (odd)
+  const bool tr = (v % 2 == 1);
+  TS Q0 = E.stage_in(tr ? SIDE_M : SIDE_N, c.Om, c.ldom, l, c.kOm);
+  TS Qr;
+  if (v == 2) {
+    E.orth(SIDE_N, Q0, nullptr, nullptr);
+    Qr = Q0;
+  } else {
+    Qr = qrqc(E, tr, Q0, v - 2, l);
+  }
+  // line 8: Y_r = A^T (A Q_r)   (two views)
+  TS Yc = E.new_ts(SIDE_M, l);
+  TS Yr = E.new_ts(SIDE_N, l);
+  E.view(SIDE_N, Qr, Yc);
+  E.view(SIDE_M, Yc, Yr);
+  // lines 9-10: nu = 2.2e-16 ||Y_r||_2, Y_r += nu Q_r
+  double* G = E.alloc((int64_t)l * l);
+  double* nu = E.alloc(1);
+  E.cross(SIDE_N, Yr, Yr, G);
+  if (E.live()) {
+    E.chk(launch_nys_nu(G, l, nu, E.st));
+    E.chk(launch_axpy_dev(Yr.p, Yr.ld, Qr.p, Qr.ld, Yr.rows, l, nu, E.st));
+  }
+  // lines 11-12: B = Q_r^T Y_r, C_L = chol((B + B^T)/2, LOWER) = R^T
+  double* B = E.alloc((int64_t)l * l);
+  double* Bs = E.alloc((int64_t)l * l);
+  double* R = E.alloc((int64_t)l * l);
+  double* Ri = E.alloc((int64_t)l * l);
+  E.cross(SIDE_N, Qr, Yr, B);
+  if (E.live()) {
+    E.chk(launch_symmetrize(B, l, Bs, E.st));
+    E.chk(launch_chol_ref(Bs, nullptr, l, 0.0, R, Ri, E.ctx->dstat, E.st));
+  }
+  // line 13: F = C_L^-1 Y_r^T  ->  F^T = Y_r R^-1
+  TS Ft = E.new_ts(SIDE_N, l);
+  if (E.live()) E.chk(launch_ts_gemm(Yr.p, Yr.ld, Yr.rows, l, Ri, l, l, Ft.p, Ft.ld, 0, E.st));
+  // line 14: [~, Lam_hat, V] = tsvd(F, k)
+  double* lam = E.alloc(l);
+  TS Qf;
+  double* Lf = nullptr;
+  tsvd_wide_right(E, Ft, l, c.k, lam, &Qf, &Lf);
+  // line 15: Lambda^2 = Lam_hat^2 - nu, negatives -> 0
+  double* lam2 = E.alloc(l);
+  if (E.live()) E.chk(launch_nys_eig(lam, c.k, nu, lam2, E.st));
+  write_normal_outputs(E, Qf, Lf, lam2, c.k);
+}
+
+// Alg. 5: modified pinched TEVD of A^T A with v views
+void alg_pinched(Exec& E) {
+  const Call& c = E.call;
+  const int l = c.k + c.p, v = c.v;
+  // lines 1-5: Q_r = QrQc(A^T, v-1) (even v) or QrQc(A, v-1) (odd v): a basis on side N
+  const bool tr = (v % 2 == 0);
+  TS Q0 = E.stage_in(tr ? SIDE_M : SIDE_N, c.Om, c.ldom, l, c.kOm);
+  TS Qr = qrqc(E, tr, Q0, v - 1, l);
+  // line 6: B_c = A Q_r (one view)
+  TS Bc = E.new_ts(SIDE_M, l);
+  E.view(SIDE_N, Qr, Bc);
+  // line 7: tevd(B_c^T B_c, k) through B_c = Q_b R_b: eigenvectors = right singular vectors of
+  // R_b, eigenvalues = sigma(R_b)^2 (the same TEVD without forming the Gram)
+  double* Rb = E.alloc((int64_t)l * l);
+  E.orth(SIDE_M, Bc, Rb, nullptr);
+  double* Ul = E.alloc((int64_t)l * l);
+  double* Vr = E.alloc((int64_t)l * l);
+  double* lam = E.alloc(l);
+  E.core_svd(Rb, l, /*trans=*/1, Vr, lam, Ul);  // Jacobi on R_b^T: its left vectors = right(R_b)
+  if (E.live()) E.chk(launch_square(lam, l, E.st));
+  // line 8: V_p = Q_r Vhat_p
+  write_normal_outputs(E, Qr, Vr, lam, c.k);
+}
+
 // primitives -------------------------------------------------------------------------------
 void prim_view(Exec& E) {
   const Call& c = E.call;
@@ -852,6 +975,8 @@ void run_alg(Exec& E) {
     case 0: alg_subspace(E); break;
     case 1: alg_krylov(E); break;
     case 2: alg_single_pass(E); break;
+    case 3: alg_nystrom(E); break;
+    case 4: alg_pinched(E); break;
     case 10: prim_view(E); break;
     case 11: prim_fused(E); break;
     case 12: prim_orth(E); break;
@@ -1334,6 +1459,53 @@ int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int
     info->lc_used = lc;
   }
   return r;
+}
+
+static int normal_entry(int alg, rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, const void* Omega,
+                        int64_t ld_omega, void* S, void* V, int64_t ldv, unsigned flags, rsvd_info* info) {
+  int r = common_checks(ctx, A, k, p);
+  if (r == RSVD_OK) {
+    // Omega lives on the side the first basis is built from: Alg. 4 starts from A for even v
+    // and from A^T for odd v; Alg. 5 the other way round
+    const bool om_m = (alg == 3) ? (v % 2 == 1) : (v % 2 == 0);
+    const int64_t om_rows = om_m ? A->m_local : A->n;
+    if (v < 2) { set_err(ctx, "v >= 2 required (Alg. 4 / Alg. 5)"); r = RSVD_E_ARG; }
+    else if (!Omega || ld_omega < om_rows) { set_err(ctx, "Omega NULL or ld_omega < %lld", (long long)om_rows); r = RSVD_E_ARG; }
+    else if (V && ldv < A->n) { set_err(ctx, "ldv < n"); r = RSVD_E_ARG; }
+  }
+  if (r != RSVD_OK) {
+    if (info) { memset(info, 0, sizeof(*info)); info->status = r; }
+    return r;
+  }
+  Call c;
+  c.alg = alg;
+  c.A = A;
+  c.k = k;
+  c.p = p;
+  c.v = v;
+  c.Om = Omega;
+  c.ldom = ld_omega;
+  c.S = S;
+  c.V = V;
+  c.ldv = ldv;
+  c.flags = flags;
+  r = execute(ctx, c, info);
+  if (info) {
+    info->status = r;
+    info->views = v;
+    info->vectors = (int64_t)v * (k + p);
+  }
+  return r;
+}
+
+int rsvd_nystrom(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, const void* Omega, int64_t ld_omega, void* S,
+                 void* V, int64_t ldv, unsigned flags, rsvd_info* info) {
+  return normal_entry(3, ctx, A, k, p, v, Omega, ld_omega, S, V, ldv, flags, info);
+}
+
+int rsvd_pinched(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, const void* Omega, int64_t ld_omega, void* S,
+                 void* V, int64_t ldv, unsigned flags, rsvd_info* info) {
+  return normal_entry(4, ctx, A, k, p, v, Omega, ld_omega, S, V, ldv, flags, info);
 }
 
 int rsvd_view(rsvd_ctx* ctx, const rsvd_mat* A, int trans, const void* X, int64_t ldx, int w, void* Y, int64_t ldy,

@@ -433,6 +433,9 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
   if (c < 1 || c > kJacMaxC || r < c || r > kJacMaxC) return RSVD_E_ARG;
   if (r <= 64) return launch_jacobi_small(M, ldm, trans, r, c, Ul, S, Vr, status, st, want_j);
   if (c > 128) return launch_jacobi_cluster(M, ldm, trans, r, c, Ul, S, Vr, scratch, status, st, want_j);
+  // 64 < c <= 128: always accumulate J — both singular-vector sets then stay orthonormal to
+  // rounding even for the trailing small sigma (C4's k = 100 core, sigma_100 / sigma_1 = 1e-3)
+  want_j = 1;
   const int ce = c + (c & 1);
   const size_t wbytes = (size_t)r * ce * 8, jbytes = want_j ? (size_t)ce * ce * 8 : 0;
   const size_t budget = 200 * 1024;
@@ -1229,3 +1232,86 @@ void reset_phases() {
 }
 }  // namespace rsvd
 #endif
+
+// ------------------------------------------------------------------ Nystrom helpers (Alg. 4)
+namespace rsvd {
+namespace {
+// out[0] = 2.2e-16 * sqrt(lambda_max(G)) for the symmetric psd G (w x w): ||Y_r||_2 from its
+// Gram by power iteration (fixed 200 iterations, Rayleigh quotient; deterministic), line 9.
+__global__ void __launch_bounds__(256) k_nys_nu(const double* __restrict__ G, int w, double* __restrict__ out) {
+  __shared__ double x[512], y[512], red[8];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < w; i += 256) x[i] = 1.0 + 1e-3 * i;   // generic start, not orthogonal to the top space
+  __syncthreads();
+  double rq = 0.0;
+  for (int it = 0; it < 200; ++it) {
+    for (int i = tid; i < w; i += 256) {
+      double s = 0.0;
+      for (int k = 0; k < w; ++k) s = fma(G[(int64_t)k * w + i], x[k], s);
+      y[i] = s;
+    }
+    __syncthreads();
+    double nn = 0.0, xy = 0.0;
+    for (int i = tid; i < w; i += 256) { nn = fma(y[i], y[i], nn); xy = fma(x[i], y[i], xy); }
+    nn = warp_sum(nn);
+    xy = warp_sum(xy);
+    if ((tid & 31) == 0) { red[tid >> 5] = nn; }
+    __syncthreads();
+    double tn = 0.0;
+    for (int q = 0; q < 8; ++q) tn += red[q];
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = xy;
+    __syncthreads();
+    double txy = 0.0;
+    for (int q = 0; q < 8; ++q) txy += red[q];
+    double txx = 0.0;
+    for (int k = 0; k < w; ++k) txx = fma(x[k], x[k], txx);
+    rq = (txx > 0.0) ? txy / txx : 0.0;
+    const double sc = tn > 0.0 ? rsqrt(tn) : 0.0;
+    __syncthreads();
+    for (int i = tid; i < w; i += 256) x[i] = y[i] * sc;
+    __syncthreads();
+  }
+  if (tid == 0) out[0] = 2.2e-16 * sqrt(fmax(rq, 0.0));
+}
+// Y += nu * Q  (column-major rows x w), nu read from device memory
+__global__ void k_axpy_dev(double* __restrict__ Y, int64_t ldy, const double* __restrict__ Q, int64_t ldq, int64_t rows,
+                           int w, const double* __restrict__ nu) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (r < rows && c < w) Y[(int64_t)c * ldy + r] = fma(nu[0], Q[(int64_t)c * ldq + r], Y[(int64_t)c * ldy + r]);
+}
+// S (w x w) = (B + B^T) / 2
+__global__ void k_symmetrize(const double* __restrict__ B, int w, double* __restrict__ S) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= w * w) return;
+  const int i = e % w, j = e / w;
+  S[e] = 0.5 * (B[e] + B[(int64_t)i * w + j]);
+}
+// lam2[i] = max(lam[i]^2 - nu, 0)   (line 15); lam2 may alias lam
+__global__ void k_nys_eig(const double* lam, int k, const double* __restrict__ nu, double* lam2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) lam2[i] = fmax(lam[i] * lam[i] - nu[0], 0.0);
+}
+}  // namespace
+
+int launch_nys_nu(const double* G, int w, double* out, cudaStream_t st) {
+  if (w < 1 || w > 512) return RSVD_E_ARG;
+  k_nys_nu<<<1, 256, 0, st>>>(G, w, out);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+int launch_axpy_dev(double* Y, int64_t ldy, const double* Q, int64_t ldq, int64_t rows, int w, const double* nu,
+                    cudaStream_t st) {
+  if (rows <= 0 || w <= 0) return RSVD_OK;
+  k_axpy_dev<<<dim3((unsigned)((rows + 255) / 256), (unsigned)w), 256, 0, st>>>(Y, ldy, Q, ldq, rows, w, nu);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+int launch_symmetrize(const double* B, int w, double* S, cudaStream_t st) {
+  k_symmetrize<<<(w * w + 255) / 256, 256, 0, st>>>(B, w, S);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+int launch_nys_eig(const double* lam, int k, const double* nu, double* lam2, cudaStream_t st) {
+  k_nys_eig<<<(k + 255) / 256, 256, 0, st>>>(lam, k, nu, lam2);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+}  // namespace rsvd

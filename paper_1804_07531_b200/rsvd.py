@@ -25,7 +25,8 @@ ERR = {0: "RSVD_OK", -1: "RSVD_E_ARG", -2: "RSVD_E_DTYPE", -3: "RSVD_E_CUDA", -4
 
 EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_strerror", "rsvd_last_error", "rsvd_version", "rsvd_sm_count",
            "rsvd_recommend_input", "rsvd_probe_peaks", "rsvd_get_unique_id", "rsvd_comm_init", "rsvd_comm_nranks", "rsvd_subspace",
-           "rsvd_block_krylov", "rsvd_single_pass", "rsvd_view", "rsvd_view_fused", "rsvd_orth", "rsvd_core_svd"]
+           "rsvd_block_krylov", "rsvd_single_pass", "rsvd_nystrom", "rsvd_pinched", "rsvd_view", "rsvd_view_fused",
+           "rsvd_orth", "rsvd_core_svd"]
 
 
 class RsvdMat(ctypes.Structure):
@@ -82,6 +83,8 @@ def lib():
     L.rsvd_subspace.argtypes = alg
     L.rsvd_block_krylov.argtypes = alg
     L.rsvd_single_pass.argtypes = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
+    L.rsvd_nystrom.argtypes = [vp, pmat, i32, i32, i32, vp, i64, vp, vp, i64, u32, pinfo]
+    L.rsvd_pinched.argtypes = [vp, pmat, i32, i32, i32, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_view.argtypes = [vp, pmat, i32, vp, i64, i32, vp, i64, u32, pinfo]
     L.rsvd_view_fused.argtypes = [vp, pmat, vp, i64, i32, vp, i64, i32, vp, i64, vp, i64, u32, pinfo]
     L.rsvd_orth.argtypes = [vp, i64, i32, vp, i64, vp, u32, pinfo]
@@ -224,6 +227,25 @@ class Context:
                                     ctypes.byref(info))
         self._check(rc, "rsvd_single_pass")
         return U, S, V, info
+
+    def _normal(self, fn, name, A, k, p, v, Omega, flags=0, m=None, row0=0, host_out=False):
+        Om = _colmajor(Omega)
+        M = self.mat(A, m, row0)
+        V = self._out_like(A, A.shape[1], k, host_out)
+        S = (torch.empty(k, dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
+             else torch.empty(k, dtype=A.dtype, device=A.device))
+        info = RsvdInfo()
+        self._check(fn(self._h, ctypes.byref(M), k, p, v, Om.data_ptr(), _ld(Om), S.data_ptr(), V.data_ptr(), _ld(V),
+                       flags, ctypes.byref(info)), name)
+        return S, V, info
+
+    def nystrom(self, A, k, p, v, Omega, **kw):
+        """Alg. 4: A^T A ~ V diag(S) V^T.  Omega: n x (k+p) for even v, m x (k+p) for odd v."""
+        return self._normal(lib().rsvd_nystrom, "rsvd_nystrom", A, k, p, v, Omega, **kw)
+
+    def pinched(self, A, k, p, v, Omega, **kw):
+        """Alg. 5: A^T A ~ V diag(S) V^T.  Omega: m x (k+p) for even v, n x (k+p) for odd v."""
+        return self._normal(lib().rsvd_pinched, "rsvd_pinched", A, k, p, v, Omega, **kw)
 
     # ------------------------------------------------------------------ primitives
     def view(self, A, X, trans=False, flags=0):

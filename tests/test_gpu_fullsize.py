@@ -185,3 +185,41 @@ def test_c4_normal_mode_full_size(ctx, c4):
     AtU = np.stack([A[:, c].cpu().numpy() for c in cols]) @ Uh
     err = np.abs(AtU - Vh[cols] * s) / s[0]
     assert err.max() <= 1e-12
+
+
+# ------------------------------------------------------------------ C5 at full size (fp32, 40 GB)
+@pytest.fixture(scope="module")
+def c5():
+    free, _ = torch.cuda.mem_get_info()
+    if free < 60e9:
+        pytest.skip(f"C5 needs ~60 GB of free device memory, have {free / 1e9:.0f}")
+    cfg = S.CONFIGS["C5"]
+    A = S.make_matrix_torch(cfg, torch.device("cuda", 0), panel_rows=2048)
+    Om = S.gaussian_test_matrix_torch(cfg.n, cfg.l, cfg, S.ROLE_OMEGA, torch.device("cuda", 0))
+    torch.cuda.synchronize()
+    yield cfg, A, Om
+    del A
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("alg,v", [("subspace", 3), ("krylov", 5)])
+def test_c5_full_size(ctx, c5, alg, v):
+    """C5 (fp32, tcgen05 3xTF32 views): odd v ends with [Q_c, R_c] = qr(A Q_r), tsvd(R_c), so A V = U S
+    row by row (checked in fp64 on sampled rows of the fp32 A, to fp32-accumulation accuracy);
+    orthonormal factors; leading values at the construction sigma_i = exp(-i/100) to the noise level."""
+    cfg, A, Om = c5
+    fn = ctx.subspace if alg == "subspace" else ctx.block_krylov
+    U, s, V, info = fn(A, cfg.k, cfg.p, v, Om)
+    assert U.dtype == torch.float32 and info.views == v
+    U, s, V = host(U).astype(np.float64), host(s).astype(np.float64), host(V).astype(np.float64)
+    k = cfg.k
+    np.testing.assert_allclose(U.T @ U, np.eye(k), atol=2e-5)
+    np.testing.assert_allclose(V.T @ V, np.eye(k), atol=2e-5)
+    assert np.all(np.diff(s) <= 1e-7 * s[0])
+    sig = S.sigma_c5(cfg.rank)[:k]
+    noise = cfg.noise * (np.sqrt(cfg.m) + np.sqrt(cfg.n)) * 1.1
+    np.testing.assert_allclose(s[:20], sig[:20], rtol=1e-4, atol=noise)
+    rows = [0, 1, 4999, 50000, cfg.m - 1]
+    Ar = np.stack([A[r].double().cpu().numpy() for r in rows])
+    err = np.abs(Ar @ V - U[rows] * s) / s[0]
+    assert err.max() <= 1e-4

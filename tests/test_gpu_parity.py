@@ -300,3 +300,27 @@ def test_argument_errors(ctx):
     with pytest.raises(rsvd.RsvdError) as e:
         ctx.subspace(dev(np.zeros((50, 40), dtype=np.float16)), 5, 5, 2, colmajor_dev(np.zeros((40, 10), np.float16)))
     assert e.value.code == -2  # only fp64 and fp32 are defined
+
+
+# ------------------------------------------------------------------ Alg. 4 / Alg. 5 (normal matrix)
+
+NORMAL_CASES = [("C1", None, None, v) for v in (2, 3, 4, 5)] + [("C2", None, None, v) for v in (2, 3, 4)] + \
+               [("C3", 3000, 1200, 3), ("C1", 333, 151, 4)]
+
+
+@pytest.mark.parametrize("name,m,n,v", NORMAL_CASES)
+@pytest.mark.parametrize("alg", ["nystrom", "pinched"])
+def test_normal_matrix_parity(ctx, alg, name, m, n, v):
+    cfg = S.CONFIGS[name]
+    A = S.make_matrix(cfg, m, n)
+    mm, nn = A.shape
+    from_At = (v % 2 == 1) if alg == "nystrom" else (v % 2 == 0)
+    Om = S.gaussian_test_matrix(mm if from_At else nn, cfg.l, cfg, S.ROLE_OMEGA)
+    fn = ctx.nystrom if alg == "nystrom" else ctx.pinched
+    s2, V, info = fn(dev(A), cfg.k, cfg.p, v, colmajor_dev(Om))
+    ofn = O.nystrom_tevd if alg == "nystrom" else O.pinched_tevd
+    Vo, s2o = ofn(A, cfg.k, cfg.p, v, Om)
+    s2 = host(s2)
+    assert info.views == v
+    assert np.max(np.abs(s2 - s2o) / s2o) <= 2 * TOL_S  # eigenvalues = sigma^2: twice sigma's relative error
+    assert O.projector_distance(host(V), Vo) <= TOL_P

@@ -418,3 +418,74 @@ def test_projector_distance_stable_form():
     Uo = np.linalg.qr(U + 1e-3 * S.random_gaussian_matrix(30, 4, seed=2))[0]
     explicit = np.linalg.norm(U @ U.T - Uo @ Uo.T)
     assert abs(O.projector_distance(U, Uo) - explicit) < 1e-12
+
+
+# ------------------------------------------------------------------ Alg. 4 (Nystrom) and Alg. 5 (pinched)
+
+def _nys_inputs(v, pinched=False, seed=1):
+    cfg = S.CONFIGS["C1"]
+    A = S.make_matrix(cfg)
+    # Alg. 4 builds Q_r from J for even v and from J^* for odd v; Alg. 5 the other way round
+    from_At = (v % 2 == 0) if pinched else (v % 2 == 1)
+    rows = A.shape[0] if from_At else A.shape[1]
+    return cfg, A, S.gaussian_test_matrix(rows, cfg.l, cfg, S.ROLE_OMEGA, seed)
+
+
+@pytest.mark.parametrize("v", [2, 3, 4, 5, 6])
+def test_nystrom_equals_alg2_recommended(v):
+    """P:365 (with P:343, eq. gennystrom2): Alg. 4 with v views is algebraically the recommended
+    use of Alg. 2 for J^* J (input J for even v, J^* for odd v) — same Omega, same TEVD."""
+    cfg, A, Om = _nys_inputs(v)
+    V, lam2 = O.nystrom_tevd(A, cfg.k, cfg.p, v, Om)
+    Vs, s2 = O.normal_matrix_tevd(A, cfg.k, cfg.p, v, Om)   # Alg. 2, recommended orientation
+    assert np.max(np.abs(lam2 - s2) / s2) <= 1e-12
+    assert proj(V, Vs) <= 1e-12
+
+
+@pytest.mark.parametrize("v", [2, 3, 4, 5])
+def test_pinched_equals_alg2_other_orientation(v):
+    """Alg. 5 with v views equates to Alg. 2 for J^* J in the NON-recommended
+    orientation (input J^* for even v, J for odd v)."""
+    cfg, A, Om = _nys_inputs(v, pinched=True)
+    V, lam2 = O.pinched_tevd(A, cfg.k, cfg.p, v, Om)
+    Vs, s2 = O.normal_matrix_tevd(A, cfg.k, cfg.p, v, Om, transpose=(v % 2 == 0))
+    assert np.max(np.abs(lam2 - s2) / s2) <= 1e-12
+    assert proj(V, Vs) <= 1e-12
+
+
+@pytest.mark.parametrize("v", [2, 3, 4])
+def test_nystrom_exact_rank_and_full_sampling(v):
+    """Exactly rank-r J (r <= p + l): the Nystrom TEVD recovers eig(J^* J) (the nu shift of
+    P:289-296 is removed again in line 15).  Full sampling l = n: same, for any J."""
+    sig = np.array([5.0, 3.0, 2.0, 1.5, 1.0, 0.5])
+    A = S.exact_rank_matrix(60, 40, sig, seed=3)
+    k, p = 4, 4
+    Om = S.random_gaussian_matrix(60 if v % 2 else 40, k + p, seed=v)
+    V, lam2 = O.nystrom_tevd(A, k, p, v, Om)
+    np.testing.assert_allclose(lam2, sig[:k] ** 2, rtol=1e-12)
+    X, Y = S.exact_rank_factors(60, 40, len(sig), seed=3)
+    assert proj(V, Y[:, :k]) <= 1e-11
+    B = S.random_gaussian_matrix(12, 9, seed=11)
+    Om = S.random_gaussian_matrix(12 if v % 2 else 9, 9, seed=12)
+    V, lam2 = O.nystrom_tevd(B, 9, 0, v, Om)
+    ev = np.sort(np.linalg.eigvalsh(B.T @ B))[::-1]
+    np.testing.assert_allclose(lam2, ev, rtol=1e-10, atol=1e-13 * ev[0])
+
+
+def test_nystrom_more_accurate_than_pinched():
+    """P:369 / section 'results normal matrix': with the same view budget the modified prolonged
+    (Nystrom) TEVD is more accurate than the pinched one (mean over seeds, PolySlow-like decay)."""
+    n = 120
+    d = 1.0 / np.arange(1, n + 1) ** 0.5
+    A = np.diag(d)
+    k, p = 10, 5
+    err_n, err_p = [], []
+    for seed in range(20):
+        for v in (2, 3):
+            On = S.random_gaussian_matrix(n, k + p, seed=1000 + seed)
+            V, lam2 = O.nystrom_tevd(A, k, p, v, On)
+            Vp, lp = O.pinched_tevd(A, k, p, v, On)
+            N = A.T @ A
+            err_n.append(np.linalg.norm(N - (V * lam2) @ V.T, 2))
+            err_p.append(np.linalg.norm(N - (Vp * lp) @ Vp.T, 2))
+    assert np.mean(err_n) < np.mean(err_p)
