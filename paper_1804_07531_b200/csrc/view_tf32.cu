@@ -160,7 +160,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmXh);
       tma_prefetch_desc(&tmXl);
-      const uint64_t pa = policy_evict_first(), px = policy_evict_last();
+      // A x X reads each row of A in 64-byte k-chunks: with 256-byte L2 promotion the other three
+      // chunks of a promoted line are used by the next three stages, so A must not be marked
+      // evict-first there (ncu: 1.66x DRAM over-fetch with evict_first).  A^T x Y reads 128-byte
+      // rows of 4 adjacent boxes per stage: evict_first is safe.
+      const uint64_t pa = (KIND == VIEW_AX) ? policy_evict_normal() : policy_evict_first();
+      const uint64_t px = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < U; u += gridDim.x) {
