@@ -125,7 +125,11 @@ int  rsvd_recommend_input(int goal, int v);
 
 /* ---- multi-GPU (NCCL, loaded at run time from libnccl.so.2) --------------------------------- */
 int  rsvd_get_unique_id(void* id128);                  /* rank 0: fills 128 bytes             */
-int  rsvd_comm_init(rsvd_ctx* ctx, int nranks, int rank, const void* id128);   /* collective */
+/* Collective over nranks processes (one per GPU): every rank passes the same 128-byte NCCL unique
+ * id (rank 0's rsvd_get_unique_id, broadcast by the caller).  nranks == 1 also creates a
+ * one-rank communicator: the calls then take the sharded code path (all-reduced Grams and
+ * A^T Y partials, NCCL inside the CUDA graph) on a single GPU.  RSVD_E_STATE if already set. */
+int  rsvd_comm_init(rsvd_ctx* ctx, int nranks, int rank, const void* id128);
 int  rsvd_comm_nranks(const rsvd_ctx* ctx);
 
 /* ---- algorithms ----------------------------------------------------------------------------- */

@@ -228,7 +228,10 @@ struct Exec {
     s.w = wc;
     return s;
   }
-  bool sharded(Side s) const { return s == SIDE_M && ctx->nranks > 1; }
+  // a communicator exists (rsvd_comm_init; also with one rank, which runs the sharded code path
+  // on one GPU: sharded CholeskyQR, all-reduced Grams and A^T Y partials, NCCL in the graph)
+  bool collective() const { return ctx->comm != nullptr; }
+  bool sharded(Side s) const { return s == SIDE_M && collective(); }
 
   void allreduce(double* p, int64_t count) {
     if (!live()) return;
@@ -289,7 +292,7 @@ struct Exec {
       }
       release(mk);
     }
-    if (from == SIDE_M && ctx->nranks > 1) allreduce(Y.p, Y.ld * Y.w);
+    if (from == SIDE_M && collective()) allreduce(Y.p, Y.ld * Y.w);
   }
 
   // fp32 A: split X into tf32 hi / lo parts, tcgen05 3xTF32 view into fp64 partial slots
@@ -331,7 +334,7 @@ struct Exec {
       }
       release(mk);
     }
-    if (from == SIDE_M && ctx->nranks > 1) allreduce(Y.p, Y.ld * Y.w);
+    if (from == SIDE_M && collective()) allreduce(Y.p, Y.ld * Y.w);
   }
 
   // G (a x b, col-major ld a) = Xa^T Xb over the side's rows (+ all-reduce when sharded)
@@ -666,7 +669,7 @@ void alg_single_pass(Exec& E) {
       if (!a.yc_atomic) E.chk(launch_slot_sum(ycs, Yc.ld, a.yc_slot_stride, nsb, Yc.rows, l, Yc.p, Yc.ld, E.st));
       if (a.S > 1) E.chk(launch_slot_sum(yrs, Yr.ld, a.yr_slot_stride, a.S, Yr.rows, l2, Yr.p, Yr.ld, E.st));
     }
-    if (E.ctx->nranks > 1) E.allreduce(Yr.p, Yr.ld * l2);
+    if (E.collective()) E.allreduce(Yr.p, Yr.ld * l2);
     E.release(mk);
   } else {
     // widths beyond the fused kernel's register budget: two views (documented; info->view_launches = 2)
@@ -991,7 +994,7 @@ std::string call_key(const Call& c, const Exec& E, const rsvd_ctx* ctx) {
   snprintf(buf, sizeof buf, "a%d k%d p%d v%d in%d l2%d lc%d t%d w%d r%lld c%d f%u A%p m%lld n%lld lda%lld U%d S%d V%d R%d ar%p nr%d",
            c.alg, c.k, c.p, c.v, c.input, c.l2, c.lc, c.trans, c.w, (long long)c.rows, c.cols, c.flags,
            (const void*)E.A, (long long)E.m, (long long)E.n, (long long)E.lda, c.kU != PTR_NULL, c.kS != PTR_NULL,
-           c.kV != PTR_NULL, c.kR != PTR_NULL, (void*)ctx->arena, ctx->nranks);
+           c.kV != PTR_NULL, c.kR != PTR_NULL, (void*)ctx->arena, ctx->nranks + (ctx->comm ? 1000 : 0));
   return std::string(buf);
 }
 
@@ -1321,7 +1324,7 @@ int rsvd_get_unique_id(void* id128) {
 int rsvd_comm_init(rsvd_ctx* c, int nranks, int rank, const void* id128) {
   if (!c || nranks < 1 || rank < 0 || rank >= nranks || !id128) return RSVD_E_ARG;
   if (c->comm) return RSVD_E_STATE;
-  if (nranks == 1) return RSVD_OK;
+  // nranks == 1 also creates a (1-rank) communicator: the sharded code path then runs on one GPU
   if (!g_nccl.load()) {
     set_err(c, "libnccl.so.2 not loadable");
     return RSVD_E_NCCL;

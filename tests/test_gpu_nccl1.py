@@ -1,0 +1,76 @@
+"""The row-sharded (multi-GPU) code path on one GPU: a one-rank NCCL communicator makes every
+call take the sharded route of SURVEY §8(e) — CholeskyQR of side-M blocks through all-reduced
+Grams (no single-launch cluster path), the A^T Y partial followed by ncclAllReduce, NCCL calls
+captured in the CUDA graph.  Results must match the CPU oracle within the north_star tolerances
+and the communicator-free context to rounding.  (The pool gives one GPU per call; the N > 1
+schedule itself is checked against the oracle on CPU in test_multirank_cpu.py.)"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth as S
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctxs():
+    from paper_1804_07531_b200 import build, rsvd
+
+    build.build()
+    c1 = rsvd.Context(0)
+    c1.comm_init(1, 0, rsvd.get_unique_id())
+    c0 = rsvd.Context(0)
+    yield c1, c0
+    c1.close()
+    c0.close()
+
+
+def colmajor_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a).T)).cuda().t()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+CASES = [("C2", None, None, "subspace", 3), ("C2", None, None, "krylov", 4), ("C2", None, None, "single_pass", 1),
+         ("C3", 3000, 1200, "subspace", 2), ("C3", 3000, 1200, "krylov", 5), ("C1", None, None, "subspace", 4)]
+
+
+@pytest.mark.parametrize("name,m,n,alg,v", CASES)
+def test_one_rank_comm_matches_oracle(ctxs, name, m, n, alg, v):
+    c1, c0 = ctxs
+    assert c1.nranks == 1
+    cfg = S.CONFIGS[name]
+    A = S.make_matrix(cfg, m, n)
+    Om = S.gaussian_test_matrix(A.shape[1], cfg.l, cfg, S.ROLE_OMEGA)
+    Phi = S.gaussian_test_matrix(A.shape[0], cfg.l2, cfg, S.ROLE_PHI)
+    Ad = torch.from_numpy(A).cuda()
+    outs = []
+    for c in (c1, c0):
+        if alg == "subspace":
+            r = c.subspace(Ad, cfg.k, cfg.p, v, colmajor_dev(Om))
+        elif alg == "krylov":
+            r = c.block_krylov(Ad, cfg.k, cfg.p, v, colmajor_dev(Om))
+        else:
+            r = c.single_pass(Ad, cfg.k, cfg.p, cfg.l2, colmajor_dev(Om), colmajor_dev(Phi))
+        outs.append([host(x) for x in r[:3]])
+    Uo, so, Vo, _ = O.svd_of(A, alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi)
+    (U, s, V), (U0, s0, V0) = outs
+    assert np.max(np.abs(s - so) / so) <= 1e-10
+    assert O.projector_distance(U, Uo) <= 1e-9 and O.projector_distance(V, Vo) <= 1e-9
+    assert np.max(np.abs(s - s0) / s0) <= 1e-12
+    assert O.projector_distance(U, U0) <= 1e-11 and O.projector_distance(V, V0) <= 1e-11
+
+
+def test_one_rank_comm_nystrom(ctxs):
+    c1, _ = ctxs
+    cfg = S.CONFIGS["C2"]
+    A = S.make_matrix(cfg)
+    Om = S.gaussian_test_matrix(A.shape[0], cfg.l, cfg, S.ROLE_OMEGA)   # odd v: m x l
+    s2, V, info = c1.nystrom(torch.from_numpy(A).cuda(), cfg.k, cfg.p, 3, colmajor_dev(Om))
+    Vo, s2o = O.nystrom_tevd(A, cfg.k, cfg.p, 3, Om)
+    assert np.max(np.abs(host(s2) - s2o) / s2o) <= 2e-10
+    assert O.projector_distance(host(V), Vo) <= 1e-9
