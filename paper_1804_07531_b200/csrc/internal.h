@@ -112,6 +112,8 @@ int launch_small_gemm(int ta, int tb, int m, int n, int k, const double* A, int6
 int launch_copy_cols(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int cols,
                      cudaStream_t st);
 int launch_fill(double* dst, int64_t count, double v, cudaStream_t st);
+// out (rows x c) -= T (rows x c), column-major
+int launch_sub_cols(const double* T, int64_t ldt, double* out, int64_t ldo, int64_t rows, int c, cudaStream_t st);
 // triangular-system helpers for Alg. 7: out (c x c) = upper-triangular inverse of R (c x c)
 int launch_tri_inv(const double* R, int c, double* Rinv, DevStatus* status, cudaStream_t st);
 // S[i] <- S[i]^2

@@ -83,12 +83,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int br = 0; br < nb - 1; ++br) {
       int P, Q;
       pair_of(br, rank, nb, &P, &Q);
-      // load blocks P, Q -> local columns [0, b) and [b, 2b)
-      for (int e = tid; e < b2 * r; e += kThreads) {
-        const int lj = e / r, i = e % r;
-        const int gj = (lj < b ? P * b + lj : Q * b + (lj - b));
-        sW[e] = W[(int64_t)gj * r + i];
-      }
+      // load blocks P, Q -> local columns [0, b) and [b, 2b): column loops, 8 loads in flight
+      for (int lj0 = 0; lj0 < b2; lj0 += 8)
+        for (int i = tid; i < r; i += kThreads) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int lj = lj0 + u;
+            const int gj = (lj < b ? P * b + lj : Q * b + (lj - b));
+            v[u] = (lj < b2) ? W[(int64_t)gj * r + i] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (lj0 + u < b2) sW[(lj0 + u) * r + i] = v[u];
+        }
       __syncthreads();
       // one cyclic sweep over the 2b local columns
       for (int ir = 0; ir < b2 - 1; ++ir) {
@@ -97,13 +105,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           pair_of(ir, pk, b2, &p, &q);
           double* wp = sW + p * r;
           double* wq = sW + q * r;
-          double a = 0.0, bb = 0.0, cc = 0.0;
-          for (int i = lane; i < r; i += 32) {
-            const double x = wp[i], y = wq[i];
-            a = fma(x, x, a);
-            bb = fma(y, y, bb);
-            cc = fma(x, y, cc);
+          // the lane's slice of both columns in registers: every load is issued before any
+          // store (a load -> rotate -> store loop serialises on the possible aliasing)
+          constexpr int RPL = kMaxC / 32;
+          double x[RPL], y[RPL];
+#pragma unroll
+          for (int t = 0; t < RPL; ++t) {
+            const int i = lane + 32 * t;
+            x[t] = (i < r) ? wp[i] : 0.0;
+            y[t] = (i < r) ? wq[i] : 0.0;
           }
+          double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int t = 0; t < RPL; t += 2) {
+            a0 = fma(x[t], x[t], a0);
+            b0 = fma(y[t], y[t], b0);
+            c0 = fma(x[t], y[t], c0);
+            a1 = fma(x[t + 1], x[t + 1], a1);
+            b1 = fma(y[t + 1], y[t + 1], b1);
+            c1 = fma(x[t + 1], y[t + 1], c1);
+          }
+          double a = a0 + a1, bb = b0 + b1, cc = c0 + c1;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
             a += __shfl_xor_sync(0xffffffffu, a, o);
@@ -114,10 +136,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const double t = rot_t(a, bb, cc);
             const double cs = rsqrt(fma(t, t, 1.0));
             const double sn = cs * t;
-            for (int i = lane; i < r; i += 32) {
-              const double x = wp[i], y = wq[i];
-              wp[i] = cs * x - sn * y;
-              wq[i] = sn * x + cs * y;
+#pragma unroll
+            for (int k = 0; k < RPL; ++k) {
+              const int i = lane + 32 * k;
+              if (i < r) {
+                wp[i] = cs * x[k] - sn * y[k];
+                wq[i] = sn * x[k] + cs * y[k];
+              }
             }
             if (want_j) {
               const int gp = p < b ? P * b + p : Q * b + (p - b);
@@ -137,10 +162,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncthreads();
       }
       // write the pair back in place (each block is owned by exactly one CTA per block round)
-      for (int e = tid; e < b2 * r; e += kThreads) {
-        const int lj = e / r, i = e % r;
+      for (int lj = 0; lj < b2; ++lj) {
         const int gj = (lj < b ? P * b + lj : Q * b + (lj - b));
-        W[(int64_t)gj * r + i] = sW[e];
+        for (int i = tid; i < r; i += kThreads) W[(int64_t)gj * r + i] = sW[lj * r + i];
       }
       __threadfence();
       cluster.sync();

@@ -340,14 +340,80 @@ struct Exec {
   // G (a x b, col-major ld a) = Xa^T Xb over the side's rows (+ all-reduce when sharded)
   void cross(Side s, const TS& Xa, const TS& Xb, double* G) {
     const size_t mk = mark();
-    const int ns = gram_slots(Xa.rows);
-    double* slots = alloc((int64_t)ns * Xa.w * Xb.w);
-    if (live()) {
-      chk(launch_cross_gram(Xa.p, Xa.ld, Xa.w, Xb.p, Xb.ld, Xb.w, Xa.rows, slots, ns, st));
-      chk(launch_slots_reduce_small(slots, ns, (int64_t)Xa.w * Xb.w, G, st));
+    if (big_skinny(Xa.rows, Xa.w, Xb.w) && Xa.w >= 8) {
+      gram_dmma(Xa, Xb, G);
+    } else {
+      const int ns = gram_slots(Xa.rows);
+      double* slots = alloc((int64_t)ns * Xa.w * Xb.w);
+      if (live()) {
+        chk(launch_cross_gram(Xa.p, Xa.ld, Xa.w, Xb.p, Xb.ld, Xb.w, Xa.rows, slots, ns, st));
+        chk(launch_slots_reduce_small(slots, ns, (int64_t)Xa.w * Xb.w, G, st));
+      }
     }
     release(mk);
     if (sharded(s)) allreduce(G, (int64_t)Xa.w * Xb.w);
+  }
+
+  // ---- tall-skinny products on the FP64 tensor cores, as views of a transposed operand.
+  // A column-major rows x w block Q is, byte for byte, a row-major w x rows matrix Q^T, so
+  //   Q^T X  = view A X   with A = Q^T   (k_view_ax; reduction over the long dimension)
+  //   Q M    = view A^T M with A = Q^T   (k_view_aty; reduction over w)
+  // Used where the product is large enough for the view kernels' fixed costs (C3-C5 blocks).
+  static bool big_skinny(int64_t rows, int w, int c) { return (double)rows * w * c >= 5.0e7 && rows >= 8192; }
+
+  // one view launch (fp64) on the row-major matrix Ar (ar x nr, lda), X column-major (kdim x w, ldx);
+  // result column-major (out_rows x w) into dst (ldd), split-K partial slots summed in order
+  void view_raw(int kind, const double* Ar, int64_t ar, int64_t nr, int64_t lda_r, const double* X, int64_t ldx,
+                int w, double* dst, int64_t ldd) {
+    for (int c0 = 0; c0 < w; c0 += kMaxWT * 8) {
+      const int wc = std::min(kMaxWT * 8, w - c0);
+      const size_t mk = mark();
+      ViewArgs a;
+      a.A = Ar;
+      a.rows = ar;
+      a.n = nr;
+      a.lda = lda_r;
+      a.X = X + (int64_t)c0 * ldx;
+      a.ldx = ldx;
+      a.w = wc;
+      a.grid_cap = ctx->sms;
+      plan_view(kind, ar, nr, wc, ctx->sms, &a.S, &a.KTS);
+      const int64_t orows = (kind == VIEW_AX) ? ar : nr;
+      double* d = dst + (int64_t)c0 * ldd;
+      double* slots = (a.S == 1) ? d : alloc((int64_t)a.S * ldd * wc);
+      a.out = slots;
+      a.ldo = ldd;
+      a.slot_stride = ldd * wc;
+      if (live()) {
+        chk(kind == VIEW_AX ? launch_view_ax(a, st) : launch_view_aty(a, st));
+        if (a.S > 1) chk(launch_slot_sum(slots, ldd, a.slot_stride, a.S, orows, wc, d, ldd, st));
+      }
+      release(mk);
+    }
+  }
+
+  // G (a x b, col-major ld a) = Xa^T Xb over the rows (no all-reduce here)
+  void gram_dmma(const TS& Xa, const TS& Xb, double* G) {
+    view_raw(VIEW_AX, Xa.p, Xa.w, Xa.rows, Xa.ld, Xb.p, Xb.ld, Xb.w, G, Xa.w);
+  }
+
+  // out (rows x c, ldo) = in (rows x w, ldi) M (w x c, ldm); mode 1: out -= in M
+  void tsmm(const double* in, int64_t ldi, int64_t rows, int w, const double* M, int64_t ldm, int c, double* out,
+            int64_t ldo, int mode) {
+    if (!big_skinny(rows, w, c) || w < 8 || ((ldm * 8) & 15) || (reinterpret_cast<uintptr_t>(M) & 15)) {
+      if (live()) chk(launch_ts_gemm(in, ldi, rows, w, M, ldm, c, out, ldo, mode, st));
+      return;
+    }
+    if (mode == 0) {
+      view_raw(VIEW_ATY, in, w, rows, ldi, M, ldm, c, out, ldo);
+      return;
+    }
+    const size_t mk = mark();
+    const int64_t ldt = round_up(rows, 32);
+    double* T = alloc(ldt * c);
+    view_raw(VIEW_ATY, in, w, rows, ldi, M, ldm, c, T, ldt);
+    if (live()) chk(launch_sub_cols(T, ldt, out, ldo, rows, c, st));
+    release(mk);
   }
 
   // CholeskyQR2 in place: Y <- Q, R_out (w x w) = R2 R1 if requested.  `ref` (w) optional
@@ -374,24 +440,18 @@ struct Exec {
       const double rows_all = (double)(s == SIDE_M ? m * ctx->nranks : Y.rows);
       const double coef = 11.0 * (rows_all * w + (double)w * (w + 1)) * 1.1102230246251565e-16;
       cross(s, Y, Y, G);
-      if (live()) {
-        chk(launch_chol_ref(G, nullptr, w, 0.0, R0, R0i, nullptr, st, coef));
-        chk(launch_ts_gemm(Y.p, Y.ld, Y.rows, w, R0i, w, w, T.p, T.ld, 0, st));
-        chk(launch_copy_cols(T.p, T.ld, Y.p, Y.ld, Y.rows, w, st));
-      }
+      if (live()) chk(launch_chol_ref(G, nullptr, w, 0.0, R0, R0i, nullptr, st, coef));
+      tsmm(Y.p, Y.ld, Y.rows, w, R0i, w, w, T.p, T.ld, 0);
+      if (live()) chk(launch_copy_cols(T.p, T.ld, Y.p, Y.ld, Y.rows, w, st));
       if (R_out) set_err(ctx, "internal: shifted orth does not return R");
     }
     cross(s, Y, Y, G);
-    if (live()) {
-      chk(launch_chol_ref(G, ref, w, 1e-12, R1, R1i, ctx->dstat, st));
-      chk(launch_ts_gemm(Y.p, Y.ld, Y.rows, w, R1i, w, w, T.p, T.ld, 0, st));
-    }
+    if (live()) chk(launch_chol_ref(G, ref, w, 1e-12, R1, R1i, ctx->dstat, st));
+    tsmm(Y.p, Y.ld, Y.rows, w, R1i, w, w, T.p, T.ld, 0);
     cross(s, T, T, G);
-    if (live()) {
-      chk(launch_chol_ref(G, nullptr, w, 1e-12, R2, R2i, nullptr, st));
-      chk(launch_ts_gemm(T.p, T.ld, T.rows, w, R2i, w, w, Y.p, Y.ld, 0, st));
-      if (R_out) chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R_out, w, st));
-    }
+    if (live()) chk(launch_chol_ref(G, nullptr, w, 1e-12, R2, R2i, nullptr, st));
+    tsmm(T.p, T.ld, T.rows, w, R2i, w, w, Y.p, Y.ld, 0);
+    if (live() && R_out) chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R_out, w, st));
     release(mk);
   }
 
@@ -425,7 +485,7 @@ struct Exec {
                                R1i, ctx->dstat, st));
         chk(launch_cholqr_pass(Y.p, Y.ld, T.p, T.ld, Y.rows, w, R1i, slots, ctx->counter, 1e-12, 0.0, 1, R2, R2i,
                                nullptr, st));
-        chk(launch_ts_gemm(T.p, T.ld, T.rows, w, R2i, w, w, Y.p, Y.ld, 0, st));
+        chk(launch_ts_gemm(T.p, T.ld, T.rows, w, R2i, w, w, Y.p, Y.ld, 0, st));   // w <= 64: FMA kernel
         if (R_out) chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R_out, w, st));
       } else {
         chk(launch_cholqr_pass(Y.p, Y.ld, nullptr, 0, Y.rows, w, nullptr, slots, ctx->counter, 0.0, coef, 0, R0,
@@ -456,10 +516,10 @@ struct Exec {
         TS Qp = slice(K, 0, c0);
         double* C = alloc((int64_t)c0 * wc);
         cross(s, Qp, Wb, C);
-        if (live()) chk(launch_ts_gemm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1, st));
+        tsmm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1);
         orth(s, Wb, nullptr, nullptr, /*shifted=*/true);
         cross(s, Qp, Wb, C);
-        if (live()) chk(launch_ts_gemm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1, st));
+        tsmm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1);
       }
       orth(s, Wb, nullptr, nullptr);
       release(mk);
@@ -468,7 +528,7 @@ struct Exec {
 
   // out (rows x k, ldo) = Q (rows x w) * Mk (w x k, ld w)
   void lift(const TS& Q, const double* Mk, int k, double* out, int64_t ldo) {
-    if (live()) chk(launch_ts_gemm(Q.p, Q.ld, Q.rows, Q.w, Mk, Q.w, k, out, ldo, 0, st));
+    tsmm(Q.p, Q.ld, Q.rows, Q.w, Mk, Q.w, k, out, ldo, 0);
   }
 
   void core_svd(const double* M, int w, int trans, double* Ul, double* Sv, double* Vr) {
@@ -686,7 +746,7 @@ void alg_single_pass(Exec& E) {
     double* sv = E.alloc(l);
     E.core_svd(Rc, l, 1, Vr, sv, Ul);
     TS Q2 = E.new_ts(SIDE_M, lp);
-    if (E.live()) E.chk(launch_ts_gemm(Yc.p, Yc.ld, Yc.rows, l, Ul, l, lp, Q2.p, Q2.ld, 0, E.st));
+    E.tsmm(Yc.p, Yc.ld, Yc.rows, l, Ul, l, lp, Q2.p, Q2.ld, 0);
     Qc = Q2;
   }
   // ---- line 11: [Qh, Rh] = qr(Phi^* Q_c)   (l2 x lp, tiny; replicated)
@@ -721,7 +781,7 @@ void alg_single_pass(Exec& E) {
     E.chk(launch_small_gemm(0, 1, l2, lp, lp, C.p, C.ld, Rhi, lp, T, l2, E.st));
   }
   TS Xt = E.new_ts(SIDE_N, lp);
-  if (E.live()) E.chk(launch_ts_gemm(Yr.p, Yr.ld, Yr.rows, l2, T, l2, lp, Xt.p, Xt.ld, 0, E.st));
+  E.tsmm(Yr.p, Yr.ld, Yr.rows, l2, T, l2, lp, Xt.p, Xt.ld, 0);
   // ---- line 13: tsvd(X, k) via X^T = Qx Rx  ->  X = Rx^T Qx^T,  svd(Rx^T) = Uh Lam Wh^T
   double* Rx = E.alloc((int64_t)lp * lp);
   E.orth(SIDE_N, Xt, Rx, nullptr);
@@ -820,7 +880,7 @@ void alg_nystrom(Exec& E) {
   }
   // line 13: F = C_L^-1 Y_r^T  ->  F^T = Y_r R^-1
   TS Ft = E.new_ts(SIDE_N, l);
-  if (E.live()) E.chk(launch_ts_gemm(Yr.p, Yr.ld, Yr.rows, l, Ri, l, l, Ft.p, Ft.ld, 0, E.st));
+  E.tsmm(Yr.p, Yr.ld, Yr.rows, l, Ri, l, l, Ft.p, Ft.ld, 0);
   // line 14: [~, Lam_hat, V] = tsvd(F, k)
   double* lam = E.alloc(l);
   TS Qf;

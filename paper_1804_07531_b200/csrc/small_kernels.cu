@@ -1315,3 +1315,19 @@ int launch_nys_eig(const double* lam, int k, const double* nu, double* lam2, cud
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 }  // namespace rsvd
+
+namespace rsvd {
+namespace {
+__global__ void k_sub_cols(const double* __restrict__ T, int64_t ldt, double* __restrict__ out, int64_t ldo,
+                           int64_t rows, int c) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (r < rows && j < c) out[(int64_t)j * ldo + r] -= T[(int64_t)j * ldt + r];
+}
+}  // namespace
+int launch_sub_cols(const double* T, int64_t ldt, double* out, int64_t ldo, int64_t rows, int c, cudaStream_t st) {
+  if (rows <= 0 || c <= 0) return RSVD_OK;
+  k_sub_cols<<<dim3((unsigned)((rows + 255) / 256), (unsigned)c), 256, 0, st>>>(T, ldt, out, ldo, rows, c);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+}  // namespace rsvd
