@@ -278,6 +278,10 @@ int launch_ts_gemm(const double* in, int64_t ldi, int64_t rows, int w, const dou
 // M = (W S^-1) S J^T  ->  left vectors W_j / s_j, right vectors J, values s_j = |W_j|.
 constexpr int kJacThreads = 1024;
 constexpr int kJacMaxC = 512;
+// RPL: rows (and J entries) per lane held in registers during a rotation (r, ce <= 32 RPL): every
+// load of a column pair is issued before any store (a load -> rotate -> store loop serialises on
+// the possible aliasing of the two columns)
+template <int RPL>
 __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict__ M, int64_t ldm, int trans, int r,
                                                         int c, double* __restrict__ Ul, double* __restrict__ Sv,
                                                         double* __restrict__ Vr, double* __restrict__ gW,
@@ -318,12 +322,19 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
         if (p > q) { const int tt = p; p = q; q = tt; }
         double* wp = W + (int64_t)p * r;
         double* wq = W + (int64_t)q * r;
+        double xr[RPL], yr[RPL];
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+          const int i = lane + 32 * t;
+          xr[t] = (i < r) ? wp[i] : 0.0;
+          yr[t] = (i < r) ? wq[i] : 0.0;
+        }
         double a = 0.0, b = 0.0, cc = 0.0;
-        for (int i = lane; i < r; i += 32) {
-          const double x = wp[i], y = wq[i];
-          a = fma(x, x, a);
-          b = fma(y, y, b);
-          cc = fma(x, y, cc);
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+          a = fma(xr[t], xr[t], a);
+          b = fma(yr[t], yr[t], b);
+          cc = fma(xr[t], yr[t], cc);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -333,23 +344,46 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
         }
         if (cc != 0.0 && fabs(cc) > tol * sqrt(a * b)) {
           // t = tan(theta), the smaller root of t^2 + 2 zeta t - 1 = 0, zeta = (b - a) / (2 c):
-          // t = sign(d) e / (|d| + sqrt(d^2 + e^2)) with d = b - a, e = 2c
+          // t = sign(d) e / (|d| + sqrt(d^2 + e^2)) with d = b - a, e = 2c.  Formed in fp32 from
+          // the fp64 ratio when it is in range (any t gives an exactly orthogonal fp64 rotation,
+          // cs = rsqrt(1 + t^2), sn = cs t; an approximate angle only leaves a ~1e-7 fraction of
+          // the off-diagonal for the next sweep) — as in k_jacobi_small
           const double d = b - a, e = 2.0 * cc;
-          const double t = copysign(1.0, d) * e / (fabs(d) + sqrt(fma(d, d, e * e)));
+          const double ad = fabs(d), ae = fabs(e);
+          double t;
+          if (ad > 1e-30 && ad < 1e30 && ae > 1e-30 && ae < 1e30) {
+            const float rf = (float)e / (float)ad;
+            t = copysign(1.0, d) * (double)(rf / (1.0f + sqrtf(fmaf(rf, rf, 1.0f))));
+          } else {
+            t = copysign(1.0, d) * e / (ad + sqrt(fma(d, d, e * e)));
+          }
           const double cs = rsqrt(fma(t, t, 1.0));
           const double sn = cs * t;
-          for (int i = lane; i < r; i += 32) {
-            const double x = wp[i], y = wq[i];
-            wp[i] = cs * x - sn * y;
-            wq[i] = sn * x + cs * y;
+#pragma unroll
+          for (int t = 0; t < RPL; ++t) {
+            const int i = lane + 32 * t;
+            if (i < r) {
+              wp[i] = cs * xr[t] - sn * yr[t];
+              wq[i] = sn * xr[t] + cs * yr[t];
+            }
           }
           if (want_j) {
             double* jp = J + (int64_t)p * ce;
             double* jq = J + (int64_t)q * ce;
-            for (int i = lane; i < ce; i += 32) {
-              const double x = jp[i], y = jq[i];
-              jp[i] = cs * x - sn * y;
-              jq[i] = sn * x + cs * y;
+            double xj[RPL], yj[RPL];
+#pragma unroll
+            for (int t = 0; t < RPL; ++t) {
+              const int i = lane + 32 * t;
+              xj[t] = (i < ce) ? jp[i] : 0.0;
+              yj[t] = (i < ce) ? jq[i] : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < RPL; ++t) {
+              const int i = lane + 32 * t;
+              if (i < ce) {
+                jp[i] = cs * xj[t] - sn * yj[t];
+                jq[i] = sn * xj[t] + cs * yj[t];
+              }
             }
           }
           if (lane == 0) rotated = 1;
@@ -444,12 +478,17 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
   const size_t smem = (w_in ? wbytes : 0) + (j_in ? jbytes : 0);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
+    cudaFuncSetAttribute(k_jacobi<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
+    cudaFuncSetAttribute(k_jacobi<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
     attr = true;
   }
   const double tol = 2.220446049250313e-16 * sqrt((double)r);  // LAPACK dgesvj's CTOL
-  k_jacobi<<<1, kJacThreads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, scratch + kJacMaxC * kJacMaxC,
-                                         w_in, j_in, tol, 60, want_j, status);
+  if (r <= 128)
+    k_jacobi<4><<<1, kJacThreads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, scratch + kJacMaxC * kJacMaxC,
+                                              w_in, j_in, tol, 60, want_j, status);
+  else
+    k_jacobi<16><<<1, kJacThreads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, scratch + kJacMaxC * kJacMaxC,
+                                               w_in, j_in, tol, 60, want_j, status);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
