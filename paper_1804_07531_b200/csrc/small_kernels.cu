@@ -6,6 +6,7 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace rsvd {
 
@@ -203,7 +204,11 @@ int launch_chol_big(const double* G, const double* ref, int w, double tol, doubl
 
 int launch_chol_ref(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
                     DevStatus* status, cudaStream_t st, double shift_coef) {
-  if (w > kCholMaxW) return launch_chol_big(G, ref, w, tol, R, Rinv, status, st, shift_coef);
+  static const int big_from = [] {
+    const char* e = getenv("RSVD_CHOL_BIG_FROM");
+    return e ? atoi(e) : kCholMaxW + 1;
+  }();
+  if (w > kCholMaxW || w >= big_from) return launch_chol_big(G, ref, w, tol, R, Rinv, status, st, shift_coef);
   if (w < 1) return RSVD_E_ARG;
   const size_t smem = (size_t)w * w * 8 + (size_t)w * 4 + 16;
   static bool attr = false;
@@ -466,7 +471,11 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
                     double* scratch, DevStatus* status, cudaStream_t st, int want_j) {
   if (c < 1 || c > kJacMaxC || r < c || r > kJacMaxC) return RSVD_E_ARG;
   if (r <= 64) return launch_jacobi_small(M, ldm, trans, r, c, Ul, S, Vr, status, st, want_j);
-  if (c > 128) return launch_jacobi_cluster(M, ldm, trans, r, c, Ul, S, Vr, scratch, status, st, want_j);
+  static const int cl_from = [] {
+    const char* e = getenv("RSVD_JACOBI_CLUSTER_FROM");
+    return e ? atoi(e) : 129;
+  }();
+  if (c >= cl_from) return launch_jacobi_cluster(M, ldm, trans, r, c, Ul, S, Vr, scratch, status, st, want_j);
   // 64 < c <= 128: always accumulate J — both singular-vector sets then stay orthonormal to
   // rounding even for the trailing small sigma (C4's k = 100 core, sigma_100 / sigma_1 = 1e-3)
   want_j = 1;
