@@ -310,7 +310,9 @@ struct FusedCfg {
   static constexpr int SMEM = STAGES * STAGE + OM_BYTES + 1024 + (2 * STAGES + 2) * 8;
 };
 
-template <int L2T>
+// LTC: Y_c n-tiles per warp (warp groups 0/1 take n-tiles g, g+2, ...; LTC = ceil(LT/2)) — a
+// compile-time count, because predicated-off DMMAs still take issue slots
+template <int L2T, int LTC>
 __global__ void __launch_bounds__(kThreads, 1)
     k_view_fused(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmOm,
                  const __grid_constant__ CUtensorMap tmPhi, double* __restrict__ yc, int64_t ldyc,
@@ -421,32 +423,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // ---- Y_c(tile rows) = A_tile Omega_strip  (ax pattern; K = BN = 64 -> 8 double-steps)
       {
-        double accc[5][2];
+        double accc[LTC][2];
 #pragma unroll
-        for (int i = 0; i < 5; ++i) accc[i][0] = accc[i][1] = 0.0;
+        for (int i = 0; i < LTC; ++i) accc[i][0] = accc[i][1] = 0.0;
 #pragma unroll 1
         for (int kk = 0; kk < C::BN / 8; ++kk) {
           const int box = kk >> 1;
           const uint32_t q = ((kk & 1) << 2) + t;
           const double2 a = *reinterpret_cast<const double2*>(As + box * kBK * 128 + sw128(yc_mt * 8 + pg, q));
-          double2 b[5];
+          double2 b[LTC];
 #pragma unroll
-          for (int i = 0; i < 5; ++i) {
+          for (int i = 0; i < LTC; ++i) {
             const int nt = yc_n0 + 2 * i;
             if (nt < LT) b[i] = *reinterpret_cast<const double2*>(om + box * LP * 128 + sw128(nt * 8 + pg, q));
           }
 #pragma unroll
-          for (int i = 0; i < 5; ++i)
+          for (int i = 0; i < LTC; ++i)
             if (yc_n0 + 2 * i < LT) dmma(accc[i][0], accc[i][1], a.x, b[i].x);
 #pragma unroll
-          for (int i = 0; i < 5; ++i)
+          for (int i = 0; i < LTC; ++i)
             if (yc_n0 + 2 * i < LT) dmma(accc[i][0], accc[i][1], a.y, b[i].y);
         }
         const int r = kt * kBK + yc_mt * 8 + pg;
         if (r < rows) {
           double* o = yc + (yc_atomic ? 0 : (int64_t)sb * yc_slot_stride);
 #pragma unroll
-          for (int i = 0; i < 5; ++i) {
+          for (int i = 0; i < LTC; ++i) {
             const int nt = yc_n0 + 2 * i;
             if (nt < LT) {
               const int c0 = nt * 8 + t, c1 = c0 + 4;
@@ -570,7 +572,7 @@ int launch_aty_t(const ViewArgs& a, cudaStream_t st) {
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
-template <int L2T>
+template <int L2T, int LTC>
 int launch_fused_t(const FusedArgs& a, cudaStream_t st) {
   using C = FusedCfg<L2T>;
   const int LP = ((a.l + 7) / 8) * 8;
@@ -584,10 +586,10 @@ int launch_fused_t(const FusedArgs& a, cudaStream_t st) {
   const int grid = std::min(U, a.grid_cap);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_view_fused<L2T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(k_view_fused<L2T, LTC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  k_view_fused<L2T><<<grid, kThreads, C::SMEM, st>>>(tmA, tmOm, tmPhi, a.yc, a.ldyc, a.yc_slot_stride, a.yc_atomic,
+  k_view_fused<L2T, LTC><<<grid, kThreads, C::SMEM, st>>>(tmA, tmOm, tmPhi, a.yc, a.ldyc, a.yc_slot_stride, a.yc_atomic,
                                                        a.yr, a.ldyr, a.yr_slot_stride, (int)a.rows, (int)a.n, a.l,
                                                        LP, a.l2, NSB, a.S, KT, a.KTS);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
@@ -607,8 +609,11 @@ template <int WT>
 struct AxRun { static int run(const ViewArgs& a, cudaStream_t st) { return launch_ax_t<WT>(a, st); } };
 template <int WT>
 struct AtyRun { static int run(const ViewArgs& a, cudaStream_t st) { return launch_aty_t<WT>(a, st); } };
-template <int L2T>
-struct FusedRun { static int run(const FusedArgs& a, cudaStream_t st) { return launch_fused_t<L2T>(a, st); } };
+template <int LTC>
+struct FusedRunL {
+  template <int L2T>
+  struct R { static int run(const FusedArgs& a, cudaStream_t st) { return launch_fused_t<L2T, LTC>(a, st); } };
+};
 
 }  // namespace
 
@@ -645,7 +650,15 @@ int launch_view_aty(const ViewArgs& a, cudaStream_t st) {
 int launch_view_fused(const FusedArgs& a, cudaStream_t st) {
   const int L2T = (a.l2 + 7) / 8;
   if (a.l < 1 || a.l > kFusedMaxL || L2T < 1 || L2T > kFusedMaxL2T) return RSVD_E_ARG;
-  return dispatch<FusedRun>(L2T, a, st, Seq<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17>{});
+  using S18 = Seq<0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17>;
+  const int LTC = ((a.l + 7) / 8 + 1) / 2;  // 1..5 (l <= 72)
+  switch (LTC) {
+    case 1: return dispatch<FusedRunL<1>::template R>(L2T, a, st, S18{});
+    case 2: return dispatch<FusedRunL<2>::template R>(L2T, a, st, S18{});
+    case 3: return dispatch<FusedRunL<3>::template R>(L2T, a, st, S18{});
+    case 4: return dispatch<FusedRunL<4>::template R>(L2T, a, st, S18{});
+    default: return dispatch<FusedRunL<5>::template R>(L2T, a, st, S18{});
+  }
 }
 
 }  // namespace rsvd
