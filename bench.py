@@ -243,10 +243,17 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = S.CONFIGS[args.config]
-    ctx = rsvd.Context(local)
+    # the step's three SVD calls are independent: one context (own stream, own communicator)
+    # per call, enqueued with RSVD_ASYNC and run concurrently; `ctx` (the first) also serves the
+    # sequential per-algorithm timings
+    # the first context keeps torch's current stream (ordered with the inputs' producers)
+    streams = [torch.cuda.current_stream(dev)] + [torch.cuda.Stream(dev) for _ in STEP_PLAN[1:]]
+    ctxs = [rsvd.Context(local, stream=s_) for s_ in streams]
+    ctx = ctxs[0]
     if world > 1:
-        uid = broadcast_uid(rsvd.get_unique_id() if rank == 0 else None, rank)
-        ctx.comm_init(world, rank, uid)
+        for c_ in ctxs:
+            uid = broadcast_uid(rsvd.get_unique_id() if rank == 0 else None, rank)
+            c_.comm_init(world, rank, uid)
 
     # ---- inputs: rank r holds rows [r*m, (r+1)*m) of A_global = [U_1;..;U_N] diag(sigma) V^T / sqrt(N)
     m, n = cfg.m, cfg.n
@@ -261,16 +268,27 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def step(flags=0, Ax=A, Omx=Om, Phix=Phi, host_out=False):
+        concurrent = not (flags & rsvd.RSVD_PROFILE)
+        cur = torch.cuda.current_stream(dev)
         infos = []
-        for alg, v in STEP_PLAN:
+        for (alg, v), c_, s_ in zip(STEP_PLAN, ctxs, streams):
+            c = c_ if concurrent else ctx
+            fl = flags | (rsvd.RSVD_ASYNC if concurrent else 0)
+            if concurrent and s_ != cur:
+                s_.wait_stream(cur)   # after the L2 flush / start event on the current stream
             if alg == "subspace":
-                r = ctx.subspace(Ax, cfg.k, cfg.p, v, Omx, flags=flags, m=M_glob, row0=row0, host_out=host_out)
+                r = c.subspace(Ax, cfg.k, cfg.p, v, Omx, flags=fl, m=M_glob, row0=row0, host_out=host_out)
             elif alg == "krylov":
-                r = ctx.block_krylov(Ax, cfg.k, cfg.p, v, Omx, flags=flags, m=M_glob, row0=row0, host_out=host_out)
+                r = c.block_krylov(Ax, cfg.k, cfg.p, v, Omx, flags=fl, m=M_glob, row0=row0, host_out=host_out)
             else:
-                r = ctx.single_pass(Ax, cfg.k, cfg.p, cfg.l2, Omx, Phix, flags=flags, m=M_glob, row0=row0,
-                                    host_out=host_out)
+                r = c.single_pass(Ax, cfg.k, cfg.p, cfg.l2, Omx, Phix, flags=fl, m=M_glob, row0=row0,
+                                  host_out=host_out)
             infos.append(r[3])
+        if concurrent:
+            for c_, s_, inf in zip(ctxs, streams, infos):
+                c_.wait(inf)
+                if s_ != cur:
+                    cur.wait_stream(s_)   # the end event follows all three calls
         return infos
 
     def barrier():
@@ -381,7 +399,8 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: fp64 {m * world}x{n} (row block {m}x{n} per GPU), Haar factors, "
                                    f"sigma_i=1 (i<=20) then 10^(-0.25(i-20)); k={cfg.k}, p={cfg.p}, l2={cfg.l2}; "
-                                   "step = subspace v=3 + block Krylov v=4 + single pass (8 views of A)",
+                                   "step = subspace v=3 + block Krylov v=4 + single pass (8 views of A), "
+                                   "the three independent calls concurrent on three streams (RSVD_ASYNC)",
                        "l2_flush": "256 MiB write before every timed step (outside the events)",
                        "parallelism": f"row-sharded A over {world} GPU(s), NCCL all-reduce" if world > 1 else "1 GPU"},
             "views_per_s": world * step_views() * args.steps / (total_ms * 1e-3) / world,
@@ -394,7 +413,8 @@ def main():
         line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    ctx.close()
+    for c_ in ctxs:
+        c_.close()
     if world > 1:
         dist.destroy_process_group()
 

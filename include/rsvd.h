@@ -77,6 +77,7 @@ enum {
 #define RSVD_NO_GRAPH     2u   /* enqueue kernels directly instead of replaying a CUDA graph    */
 #define RSVD_PROFILE      4u   /* record CUDA events around every view kernel (info->view_*)     */
 #define RSVD_CORE_NO_J    16u  /* rsvd_core_svd: V = M^T U S^-1 instead of accumulated rotations  */
+#define RSVD_ASYNC        32u  /* enqueue only: outputs and info complete after rsvd_wait(ctx) */
 #define RSVD_SIM_SHARDS_SHIFT 8 /* debug: bits 8..15 = number of virtual row shards (loopback) */
 
 typedef struct {
@@ -115,6 +116,12 @@ const char* rsvd_strerror(int code);
 const char* rsvd_last_error(const rsvd_ctx* ctx);
 int  rsvd_version(void);                                /* 100 * major + minor               */
 int  rsvd_sm_count(const rsvd_ctx* ctx);
+/* Completes a call made with RSVD_ASYNC on this ctx: synchronises the ctx stream, fills the
+ * device-side fields of info (rank-deficient columns, Jacobi sweeps) and returns the call's
+ * numerical status.  Until then the caller must not read the outputs nor modify the inputs,
+ * and the ctx accepts no other call (RSVD_E_STATE).  Several contexts on different streams run
+ * their asynchronous calls concurrently.  Returns RSVD_OK when nothing is pending. */
+int  rsvd_wait(rsvd_ctx* ctx, rsvd_info* info);
 /* Roofline denominators measured on this device: FP64 DMMA (mma.sync m8n8k4) throughput in
  * TFLOP/s (register operands, all SMs) and streaming HBM read bandwidth in GB/s (4 GiB buffer,
  * best of 5).  Allocates 4 GiB temporarily; synchronous. */

@@ -94,6 +94,9 @@ struct rsvd_ctx {
   std::map<std::string, int> graph_kernels;  // kernel nodes per cached graph
   std::vector<cudaEvent_t> events;
   std::string err;
+  // RSVD_ASYNC: the call's host-side results, completed by rsvd_wait
+  bool pending = false;
+  rsvd_info pending_info;
 };
 
 namespace {
@@ -1096,6 +1099,14 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
   call.kV = ptr_kind(call.V, ctx->device);
   call.kR = ptr_kind(call.R, ctx->device);
   const bool profile = (call.flags & RSVD_PROFILE) != 0;
+  if (ctx->pending) {
+    set_err(ctx, "a RSVD_ASYNC call on this ctx has not been completed by rsvd_wait");
+    return RSVD_E_STATE;
+  }
+  if (profile && (call.flags & RSVD_ASYNC)) {
+    set_err(ctx, "RSVD_PROFILE cannot be combined with RSVD_ASYNC");
+    return RSVD_E_ARG;
+  }
   // ---- 1. sizing pass (fake base)
   Exec sz(ctx, call, true, nullptr);
   bind_A(sz, call);
@@ -1211,6 +1222,26 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
       }
   }
   if (rc == RSVD_OK) cudaMemcpyAsync(ctx->hstat, ctx->dstat, sizeof(DevStatus), cudaMemcpyDefault, st);
+  rsvd_info base_info;
+  memset(&base_info, 0, sizeof(base_info));
+  base_info.graph_replayed = replay ? 1 : 0;
+  base_info.host_staged = (call.kA == PTR_HOST || call.kOm == PTR_HOST || call.kPhi == PTR_HOST ||
+                           call.kU == PTR_HOST || call.kV == PTR_HOST || call.kS == PTR_HOST)
+                              ? 1
+                              : 0;
+  if (sz.a_restaged && call.kA == PTR_DEVICE) base_info.host_staged = 2;
+  base_info.view_launches = sz.view_launches;
+  if (use_graph) base_info.kernel_launches = ctx->graph_kernels[key];
+  base_info.view_bytes = sz.view_bytes;
+  base_info.view_flops = sz.view_flops;
+  base_info.nondeterministic = sz.nondet;
+  if ((call.flags & RSVD_ASYNC) && rc == RSVD_OK) {
+    // enqueued only: rsvd_wait synchronises the stream and completes the info
+    ctx->pending = true;
+    ctx->pending_info = base_info;
+    if (info) *info = base_info;
+    return RSVD_OK;
+  }
   cudaError_t se = cudaStreamSynchronize(st);
   if (se != cudaSuccess) {
     set_err(ctx, "CUDA error: %s", cudaGetErrorString(se));
@@ -1223,19 +1254,11 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
   }
   const DevStatus hs = *ctx->hstat;
   if (info) {
+    const int32_t st0 = info->status;
+    *info = base_info;
+    info->status = st0;
     info->rank_deficient_cols = hs.deficient;
     info->jacobi_sweeps = hs.jacobi_sweeps;
-    info->graph_replayed = replay ? 1 : 0;
-    info->host_staged = (call.kA == PTR_HOST || call.kOm == PTR_HOST || call.kPhi == PTR_HOST ||
-                         call.kU == PTR_HOST || call.kV == PTR_HOST || call.kS == PTR_HOST)
-                            ? 1
-                            : 0;
-    if (sz.a_restaged && call.kA == PTR_DEVICE) info->host_staged = 2;
-    info->view_launches = sz.view_launches;
-    if (use_graph) info->kernel_launches = ctx->graph_kernels[key];
-    info->view_bytes = sz.view_bytes;
-    info->view_flops = sz.view_flops;
-    info->nondeterministic = sz.nondet;
     if (profile && !E.ev_pairs.empty()) {
       double vm = 0;
       for (size_t i = 1; i < E.ev_pairs.size(); ++i) {
@@ -1365,6 +1388,38 @@ int rsvd_destroy(rsvd_ctx* c) {
 }
 
 int rsvd_sm_count(const rsvd_ctx* c) { return c ? c->sms : 0; }
+
+int rsvd_wait(rsvd_ctx* c, rsvd_info* info) {
+  if (!c) return RSVD_E_ARG;
+  if (!c->pending) return RSVD_OK;
+  cudaSetDevice(c->device);
+  c->pending = false;
+  cudaError_t se = cudaStreamSynchronize(c->stream);
+  if (se != cudaSuccess) {
+    set_err(c, "CUDA error: %s", cudaGetErrorString(se));
+    if (info) info->status = RSVD_E_CUDA;
+    return RSVD_E_CUDA;
+  }
+  const DevStatus hs = *c->hstat;
+  if (info) {
+    const int32_t views = info->views;
+    const int64_t vectors = info->vectors;
+    const int32_t lc = info->lc_used;
+    *info = c->pending_info;
+    info->views = views;
+    info->vectors = vectors;
+    info->lc_used = lc;
+    info->rank_deficient_cols = hs.deficient;
+    info->jacobi_sweeps = hs.jacobi_sweeps;
+    info->status = RSVD_OK;
+  }
+  if (hs.jacobi_fail) {
+    set_err(c, "Jacobi SVD of the core did not converge");
+    if (info) info->status = RSVD_E_NUMERIC;
+    return RSVD_E_NUMERIC;
+  }
+  return RSVD_OK;
+}
 
 int rsvd_probe_peaks(rsvd_ctx* c, double* dmma_tflops, double* read_gbs) {
   if (!c || !dmma_tflops || !read_gbs) return RSVD_E_ARG;

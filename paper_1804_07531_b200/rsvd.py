@@ -19,11 +19,11 @@ LIB_PATH = os.path.join(_HERE, "librsvd.so")
 RSVD_F32, RSVD_F64 = 1, 2
 RSVD_INPUT_A, RSVD_INPUT_AT = 0, 1
 RSVD_GOAL_SVD, RSVD_GOAL_LEFT, RSVD_GOAL_RIGHT, RSVD_GOAL_NORMAL = 0, 1, 2, 3
-RSVD_SQUARED, RSVD_NO_GRAPH, RSVD_PROFILE, RSVD_CORE_NO_J = 1, 2, 4, 16
+RSVD_SQUARED, RSVD_NO_GRAPH, RSVD_PROFILE, RSVD_CORE_NO_J, RSVD_ASYNC = 1, 2, 4, 16, 32
 ERR = {0: "RSVD_OK", -1: "RSVD_E_ARG", -2: "RSVD_E_DTYPE", -3: "RSVD_E_CUDA", -4: "RSVD_E_NCCL",
        -5: "RSVD_E_NOMEM", -6: "RSVD_E_NUMERIC", -7: "RSVD_E_STATE"}
 
-EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_strerror", "rsvd_last_error", "rsvd_version", "rsvd_sm_count",
+EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_wait", "rsvd_strerror", "rsvd_last_error", "rsvd_version", "rsvd_sm_count",
            "rsvd_recommend_input", "rsvd_probe_peaks", "rsvd_get_unique_id", "rsvd_comm_init", "rsvd_comm_nranks", "rsvd_subspace",
            "rsvd_block_krylov", "rsvd_single_pass", "rsvd_nystrom", "rsvd_pinched", "rsvd_view", "rsvd_view_fused",
            "rsvd_orth", "rsvd_core_svd"]
@@ -74,6 +74,7 @@ def lib():
     L.rsvd_last_error.argtypes = [vp]
     L.rsvd_last_error.restype = ctypes.c_char_p
     L.rsvd_sm_count.argtypes = [vp]
+    L.rsvd_wait.argtypes = [vp, pinfo]
     L.rsvd_recommend_input.argtypes = [i32, i32]
     L.rsvd_get_unique_id.argtypes = [vp]
     L.rsvd_probe_peaks.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
@@ -161,6 +162,12 @@ class Context:
         t, g = ctypes.c_double(), ctypes.c_double()
         self._check(lib().rsvd_probe_peaks(self._h, ctypes.byref(t), ctypes.byref(g)), "rsvd_probe_peaks")
         return t.value, g.value
+
+    def wait(self, info=None):
+        """Complete an RSVD_ASYNC call on this context (synchronises its stream)."""
+        inf = info if info is not None else RsvdInfo()
+        self._check(lib().rsvd_wait(self._h, ctypes.byref(inf)), "rsvd_wait")
+        return inf
 
     def _check(self, rc, what):
         if rc:
