@@ -289,29 +289,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     OT(2 + 6 * ps);
     cluster.sync();
     OT(3 + 6 * ps);
+    // reduce-scatter over the whole cluster: upper-triangle entry e is summed (partials of CTA
+    // 0..C-1, in that order) by one thread of one CTA and written into CTA 0's G over DSMEM; the
+    // thread reads CTA 0's partial of e before overwriting it and no other thread touches e
+    {
+      double* G0 = cluster.map_shared_rank(G, 0);
+      for (int e = crank * kThreads + tid; e < W * W; e += C * kThreads) {
+        const int i = e % W, jj = e / W;
+        if (i <= jj) {
+          double v[kCluster];
+#pragma unroll
+          for (int k = 0; k < kCluster; ++k) v[k] = (k < C) ? cluster.map_shared_rank(G, k)[e] : 0.0;
+          double sum = v[0];
+#pragma unroll
+          for (int k = 1; k < kCluster; ++k) sum += v[k];
+          if (jj >= w) sum = (i == jj) ? 1.0 : 0.0;
+          G0[e] = sum;
+        }
+      }
+    }
+    cluster.sync();
     if (crank == 0) {
-      // bookkeeping warps (>= CW): fixed-order DSMEM sum of the cluster's upper-triangle
-      // partials, identity padding, mirror, second-pass test; factorisation warps (< CW) wait
+      // bookkeeping warps (>= CW): mirror, second-pass test; factorisation warps (< CW) wait
       constexpr int CW = chol_warps<W>();
       const int bt = tid - 32 * CW, nbt = kThreads - 32 * CW;
-      if (warp >= CW) {
-        for (int e = bt; e < W * W; e += nbt) {
-          const int i = e % W, jj = e / W;
-          if (i <= jj) {
-            double v[kCluster];
-#pragma unroll
-            for (int k = 0; k < kCluster; ++k) v[k] = (k < C) ? cluster.map_shared_rank(G, k)[e] : 0.0;
-            double sum = v[0];
-#pragma unroll
-            for (int k = 1; k < kCluster; ++k) sum += v[k];
-            if (jj >= w) sum = (i == jj) ? 1.0 : 0.0;
-            G[e] = sum;
-          }
-        }
-        if (bt == 0) {
-          fast = (kind == PASS_SECOND) ? 1 : 0;
-          mode = (kind == PASS_SECOND) ? 0 : 1;
-        }
+      if (warp >= CW && bt == 0) {
+        fast = (kind == PASS_SECOND) ? 1 : 0;
+        mode = (kind == PASS_SECOND) ? 0 : 1;
       }
       __syncthreads();
       if (warp >= CW)
