@@ -32,7 +32,9 @@ import numpy as np
 
 __all__ = [
     "qr", "orth", "tsvd", "chol_lower", "jacobi_svd",
-    "std_subspace_iteration", "gen_subspace_iteration", "qrqc", "one_view_tropp",
+    "std_subspace_iteration", "gen_subspace_iteration", "qrqc", "one_view_tropp", "one_view_woolfe",
+    "plan_flat", "plan_decay", "plan_rapid", "plan_balanced", "minvar_spectra", "minvar_select",
+    "one_view_minvar",
     "gen_block_krylov", "normal_matrix_tevd", "nystrom_tevd", "pinched_tevd", "recommend_input", "svd_of",
     "views_and_vectors", "rel_frobenius_error", "rel_spectral_error", "projector_distance",
     "residual_fro", "half_power_lhs_rhs", "thm_bound",
@@ -248,6 +250,151 @@ def one_view_tropp(A, p, l1, l2, lc, Omega_r, Omega_c, transpose=False, _op=None
     return Qc @ Uh, lam, Vp                       # line 14
 
 
+# ============================================================ Algorithm 8
+
+def one_view_woolfe(A, p, l1, l2, lc, Omega_r, Omega_c, transpose=False, _op=None):
+    """Alg. 8 — randomized 1-view TSVD, Woolfe variant.
+
+    Both bases are truncated to their p + l_c leading singular directions (lines 4-6) and the
+    small least-squares problem (Omega_c^* Q_c) Xh = Y_r^* Q_r (line 7) is solved by QR, as
+    Alg. 7 line 11-12 does."""
+    if not (0 <= lc <= l1 <= l2):
+        raise ValueError("Alg. 8 needs 0 <= l_c <= l_1 <= l_2 (P:701)")
+    op = _op or _Op(A, transpose)
+    Omega_r = _f64(Omega_r)
+    Omega_c = _f64(Omega_c)
+    Yc = op.apply(Omega_r)                        # line 3 a)
+    Yr = op.adjoint(Omega_c)                      # line 3 b)
+    op.views -= 1                                 # one logical pass (P:684)
+    Qc, Rc = qr(Yc)                               # line 4 a)
+    Qr, Rr = qr(Yr)                               # line 4 b)
+    Qhc, _, _ = tsvd(Rc, p + lc)                  # line 5 a)
+    Qhr, _, _ = tsvd(Rr, p + lc)                  # line 5 b)
+    Qc = Qc @ Qhc                                 # line 6 a)
+    Qr = Qr @ Qhr                                 # line 6 b)
+    Qh, Rh = qr(Omega_c.T @ Qc)                   # line 7: least squares via QR
+    Xh = np.linalg.solve(Rh, Qh.T @ (Yr.T @ Qr))
+    Uh, lam, Vh = tsvd(Xh, p)                     # line 8
+    return Qc @ Uh, lam, Qr @ Vh                  # line 9 c), d)
+
+
+# ============================================================ oversampling (P:600-641, P:722-728)
+
+def plan_flat(p, T):
+    """Eq. (overflat): l_1 for a flat spectrum, l_2 = T - 2p - l_1 (needs T >= 2p + 6,
+    P:604)."""
+    if T < 2 * p + 6:
+        raise ValueError("T >= 2p + 6 required (P:604)")
+    num = np.sqrt(p * (T - p - 2) * (1.0 - 2.0 / (T - 1))) - (p - 1)
+    l1 = max(2, int(np.floor((T - 1) * num / (T - 2 * p - 1))) - p)
+    return l1, T - 2 * p - l1
+
+
+def plan_decay(p, T):
+    """Eq. (overmed), P:620-629: l_1 = max{2, floor((T-1)/3) - p}."""
+    if T < 2 * p + 6:
+        raise ValueError("T >= 2p + 6 required (P:604)")
+    l1 = max(2, (T - 1) // 3 - p)
+    return l1, T - 2 * p - l1
+
+
+def plan_rapid(p, T):
+    """Eq. (overrapid), P:631-639: l_1 = floor((T-2)/2) - p."""
+    if T < 2 * p + 6:
+        raise ValueError("T >= 2p + 6 required (P:604)")
+    l1 = (T - 2) // 2 - p
+    return l1, T - 2 * p - l1
+
+
+def plan_balanced(p, T, alpha):
+    """l_1 ~= l_2 with l_1 = floor(T/2) - p and l_c = floor(alpha l_1), 0 <= alpha <= 1
+    (Eq. lcutfixedratio, P:716-722).  Returns (l1, l2, lc)."""
+    if not (0.0 <= alpha <= 1.0):
+        raise ValueError("0 <= alpha <= 1 (P:720)")
+    l1 = T // 2 - p
+    l2 = T - 2 * p - l1
+    return l1, l2, int(np.floor(alpha * l1))
+
+
+# ============================================================ minimum-variance l_c (P:739-794)
+
+def minvar_spectra(Yc, Yr, Omega_c, p, l1):
+    """lambda_{1..p}(l_c) for l_c = 0..l_1: the top-p singular values of X(l_c) of Alg. 7 with
+    Q_c = the p + l_c leading left singular vectors of Y_c (one SVD of Y_c, one
+    Omega_c^* Q_c product, the first p + l_c columns per trial).  Each trial solves its own
+    least-squares problem by QR as Alg. 7 lines 11-12.  Returns a (l_1 + 1) x p array."""
+    Yc, Yr, Omega_c = _f64(Yc), _f64(Yr), _f64(Omega_c)
+    Qc, Rc = qr(Yc)
+    Uc, _, _ = tsvd(Rc, Rc.shape[1])              # left singular vectors of Y_c = Q_c U_c
+    M = Omega_c.T @ (Qc @ Uc)
+    lam = np.zeros((l1 + 1, p))
+    for lc in range(l1 + 1):
+        Qh, Rh = qr(M[:, :p + lc])
+        X = np.linalg.solve(Rh, Qh.T @ Yr.T)
+        lam[lc] = np.linalg.svd(X, compute_uv=False)[:p]
+    return lam
+
+
+def _ratio(a, b):
+    """lambda_i(j) / lambda_i(l_c) with 0/0 = 1 and a/0 = inf (reading R20)."""
+    if b > 0:
+        return a / b
+    return 1.0 if a == 0 else np.inf
+
+
+def minvar_select(lam):
+    """Eq. (MinVar): s(l_c) stacks lambda_i(l_c - 1)/lambda_i(l_c) (l_c > 0),
+    lambda_i(l_c)/lambda_i(l_c) and lambda_i(l_c + 1)/lambda_i(l_c); l_c^MinVar = argmin Var[s(l_c)]
+    over 0 <= l_c < l_1.  Var is the unbiased sample variance and ties go to the smallest l_c
+    (readings R19, R20).  lam: (l_1 + 1) x p.  Returns (lc, variances)."""
+    l1 = lam.shape[0] - 1
+    if l1 <= 0:
+        return 0, np.zeros(0)
+    var = np.zeros(l1)
+    for lc in range(l1):
+        s = []
+        for j in ([lc - 1] if lc > 0 else []) + [lc, lc + 1]:
+            s += [_ratio(lam[j, i], lam[lc, i]) for i in range(lam.shape[1])]
+        s = np.array(s)
+        if not np.all(np.isfinite(s)):
+            var[lc] = np.inf
+            continue
+        mu = sum(s) / len(s)
+        var[lc] = sum((x - mu) ** 2 for x in s) / (len(s) - 1)
+    best = 0
+    for lc in range(1, l1):
+        if var[lc] < var[best]:
+            best = lc
+    return best, var
+
+
+def one_view_minvar(A, p, l1, l2, Omega_r, Omega_c, transpose=False, _op=None):
+    """Alg. 7 with l_c chosen by the minimum-variance post-processing.  The trials
+    reuse the one view's sketches ('does not require re-evaluating the sketches').
+    Returns (U, lam, V, lc)."""
+    op = _op or _Op(A, transpose)
+    Yc = op.apply(_f64(Omega_r))
+    Yr = op.adjoint(_f64(Omega_c))
+    op.views -= 1
+    lc, _ = minvar_select(minvar_spectra(Yc, Yr, Omega_c, p, l1))
+    U, lam, V = one_view_tropp(None, p, l1, l2, lc, Omega_r, Omega_c, _op=_Sketched(op, Yc, Yr))
+    return U, lam, V, lc
+
+
+class _Sketched:
+    """Replays an already-taken pair of sketches (Y_c, Y_r) to Alg. 7 without touching A again."""
+
+    def __init__(self, op, Yc, Yr):
+        self.op, self.Yc, self.Yr = op, Yc, Yr
+        self.views = op.views + 1
+
+    def apply(self, X):
+        return self.Yc
+
+    def adjoint(self, X):
+        return self.Yr
+
+
 # ============================================================ Algorithm 9 (P:900-928)
 
 def gen_block_krylov(A, p, l, v, Omega_r, transpose=False, _op=None, return_basis=False):
@@ -307,9 +454,14 @@ def svd_of(A, algorithm, k, p, v=None, Omega=None, l2=None, lc=None, Phi=None, t
         U, s, V = gen_subspace_iteration(None, k, p, v, Omega, _op=op)
     elif algorithm == "krylov":
         U, s, V = gen_block_krylov(None, k, p, v, Omega, _op=op)
+    elif algorithm == "single_pass" and lc == "minvar":
+        U, s, V, _ = one_view_minvar(None, k, p, l2 - k, Omega, Phi, _op=op)
     elif algorithm == "single_pass":
         lc = p if lc is None else lc
         U, s, V = one_view_tropp(None, k, p, l2 - k, lc, Omega, Phi, _op=op)
+    elif algorithm == "woolfe":
+        lc = p if lc is None else lc
+        U, s, V = one_view_woolfe(None, k, p, l2 - k, lc, Omega, Phi, _op=op)
     else:
         raise ValueError(algorithm)
     if transpose:

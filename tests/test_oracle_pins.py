@@ -489,3 +489,113 @@ def test_nystrom_more_accurate_than_pinched():
             err_n.append(np.linalg.norm(N - (V * lam2) @ V.T, 2))
             err_p.append(np.linalg.norm(N - (Vp * lp) @ Vp.T, 2))
     assert np.mean(err_n) < np.mean(err_p)
+
+
+# ---------------------------------------------------------------- f3: adaptive single pass
+
+@pytest.mark.parametrize("plan,p,T,expect", [
+    # hand evaluation of Eq. (overflat) P:610-618 at p=5, T=24:
+    # sqrt(5*17*(1-2/23)) = 8.8096; -(p-1) -> 4.8096; *23/13 = 8.509 -> 8 - 5 = 3; l2 = 24-10-3 = 11
+    ("flat", 5, 24, (3, 11)),
+    ("flat", 5, 16, (2, 4)),        # max{2, .} floor
+    ("decay", 5, 24, (2, 12)),      # max{2, floor(23/3) - 5 = 2}
+    ("decay", 5, 40, (8, 22)),      # floor(39/3) - 5 = 8
+    ("rapid", 5, 24, (6, 8)),       # floor(22/2) - 5 = 6
+    ("rapid", 5, 16, (2, 4)),       # floor(14/2) - 5 = 2
+])
+def test_oversampling_plans_worked_values(plan, p, T, expect):
+    f = {"flat": O.plan_flat, "decay": O.plan_decay, "rapid": O.plan_rapid}[plan]
+    assert f(p, T) == expect
+    l1, l2 = f(p, T)
+    assert 0 <= l1 <= l2 and 2 * p + l1 + l2 == T
+
+
+def test_oversampling_plans_invariants_and_errors():
+    for p in range(1, 12):
+        for T in range(2 * p + 6, 2 * p + 80):
+            for f in (O.plan_flat, O.plan_decay, O.plan_rapid):
+                l1, l2 = f(p, T)
+                assert 2 <= l1 <= l2 and 2 * p + l1 + l2 == T
+    # l1 = floor(T/2) - p = 7, l2 = 7, lc = floor(0.5 * 7) = 3   (Eq. lcutfixedratio)
+    assert O.plan_balanced(5, 24, 0.5) == (7, 7, 3)
+    assert O.plan_balanced(5, 24, 1.0)[2] == 7 and O.plan_balanced(5, 24, 0.0)[2] == 0
+    with pytest.raises(ValueError):
+        O.plan_flat(5, 15)
+
+
+def test_minvar_select_hand_table():
+    """Eq. (MinVar) on hand-made spectra (p = 2, l_1 = 3).
+    s(0) = [1, 1, .5, .5]          -> unbiased var = 4 * (1/4)^2 / 3 = 1/12
+    s(1) = [2, 2, 1, 1, 1, 1]      -> mean 4/3, sum sq dev = 2*(2/3)^2 + 4*(1/3)^2 = 4/3 -> /5 = 4/15
+    s(2) = [1, 1, 1, 1, 1, 1]      -> 0   => l_c = 2."""
+    lam = np.array([[4.0, 2.0], [2.0, 1.0], [2.0, 1.0], [2.0, 1.0]])
+    lc, var = O.minvar_select(lam)
+    assert lc == 2
+    np.testing.assert_allclose(var, [1 / 12, 4 / 15, 0.0], atol=1e-15)
+    # ties: all variances zero -> the smallest l_c (reading R19)
+    lc, var = O.minvar_select(np.array([[2.0, 1.0]] * 4))
+    assert lc == 0 and np.all(var == 0)
+    # l_1 = 1: the only candidate is 0; l_1 = 0: l_c = 0 (empty range, reading R20)
+    assert O.minvar_select(np.array([[3.0, 1.0], [1.0, 1.0]]))[0] == 0
+    assert O.minvar_select(np.array([[3.0, 1.0]]))[0] == 0
+    # zero spectra: 0/0 = 1, a/0 = inf -> that candidate is skipped (reading R20)
+    lam = np.array([[1.0, 0.0], [1.0, 1.0], [1.0, 1.0], [1.0, 1.0]])
+    lc, var = O.minvar_select(lam)
+    # s(1) = [1, 0, 1, 1, 1, 1] (var 1/6), s(2) = ones (var 0)
+    assert np.isinf(var[0]) and lc == 2 and abs(var[1] - 1 / 6) <= 1e-15
+
+
+def test_minvar_spectra_equal_alg7_per_trial():
+    """The trial spectra reuse one SVD of Y_c and slice Omega_c^* Q_c; each must equal
+    the lambda of a full Alg. 7 run at that l_c (Alg. 7 lines 4-13, its own QR-then-TSVD path)."""
+    cfg = S.CONFIGS["C2"]
+    A = S.make_matrix(cfg, 600, 500)
+    k, l1, l2 = 8, 6, 14
+    Om = S.random_gaussian_matrix(500, k + l1, seed=11)
+    Phi = S.random_gaussian_matrix(600, k + l2, seed=12)
+    lam = O.minvar_spectra(A @ Om, A.T @ Phi, Phi, k, l1)
+    for lc in range(l1 + 1):
+        _, ref, _ = O.one_view_tropp(A, k, l1, l2, lc, Om, Phi)
+        np.testing.assert_allclose(lam[lc], ref, rtol=1e-10)
+
+
+def test_minvar_exact_rank_picks_zero():
+    """Exactly rank r <= p: every trial recovers sigma(A) exactly, s(l_c) = 1, all variances ~0;
+    the chosen l_c's output is exact."""
+    rng = np.random.default_rng(3)
+    X = np.linalg.qr(rng.standard_normal((300, 4)))[0]
+    Y = np.linalg.qr(rng.standard_normal((200, 4)))[0]
+    sig = np.array([5.0, 3.0, 2.0, 1.0])
+    A = X @ np.diag(sig) @ Y.T
+    Om = rng.standard_normal((200, 9))
+    Phi = rng.standard_normal((300, 14))
+    U, s, V, lc = O.one_view_minvar(A, 5, 4, 9, Om, Phi)
+    lam = O.minvar_spectra(A @ Om, A.T @ Phi, Phi, 5, 4)
+    np.testing.assert_allclose(lam[:, :4], np.tile(sig, (5, 1)), rtol=1e-10)
+    np.testing.assert_allclose(s[:4], sig, rtol=1e-10)
+    assert np.linalg.norm(A - (U * s) @ V.T) <= 1e-10 * np.linalg.norm(A)
+
+
+def test_woolfe_equals_tropp_when_square():
+    """l_c = l_1 = l_2: Q_r spans A^* Omega_c exactly, so Y_r^* Q_r Q_r^* = Y_r^* and Alg. 8's
+    X_hat Q_r^* equals Alg. 7's X: identical rank-p approximations (P:696-713 vs P:660-682)."""
+    cfg = S.CONFIGS["C2"]
+    A = S.make_matrix(cfg, 400, 300)
+    k, l1 = 6, 6
+    Om = S.random_gaussian_matrix(300, k + l1, seed=21)
+    Phi = S.random_gaussian_matrix(400, k + l1, seed=22)
+    Uw, sw, Vw = O.one_view_woolfe(A, k, l1, l1, l1, Om, Phi)
+    Ut, st, Vt = O.one_view_tropp(A, k, l1, l1, l1, Om, Phi)
+    np.testing.assert_allclose(sw, st, rtol=1e-9)
+    assert proj(Uw, Ut) <= 1e-8 and proj(Vw, Vt) <= 1e-8
+
+
+def test_woolfe_exact_rank_and_orthonormal():
+    rng = np.random.default_rng(5)
+    X = np.linalg.qr(rng.standard_normal((250, 3)))[0]
+    Y = np.linalg.qr(rng.standard_normal((180, 3)))[0]
+    A = X @ np.diag([4.0, 2.0, 1.0]) @ Y.T
+    U, s, V = O.one_view_woolfe(A, 3, 3, 6, 1, rng.standard_normal((180, 6)), rng.standard_normal((250, 9)))
+    np.testing.assert_allclose(s, [4.0, 2.0, 1.0], rtol=1e-10)
+    assert np.linalg.norm(A - (U * s) @ V.T) <= 1e-10 * np.linalg.norm(A)
+    np.testing.assert_allclose(V.T @ V, np.eye(3), atol=1e-12)
