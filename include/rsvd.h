@@ -78,6 +78,8 @@ enum {
 #define RSVD_PROFILE      4u   /* record CUDA events around every view kernel (info->view_*)     */
 #define RSVD_CORE_NO_J    16u  /* rsvd_core_svd: V = M^T U S^-1 instead of accumulated rotations  */
 #define RSVD_ASYNC        32u  /* enqueue only: outputs and info complete after rsvd_wait(ctx) */
+#define RSVD_WOOLFE       64u  /* rsvd_single_pass: Alg. 8 (Woolfe variant) instead of Alg. 7   */
+#define RSVD_LC_MINVAR    (-2) /* rsvd_single_pass lc: minimum-variance l_c          */
 #define RSVD_SIM_SHARDS_SHIFT 8 /* debug: bits 8..15 = number of virtual row shards (loopback) */
 
 typedef struct {
@@ -95,7 +97,7 @@ typedef struct {
   int64_t vectors;              /* matrix-vector products (Alg. 2: v l; Alg. 9: (v+floor(v/2)-1) l) */
   int32_t rank_deficient_cols;  /* columns zeroed by the guarded Cholesky (exact rank < l)   */
   int32_t jacobi_sweeps;        /* sweeps of the last core SVD                               */
-  int32_t lc_used;              /* l_c of the single pass                                     */
+  int32_t lc_used;              /* l_c of the single pass (the chosen one for RSVD_LC_MINVAR) */
   int32_t host_staged;          /* 1 if any argument was host memory; 2 if a device A had to be
                                    copied to a 16-byte-aligned block (TMA needs lda*8 % 16 == 0) */
   int32_t graph_replayed;       /* 1 if the call replayed a cached CUDA graph                 */
@@ -158,11 +160,34 @@ int rsvd_block_krylov(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, int
                       unsigned flags, rsvd_info* info);
 
 /* Alg. 7, input = A.  Omega n x (k+p) replicated; Phi m_local x l2 (this rank's rows
- * of the co-range test matrix, P:667b); l2 >= k + p (P:663 l_2 >= l_1); lc in [0, p] or -1 (= p). */
+ * of the co-range test matrix, P:667b); l2 >= k + p (P:663 l_2 >= l_1); lc in [0, p] or -1 (= p).
+ *
+ * lc = RSVD_LC_MINVAR: l_c = argmin_{0 <= l_c < p} Var[s(l_c)] (Eq. MinVar), chosen on
+ *   the device from the one view's sketches (no second view): one SVD of Y_c, one QR of
+ *   M = Phi^T Q_c U_c, the trial spectra of X(l_c) for l_c = 0..p (one CTA each), Var = unbiased
+ *   sample variance, ties -> smallest l_c, 0/0 = 1 and a/0 = inf in s(l_c) (R19-R20);
+ *   p = 0 gives l_c = 0.  The rest of Alg. 7 then runs at width k + p with the columns beyond
+ *   k + l_c zeroed (identical to truncating).  info->lc_used returns the choice;
+ *   info->rank_deficient_cols then also counts those zeroed columns.  Needs k + p <= 512.
+ * flags & RSVD_WOOLFE: Alg. 8 instead: Q_c and Q_r both truncated to their k + l_c
+ *   leading singular directions, Xh from (Phi^T Q_c) Xh = Y_r^T Q_r (QR), U = Q_c Uh, V = Q_r Vh.
+ *   Not combinable with RSVD_LC_MINVAR (RSVD_E_ARG). */
 int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int lc,
                      const void* Omega, int64_t ld_omega, const void* Phi, int64_t ld_phi,
                      void* U, int64_t ldu, void* S, void* V, int64_t ldv,
                      unsigned flags, rsvd_info* info);
+
+/* Oversampling plans for the single pass from a sketch-size budget T = 2k + l_1 + l_2 (host only,
+ * no GPU needed).  Writes the ABI arguments: *p = l_1, *l2 = k + l_2 (the co-range width), *lc.
+ *   RSVD_PLAN_FLAT      Eq. (overflat)  P:610-618, lc = l_1        (needs T >= 2k + 6)
+ *   RSVD_PLAN_DECAY     Eq. (overmed)   P:620-629, lc = l_1
+ *   RSVD_PLAN_RAPID     Eq. (overrapid), lc = l_1
+ *   RSVD_PLAN_BALANCED  l_1 = floor(T/2) - k, l_2 = T - 2k - l_1, lc = floor(alpha l_1)
+ *                       (Eq. lcutfixedratio, P:716-722, 0 <= alpha <= 1); pass lc = RSVD_LC_MINVAR
+ *                       to the single pass instead for the adaptive choice.
+ * Returns RSVD_E_ARG for a budget below 2k + 6, k < 1 or alpha outside [0, 1]. */
+enum { RSVD_PLAN_FLAT = 0, RSVD_PLAN_DECAY = 1, RSVD_PLAN_RAPID = 2, RSVD_PLAN_BALANCED = 3 };
+int rsvd_plan(int scheme, int k, int T, double alpha, int* p, int* l2, int* lc);
 
 /* ---- primitives (single GPU; for unit tests and the benchmark's kernel timing) -------------- */
 /* ---------------------------------------------------------------------------------------------

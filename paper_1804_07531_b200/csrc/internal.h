@@ -83,6 +83,7 @@ struct DevStatus {
   int jacobi_sweeps;
   int jacobi_fail;
   int numeric_fail;     // e.g. singular R-hat
+  int minvar_lc;        // l_c chosen by the minimum-variance post-processing (minvar.cu)
 };
 
 // out[c][r] = sum_{s<S} in[s][c][r] for c < w, r < rows   (column-major, slot stride)
@@ -125,5 +126,13 @@ int launch_axpy_dev(double* Y, int64_t ldy, const double* Q, int64_t ldq, int64_
                     cudaStream_t st);
 int launch_symmetrize(const double* B, int w, double* S, cudaStream_t st);
 int launch_nys_eig(const double* lam, int k, const double* nu, double* lam2, cudaStream_t st);
+
+// minimum-variance l_c (minvar.cu): trial spectra lam ((p+1) x k) from Z = R_y Qh
+// (l2 x l, ld l2) and Rhi = Rh^-1 (l x l, ld l); the selection into *out; zero columns >= k + *lc.
+int64_t minvar_scratch(int l2, int l, int p);
+int launch_minvar_trials(const double* Z, int l2, int l, const double* Rhi, int k, int p, double* lam,
+                         double* scratch, cudaStream_t st);
+int launch_minvar_select(const double* lam, int k, int p, int* out, cudaStream_t st);
+int launch_mask_cols(double* X, int64_t ld, int64_t rows, int w, int k, const int* lc, cudaStream_t st);
 
 }  // namespace rsvd

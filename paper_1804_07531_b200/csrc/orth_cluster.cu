@@ -9,7 +9,7 @@
 //              CTA 0: fixed-order DSMEM sum of the partials, guarded Cholesky G = R^T R and
 //              R^-1 (thread j owns column j, in registers)          -> cluster barrier
 //              every CTA copies R^-1 from CTA 0's shared memory (DSMEM)
-//   end:       apply the last R^-1, write Q over Y; R_out = R_2 R_1
+//   end:       apply the last R^-1, write Q over Y; R_out = R_2 R_1 (R_2 R_1 R_0 when shifted)
 // Same numerics as the pass kernels (small_kernels.cu): rank guard d_j <= tol * ref_j zeroes
 // row j of R and column j of R^-1; the second pass takes the first-order closed form when
 // |G - I| <= 1e-8.  The kernel is compiled per padded width W (multiple of 8): the padding
@@ -243,7 +243,7 @@ __device__ __forceinline__ void gram_tiles(const double* Yc, int rpc, double* G,
 template <int W>
 __global__ void __launch_bounds__(kThreads, 1)
     k_orth_cluster(double* __restrict__ Y, int64_t ldy, int64_t rows, int w, int rpc, int shifted, double shift_coef,
-                   double* __restrict__ Rout, double* __restrict__ Rw /* 2 w*w global scratch */,
+                   double* __restrict__ Rout, double* __restrict__ Rw /* 3 w*w global scratch */,
                    DevStatus* status) {
   constexpr int NT = W / 8, NTILES = NT * (NT + 1) / 2;
   constexpr int ld = oc_ld(W);
@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int npass = shifted ? 3 : 2;
   double* R1 = Rw;             // R of the guard pass (global scratch, w x w)
   double* Rc = Rw + w * w;     // R of the current pass
+  double* R0 = Rw + 2 * w * w; // R of the shift pass (shifted only)
   for (int ps = 0; ps < npass; ++ps) {
     const int kind = shifted ? ps : ps + 1;  // PASS_SHIFT / PASS_GUARD / PASS_SECOND
     if (ps > 0) {
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           shift = shift_coef * tr;
         }
         const double tol = (kind == PASS_SHIFT) ? 0.0 : 1e-12;
-        double* Rdst = (kind == PASS_GUARD) ? R1 : Rc;
+        double* Rdst = (kind == PASS_GUARD) ? R1 : (kind == PASS_SHIFT) ? R0 : Rc;
         const int cnt = chol_inv_cols<W>(G, w, shift, tol, Rdst, Ri, ld, bc);
         if (tid == 0) mode = 1;
         if (tid == 0 && kind == PASS_GUARD && cnt && status) atomicAdd(&status->deficient, cnt);
@@ -385,10 +386,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     apply_rinv<W>(Yc, Ri, rpc, warp, g, t4, Y + r0, ldy, nr, w);
   }
-  // R_out = R_2 R_1 (upper triangular product), CTA 0
+  // R_out = R_2 R_1 (R_2 R_1 R_0 when shifted; upper triangular products), CTA 0
   if (Rout && crank == 0) {
-    // stage R_2 in shared memory (G is free on CTA 0 now), R_1 is read from global (L1/L2)
     __syncthreads();
+    if (shifted) {
+      // R_1 <- R_1 R_0: stage R_1 in shared memory (G is free on CTA 0 now), R_0 from global
+      for (int e = tid; e < w * w; e += kThreads) G[e] = R1[e];
+      __syncthreads();
+      for (int e = tid; e < w * w; e += kThreads) {
+        const int i = e % w, k = e / w;
+        double sa[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = i; q <= k; ++q) sa[q & 3] = fma(G[q * w + i], R0[k * w + q], sa[q & 3]);
+        R1[e] = (i <= k) ? (sa[0] + sa[1]) + (sa[2] + sa[3]) : 0.0;
+      }
+      __syncthreads();
+    }
+    // stage R_2 in shared memory, R_1 is read from global (L1/L2)
     const double* R1s = R1;
     for (int e = tid; e < w * w; e += kThreads) G[e] = Rc[e];
     __syncthreads();

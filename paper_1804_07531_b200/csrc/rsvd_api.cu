@@ -32,7 +32,7 @@ int probe_peaks(int sms, cudaStream_t st, double* dmma_tflops, double* read_gbs)
 int cholqr_pass_ctas(int64_t rows);
 bool orth_cluster_fits(int64_t rows, int w);
 int launch_orth_cluster(double* Y, int64_t ldy, int64_t rows, int w, int shifted, double shift_coef, double* Rout,
-                        double* Rw, DevStatus* status, cudaStream_t st);
+                        double* Rw /* 3 w*w scratch */, DevStatus* status, cudaStream_t st);
 int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo, int64_t rows, int w,
                        const double* Rin, double* slots, unsigned* counter, double tol, double shift_coef,
                        int second_pass, double* R, double* Rinv, DevStatus* status, cudaStream_t st);
@@ -437,8 +437,10 @@ struct Exec {
     double* R2 = alloc((int64_t)w * w);
     double* R2i = alloc((int64_t)w * w);
     TS T = new_ts(s, w);
+    double* R0s = nullptr;
     if (shifted) {
       double* R0 = alloc((int64_t)w * w);
+      R0s = R0;
       double* R0i = alloc((int64_t)w * w);
       const double rows_all = (double)(s == SIDE_M ? m * ctx->nranks : Y.rows);
       const double coef = 11.0 * (rows_all * w + (double)w * (w + 1)) * 1.1102230246251565e-16;
@@ -446,7 +448,6 @@ struct Exec {
       if (live()) chk(launch_chol_ref(G, nullptr, w, 0.0, R0, R0i, nullptr, st, coef));
       tsmm(Y.p, Y.ld, Y.rows, w, R0i, w, w, T.p, T.ld, 0);
       if (live()) chk(launch_copy_cols(T.p, T.ld, Y.p, Y.ld, Y.rows, w, st));
-      if (R_out) set_err(ctx, "internal: shifted orth does not return R");
     }
     cross(s, Y, Y, G);
     if (live()) chk(launch_chol_ref(G, ref, w, 1e-12, R1, R1i, ctx->dstat, st));
@@ -454,7 +455,14 @@ struct Exec {
     cross(s, T, T, G);
     if (live()) chk(launch_chol_ref(G, nullptr, w, 1e-12, R2, R2i, nullptr, st));
     tsmm(T.p, T.ld, T.rows, w, R2i, w, w, Y.p, Y.ld, 0);
-    if (live() && R_out) chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R_out, w, st));
+    if (live() && R_out) {
+      if (shifted) {  // R = R2 R1 R0 (R1i is free now)
+        chk(launch_small_gemm(0, 0, w, w, w, R1, w, R0s, w, R1i, w, st));
+        chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1i, w, R_out, w, st));
+      } else {
+        chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R_out, w, st));
+      }
+    }
     release(mk);
   }
 
@@ -466,7 +474,7 @@ struct Exec {
     const size_t mk = mark();
     if (orth_cluster_fits(Y.rows, w) && !getenv_flag("RSVD_NO_ORTH_CLUSTER")) {
       // the whole CholeskyQR2 / shifted CholeskyQR3 in one cluster launch (Y resident in smem)
-      double* Rw = alloc(2 * (int64_t)w * w);
+      double* Rw = alloc(3 * (int64_t)w * w);
       const double coef = 11.0 * ((double)Y.rows * w + (double)w * (w + 1)) * 1.1102230246251565e-16;
       if (live()) chk(launch_orth_cluster(Y.p, Y.ld, Y.rows, w, shifted ? 1 : 0, coef, R_out, Rw, ctx->dstat, st));
       release(mk);
@@ -499,7 +507,10 @@ struct Exec {
                                nullptr, st));
         chk(launch_ts_gemm(Y.p, Y.ld, Y.rows, w, R2i, w, w, T.p, T.ld, 0, st));
         chk(launch_copy_cols(T.p, T.ld, Y.p, Y.ld, Y.rows, w, st));
-        if (R_out) chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R_out, w, st));  // R0 not folded in
+        if (R_out) {  // R = R2 R1 R0
+          chk(launch_small_gemm(0, 0, w, w, w, R1, w, R0, w, R1i, w, st));
+          chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1i, w, R_out, w, st));
+        }
       }
     }
     release(mk);
@@ -684,8 +695,11 @@ constexpr double kYcSlotBudget = 4.0e9;  // bytes of deterministic Y_c partial s
 
 void alg_single_pass(Exec& E) {
   const Call& c = E.call;
-  const int l = c.k + c.p, l2 = c.l2, lc = c.lc;
-  const int lp = c.k + lc;  // width of Q_c after the optional truncation
+  const int l = c.k + c.p, l2 = c.l2;
+  const bool minvar = (c.lc == RSVD_LC_MINVAR);
+  const bool woolfe = (c.flags & RSVD_WOOLFE) != 0;
+  const int lc = minvar ? c.p : c.lc;
+  const int lp = c.k + lc;  // width of Q_c after the optional truncation; MinVar: l, masked
   TS Om = E.stage_in(SIDE_N, c.Om, c.ldom, l, c.kOm);
   TS Phi = E.stage_in(SIDE_M, c.Phi, c.ldphi, l2, c.kPhi);
   TS Yc = E.new_ts(SIDE_M, l);
@@ -743,7 +757,7 @@ void alg_single_pass(Exec& E) {
   double* Rc = E.alloc((int64_t)l * l);
   E.orth(SIDE_M, Yc, Rc, nullptr);
   TS Qc = Yc;
-  if (lc < c.p) {
+  if (lc < c.p || minvar || woolfe) {
     double* Ul = E.alloc((int64_t)l * l);
     double* Vr = E.alloc((int64_t)l * l);
     double* sv = E.alloc(l);
@@ -752,7 +766,7 @@ void alg_single_pass(Exec& E) {
     E.tsmm(Yc.p, Yc.ld, Yc.rows, l, Ul, l, lp, Q2.p, Q2.ld, 0);
     Qc = Q2;
   }
-  // ---- line 11: [Qh, Rh] = qr(Phi^* Q_c)   (l2 x lp, tiny; replicated)
+  // ---- line 11: C = Phi^* Q_c   (l2 x lp, tiny; replicated)
   TS C;
   C.rows = l2;
   C.ld = round_up(l2, 32);
@@ -763,26 +777,81 @@ void alg_single_pass(Exec& E) {
     E.cross(SIDE_M, Phi, Qc, Cg);
     if (E.live()) E.chk(launch_copy_cols(Cg, l2, C.p, C.ld, l2, lp, E.st));
   }
-  // CholeskyQR2 of C, keeping R1^-1 and R2^-1 to form Rh^-1 = R1^-1 R2^-1
+  // [Qh, Rh] = qr(X) for an l2 x lp block X (ld ldx) by CholeskyQR2: Qh overwrites X, Rh^-1 =
+  // R1^-1 R2^-1 into Rhi (lp x lp).  The guarded Cholesky zeroes exactly-zero columns.
   double* G = E.alloc((int64_t)lp * lp);
   double* R1 = E.alloc((int64_t)lp * lp);
   double* R1i = E.alloc((int64_t)lp * lp);
   double* R2 = E.alloc((int64_t)lp * lp);
   double* R2i = E.alloc((int64_t)lp * lp);
-  double* Rhi = E.alloc((int64_t)lp * lp);
-  double* T = E.alloc((int64_t)l2 * lp);
   double* Cq = E.alloc((int64_t)l2 * lp);
-  if (E.live()) {
-    E.chk(launch_small_gemm(1, 0, lp, lp, l2, C.p, C.ld, C.p, C.ld, G, lp, E.st));
+  auto qr_small = [&](double* X, int64_t ldx, double* Rhi_out) {
+    if (!E.live()) return;
+    E.chk(launch_small_gemm(1, 0, lp, lp, l2, X, ldx, X, ldx, G, lp, E.st));
     E.chk(launch_chol_ref(G, nullptr, lp, 1e-12, R1, R1i, E.ctx->dstat, E.st));
-    E.chk(launch_small_gemm(0, 0, l2, lp, lp, C.p, C.ld, R1i, lp, Cq, l2, E.st));
+    E.chk(launch_small_gemm(0, 0, l2, lp, lp, X, ldx, R1i, lp, Cq, l2, E.st));
     E.chk(launch_small_gemm(1, 0, lp, lp, l2, Cq, l2, Cq, l2, G, lp, E.st));
     E.chk(launch_chol_ref(G, nullptr, lp, 1e-12, R2, R2i, nullptr, E.st));
-    E.chk(launch_small_gemm(0, 0, l2, lp, lp, Cq, l2, R2i, lp, C.p, C.ld, E.st));   // Qh
-    E.chk(launch_small_gemm(0, 0, lp, lp, lp, R1i, lp, R2i, lp, Rhi, lp, E.st));     // Rh^-1
-    // ---- line 12: X = Rh^-1 Qh^* Y_r^*  ->  X^T = Y_r (Qh Rh^-T);  T = Qh Rh^-T  (l2 x lp)
-    E.chk(launch_small_gemm(0, 1, l2, lp, lp, C.p, C.ld, Rhi, lp, T, l2, E.st));
+    E.chk(launch_small_gemm(0, 0, l2, lp, lp, Cq, l2, R2i, lp, X, ldx, E.st));        // Qh
+    E.chk(launch_small_gemm(0, 0, lp, lp, lp, R1i, lp, R2i, lp, Rhi_out, lp, E.st));  // Rh^-1
+  };
+  double* Rhi = E.alloc((int64_t)lp * lp);
+  if (woolfe) {
+    // ---- Alg. 8 lines 4b-6b: Y_r = Q_r R_r, tsvd(R_r, k + l_c), Q_r <- Q_r Qh_r
+    double* Rr = E.alloc((int64_t)l2 * l2);
+    E.orth(SIDE_N, Yr, Rr, nullptr, /*shifted=*/true);  // Y_r can be far worse conditioned than Y_c
+    double* Ur = E.alloc((int64_t)l2 * l2);
+    double* Vrr = E.alloc((int64_t)l2 * l2);
+    double* svr = E.alloc(l2);
+    E.core_svd(Rr, l2, 1, Vrr, svr, Ur);                     // R_r = Ur S Vrr^T
+    TS Qr = E.new_ts(SIDE_N, lp);
+    E.tsmm(Yr.p, Yr.ld, Yr.rows, l2, Ur, l2, lp, Qr.p, Qr.ld, 0);
+    // ---- line 7: (Phi^* Q_c) Xh = Y_r^* Q_r = R_r^T Ur[:, :lp]   (l2 x lp)
+    double* RHS = E.alloc((int64_t)l2 * lp);
+    double* T1 = E.alloc((int64_t)lp * lp);
+    double* Xh = E.alloc((int64_t)lp * lp);
+    if (E.live()) E.chk(launch_small_gemm(1, 0, l2, lp, l2, Rr, l2, Ur, l2, RHS, l2, E.st));
+    qr_small(C.p, C.ld, Rhi);
+    if (E.live()) {
+      E.chk(launch_small_gemm(1, 0, lp, lp, l2, C.p, C.ld, RHS, l2, T1, lp, E.st));  // Qh^T RHS
+      E.chk(launch_small_gemm(0, 0, lp, lp, lp, Rhi, lp, T1, lp, Xh, lp, E.st));     // Rh^-1 (.)
+    }
+    // ---- line 8: tsvd(Xh, k) = Uh Lam Vh^T;  line 9: U = Q_c Uh, V = Q_r Vh
+    double* Ux = E.alloc((int64_t)lp * lp);
+    double* Vx = E.alloc((int64_t)lp * lp);
+    double* lam = E.alloc(lp);
+    E.core_svd(Xh, lp, 0, Ux, lam, Vx);
+    write_outputs(E, SIDE_M, SIDE_N, Qc, Qr, Ux, Vx, lam, lp, c.k);
+    return;
   }
+  if (minvar && c.p > 0) {
+    // ---- minimum-variance l_c: trial spectra from one QR of M = C (all l columns)
+    double* Cm = E.alloc((int64_t)l2 * lp);
+    double* Rhm = E.alloc((int64_t)lp * lp);
+    TS Yq = E.new_ts(SIDE_N, l2);                             // Y_r = Q_y R_y (copy: Y_r is kept)
+    double* Ry = E.alloc((int64_t)l2 * l2);
+    double* Z = E.alloc((int64_t)l2 * lp);
+    double* lamt = E.alloc((int64_t)(c.p + 1) * c.k);
+    double* scr = E.alloc(minvar_scratch(l2, lp, c.p));
+    if (E.live()) {
+      E.chk(launch_copy_cols(C.p, C.ld, Cm, l2, l2, lp, E.st));
+      E.chk(launch_copy_cols(Yr.p, Yr.ld, Yq.p, Yq.ld, Yr.rows, l2, E.st));
+    }
+    qr_small(Cm, l2, Rhm);
+    E.orth(SIDE_N, Yq, Ry, nullptr);
+    if (E.live()) {
+      E.chk(launch_small_gemm(0, 0, l2, lp, l2, Ry, l2, Cm, l2, Z, l2, E.st));       // Z = R_y Qh
+      E.chk(launch_minvar_trials(Z, l2, lp, Rhm, c.k, c.p, lamt, scr, E.st));
+      int* lc_dev = &E.ctx->dstat->minvar_lc;
+      E.chk(launch_minvar_select(lamt, c.k, c.p, lc_dev, E.st));
+      E.chk(launch_mask_cols(Qc.p, Qc.ld, Qc.rows, lp, c.k, lc_dev, E.st));
+      E.chk(launch_mask_cols(C.p, C.ld, l2, lp, c.k, lc_dev, E.st));
+    }
+  }
+  // ---- line 11: [Qh, Rh] = qr(Phi^* Q_c);  line 12: X = Rh^-1 Qh^* Y_r^*  ->  X^T = Y_r (Qh Rh^-T)
+  double* T = E.alloc((int64_t)l2 * lp);
+  qr_small(C.p, C.ld, Rhi);
+  if (E.live()) E.chk(launch_small_gemm(0, 1, l2, lp, lp, C.p, C.ld, Rhi, lp, T, l2, E.st));
   TS Xt = E.new_ts(SIDE_N, lp);
   E.tsmm(Yr.p, Yr.ld, Yr.rows, l2, T, l2, lp, Xt.p, Xt.ld, 0);
   // ---- line 13: tsvd(X, k) via X^T = Qx Rx  ->  X = Rx^T Qx^T,  svd(Rx^T) = Uh Lam Wh^T
@@ -1408,7 +1477,7 @@ int rsvd_wait(rsvd_ctx* c, rsvd_info* info) {
     *info = c->pending_info;
     info->views = views;
     info->vectors = vectors;
-    info->lc_used = lc;
+    info->lc_used = (lc == RSVD_LC_MINVAR) ? hs.minvar_lc : lc;
     info->rank_deficient_cols = hs.deficient;
     info->jacobi_sweeps = hs.jacobi_sweeps;
     info->status = RSVD_OK;
@@ -1543,7 +1612,8 @@ int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int
   if (r == RSVD_OK) {
     if (l2 < k + p) { set_err(ctx, "l2 >= k + p required (P:663)"); r = RSVD_E_ARG; }
     else if (l2 > std::min<int64_t>(A->m, 512)) { set_err(ctx, "l2 exceeds min(m, 512)"); r = RSVD_E_ARG; }
-    else if (lc < 0 || lc > p) { set_err(ctx, "lc must be in [0, p] (P:663)"); r = RSVD_E_ARG; }
+    else if ((lc < 0 || lc > p) && lc != RSVD_LC_MINVAR) { set_err(ctx, "lc must be in [0, p] (P:663)"); r = RSVD_E_ARG; }
+    else if (lc == RSVD_LC_MINVAR && (flags & RSVD_WOOLFE)) { set_err(ctx, "MinVar l_c is defined for Alg. 7 only"); r = RSVD_E_ARG; }
     else if (!Omega || !Phi) { set_err(ctx, "Omega/Phi NULL"); r = RSVD_E_ARG; }
     else if (ld_omega < A->n || ld_phi < A->m_local) { set_err(ctx, "ld_omega/ld_phi too small"); r = RSVD_E_ARG; }
     else if ((U && ldu < A->m_local) || (V && ldv < A->n)) { set_err(ctx, "ldu/ldv too small"); r = RSVD_E_ARG; }
@@ -1575,8 +1645,34 @@ int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int
     info->views = 1;
     info->vectors = (int64_t)(k + p) + l2;
     info->lc_used = lc;
+    // MinVar: the choice is made on the device (complete now unless the call is RSVD_ASYNC)
+    if (lc == RSVD_LC_MINVAR && r == RSVD_OK && !(flags & RSVD_ASYNC)) info->lc_used = ctx->hstat->minvar_lc;
   }
   return r;
+}
+
+int rsvd_plan(int scheme, int k, int T, double alpha, int* p, int* l2, int* lc) {
+  if (!p || !l2 || !lc || k < 1 || T < 2 * k + 6 || !(alpha >= 0.0 && alpha <= 1.0)) return RSVD_E_ARG;
+  int l1;
+  int cut = -1;
+  switch (scheme) {
+    case RSVD_PLAN_FLAT: {
+      const double num = std::sqrt((double)k * (T - k - 2) * (1.0 - 2.0 / (T - 1))) - (k - 1);
+      l1 = std::max(2, (int)std::floor((T - 1) * num / (T - 2 * k - 1)) - k);
+      break;
+    }
+    case RSVD_PLAN_DECAY: l1 = std::max(2, (T - 1) / 3 - k); break;
+    case RSVD_PLAN_RAPID: l1 = (T - 2) / 2 - k; break;
+    case RSVD_PLAN_BALANCED:
+      l1 = T / 2 - k;
+      cut = (int)std::floor(alpha * l1);
+      break;
+    default: return RSVD_E_ARG;
+  }
+  *p = l1;
+  *l2 = k + (T - 2 * k - l1);
+  *lc = cut >= 0 ? cut : l1;
+  return RSVD_OK;
 }
 
 static int normal_entry(int alg, rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, const void* Omega,

@@ -19,14 +19,16 @@ LIB_PATH = os.path.join(_HERE, "librsvd.so")
 RSVD_F32, RSVD_F64 = 1, 2
 RSVD_INPUT_A, RSVD_INPUT_AT = 0, 1
 RSVD_GOAL_SVD, RSVD_GOAL_LEFT, RSVD_GOAL_RIGHT, RSVD_GOAL_NORMAL = 0, 1, 2, 3
-RSVD_SQUARED, RSVD_NO_GRAPH, RSVD_PROFILE, RSVD_CORE_NO_J, RSVD_ASYNC = 1, 2, 4, 16, 32
+RSVD_SQUARED, RSVD_NO_GRAPH, RSVD_PROFILE, RSVD_CORE_NO_J, RSVD_ASYNC, RSVD_WOOLFE = 1, 2, 4, 16, 32, 64
+RSVD_LC_MINVAR = -2
+RSVD_PLAN_FLAT, RSVD_PLAN_DECAY, RSVD_PLAN_RAPID, RSVD_PLAN_BALANCED = 0, 1, 2, 3
 ERR = {0: "RSVD_OK", -1: "RSVD_E_ARG", -2: "RSVD_E_DTYPE", -3: "RSVD_E_CUDA", -4: "RSVD_E_NCCL",
        -5: "RSVD_E_NOMEM", -6: "RSVD_E_NUMERIC", -7: "RSVD_E_STATE"}
 
 EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_wait", "rsvd_strerror", "rsvd_last_error", "rsvd_version", "rsvd_sm_count",
            "rsvd_recommend_input", "rsvd_probe_peaks", "rsvd_get_unique_id", "rsvd_comm_init", "rsvd_comm_nranks", "rsvd_subspace",
            "rsvd_block_krylov", "rsvd_single_pass", "rsvd_nystrom", "rsvd_pinched", "rsvd_view", "rsvd_view_fused",
-           "rsvd_orth", "rsvd_core_svd"]
+           "rsvd_orth", "rsvd_core_svd", "rsvd_plan"]
 
 
 class RsvdMat(ctypes.Structure):
@@ -83,6 +85,8 @@ def lib():
     alg = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_subspace.argtypes = alg
     L.rsvd_block_krylov.argtypes = alg
+    L.rsvd_plan.argtypes = [i32, i32, i32, ctypes.c_double, ctypes.POINTER(i32), ctypes.POINTER(i32),
+                            ctypes.POINTER(i32)]
     L.rsvd_single_pass.argtypes = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_nystrom.argtypes = [vp, pmat, i32, i32, i32, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_pinched.argtypes = [vp, pmat, i32, i32, i32, vp, i64, vp, vp, i64, u32, pinfo]
@@ -96,6 +100,16 @@ def lib():
 
 def recommend_input(goal: int, v: int) -> int:
     return lib().rsvd_recommend_input(goal, v)
+
+
+def plan(scheme: int, k: int, T: int, alpha: float = 0.5):
+    """rsvd_plan: single-pass oversampling from the budget T = 2k + l_1 + l_2.
+    Returns the ABI arguments (p, l2, lc) of rsvd_single_pass."""
+    p, l2, lc = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    rc = lib().rsvd_plan(scheme, k, T, alpha, ctypes.byref(p), ctypes.byref(l2), ctypes.byref(lc))
+    if rc != 0:
+        raise RsvdError(rc, "rsvd_plan: T >= 2k + 6, k >= 1 and 0 <= alpha <= 1 required")
+    return p.value, l2.value, lc.value
 
 
 def get_unique_id() -> bytes:
@@ -221,7 +235,11 @@ class Context:
         return self._alg(lib().rsvd_block_krylov, "rsvd_block_krylov", A, k, p, v, Omega, input, flags, **kw)
 
     def single_pass(self, A, k, p, l2, Omega, Phi, lc=-1, flags=0, m=None, row0=0, host_out=False):
-        """Alg. 7.  lc = -1 -> lc = p (Tropp baseline)."""
+        """Alg. 7.  lc = -1 -> lc = p (Tropp baseline); lc = "minvar" (RSVD_LC_MINVAR) ->
+        minimum-variance l_c chosen on the device, returned in info.lc_used.
+        flags | RSVD_WOOLFE -> Alg. 8 (P:696-713)."""
+        if lc == "minvar":
+            lc = RSVD_LC_MINVAR
         Om, Ph = _colmajor(Omega), _colmajor(Phi)
         M = self.mat(A, m, row0)
         U = self._out_like(A, A.shape[0], k, host_out)

@@ -95,3 +95,23 @@ def test_product_package_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_rsvd_plan_matches_oracle():
+    """Host-only ABI call (no GPU): rsvd_plan against the oracle's plans."""
+    import oracle as O
+    from paper_1804_07531_b200 import rsvd
+
+    for k in range(1, 15):
+        for T in range(2 * k + 6, 2 * k + 60, 3):
+            for scheme, f in ((rsvd.RSVD_PLAN_FLAT, O.plan_flat), (rsvd.RSVD_PLAN_DECAY, O.plan_decay),
+                              (rsvd.RSVD_PLAN_RAPID, O.plan_rapid)):
+                l1, l2 = f(k, T)
+                assert rsvd.plan(scheme, k, T) == (l1, k + l2, l1)
+            for alpha in (0.0, 0.3, 0.5, 1.0):
+                l1, l2, lc = O.plan_balanced(k, T, alpha)
+                assert rsvd.plan(rsvd.RSVD_PLAN_BALANCED, k, T, alpha) == (l1, k + l2, lc)
+    for bad in ((rsvd.RSVD_PLAN_FLAT, 5, 15, 0.5), (rsvd.RSVD_PLAN_BALANCED, 5, 24, 1.5), (7, 5, 24, 0.5),
+                (rsvd.RSVD_PLAN_DECAY, 0, 24, 0.5)):
+        with pytest.raises(rsvd.RsvdError):
+            rsvd.plan(*bad)
