@@ -1060,74 +1060,80 @@ int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo
 // =====================================================================================
 namespace rsvd {
 
-// LPP lanes per column pair (2, 4 or 8), RW rows per lane (r <= LPP * RW).  With LPP = 2 and
-// c <= 32 all pairs of a round fit in one warp: rounds synchronise with __syncwarp only.
-template <int LPP, int RW>
+// LPP lanes per column pair, RW rows per lane (r <= LPP * RW); WJ: accumulate J (rotations lag one
+// round: they touch only J, and the barrier keeps each column's order).  Pair indices are computed
+// arithmetically (round-robin, player ce-1 fixed) and W's column stride is padded by 4 doubles to
+// spread the banks.  B200: the round is a latency chain (load, dots, butterfly, angle, rotate,
+// barrier); the angle uses the approximate fp64 MUFU ops (rcp/rsqrt.approx.f64): any t gives an
+// exactly orthogonal rotation because cs = rsqrt(1 + t^2) (full precision) and sn = cs t.
+template <int LPP, int RW, int WJ>
 __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__ M, int64_t ldm, int trans, int r,
                                                       int c, double* __restrict__ Ul, double* __restrict__ Sv,
                                                       double* __restrict__ Vr, double tol, int max_sweeps,
-                                                      int want_j, DevStatus* status) {
-  constexpr int RS = LPP * RW;         // padded rows of W (stride of a column)
+                                                      DevStatus* status) {
+  constexpr int RS = LPP * RW + 4;     // padded column stride of W
   extern __shared__ double jac_dyn[];
   double* W = jac_dyn;                 // 64 x RS
-  double* J = jac_dyn + 64 * RS;       // 64 x 64
-  __shared__ unsigned short pairs[63 * 32];
+  double* J = jac_dyn + 64 * RS;       // 64 x 64 (WJ); else the input B (64 x RS) for the epilogue
   __shared__ double sval[64];
   __shared__ int srank[64];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int grp = tid / LPP, sl = tid % LPP;       // pair group and its sub-lane
   const unsigned gmask = (LPP == 32 ? 0xffffffffu : ((1u << LPP) - 1u)) << (tid & 31 & ~(LPP - 1));
   const int ce = c + (c & 1);
-  const int npairs = ce >> 1;
+  const int npairs = ce >> 1, m1 = ce - 1;
   for (int e = tid; e < 64 * RS; e += nt) {
     const int i = e % RS, j = e / RS;
     double v = 0.0;
     if (i < r && j < c) v = trans ? M[(int64_t)i * ldm + j] : M[(int64_t)j * ldm + i];
     W[e] = v;
+    if (!WJ) J[e] = v;
   }
-  for (int e = tid; e < 64 * 64; e += nt) J[e] = ((e & 63) == (e >> 6)) ? 1.0 : 0.0;
-  for (int e = tid; e < (ce - 1) * npairs; e += nt) {
-    const int round = e / npairs, pi = e % npairs;
-    int p, q;
-    if (pi == 0) { p = round; q = ce - 1; }
-    else { p = (round + pi) % (ce - 1); q = (round - pi + (ce - 1)) % (ce - 1); }
-    if (p > q) { const int t = p; p = q; q = t; }
-    pairs[round * 32 + pi] = (unsigned short)(p | (q << 8));
-  }
+  if (WJ)
+    for (int e = tid; e < 64 * 64; e += nt) J[e] = ((e & 63) == (e >> 6)) ? 1.0 : 0.0;
   __syncthreads();
   const double tol2 = tol * tol;
   int sweep = 0;
   bool converged = false;
-  // J rotations lag one round (they touch only J; per-column order is kept by the barrier)
   int pj_p = 0, pj_q = 0, pj_on = 0;
   double pj_cs = 1.0, pj_sn = 0.0;
-#define RSVD_APPLY_PENDING_J()                                   \
-  if (pj_on) {                                                   \
-    double* jp = J + pj_p * 64;                                  \
-    double* jq = J + pj_q * 64;                                  \
-    for (int k = sl; k < ce; k += LPP) {                         \
-      const double u = jp[k], v = jq[k];                         \
-      jp[k] = pj_cs * u - pj_sn * v;                             \
-      jq[k] = pj_sn * u + pj_cs * v;                             \
-    }                                                            \
-    pj_on = 0;                                                   \
-  }
+  auto apply_pending_j = [&]() {
+    if (WJ && pj_on) {
+      double* jp = J + pj_p * 64;
+      double* jq = J + pj_q * 64;
+      for (int k = sl; k < ce; k += LPP) {
+        const double u = jp[k], v = jq[k];
+        jp[k] = pj_cs * u - pj_sn * v;
+        jq[k] = pj_sn * u + pj_cs * v;
+      }
+      pj_on = 0;
+    }
+  };
   const bool active = grp < npairs;
   for (; sweep < max_sweeps; ++sweep) {
     int rotated = 0;
-    for (int round = 0; round < ce - 1; ++round) {
+    for (int round = 0; round < m1; ++round) {
       if (active) {
-        const unsigned pq = pairs[round * 32 + grp];
-        const int p = pq & 255, q = pq >> 8;
+        int p, q;
+        if (grp == 0) {
+          p = round;
+          q = m1;
+        } else {
+          p = round + grp;
+          if (p >= m1) p -= m1;
+          q = round - grp;
+          if (q < 0) q += m1;
+          if (p > q) { const int tt = p; p = q; q = tt; }
+        }
         double* wp = W + p * RS;
         double* wq = W + q * RS;
         double x[RW], y[RW];
-        double a0 = 0.0, b0 = 0.0, c0 = 0.0, a1 = 0.0, b1 = 0.0, c1 = 0.0;
 #pragma unroll
         for (int t = 0; t < RW; ++t) {
           x[t] = wp[sl + LPP * t];
           y[t] = wq[sl + LPP * t];
         }
+        double a0 = 0.0, b0 = 0.0, c0 = 0.0, a1 = 0.0, b1 = 0.0, c1 = 0.0;
 #pragma unroll
         for (int t = 0; t < RW; t += 2) {
           a0 = fma(x[t], x[t], a0);
@@ -1140,7 +1146,7 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
           }
         }
         double a = a0 + a1, b = b0 + b1, cc = c0 + c1;
-        RSVD_APPLY_PENDING_J();
+        apply_pending_j();
 #pragma unroll
         for (int o = LPP / 2; o > 0; o >>= 1) {
           a += __shfl_xor_sync(gmask, a, o, LPP);
@@ -1149,20 +1155,15 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
         }
         if (cc * cc > tol2 * (a * b) && cc != 0.0) {
           rotated = 1;
-          const double d = b - a, e2 = 2.0 * cc;
-          double t;
-          const double ad = fabs(d), ae = fabs(e2);
-          if (ad > 1e-30 && ad < 1e30 && ae > 1e-30 && ae < 1e30) {
-            // tan(theta) from fp32 (any t gives an exactly orthogonal rotation below)
-            const float rf = (float)e2 / (float)ad;
-            const float tf = rf / (1.0f + sqrtf(fmaf(rf, rf, 1.0f)));
-            t = copysign(1.0, d) * (double)tf;
-          } else if (d == 0.0) {
-            t = copysign(1.0, e2);
-          } else {
-            const double rho = e2 / ad;
-            t = copysign(1.0, d) * rho / (1.0 + sqrt(fma(rho, rho, 1.0)));
-          }
+          // rho = 2c / |b - a|, t = sign(b - a) rho / (1 + sqrt(1 + rho^2)), approximate fp64 MUFU ops
+          const double d = b - a;
+          double rd, rsq, rt;
+          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(fmax(fabs(d), 1e-300)));
+          const double rho = fmin(fmax(2.0 * cc * rd, -1e100), 1e100);
+          const double s1 = fma(rho, rho, 1.0);
+          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rsq) : "d"(s1));
+          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rt) : "d"(fma(s1, rsq, 1.0)));
+          const double t = (d < 0.0 ? -rho : rho) * rt;
           const double cs = rsqrt(fma(t, t, 1.0));
           const double sn = cs * t;
 #pragma unroll
@@ -1170,10 +1171,10 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
             wp[sl + LPP * k] = cs * x[k] - sn * y[k];
             wq[sl + LPP * k] = sn * x[k] + cs * y[k];
           }
-          pj_p = p; pj_q = q; pj_cs = cs; pj_sn = sn; pj_on = want_j;
+          if (WJ) { pj_p = p; pj_q = q; pj_cs = cs; pj_sn = sn; pj_on = 1; }
         }
       }
-      if (nt <= 32) __syncwarp(); else __syncthreads();
+      __syncthreads();
     }
     if (!__syncthreads_or(rotated)) {
       converged = true;
@@ -1181,7 +1182,7 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
       break;
     }
   }
-  if (active) { RSVD_APPLY_PENDING_J(); }
+  if (active) apply_pending_j();
   __syncthreads();
   for (int j = grp; j < ce; j += (nt / LPP)) {
     double sacc = 0.0;
@@ -1213,7 +1214,7 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
       Ul[(int64_t)rk * r + i] = sj > 0.0 ? W[j * RS + i] / sj : 0.0;
     }
   }
-  if (want_j) {
+  if (WJ) {
     for (int e = tid; e < c * ce; e += nt) {
       const int i = e % c, j = e / c;
       const int rk = srank[j];
@@ -1221,20 +1222,32 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
     }
   } else {
     // right vectors from the left ones: B = W J^T with W = U S  ->  J = B^T U S^-1 (B = the
-    // input as seen by the sweep).  Accurate to ~u sigma_1 / sigma_j, i.e. for the leading
-    // triplets the algorithms use (the rsvd_core_svd primitive accumulates J instead).
-    for (int e = tid; e < c * ce; e += nt) {
-      const int a = e % c, j = e / c;       // row a of the right vector of column j
-      const int rk = srank[j];
-      if (rk < c) {
+    // input as seen by the sweep, staged in the J area).  Accurate to ~u sigma_1 / sigma_j, i.e.
+    // for the leading triplets the algorithms use (the rsvd_core_svd primitive accumulates J
+    // instead).  4 x 2 register blocks (a, j) from shared memory.
+    const double* Bs = J;
+    const int na = (c + 3) / 4, nj = ce / 2;
+    for (int e = tid; e < na * nj; e += nt) {
+      const int a0 = 4 * (e % na), j0 = 2 * (e / na);
+      double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      for (int i = 0; i < r; ++i) {
+        const double w0 = W[j0 * RS + i], w1 = W[(j0 + 1) * RS + i];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double bb = Bs[min(a0 + u, 63) * RS + i];
+          acc[u][0] = fma(bb, w0, acc[u][0]);
+          acc[u][1] = fma(bb, w1, acc[u][1]);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int j = j0 + v, rk = srank[j];
+        if (rk >= c) continue;
         const double sj = sval[j];
-        double sacc = 0.0;
-        if (sj > 0.0)
-          for (int i = 0; i < r; ++i) {
-            const double bia = trans ? M[(int64_t)i * ldm + a] : M[(int64_t)a * ldm + i];
-            sacc = fma(bia, W[j * RS + i], sacc);
-          }
-        Vr[(int64_t)rk * c + a] = sj > 0.0 ? sacc / (sj * sj) : 0.0;
+        const double inv = sj > 0.0 ? 1.0 / (sj * sj) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (a0 + u < c) Vr[(int64_t)rk * c + a0 + u] = acc[u][v] * inv;
       }
     }
   }
@@ -1251,20 +1264,26 @@ int launch_jacobi_small(const double* M, int64_t ldm, int trans, int r, int c, d
   if (c < 1 || c > 64 || r < c || r > 64) return RSVD_E_ARG;
   const int ce = c + (c & 1);
   const double tol = 2.220446049250313e-16 * sqrt((double)r);
-  const int smem = (64 * 64 + 64 * 64) * 8;
+  const int smem = 2 * 64 * (64 + 4) * 8;  // W and J (or the staged input B), stride <= 68
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_jacobi_small<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_jacobi_small<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_jacobi_small<8, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_jacobi_small<8, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_jacobi_small<4, 16, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_jacobi_small<4, 16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  // 8 lanes per column pair (a single warp per round was measured 2.8x slower: too little
-  // latency hiding); r <= 32 -> 4 rows per lane, r <= 64 -> 8
-  const int threads = ((8 * (ce / 2)) + 31) / 32 * 32;
-  if (r <= 32)
-    k_jacobi_small<8, 4><<<1, threads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, want_j, status);
-  else
-    k_jacobi_small<8, 8><<<1, threads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, want_j, status);
+  // measured on B200 (tools/jac_small_probe.cu): r <= 32 -> 8 lanes x 4 rows per pair,
+  // r <= 64 -> 4 lanes x 16 rows (one warp per SMSP; 8 x 8 was 10-20% slower)
+  if (r <= 32) {
+    const int threads = ((8 * (ce / 2)) + 31) / 32 * 32;
+    if (want_j) k_jacobi_small<8, 4, 1><<<1, threads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
+    else k_jacobi_small<8, 4, 0><<<1, threads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
+  } else {
+    const int threads = ((4 * (ce / 2)) + 31) / 32 * 32;
+    if (want_j) k_jacobi_small<4, 16, 1><<<1, threads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
+    else k_jacobi_small<4, 16, 0><<<1, threads, smem, st>>>(M, ldm, trans, r, c, Ul, S, Vr, tol, 60, status);
+  }
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
