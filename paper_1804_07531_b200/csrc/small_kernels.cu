@@ -461,6 +461,170 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
   }
 }
 
+// Medium cores (64 < c <= 128, r <= 128): the k_jacobi_small round (arithmetic round-robin pairs,
+// padded W stride, MUFU angle, lagged J rotations) with 8 lanes x 16 rows per pair and J always
+// accumulated (stride ce; in shared memory when W and J fit, else in the global scratch).
+constexpr int kMidLPP = 8, kMidRW = 16, kMidRS = kMidLPP * kMidRW + 4;
+__global__ void __launch_bounds__(512) k_jacobi_mid(const double* __restrict__ M, int64_t ldm, int trans, int r, int c,
+                                                    double* __restrict__ Ul, double* __restrict__ Sv,
+                                                    double* __restrict__ Vr, double* __restrict__ gJ, int j_in_smem,
+                                                    double tol, int max_sweeps, DevStatus* status) {
+  constexpr int LPP = kMidLPP, RW = kMidRW, RS = kMidRS;
+  extern __shared__ double jm_dyn[];
+  const int ce = c + (c & 1);
+  double* W = jm_dyn;                                 // ce x RS
+  double* J = j_in_smem ? jm_dyn + (int64_t)ce * RS : gJ;   // ce x ce
+  __shared__ double sval[128];
+  __shared__ int srank[128];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int grp = tid / LPP, sl = tid % LPP;
+  const unsigned gmask = ((1u << LPP) - 1u) << (tid & 31 & ~(LPP - 1));
+  const int npairs = ce >> 1, m1 = ce - 1;
+  for (int e = tid; e < ce * RS; e += nt) {
+    const int i = e % RS, j = e / RS;
+    double v = 0.0;
+    if (i < r && j < c) v = trans ? M[(int64_t)i * ldm + j] : M[(int64_t)j * ldm + i];
+    W[e] = v;
+  }
+  for (int e = tid; e < ce * ce; e += nt) J[e] = ((e % ce) == (e / ce)) ? 1.0 : 0.0;
+  __syncthreads();
+  const double tol2 = tol * tol;
+  int sweep = 0;
+  bool converged = false;
+  int pj_p = 0, pj_q = 0, pj_on = 0;
+  double pj_cs = 1.0, pj_sn = 0.0;
+  auto apply_pending_j = [&]() {
+    if (pj_on) {
+      double* jp = J + (int64_t)pj_p * ce;
+      double* jq = J + (int64_t)pj_q * ce;
+      for (int k = sl; k < ce; k += LPP) {
+        const double u = jp[k], v = jq[k];
+        jp[k] = pj_cs * u - pj_sn * v;
+        jq[k] = pj_sn * u + pj_cs * v;
+      }
+      pj_on = 0;
+    }
+  };
+  const bool active = grp < npairs;
+  for (; sweep < max_sweeps; ++sweep) {
+    int rotated = 0;
+    for (int round = 0; round < m1; ++round) {
+      if (active) {
+        int p, q;
+        if (grp == 0) {
+          p = round;
+          q = m1;
+        } else {
+          p = round + grp;
+          if (p >= m1) p -= m1;
+          q = round - grp;
+          if (q < 0) q += m1;
+          if (p > q) { const int tt = p; p = q; q = tt; }
+        }
+        double* wp = W + p * RS;
+        double* wq = W + q * RS;
+        double x[RW], y[RW];
+#pragma unroll
+        for (int t = 0; t < RW; ++t) {
+          x[t] = wp[sl + LPP * t];
+          y[t] = wq[sl + LPP * t];
+        }
+        double a0 = 0.0, b0 = 0.0, c0 = 0.0, a1 = 0.0, b1 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < RW; t += 2) {
+          a0 = fma(x[t], x[t], a0);
+          b0 = fma(y[t], y[t], b0);
+          c0 = fma(x[t], y[t], c0);
+          a1 = fma(x[t + 1], x[t + 1], a1);
+          b1 = fma(y[t + 1], y[t + 1], b1);
+          c1 = fma(x[t + 1], y[t + 1], c1);
+        }
+        double a = a0 + a1, b = b0 + b1, cc = c0 + c1;
+        apply_pending_j();
+#pragma unroll
+        for (int o = LPP / 2; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(gmask, a, o, LPP);
+          b += __shfl_xor_sync(gmask, b, o, LPP);
+          cc += __shfl_xor_sync(gmask, cc, o, LPP);
+        }
+        if (cc * cc > tol2 * (a * b) && cc != 0.0) {
+          rotated = 1;
+          const double d = b - a;
+          double rd, rsq, rt;
+          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(fmax(fabs(d), 1e-300)));
+          const double rho = fmin(fmax(2.0 * cc * rd, -1e100), 1e100);
+          const double s1 = fma(rho, rho, 1.0);
+          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rsq) : "d"(s1));
+          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rt) : "d"(fma(s1, rsq, 1.0)));
+          const double t = (d < 0.0 ? -rho : rho) * rt;
+          const double cs = rsqrt(fma(t, t, 1.0));
+          const double sn = cs * t;
+#pragma unroll
+          for (int k = 0; k < RW; ++k) {
+            wp[sl + LPP * k] = cs * x[k] - sn * y[k];
+            wq[sl + LPP * k] = sn * x[k] + cs * y[k];
+          }
+          pj_p = p; pj_q = q; pj_cs = cs; pj_sn = sn; pj_on = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!__syncthreads_or(rotated)) {
+      converged = true;
+      ++sweep;
+      break;
+    }
+  }
+  if (active) apply_pending_j();
+  __syncthreads();
+  for (int j = grp; j < ce; j += (nt / LPP)) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int t = 0; t < RW; ++t) {
+      const double v = W[j * RS + sl + LPP * t];
+      sacc = fma(v, v, sacc);
+    }
+#pragma unroll
+    for (int o = LPP / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(gmask, sacc, o, LPP);
+    if (sl == 0) sval[j] = sqrt(sacc);
+  }
+  __syncthreads();
+  for (int j = tid; j < ce; j += nt) {
+    const double sj = sval[j];
+    int rk = 0;
+    for (int i = 0; i < ce; ++i) {
+      const double si = sval[i];
+      rk += (si > sj) || (si == sj && i < j);
+    }
+    srank[j] = rk;
+  }
+  __syncthreads();
+  for (int e = tid; e < r * ce; e += nt) {
+    const int i = e % r, j = e / r;
+    const int rk = srank[j];
+    if (rk < c) {
+      const double sj = sval[j];
+      Ul[(int64_t)rk * r + i] = sj > 0.0 ? W[j * RS + i] / sj : 0.0;
+    }
+  }
+  for (int e = tid; e < ce * ce; e += nt) {
+    const int i = e % ce, j = e / ce;
+    const int rk = srank[j];
+    if (rk < c && i < c) Vr[(int64_t)rk * c + i] = J[(int64_t)j * ce + i];
+  }
+  for (int j = tid; j < ce; j += nt)
+    if (srank[j] < c) Sv[srank[j]] = sval[j];
+  if (tid == 0 && status) {
+    status->jacobi_sweeps = sweep;
+    if (!converged) atomicAdd(&status->jacobi_fail, 1);
+  }
+}
+
+static bool getenv_flag_jac(const char* n) {
+  const char* e = getenv(n);
+  return e && *e && *e != '0';
+}
+
 int launch_jacobi_small(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
                         DevStatus* status, cudaStream_t st, int want_j);
 int launch_jacobi_cluster(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
@@ -480,6 +644,20 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
   // rounding even for the trailing small sigma (C4's k = 100 core, sigma_100 / sigma_1 = 1e-3)
   want_j = 1;
   const int ce = c + (c & 1);
+  if (r <= kMidLPP * kMidRW && !getenv_flag_jac("RSVD_JACOBI_OLD_MID")) {
+    const size_t wb = (size_t)ce * kMidRS * 8, jb = (size_t)ce * ce * 8;
+    const int j_in = (wb + jb) <= 220 * 1024 ? 1 : 0;
+    static bool mattr = false;
+    if (!mattr) {
+      cudaFuncSetAttribute(k_jacobi_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      mattr = true;
+    }
+    const int threads = ((kMidLPP * (ce / 2)) + 31) / 32 * 32;
+    const double tolm = 2.220446049250313e-16 * sqrt((double)r);
+    k_jacobi_mid<<<1, threads, wb + (j_in ? jb : 0), st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, j_in, tolm, 60,
+                                                          status);
+    return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+  }
   const size_t wbytes = (size_t)r * ce * 8, jbytes = want_j ? (size_t)ce * ce * 8 : 0;
   const size_t budget = 200 * 1024;
   int w_in = wbytes <= budget ? 1 : 0;

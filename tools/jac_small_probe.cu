@@ -17,13 +17,13 @@ __global__ void __launch_bounds__(256) k_jac(const double* __restrict__ M, int r
   long long tA = 0;
 #define TS(i) {}
   constexpr int RS = LPP * RW + 4;  // padded column stride (bank spread)
-  extern __shared__ double W[];     // 64 x RS
+  extern __shared__ double W[];     // 128 x RS
   const int tid = threadIdx.x, nt = blockDim.x;
   const int grp = tid / LPP, sl = tid % LPP;
   const unsigned gmask = (LPP == 32 ? 0xffffffffu : ((1u << LPP) - 1u)) << (tid & 31 & ~(LPP - 1));
   const int ce = c + (c & 1);
   const int npairs = ce >> 1, m1 = ce - 1;
-  for (int e = tid; e < 64 * RS; e += nt) {
+  for (int e = tid; e < 128 * RS; e += nt) {
     const int i = e % RS, j = e / RS;
     W[e] = (i < r && j < c) ? M[(int64_t)j * r + i] : 0.0;
   }
@@ -144,11 +144,11 @@ __global__ void __launch_bounds__(256) k_jac(const double* __restrict__ M, int r
 template <int LPP, int RW, int FAST>
 void run(const char* name, const double* dM, int r, int c, const std::vector<double>& ref) {
   constexpr int RS = LPP * RW + 4;
-  const int smem = 64 * RS * 8;
+  const int smem = 128 * RS * 8;
   cudaFuncSetAttribute(k_jac<LPP, RW, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   double* dS;
   int* dsw;
-  cudaMalloc(&dS, 64 * 8);
+  cudaMalloc(&dS, 128 * 8);
   cudaMalloc(&dsw, 4);
   const int ce = c + (c & 1);
   const int threads = ((LPP * (ce / 2)) + 31) / 32 * 32;
@@ -183,7 +183,7 @@ void run(const char* name, const double* dM, int r, int c, const std::vector<dou
 }
 
 int main(int argc, char** argv) {
-  for (int w : {30, 60}) {
+  for (int w : {30, 60, 70, 120}) {
     // graded test core: R^T of QR of Yh diag(s) X^T, computed by the reference kernel below
     std::mt19937_64 g(1);
     std::normal_distribution<double> nd;
@@ -229,6 +229,9 @@ int main(int argc, char** argv) {
       run<8, 4, 3>("lpp8 rw4 mufu64+f32n", dM, r, c, ref);
       run<4, 8, 2>("lpp4 rw8 mufu64", dM, r, c, ref);
       run<4, 8, 3>("lpp4 rw8 mufu64+f32n", dM, r, c, ref);
+    } else if (w > 64) {
+      run<8, 16, 2>("lpp8 rw16 mufu64", dM, r, c, ref);
+      run<4, 32, 2>("lpp4 rw32 mufu64", dM, r, c, ref);
     } else {
       run<8, 8, 0>("lpp8 rw8 ieee", dM, r, c, ref);
       run<8, 8, 3>("lpp8 rw8 mufu64+f32n", dM, r, c, ref);
