@@ -137,31 +137,27 @@ __global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, con
     for (int j = tid; j < w; j += nt) S[j * w + j] += s_shift;
     __syncthreads();
   }
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
   for (int j = 0; j < w; ++j) {
+    // every thread derives the pivot itself (no broadcast barrier); rsqrt gives 1/R_jj and R_jj
     const double d = S[j * w + j];
     const double rf = ref ? ref[j] : (G[j * w + j] + s_shift * (shift_coef > 0.0));
     const bool def = !(d > tol * rf) || !(rf > 0.0);
-    const double rjj = def ? 0.0 : sqrt(d);
-    __syncthreads();  // everyone has read S(j,j)
+    const double inv = def ? 0.0 : rsqrt(d);
+    // row j of R: R(j,i) = S(j,i) / R_jj, i > j  (S(j,i) at S[i*w + j])
+    for (int i = j + 1 + tid; i < w; i += nt) S[i * w + j] *= inv;
+    __syncthreads();  // row j complete; everyone has read S(j,j)
     if (tid == 0) {
-      S[j * w + j] = rjj;
+      S[j * w + j] = def ? 0.0 : d * inv;
       defi[j] = def ? 1 : 0;
     }
-    // row j of R: R(j,i) = S(j,i) / rjj, i > j  (S(j,i) at S[i*w + j])
-    for (int i = j + 1 + tid; i < w; i += nt) S[i * w + j] = def ? 0.0 : S[i * w + j] / rjj;
-    __syncthreads();
     // trailing update of the upper triangle: S(i,k) -= R(j,i) R(j,k), j < i <= k
-    const int m = w - j - 1;
-    if (!def && m > 0) {
-      const int tot = m * m;
-      for (int e = tid; e < tot; e += nt) {
-        const int ii = e % m, kk = e / m;
-        if (ii <= kk) {
-          const int i = j + 1 + ii, k = j + 1 + kk;
-          S[k * w + i] -= S[i * w + j] * S[k * w + j];
-        }
+    // (warp per column k, lanes over rows i)
+    if (!def)
+      for (int k = j + 1 + warp; k < w; k += nwarp) {
+        const double rjk = S[k * w + j];
+        for (int i = j + 1 + lane; i <= k; i += 32) S[k * w + i] = fma(-S[i * w + j], rjk, S[k * w + i]);
       }
-    }
     __syncthreads();
   }
   // write R (upper, zero below)
@@ -170,22 +166,26 @@ __global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, con
     R[e] = (i <= k) ? S[k * w + i] : 0.0;
   }
   __syncthreads();
-  // R^-1 in place, row by row from the bottom: X(i,j) = -(sum_{k=i+1..j} R(i,k) X(k,j)) / R(i,i)
+  // R^-1 in place, row by row from the bottom: X(i,j) = -(sum_{k=i+1..j} R(i,k) X(k,j)) / R(i,i);
+  // each element's dot product split over lpe lanes (shuffle reduction)
+  const int lpe = (w <= nt / 8) ? 8 : 4;
+  const int el = tid / lpe, sl = tid % lpe;
   for (int i = w - 1; i >= 0; --i) {
-    double xv[1];
-    const int j = tid;
-    xv[0] = 0.0;
-    if (j < w && !defi[i] && j >= i) {
-      if (j == i) {
-        xv[0] = 1.0 / S[i * w + i];
-      } else {
-        double s = 0.0;
-        for (int k = i + 1; k <= j; ++k) s = fma(S[k * w + i], S[j * w + k], s);
-        xv[0] = -s / S[i * w + i];
-      }
+    const int j = i + el;
+    double x = 0.0;
+    const bool act = (el < w - i);
+    const bool live = act && !defi[i];
+    double s = 0.0;
+    if (live)
+      for (int k = i + 1 + sl; k <= j; k += lpe) s = fma(S[k * w + i], S[j * w + k], s);
+    __syncwarp();
+    for (int o = lpe >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, lpe);
+    if (live) {
+      const double rii = S[i * w + i];
+      x = (j == i) ? 1.0 / rii : -s / rii;
     }
     __syncthreads();
-    if (j < w && j >= i) S[j * w + i] = xv[0];
+    if (act && sl == 0) S[j * w + i] = x;
     __syncthreads();
   }
   for (int e = tid; e < w * w; e += nt) {
