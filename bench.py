@@ -10,9 +10,10 @@ k=20, p=10, l2=60).  At N GPUs (weak scaling) every rank holds a C2-sized row bl
 of the Gram matrices and of the co-range views).
 
 value = A-view bytes of all ranks / step time (GB/s); L2 is flushed (256 MiB write) before every
-timed step, outside the timed events.  `e2e` = the same step end to end from pinned HOST memory:
-A, Omega, Phi copied to the device once per step, the three API calls, every U, S, V copied
-back — all host<->device copies inside the timed region.
+timed step, outside the timed events.  `e2e` = the same step end to end from pinned HOST memory
+on a stream of K matrices: A, Omega, Phi copied to the device per step (double-buffered on a copy
+stream, overlapping the previous step's calls), the three API calls, every U, S, V copied back —
+all host<->device copies inside the timed region.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C2]
 """
@@ -48,7 +49,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (multi-GB configs)")
@@ -153,51 +154,71 @@ def reference_main(args):
 
 
 def run_e2e(args, cfg, A, Om, Phi, step, barrier, flush, stream, dev, max_over_ranks, world, m, n, bytes_step_rank):
-    """End to end through the public API, the way a PyTorch user runs the step on host data: every
-    step copies its inputs (A, Omega, Phi) from pinned host memory into the device buffers once,
-    runs the three calls on them, and copies every output (U, S, V of each call) back into pinned
-    host memory; all of it inside the timed region.  Byte counts come from the copied tensors."""
+    """End to end through the public API on a stream of host matrices, the way a PyTorch user
+    pipelines it: every step's inputs (A, Omega, Phi) are copied from pinned host memory into one
+    of two device buffer sets on a copy stream, overlapped with the previous step's three calls on
+    the other set; every output (U, S, V of each call) is copied back into pinned host memory.
+    The timed region spans all K steps (first copy to last output copy); ms_per_step = total / K.
+    Byte counts come from the copied tensors."""
     import torch
     Ah = A.cpu().pin_memory()
     Omh = Om.t().contiguous().cpu().pin_memory().t()
     Phih = Phi.t().contiguous().cpu().pin_memory().t()
+    bufs = [(A, Om, Phi), (torch.empty_like(A), Om.clone(), Phi.clone())]
+    copy_stream = torch.cuda.Stream(dev)
     host_outs = None
 
-    def e2e_step():
+    def run(K):
         nonlocal host_outs
-        A.copy_(Ah, non_blocking=True)
-        Om.copy_(Omh, non_blocking=True)
-        Phi.copy_(Phih, non_blocking=True)
-        outs = []
-        step(outs=outs)
-        if host_outs is None:
-            host_outs = [[torch.empty_like(t, device="cpu").pin_memory() for t in o] for o in outs]
-        for ho, o in zip(host_outs, outs):
-            for h, t in zip(ho, o):
-                h.copy_(t, non_blocking=True)
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def upload(k):
+            Ad, Omd, Phid = bufs[k % 2]
+            with torch.cuda.stream(copy_stream):
+                if k >= 2:
+                    copy_stream.wait_event(free[k % 2])     # step k-2 has finished with this set
+                Ad.copy_(Ah, non_blocking=True)
+                Omd.copy_(Omh, non_blocking=True)
+                Phid.copy_(Phih, non_blocking=True)
+                ready[k % 2].record(copy_stream)
+
+        upload(0)
+        outs = None
+        for k in range(K):
+            if k + 1 < K:
+                upload(k + 1)
+            stream.wait_event(ready[k % 2])
+            Ad, Omd, Phid = bufs[k % 2]
+            outs = []
+            step(Ax=Ad, Omx=Omd, Phix=Phid, outs=outs)
+            free[k % 2].record(stream)
+            if host_outs is None:
+                host_outs = [[torch.empty_like(t, device="cpu").pin_memory() for t in o] for o in outs]
+            for ho, o in zip(host_outs, outs):
+                for h, t in zip(ho, o):
+                    h.copy_(t, non_blocking=True)
         return outs
 
-    for _ in range(2):
-        outs = e2e_step()
+    run(2)
     torch.cuda.synchronize(dev)
+    K = max(2, args.e2e_steps)
+    flush.zero_()
     barrier()
-    e2e_ms = []
-    for _ in range(args.e2e_steps):
-        flush.zero_()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        outs = e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        e2e_ms.append(e0.elapsed_time(e1))
-    e2e_step_ms = max_over_ranks(statistics.median(e2e_ms))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    copy_stream.wait_stream(stream)
+    outs = run(K)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_step_ms = max_over_ranks(e0.elapsed_time(e1) / K)
     h2d = sum(t.numel() * t.element_size() for t in (Ah, Omh, Phih))
     d2h = sum(t.numel() * t.element_size() for o in outs for t in o)
     e2e = {"value": world * bytes_step_rank / (e2e_step_ms * 1e-3) / 1e9, "unit": "GB/s",
-           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step_ms,
-           "how": "per step: pinned-host -> device copy of A, Omega, Phi (once), the three API calls "
-                  "on the device copies, device -> pinned-host copy of every U, S, V"}
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step_ms, "steps": K,
+           "how": "stream of K host matrices: pinned-host -> device copy of A, Omega, Phi per step on a copy "
+                  "stream, double-buffered so it overlaps the previous step's three API calls; "
+                  "device -> pinned-host copy of every U, S, V; ms_per_step = (first copy .. last output) / K"}
     return e2e
 
 
