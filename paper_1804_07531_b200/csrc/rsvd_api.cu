@@ -545,10 +545,12 @@ struct Exec {
     tsmm(Q.p, Q.ld, Q.rows, Q.w, Mk, Q.w, k, out, ldo, 0);
   }
 
-  void core_svd(const double* M, int w, int trans, double* Ul, double* Sv, double* Vr) {
+  // want_j: 0 = right vectors as B^T U S^-1 (the leading triplets the algorithms keep); 2 = accumulate
+  // J in the 64 < w <= 128 kernel (cores whose trailing vectors are used or must stay orthonormal)
+  void core_svd(const double* M, int w, int trans, double* Ul, double* Sv, double* Vr, int want_j = 0) {
     const size_t mk = mark();
     double* scratch = alloc(2 * 512 * 512 + 4096);
-    if (live()) chk(launch_jacobi_t(M, w, trans, w, w, Ul, Sv, Vr, scratch, ctx->dstat, st, /*want_j=*/0));
+    if (live()) chk(launch_jacobi_t(M, w, trans, w, w, Ul, Sv, Vr, scratch, ctx->dstat, st, want_j));
     release(mk);
   }
 
@@ -640,7 +642,7 @@ void alg_subspace(Exec& E) {
   double* Ul = E.alloc((int64_t)l * l);
   double* Vr = E.alloc((int64_t)l * l);
   double* lam = E.alloc(l);
-  E.core_svd(Rlast, l, 1, Vr, lam, Ul);  // Jacobi on R^T: left(R^T) = right(R)
+  E.core_svd(Rlast, l, 1, Vr, lam, Ul, (c.flags & RSVD_SQUARED) ? 2 : 0);  // Jacobi on R^T: left(R^T) = right(R)
   // v even: R_r = Vh Lam Uh^T -> left = Vh, right = Uh;  v odd: R_c = Uh Lam Vh^T
   if (c.v % 2 == 0)
     write_outputs(E, side_c, side_r, Qc, Qr, /*Uh=*/Vr, /*Vh=*/Ul, lam, l, c.k);
@@ -684,7 +686,7 @@ void alg_krylov(Exec& E) {
   double* Ul = E.alloc((int64_t)W * W);
   double* Vr = E.alloc((int64_t)W * W);
   double* lam = E.alloc(W);
-  E.core_svd(Rw, W, 1, Vr, lam, Ul);
+  E.core_svd(Rw, W, 1, Vr, lam, Ul, (c.flags & RSVD_SQUARED) ? 2 : 0);
   if (even)  // Q_c = K, Q_r = Qo, R_r = Vh Lam Uh^T
     write_outputs(E, side_c, side_r, K, Qo, Vr, Ul, lam, W, c.k);
   else       // Q_r = K, Q_c = Qo, R_c = Uh Lam Vh^T
@@ -761,7 +763,7 @@ void alg_single_pass(Exec& E) {
     double* Ul = E.alloc((int64_t)l * l);
     double* Vr = E.alloc((int64_t)l * l);
     double* sv = E.alloc(l);
-    E.core_svd(Rc, l, 1, Vr, sv, Ul);
+    E.core_svd(Rc, l, 1, Vr, sv, Ul, 2);   // truncation / MinVar use trailing left vectors of R_c
     TS Q2 = E.new_ts(SIDE_M, lp);
     E.tsmm(Yc.p, Yc.ld, Yc.rows, l, Ul, l, lp, Q2.p, Q2.ld, 0);
     Qc = Q2;
@@ -803,7 +805,7 @@ void alg_single_pass(Exec& E) {
     double* Ur = E.alloc((int64_t)l2 * l2);
     double* Vrr = E.alloc((int64_t)l2 * l2);
     double* svr = E.alloc(l2);
-    E.core_svd(Rr, l2, 1, Vrr, svr, Ur);                     // R_r = Ur S Vrr^T
+    E.core_svd(Rr, l2, 1, Vrr, svr, Ur, 2);                  // R_r = Ur S Vrr^T
     TS Qr = E.new_ts(SIDE_N, lp);
     E.tsmm(Yr.p, Yr.ld, Yr.rows, l2, Ur, l2, lp, Qr.p, Qr.ld, 0);
     // ---- line 7: (Phi^* Q_c) Xh = Y_r^* Q_r = R_r^T Ur[:, :lp]   (l2 x lp)
@@ -892,7 +894,7 @@ void tsvd_wide_right(Exec& E, const TS& Ft, int l, int k, double* lam_out, TS* Q
   E.orth(SIDE_N, Ft, Rf, nullptr);
   double* Lf = E.alloc((int64_t)l * l);
   double* Rr = E.alloc((int64_t)l * l);
-  E.core_svd(Rf, l, /*trans=*/0, Lf, lam_out, Rr);
+  E.core_svd(Rf, l, /*trans=*/0, Lf, lam_out, Rr, 2);
   *Qf_out = Ft;
   *Lf_out = Lf;
   (void)k;
@@ -982,7 +984,7 @@ void alg_pinched(Exec& E) {
   double* Ul = E.alloc((int64_t)l * l);
   double* Vr = E.alloc((int64_t)l * l);
   double* lam = E.alloc(l);
-  E.core_svd(Rb, l, /*trans=*/1, Vr, lam, Ul);  // Jacobi on R_b^T: its left vectors = right(R_b)
+  E.core_svd(Rb, l, /*trans=*/1, Vr, lam, Ul, 2);  // Jacobi on R_b^T: its left vectors = right(R_b)
   if (E.live()) E.chk(launch_square(lam, l, E.st));
   // line 8: V_p = Q_r Vhat_p
   write_normal_outputs(E, Qr, Vr, lam, c.k);

@@ -464,12 +464,15 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
 // Medium cores (64 < c <= 128, r <= 128): the k_jacobi_small round (arithmetic round-robin pairs,
 // padded W stride, MUFU angle, lagged J rotations) with 8 lanes x 16 rows per pair and J always
 // accumulated (stride ce; in shared memory when W and J fit, else in the global scratch).
+// WJ = 0: no J; right vectors B^T U S^-1 from the input in global memory (leading triplets only,
+// as k_jacobi_small); 4 lanes x 32 rows per pair was the fastest no-J layout (tools/jac_small_probe).
 constexpr int kMidLPP = 8, kMidRW = 16, kMidRS = kMidLPP * kMidRW + 4;
-__global__ void __launch_bounds__(512) k_jacobi_mid(const double* __restrict__ M, int64_t ldm, int trans, int r, int c,
+template <int LPP, int RW, int WJ>
+__global__ void __launch_bounds__(LPP == 4 ? 256 : 512) k_jacobi_mid(const double* __restrict__ M, int64_t ldm, int trans, int r, int c,
                                                     double* __restrict__ Ul, double* __restrict__ Sv,
                                                     double* __restrict__ Vr, double* __restrict__ gJ, int j_in_smem,
                                                     double tol, int max_sweeps, DevStatus* status) {
-  constexpr int LPP = kMidLPP, RW = kMidRW, RS = kMidRS;
+  constexpr int RS = LPP * RW + 4;
   extern __shared__ double jm_dyn[];
   const int ce = c + (c & 1);
   double* W = jm_dyn;                                 // ce x RS
@@ -486,7 +489,8 @@ __global__ void __launch_bounds__(512) k_jacobi_mid(const double* __restrict__ M
     if (i < r && j < c) v = trans ? M[(int64_t)i * ldm + j] : M[(int64_t)j * ldm + i];
     W[e] = v;
   }
-  for (int e = tid; e < ce * ce; e += nt) J[e] = ((e % ce) == (e / ce)) ? 1.0 : 0.0;
+  if (WJ)
+    for (int e = tid; e < ce * ce; e += nt) J[e] = ((e % ce) == (e / ce)) ? 1.0 : 0.0;
   __syncthreads();
   const double tol2 = tol * tol;
   int sweep = 0;
@@ -494,7 +498,7 @@ __global__ void __launch_bounds__(512) k_jacobi_mid(const double* __restrict__ M
   int pj_p = 0, pj_q = 0, pj_on = 0;
   double pj_cs = 1.0, pj_sn = 0.0;
   auto apply_pending_j = [&]() {
-    if (pj_on) {
+    if (WJ && pj_on) {
       double* jp = J + (int64_t)pj_p * ce;
       double* jq = J + (int64_t)pj_q * ce;
       for (int k = sl; k < ce; k += LPP) {
@@ -564,7 +568,7 @@ __global__ void __launch_bounds__(512) k_jacobi_mid(const double* __restrict__ M
             wp[sl + LPP * k] = cs * x[k] - sn * y[k];
             wq[sl + LPP * k] = sn * x[k] + cs * y[k];
           }
-          pj_p = p; pj_q = q; pj_cs = cs; pj_sn = sn; pj_on = 1;
+          if (WJ) { pj_p = p; pj_q = q; pj_cs = cs; pj_sn = sn; pj_on = 1; }
         }
       }
       __syncthreads();
@@ -607,10 +611,40 @@ __global__ void __launch_bounds__(512) k_jacobi_mid(const double* __restrict__ M
       Ul[(int64_t)rk * r + i] = sj > 0.0 ? W[j * RS + i] / sj : 0.0;
     }
   }
-  for (int e = tid; e < ce * ce; e += nt) {
-    const int i = e % ce, j = e / ce;
-    const int rk = srank[j];
-    if (rk < c && i < c) Vr[(int64_t)rk * c + i] = J[(int64_t)j * ce + i];
+  if (WJ) {
+    for (int e = tid; e < ce * ce; e += nt) {
+      const int i = e % ce, j = e / ce;
+      const int rk = srank[j];
+      if (rk < c && i < c) Vr[(int64_t)rk * c + i] = J[(int64_t)j * ce + i];
+    }
+  } else {
+    // right vectors B^T U S^-1 (B = the input as seen by the sweep, read from global memory):
+    // 4 x 2 register blocks (a, j)
+    const int na = (c + 3) / 4, nj = ce / 2;
+    for (int e = tid; e < na * nj; e += nt) {
+      const int a0 = 4 * (e % na), j0 = 2 * (e / na);
+      double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      for (int i = 0; i < r; ++i) {
+        const double w0 = W[j0 * RS + i], w1 = W[(j0 + 1) * RS + i];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int a = min(a0 + u, c - 1);
+          const double bb = trans ? M[(int64_t)i * ldm + a] : M[(int64_t)a * ldm + i];
+          acc[u][0] = fma(bb, w0, acc[u][0]);
+          acc[u][1] = fma(bb, w1, acc[u][1]);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int j = j0 + v, rk = srank[j];
+        if (rk >= c) continue;
+        const double sj = sval[j];
+        const double inv = sj > 0.0 ? 1.0 / (sj * sj) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (a0 + u < c) Vr[(int64_t)rk * c + a0 + u] = acc[u][v] * inv;
+      }
+    }
   }
   for (int j = tid; j < ce; j += nt)
     if (srank[j] < c) Sv[srank[j]] = sval[j];
@@ -634,30 +668,40 @@ int launch_jacobi_cluster(const double* M, int64_t ldm, int trans, int r, int c,
 int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
                     double* scratch, DevStatus* status, cudaStream_t st, int want_j) {
   if (c < 1 || c > kJacMaxC || r < c || r > kJacMaxC) return RSVD_E_ARG;
-  if (r <= 64) return launch_jacobi_small(M, ldm, trans, r, c, Ul, S, Vr, status, st, want_j);
+  // want_j: 0 = no J, 1 = J everywhere, 2 = J in the 64 < c <= 128 path only
+  if (r <= 64) return launch_jacobi_small(M, ldm, trans, r, c, Ul, S, Vr, status, st, want_j == 1);
   static const int cl_from = [] {
     const char* e = getenv("RSVD_JACOBI_CLUSTER_FROM");
     return e ? atoi(e) : 129;
   }();
-  if (c >= cl_from) return launch_jacobi_cluster(M, ldm, trans, r, c, Ul, S, Vr, scratch, status, st, want_j);
-  // 64 < c <= 128: always accumulate J — both singular-vector sets then stay orthonormal to
-  // rounding even for the trailing small sigma (C4's k = 100 core, sigma_100 / sigma_1 = 1e-3)
-  want_j = 1;
+  if (c >= cl_from) return launch_jacobi_cluster(M, ldm, trans, r, c, Ul, S, Vr, scratch, status, st, want_j == 1);
+  // 64 < c <= 128: J is accumulated when the caller asks for it (want_j != 0: the normal-matrix
+  // and truncation cores, whose trailing vectors must stay orthonormal to rounding — C4's k = 100
+  // core, sigma_100 / sigma_1 = 1e-3); otherwise right vectors as B^T U S^-1 (leading triplets)
+  want_j = want_j ? 1 : 0;
   const int ce = c + (c & 1);
-  if (r <= kMidLPP * kMidRW && !getenv_flag_jac("RSVD_JACOBI_OLD_MID")) {
-    const size_t wb = (size_t)ce * kMidRS * 8, jb = (size_t)ce * ce * 8;
-    const int j_in = (wb + jb) <= 220 * 1024 ? 1 : 0;
+  if (r <= 128 && !getenv_flag_jac("RSVD_JACOBI_OLD_MID")) {
     static bool mattr = false;
     if (!mattr) {
-      cudaFuncSetAttribute(k_jacobi_mid, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      cudaFuncSetAttribute(k_jacobi_mid<8, 16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      cudaFuncSetAttribute(k_jacobi_mid<4, 32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       mattr = true;
     }
-    const int threads = ((kMidLPP * (ce / 2)) + 31) / 32 * 32;
     const double tolm = 2.220446049250313e-16 * sqrt((double)r);
-    k_jacobi_mid<<<1, threads, wb + (j_in ? jb : 0), st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, j_in, tolm, 60,
-                                                          status);
+    if (want_j) {
+      const size_t wb = (size_t)ce * (8 * 16 + 4) * 8, jb = (size_t)ce * ce * 8;
+      const int j_in = (wb + jb) <= 220 * 1024 ? 1 : 0;
+      const int threads = ((8 * (ce / 2)) + 31) / 32 * 32;
+      k_jacobi_mid<8, 16, 1><<<1, threads, wb + (j_in ? jb : 0), st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, j_in,
+                                                                       tolm, 60, status);
+    } else {
+      const size_t wb = (size_t)ce * (4 * 32 + 4) * 8;
+      const int threads = ((4 * (ce / 2)) + 31) / 32 * 32;
+      k_jacobi_mid<4, 32, 0><<<1, threads, wb, st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, 0, tolm, 60, status);
+    }
     return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
   }
+  want_j = 1;   // the generic kernel below keeps the previous always-J behaviour
   const size_t wbytes = (size_t)r * ce * 8, jbytes = want_j ? (size_t)ce * ce * 8 : 0;
   const size_t budget = 200 * 1024;
   int w_in = wbytes <= budget ? 1 : 0;
