@@ -40,12 +40,8 @@ __device__ __forceinline__ void pair_of(int round, int k, int n, int* p, int* q)
   *q = a < b ? b : a;
 }
 
-__device__ __forceinline__ double rot_t(double a, double b, double cc) {
-  // t = tan(theta), the smaller root of t^2 + 2 zeta t - 1 = 0, zeta = (b - a) / (2 cc)
-  const double d = b - a, e = 2.0 * cc;
-  return copysign(1.0, d) * e / (fabs(d) + sqrt(fma(d, d, e * e)));
-}
 
+template <int RPL>
 __global__ void __launch_bounds__(kThreads, 1)
     k_jacobi_cluster(const double* __restrict__ M, int64_t ldm, int trans, int r, int c, int b, int nb,
                      double* __restrict__ Ul, double* __restrict__ Sv, double* __restrict__ Vr,
@@ -107,8 +103,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           double* wq = sW + q * r;
           // the lane's slice of both columns in registers: every load is issued before any
           // store (a load -> rotate -> store loop serialises on the possible aliasing)
-          constexpr int RPL = kMaxC / 32;
-          double x[RPL], y[RPL];
+          double x[RPL], y[RPL];   // RPL = rows per lane (r <= 32 RPL)
 #pragma unroll
           for (int t = 0; t < RPL; ++t) {
             const int i = lane + 32 * t;
@@ -132,8 +127,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             bb += __shfl_xor_sync(0xffffffffu, bb, o);
             cc += __shfl_xor_sync(0xffffffffu, cc, o);
           }
-          if (cc != 0.0 && fabs(cc) > tol * sqrt(a * bb)) {
-            const double t = rot_t(a, bb, cc);
+          if (cc != 0.0 && cc * cc > tol * tol * (a * bb)) {
+            // rho = 2c / |b - a|, t = sign(b - a) rho / (1 + sqrt(1 + rho^2)) from the approximate
+            // fp64 MUFU ops: any t gives an exactly orthogonal rotation (cs full precision)
+            const double d = bb - a;
+            double rd, rsq, rt;
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(fmax(fabs(d), 1e-300)));
+            const double rho = fmin(fmax(2.0 * cc * rd, -1e100), 1e100);
+            const double s1 = fma(rho, rho, 1.0);
+            asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rsq) : "d"(s1));
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rt) : "d"(fma(s1, rsq, 1.0)));
+            const double t = (d < 0.0 ? -rho : rho) * rt;
             const double cs = rsqrt(fma(t, t, 1.0));
             const double sn = cs * t;
 #pragma unroll
@@ -265,8 +269,10 @@ int launch_jacobi_cluster(const double* M, int64_t ldm, int trans, int r, int c,
   const size_t smem = (size_t)2 * b * r * 8;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_jacobi_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 * kMaxC * 8);
-    cudaFuncSetAttribute(k_jacobi_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_jacobi_cluster<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 * kMaxC * 8);
+    cudaFuncSetAttribute(k_jacobi_cluster<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_jacobi_cluster<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 * kMaxC * 8);
+    cudaFuncSetAttribute(k_jacobi_cluster<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -282,8 +288,12 @@ int launch_jacobi_cluster(const double* M, int64_t ldm, int trans, int r, int c,
   cfg.attrs = at;
   cfg.numAttrs = 1;
   const double tol = 2.220446049250313e-16 * sqrt((double)r);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_jacobi_cluster, M, ldm, trans, r, c, b, nb, Ul, S, Vr, W, J, ncol, sval,
-                                     flags, tol, 60, want_j, status);
+  // rows per lane as a compile-time count: r <= 256 -> 8 (C3's 140, C5's 250), else 16
+  cudaError_t e = (r <= 256)
+      ? cudaLaunchKernelEx(&cfg, k_jacobi_cluster<8>, M, ldm, trans, r, c, b, nb, Ul, S, Vr, W, J, ncol, sval, flags,
+                           tol, 60, want_j, status)
+      : cudaLaunchKernelEx(&cfg, k_jacobi_cluster<16>, M, ldm, trans, r, c, b, nb, Ul, S, Vr, W, J, ncol, sval,
+                           flags, tol, 60, want_j, status);
   return e == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
