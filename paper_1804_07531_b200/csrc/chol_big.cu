@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(kThr, 1) k_chol_big(const double* __restrict__
   double* gdiag = Xd + kNB * 33;        // w (diagonal of G, the default rank-guard reference)
   int* defi = reinterpret_cast<int*>(gdiag + kMaxW);
   __shared__ double s_shift;
+  __shared__ int s_fast;
   const int tid = threadIdx.x;
+  if (ref == nullptr && shift_coef == 0.0 && chol_near_identity(G, w, R, Rinv, status, &s_fast)) return;
   // working copy: upper triangle of G (+ shift on the diagonal), zero below
   if (tid == 0) {
     double tr = 0.0;

@@ -122,3 +122,43 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 }  // namespace rsvd
+
+#include "internal.h"
+namespace rsvd {
+// CholeskyQR's second pass: the Gram of an already nearly orthonormal block is G = I + E with tiny
+// E.  When max |E| <= 1e-8 over the non-zero columns, R = I + triu(E, 1) + diag(E) / 2 and
+// R^-1 = I - triu(E, 1) - diag(E) / 2 to O(|E|^2) = O(u); columns with a zero Gram diagonal (zeroed
+// by an earlier guard) stay zero and count as deficient.  Called by every thread of the block with
+// uniform arguments; returns true (R, Rinv written) when the closed form applies.
+__device__ __forceinline__ bool chol_near_identity(const double* __restrict__ G, int w, double* __restrict__ R,
+                                                   double* __restrict__ Rinv, DevStatus* status, int* s_flag) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) *s_flag = 1;
+  __syncthreads();
+  for (int e = tid; e < w * w; e += nt) {
+    const int i = e % w, k = e / w;
+    if (G[(int64_t)i * w + i] != 0.0 && G[(int64_t)k * w + k] != 0.0) {
+      const double E = G[e] - (i == k ? 1.0 : 0.0);
+      if (!(fabs(E) <= 1e-8)) *s_flag = 0;
+    }
+  }
+  __syncthreads();
+  if (!*s_flag) return false;
+  int ndef = 0;
+  for (int e = tid; e < w * w; e += nt) {
+    const int i = e % w, k = e / w;
+    const bool dz = G[(int64_t)i * w + i] == 0.0 || G[(int64_t)k * w + k] == 0.0;
+    double r = 0.0, ri = 0.0;
+    if (!dz && i <= k) {
+      const double E = G[e] - (i == k ? 1.0 : 0.0);
+      r = (i == k) ? 1.0 + 0.5 * E : E;
+      ri = (i == k) ? 1.0 - 0.5 * E : -E;
+    }
+    R[e] = r;
+    Rinv[e] = ri;
+    if (i == k && G[e] == 0.0) ++ndef;
+  }
+  if (status && ndef) atomicAdd(&status->deficient, ndef);
+  return true;
+}
+}  // namespace rsvd

@@ -124,7 +124,9 @@ __global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, con
   extern __shared__ double S[];  // w*w (col-major), then deficient flags
   int* defi = reinterpret_cast<int*>(S + w * w);
   __shared__ double s_shift;
+  __shared__ int s_fast;
   const int tid = threadIdx.x, nt = blockDim.x;
+  if (ref == nullptr && shift_coef == 0.0 && chol_near_identity(G, w, R, Rinv, status, &s_fast)) return;
   for (int e = tid; e < w * w; e += nt) S[e] = G[e];
   if (tid == 0) {
     // shifted CholeskyQR (Fukaya et al.): G + s I, s = shift_coef * ||Y||_F^2 >= shift_coef ||Y||_2^2
