@@ -114,3 +114,20 @@ def test_single_pass_min_l2_and_lc(ctx, lc):
     assert info.lc_used == lc
     assert np.max(np.abs(host(s) - so) / so) <= 1e-10
     assert O.projector_distance(host(U), Uo) <= 1e-9 and O.projector_distance(host(V), Vo) <= 1e-9
+
+
+@pytest.mark.parametrize("alg,v", ALGS)
+def test_fp32_zero_and_rank_one(ctx, alg, v):
+    """The fp32 path (tcgen05 3xTF32 views, fp64 in between): A = 0 gives sigma = 0 exactly and
+    finite vectors; a rank-1 spike gives sigma_1 = 3 and U_1 = +-e_i, V_1 = +-e_j (fp32 tolerances)."""
+    m, n, k, p = 300, 200, 5, 5
+    Om = S.random_gaussian_matrix(n, k + p, seed=31).astype(np.float32)
+    Phi = S.random_gaussian_matrix(m, 2 * (k + p), seed=32).astype(np.float32)
+    A = np.zeros((m, n), dtype=np.float32)
+    U, s, V, _ = run(ctx, alg, A, k, p, v, Om, Phi, 2 * (k + p))
+    assert np.all(host(s) == 0.0) and np.all(np.isfinite(host(U))) and np.all(np.isfinite(host(V)))
+    A[123, 45] = 3.0
+    U, s, V, _ = run(ctx, alg, A, k, p, v, Om, Phi, 2 * (k + p))
+    s, U, V = host(s).astype(np.float64), host(U).astype(np.float64), host(V).astype(np.float64)
+    assert abs(s[0] - 3.0) <= 1e-5 * 3.0 and np.all(np.abs(s[1:]) <= 1e-5)
+    assert abs(abs(U[123, 0]) - 1.0) <= 1e-5 and abs(abs(V[45, 0]) - 1.0) <= 1e-5

@@ -74,3 +74,31 @@ def test_one_rank_comm_nystrom(ctxs):
     Vo, s2o = O.nystrom_tevd(A, cfg.k, cfg.p, 3, Om)
     assert np.max(np.abs(host(s2) - s2o) / s2o) <= 2e-10
     assert O.projector_distance(host(V), Vo) <= 1e-9
+
+
+@pytest.mark.parametrize("variant", ["minvar", "woolfe"])
+def test_one_rank_comm_adaptive_single_pass(ctxs, variant):
+    """MinVar l_c (masks on the row-sharded Q_c, C = Phi^T Q_c all-reduced) and Alg. 8 (Y_r on the
+    replicated side) through the sharded route: same l_c and results as the communicator-free ctx."""
+    from paper_1804_07531_b200 import rsvd
+
+    c1, c0 = ctxs
+    cfg = S.CONFIGS["C2"]
+    A = S.make_matrix(cfg, 1500, 1300)
+    Om = S.gaussian_test_matrix(A.shape[1], cfg.l, cfg, S.ROLE_OMEGA)
+    Phi = S.gaussian_test_matrix(A.shape[0], cfg.l2, cfg, S.ROLE_PHI)
+    Ad = torch.from_numpy(A).cuda()
+    kw = dict(lc="minvar") if variant == "minvar" else dict(lc=cfg.p // 2, flags=rsvd.RSVD_WOOLFE)
+    outs = []
+    for c in (c1, c0):
+        r = c.single_pass(Ad, cfg.k, cfg.p, cfg.l2, colmajor_dev(Om), colmajor_dev(Phi), **kw)
+        outs.append(([host(x) for x in r[:3]], r[3].lc_used))
+    ((U, s, V), lc1), ((U0, s0, V0), lc0) = outs
+    assert lc1 == lc0
+    if variant == "minvar":
+        Uo, so, Vo = O.one_view_tropp(A, cfg.k, cfg.p, cfg.l2 - cfg.k, lc1, Om, Phi)
+    else:
+        Uo, so, Vo = O.one_view_woolfe(A, cfg.k, cfg.p, cfg.l2 - cfg.k, cfg.p // 2, Om, Phi)
+    assert np.max(np.abs(s - so) / so) <= 1e-10
+    assert O.projector_distance(U, Uo) <= 1e-9 and O.projector_distance(V, Vo) <= 1e-9
+    assert np.max(np.abs(s - s0) / s0) <= 1e-12
