@@ -34,7 +34,7 @@ __all__ = [
     "qr", "orth", "tsvd", "chol_lower", "jacobi_svd",
     "std_subspace_iteration", "gen_subspace_iteration", "qrqc", "one_view_tropp", "one_view_woolfe",
     "plan_flat", "plan_decay", "plan_rapid", "plan_balanced", "minvar_spectra", "minvar_select",
-    "one_view_minvar",
+    "one_view_minvar", "one_view_extended", "plan_extended", "pinv",
     "gen_block_krylov", "normal_matrix_tevd", "nystrom_tevd", "pinched_tevd", "recommend_input", "svd_of",
     "views_and_vectors", "rel_frobenius_error", "rel_spectral_error", "projector_distance",
     "residual_fro", "half_power_lhs_rhs", "thm_bound",
@@ -393,6 +393,64 @@ class _Sketched:
 
     def adjoint(self, X):
         return self.Yr
+
+
+# ============================================================ extended sketch
+
+def pinv(M, rcond=1e-12):
+    """Moore-Penrose pseudo-inverse with singular values below rcond * sigma_max dropped (the
+    paper writes the dagger without a cutoff; reading R24)."""
+    return np.linalg.pinv(_f64(M), rcond=rcond)
+
+
+def one_view_extended(A, p, l1, l2, Omega_r, Omega_c, Phi_r, Phi_c, variant="bwz2", transpose=False, _op=None):
+    """Extended 1-view sketch: Y_c = A Omega_r, Y_r = A^* Omega_c, Z = Phi_r^* A Phi_c
+    (Phi_r n_r x s, Phi_c n_c x s, SRFT inputs, s >= p + l1); Q_c R_c := Y_c, Q_r R_r := Y_r,
+    U_c T_c := Phi_r^* Q_c, U_r T_r := Phi_c^* Q_r, and
+      bwz  (Eq. bwz):         A ~ Q_c T_c^+ [[U_c^* Z U_r]]_p (T_r^*)^+ Q_r^*
+      bwz2 (Eq. bwzimproved): A ~ Q_c [[T_c^+ U_c^* Z U_r (T_r^*)^+]]_p Q_r^*
+    Returns the rank-p SVD (U, lambda, V) of the approximation.  A Omega_r and A Phi_c are one
+    product with the test matrices side by side, and Y_r comes from the same access: one view."""
+    if variant not in ("bwz", "bwz2"):
+        raise ValueError(variant)
+    op = _op or _Op(A, transpose)
+    Omega_r, Omega_c = _f64(Omega_r), _f64(Omega_c)
+    Phi_r, Phi_c = _f64(Phi_r), _f64(Phi_c)
+    if Phi_r.shape[1] < p + l1 or Phi_c.shape[1] < p + l1:
+        raise ValueError("s >= p + l_1 (P:805)")
+    Yc = op.apply(Omega_r)
+    Yr = op.adjoint(Omega_c)
+    W = op.apply(Phi_c)
+    op.views -= 2
+    Z = Phi_r.T @ W                               # Z = Phi_r^* A Phi_c
+    Qc, _ = qr(Yc)
+    Qr, _ = qr(Yr)
+    Uc, Tc = qr(Phi_r.T @ Qc)
+    Ur, Tr = qr(Phi_c.T @ Qr)
+    Tcp, Trp = pinv(Tc), pinv(Tr)
+    if variant == "bwz2":
+        core = Tcp @ (Uc.T @ Z @ Ur) @ Trp.T
+    else:
+        Ux, sx, Vx = tsvd(Uc.T @ Z @ Ur, p)
+        core = (Tcp @ Ux) @ np.diag(sx) @ (Trp @ Vx).T
+    Uk, lam, Vk = tsvd(core, p)
+    return Qc @ Uk, lam, Qr @ Vk
+
+
+def plan_extended(p, T, n_r, n_c):
+    """Eq. (bwzafac8): l_1 = l_2 = floor(0.8 floor(T/2 - p)) and s the largest value with
+    (2p + l_1 + l_2 + 1)(n_r + n_c) + s(s + 2) <= T (n_r + n_c) (reading R25: 'approximately
+    equals' taken as <=, floored at p + l_1).  Returns (l1, l2, s)."""
+    if T < 2 * p + 6:
+        raise ValueError("T >= 2p + 6 required (P:604)")
+    l1 = int(np.floor(0.8 * np.floor(T / 2 - p)))
+    budget = T * (n_r + n_c) - (2 * p + 2 * l1 + 1) * (n_r + n_c)
+    s = 0
+    while (s + 1) * (s + 3) <= budget:
+        s += 1
+    if s < p + l1:
+        raise ValueError("budget leaves s < p + l_1")
+    return l1, l1, s
 
 
 # ============================================================ Algorithm 9 (P:900-928)

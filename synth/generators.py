@@ -221,6 +221,22 @@ def integer_matrix(m: int, n: int, lo: int, hi: int, seed: int, dtype=np.float64
 
 # ---------------------------------------------------------------- torch (device) builders
 
+def srft_matrix(n: int, s: int, seed: int) -> np.ndarray:
+    """A subsampled randomized Fourier transform test matrix Phi = D F P (n x s) for real A
+    (P:806-812): D = diag of Rademacher signs, F = the orthonormal DCT-II matrix (n x n), P = s
+    columns of I_n sampled without replacement.  Random test matrices are inputs of the method
+    (reading R3): this only draws one; it is materialised dense (the GPU applies it as a dense
+    test matrix in the same view).  Columns are orthonormal (F orthogonal)."""
+    if not (1 <= s <= n):
+        raise ValueError("need 1 <= s <= n")
+    from scipy.fft import dct
+    g = np.random.default_rng(np.random.SeedSequence([0x5A7F, seed]))
+    d = g.choice(np.array([-1.0, 1.0]), size=n)
+    cols = np.sort(g.choice(n, size=s, replace=False))
+    F = dct(np.eye(n), type=2, norm="ortho", axis=0)   # F[:, j] = DCT-II of e_j
+    return (d[:, None] * F)[:, cols]
+
+
 def make_matrix_torch(cfg: Config, device, m: int | None = None, n: int | None = None,
                       panel_rows: int = 4096, seed_offset: int = 0):
     """Same recipe as ``make_matrix`` built on a CUDA device with torch's Philox generator

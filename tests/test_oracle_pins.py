@@ -599,3 +599,68 @@ def test_woolfe_exact_rank_and_orthonormal():
     np.testing.assert_allclose(s, [4.0, 2.0, 1.0], rtol=1e-10)
     assert np.linalg.norm(A - (U * s) @ V.T) <= 1e-10 * np.linalg.norm(A)
     np.testing.assert_allclose(V.T @ V, np.eye(3), atol=1e-12)
+
+
+# ---------------------------------------------------------------- f4: extended sketch (bwz / bwz2)
+
+def test_srft_generator_orthonormal():
+    """Phi = D F P with F the orthonormal DCT-II: orthonormal columns, and each
+    column is a signed DCT basis vector (entries of modulus sqrt(2/n) cos(.) or sqrt(1/n))."""
+    P = S.srft_matrix(64, 20, seed=1)
+    np.testing.assert_allclose(P.T @ P, np.eye(20), atol=1e-14)
+    # row k = 0 of the DCT-II matrix is the constant 1/sqrt(n) and D scales rows by +-1: with all
+    # columns sampled, the first row of D F P has entries of modulus 1/8 (n = 64)
+    P0 = S.srft_matrix(64, 64, seed=2)
+    np.testing.assert_allclose(np.abs(P0[0, :]), np.full(64, 1 / 8), rtol=1e-14)
+
+
+def test_plan_extended_worked_value_and_budget():
+    # hand evaluation (SPEC S:386): l1 = l2 = floor(0.8 * 7) = 5; s(s+2) <= (24 - 21) * 2000 = 6000
+    # -> s = 76 (76 * 78 = 5928, 77 * 79 = 6083)
+    assert O.plan_extended(5, 24, 1000, 1000) == (5, 5, 76)
+    prev = 0
+    for T in range(16, 60):
+        l1, l2, s = O.plan_extended(5, T, 1000, 1000)
+        assert (2 * 5 + l1 + l2 + 1) * 2000 + s * (s + 2) <= T * 2000 < (2 * 5 + l1 + l2 + 1) * 2000 + (s + 1) * (s + 3)
+        if l1 == O.plan_extended(5, max(16, T - 1), 1000, 1000)[0]:
+            assert s >= prev
+        prev = s
+    with pytest.raises(ValueError):
+        O.plan_extended(5, 15, 1000, 1000)
+
+
+@pytest.mark.parametrize("variant", ["bwz", "bwz2"])
+def test_extended_exact_rank_recovery(variant):
+    """Exactly rank r <= p with s >= p + l1: Z, Y_c, Y_r capture A exactly, both estimators
+    reproduce A (the rank-p truncation is the identity on an exact rank-p core)."""
+    rng = np.random.default_rng(7)
+    m, n, r, p, l1 = 300, 240, 4, 5, 5
+    X = np.linalg.qr(rng.standard_normal((m, r)))[0]
+    Y = np.linalg.qr(rng.standard_normal((n, r)))[0]
+    A = X @ np.diag([4.0, 3.0, 2.0, 1.0]) @ Y.T
+    Om_r = rng.standard_normal((n, p + l1))
+    Om_c = rng.standard_normal((m, p + l1))
+    s = 24
+    U, lam, V = O.one_view_extended(A, p, l1, l1, Om_r, Om_c, S.srft_matrix(m, s, 3), S.srft_matrix(n, s, 4),
+                                    variant=variant)
+    np.testing.assert_allclose(lam[:4], [4.0, 3.0, 2.0, 1.0], rtol=1e-10)
+    assert np.linalg.norm(A - (U * lam) @ V.T) <= 1e-10 * np.linalg.norm(A)
+
+
+def test_extended_bwz2_at_least_as_accurate_on_average():
+    """P:830 ('a more accurate low-rank approximation can be found'): mean relative Frobenius error
+    of bwz2 <= that of bwz over 12 draws on a low-rank + noise matrix (p = 5, l1 = l2 = 5, s = 40)."""
+    rng = np.random.default_rng(11)
+    m, n, p, l1 = 400, 300, 5, 5
+    X = np.linalg.qr(rng.standard_normal((m, 10)))[0]
+    Y = np.linalg.qr(rng.standard_normal((n, 10)))[0]
+    A = X @ np.diag(np.linspace(1, 0.5, 10)) @ Y.T + 0.02 * rng.standard_normal((m, n)) / np.sqrt(n)
+    errs = {"bwz": [], "bwz2": []}
+    for t in range(12):
+        Om_r = rng.standard_normal((n, p + l1))
+        Om_c = rng.standard_normal((m, p + l1))
+        Pr, Pc = S.srft_matrix(m, 40, 100 + t), S.srft_matrix(n, 40, 200 + t)
+        for v in errs:
+            U, lam, V = O.one_view_extended(A, p, l1, l1, Om_r, Om_c, Pr, Pc, variant=v)
+            errs[v].append(np.linalg.norm(A - (U * lam) @ V.T) / np.linalg.norm(A))
+    assert np.mean(errs["bwz2"]) <= np.mean(errs["bwz"]) * 1.0001
