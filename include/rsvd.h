@@ -80,6 +80,8 @@ enum {
 #define RSVD_ASYNC        32u  /* enqueue only: outputs and info complete after rsvd_wait(ctx) */
 #define RSVD_WOOLFE       64u  /* rsvd_single_pass: Alg. 8 (Woolfe variant) instead of Alg. 7   */
 #define RSVD_LC_MINVAR    (-2) /* rsvd_single_pass lc: minimum-variance l_c          */
+#define RSVD_EXT_BWZ      0    /* rsvd_single_pass_extended: Eq. (bwz)               */
+#define RSVD_EXT_BWZ2     1    /* rsvd_single_pass_extended: Eq. (bwzimproved)       */
 #define RSVD_SIM_SHARDS_SHIFT 8 /* debug: bits 8..15 = number of virtual row shards (loopback) */
 
 typedef struct {
@@ -176,6 +178,23 @@ int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int
                      const void* Omega, int64_t ld_omega, const void* Phi, int64_t ld_phi,
                      void* U, int64_t ldu, void* S, void* V, int64_t ldv,
                      unsigned flags, rsvd_info* info);
+
+/* Extended 1-view sketch: from ONE view of A, Y_c = A Omega (n x (k+p) Omega),
+ * Y_r = A^T Phi (Phi m_local x l2) and Z = Xi_r^T A Xi_c (s x s), with Xi_r (m_local x s) and Xi_c
+ * (n x s) the paper's SRFT matrices Phi_r, Phi_c, materialised dense by the caller and
+ * applied as test matrices in the same view ([A Omega | A Xi_c] is one range product).  Then
+ * Q_c R_c := Y_c, Q_r R_r := Y_r, U_c T_c := Xi_r^T Q_c, U_r T_r := Xi_c^T Q_r and
+ *   variant RSVD_EXT_BWZ :   A ~ Q_c T_c^+ [[U_c^T Z U_r]]_k (T_r^T)^+ Q_r^T      (Eq. bwz)
+ *   variant RSVD_EXT_BWZ2:   A ~ Q_c [[T_c^+ U_c^T Z U_r (T_r^T)^+]]_k Q_r^T      (Eq. bwzimproved)
+ * returned as its rank-k SVD (U m_local x k, S k, V n x k).  ^+ drops singular values below
+ * 1e-12 of the largest.  Requires l2 >= k + p and k + p <= s <= min(m, n, 512) (s >= p + l_1);
+ * the paper assumes l_1 = l_2 (l2 = k + p) but any l2 >= k + p is accepted.  Same pointer, dtype
+ * and error rules as rsvd_single_pass; info->views = 1. */
+int rsvd_single_pass_extended(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int s,
+                              const void* Omega, int64_t ld_omega, const void* Phi, int64_t ld_phi,
+                              const void* Xi_r, int64_t ld_xi_r, const void* Xi_c, int64_t ld_xi_c, int variant,
+                              void* U, int64_t ldu, void* S, void* V, int64_t ldv,
+                              unsigned flags, rsvd_info* info);
 
 /* Oversampling plans for the single pass from a sketch-size budget T = 2k + l_1 + l_2 (host only,
  * no GPU needed).  Writes the ABI arguments: *p = l_1, *l2 = k + l_2 (the co-range width), *lc.

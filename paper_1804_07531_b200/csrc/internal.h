@@ -117,6 +117,10 @@ int launch_fill(double* dst, int64_t count, double v, cudaStream_t st);
 int launch_sub_cols(const double* T, int64_t ldt, double* out, int64_t ldo, int64_t rows, int c, cudaStream_t st);
 // triangular-system helpers for Alg. 7: out (c x c) = upper-triangular inverse of R (c x c)
 int launch_tri_inv(const double* R, int c, double* Rinv, DevStatus* status, cudaStream_t st);
+// Tp = V diag(s^+) U^T (w x w) from T = U diag(s) V^T, s_i <= rcut s_0 dropped; X(:, j) *= d[j]
+int launch_pinv_svd(const double* U, const double* s, const double* V, int w, double rcut, double* Tp,
+                    cudaStream_t st);
+int launch_scale_cols(double* X, int64_t ld, int rows, int cols, const double* d, cudaStream_t st);
 // S[i] <- S[i]^2
 int launch_square(double* S, int n, cudaStream_t st);
 // Nystrom (Alg. 4) helpers: nu = 2.2e-16 ||Y_r||_2 from the Gram of Y_r (power iteration);

@@ -159,9 +159,15 @@ struct Call {
   int64_t ldv = 0;
   void* R = nullptr;
   unsigned flags = 0;
+  // extended 1-view sketch (alg 5): SRFT test matrices Xi_r (m_local x s), Xi_c (n x s), variant
+  int s = 0, variant = 0;
+  const void* Xr = nullptr;
+  int64_t ldxr = 0;
+  const void* Xc = nullptr;
+  int64_t ldxc = 0;
   // resolved kinds
   PtrKind kA = PTR_NULL, kOm = PTR_NULL, kPhi = PTR_NULL, kU = PTR_NULL, kS = PTR_NULL, kV = PTR_NULL,
-          kR = PTR_NULL;
+          kR = PTR_NULL, kXr = PTR_NULL, kXc = PTR_NULL;
 };
 
 // ---------------------------------------------------------------- executor
@@ -571,6 +577,17 @@ struct Exec {
     }
     return t;
   }
+  // stage a caller array (rows of dst x w) into columns [col0, col0 + w) of an existing block
+  void stage_into(const TS& dst, int col0, const void* src, int64_t ld_user, int w) {
+    double* d = dst.p + (int64_t)col0 * dst.ld;
+    if (dtype == RSVD_F32) {
+      float* f = alloc_f(dst.ld * w);
+      h2d.push_back({f, dst.ld, src, ld_user, dst.rows, w, 4});
+      if (live()) chk(launch_f32_to_f64(f, dst.ld, d, dst.ld, dst.rows, w, st));
+    } else {
+      h2d.push_back({d, dst.ld, src, ld_user, dst.rows, w});
+    }
+  }
   // where to write a caller output of rows x cols (col-major, ld): direct if device, else staging
   double* out_ptr(void* user, int64_t ld_user, int64_t rows, int cols, PtrKind kind, int64_t* ld_out) {
     const int64_t ld = round_up(std::max<int64_t>(rows, 1), 32);
@@ -695,18 +712,11 @@ void alg_krylov(Exec& E) {
 
 constexpr double kYcSlotBudget = 4.0e9;  // bytes of deterministic Y_c partial slots
 
-void alg_single_pass(Exec& E) {
-  const Call& c = E.call;
-  const int l = c.k + c.p, l2 = c.l2;
-  const bool minvar = (c.lc == RSVD_LC_MINVAR);
-  const bool woolfe = (c.flags & RSVD_WOOLFE) != 0;
-  const int lc = minvar ? c.p : c.lc;
-  const int lp = c.k + lc;  // width of Q_c after the optional truncation (P:672-673); MinVar: l, masked
-  TS Om = E.stage_in(SIDE_N, c.Om, c.ldom, l, c.kOm);
-  TS Phi = E.stage_in(SIDE_M, c.Phi, c.ldphi, l2, c.kPhi);
-  TS Yc = E.new_ts(SIDE_M, l);
-  TS Yr = E.new_ts(SIDE_N, l2);
-  // ---- line 3: a) Y_c = A Omega  and  b) Y_r = A^* Phi  from one read of A
+// One view of A for the 1-view methods (Alg. 7 line 3; the extended sketch):
+// Yc = A Om and Yr = A^* Phi from one read of every A tile (k_view_fused), or two view launches
+// when the widths exceed the fused kernel's register budget or A is fp32 (info.view_launches = 2).
+void sketch_view(Exec& E, const TS& Om, const TS& Phi, const TS& Yc, const TS& Yr) {
+  const int l = Om.w, l2 = Phi.w;
   const bool fused_ok = (E.dtype == RSVD_F64) && (l <= kFusedMaxL) && ((l2 + 7) / 8 <= kFusedMaxL2T);
   if (fused_ok) {
     const size_t mk = E.mark();
@@ -755,6 +765,21 @@ void alg_single_pass(Exec& E) {
     E.view(SIDE_N, Om, Yc);
     E.view(SIDE_M, Phi, Yr);
   }
+}
+
+void alg_single_pass(Exec& E) {
+  const Call& c = E.call;
+  const int l = c.k + c.p, l2 = c.l2;
+  const bool minvar = (c.lc == RSVD_LC_MINVAR);
+  const bool woolfe = (c.flags & RSVD_WOOLFE) != 0;
+  const int lc = minvar ? c.p : c.lc;
+  const int lp = c.k + lc;  // width of Q_c after the optional truncation (P:672-673); MinVar: l, masked
+  TS Om = E.stage_in(SIDE_N, c.Om, c.ldom, l, c.kOm);
+  TS Phi = E.stage_in(SIDE_M, c.Phi, c.ldphi, l2, c.kPhi);
+  TS Yc = E.new_ts(SIDE_M, l);
+  TS Yr = E.new_ts(SIDE_N, l2);
+  // ---- line 3: a) Y_c = A Omega  and  b) Y_r = A^* Phi  from one read of A
+  sketch_view(E, Om, Phi, Yc, Yr);
   // ---- lines 4-10: Q_c (optionally truncated to the top k+l_c left singular vectors of R_c)
   double* Rc = E.alloc((int64_t)l * l);
   E.orth(SIDE_M, Yc, Rc, nullptr);
@@ -865,6 +890,99 @@ void alg_single_pass(Exec& E) {
   E.core_svd(Rx, lp, /*trans=*/0, Vr, lam, Ul);  // svd(Rx^T) from Jacobi on Rx
   // U = Q_c Uh (side M), V = Qx Wh (side N)           (line 14)
   write_outputs(E, SIDE_M, SIDE_N, Qc, Xt, Ul, Vr, lam, lp, c.k);
+}
+
+// [Q, R] = qr(X) of a small replicated block (rows x w, col-major ld rows) by CholeskyQR2 with
+// the rank guard: Q overwrites X, R = R2 R1 (w x w).
+void small_qr(Exec& E, double* X, int rows, int w, double* R) {
+  double* G = E.alloc((int64_t)w * w);
+  double* R1 = E.alloc((int64_t)w * w);
+  double* R1i = E.alloc((int64_t)w * w);
+  double* R2 = E.alloc((int64_t)w * w);
+  double* R2i = E.alloc((int64_t)w * w);
+  double* T = E.alloc((int64_t)rows * w);
+  if (!E.live()) return;
+  E.chk(launch_small_gemm(1, 0, w, w, rows, X, rows, X, rows, G, w, E.st));
+  E.chk(launch_chol_ref(G, nullptr, w, 1e-12, R1, R1i, nullptr, E.st));
+  E.chk(launch_small_gemm(0, 0, rows, w, w, X, rows, R1i, w, T, rows, E.st));
+  E.chk(launch_small_gemm(1, 0, w, w, rows, T, rows, T, rows, G, w, E.st));
+  E.chk(launch_chol_ref(G, nullptr, w, 1e-12, R2, R2i, nullptr, E.st));
+  E.chk(launch_small_gemm(0, 0, rows, w, w, T, rows, R2i, w, X, rows, E.st));
+  E.chk(launch_small_gemm(0, 0, w, w, w, R2, w, R1, w, R, w, E.st));
+}
+
+// T^+ (w x w) with singular values below 1e-12 sigma_max dropped (reading R24): one-sided Jacobi
+// with J accumulated (every singular pair is used), then V S^+ U^T.
+void small_pinv(Exec& E, const double* T, int w, double* Tp) {
+  double* Ul = E.alloc((int64_t)w * w);
+  double* Vr = E.alloc((int64_t)w * w);
+  double* sv = E.alloc(w);
+  E.core_svd(T, w, 0, Ul, sv, Vr, 1);
+  if (E.live()) E.chk(launch_pinv_svd(Ul, sv, Vr, w, 1e-12, Tp, E.st));
+}
+
+// Extended 1-view sketch, bwz (Eq. bwz) or bwz2 (Eq. bwzimproved).  Xi_r / Xi_c are
+// the paper's SRFT matrices Phi_r (m x s) and Phi_c (n x s), materialised by the caller (R3, R23).
+void alg_extended(Exec& E) {
+  const Call& c = E.call;
+  const int l = c.k + c.p, l2 = c.l2, s = c.s, k = c.k;
+  // one view: [Y_c | A Xi_c] = A [Omega | Xi_c] and Y_r = A^* Phi
+  TS OmX = E.new_ts(SIDE_N, l + s);
+  E.stage_into(OmX, 0, c.Om, c.ldom, l);
+  E.stage_into(OmX, l, c.Xc, c.ldxc, s);
+  TS Phi = E.stage_in(SIDE_M, c.Phi, c.ldphi, l2, c.kPhi);
+  TS Xr = E.stage_in(SIDE_M, c.Xr, c.ldxr, s, c.kXr);
+  TS YW = E.new_ts(SIDE_M, l + s);
+  TS Yr = E.new_ts(SIDE_N, l2);
+  sketch_view(E, OmX, Phi, YW, Yr);
+  TS Yc = E.slice(YW, 0, l), W = E.slice(YW, l, s), Xc = E.slice(OmX, l, s);
+  double* Z = E.alloc((int64_t)s * s);
+  E.cross(SIDE_M, Xr, W, Z);                      // Z = Xi_r^* A Xi_c      (s x s)
+  E.orth(SIDE_M, Yc, nullptr, nullptr);           // Q_c R_c := Y_c
+  E.orth(SIDE_N, Yr, nullptr, nullptr, true);     // Q_r R_r := Y_r (shifted CholeskyQR3, R22)
+  double* Uc = E.alloc((int64_t)s * l);
+  double* Ur = E.alloc((int64_t)s * l2);
+  E.cross(SIDE_M, Xr, Yc, Uc);                    // Xi_r^* Q_c            (s x l)
+  E.cross(SIDE_N, Xc, Yr, Ur);                    // Xi_c^* Q_r            (s x l2)
+  double* Tc = E.alloc((int64_t)l * l);
+  double* Tr = E.alloc((int64_t)l2 * l2);
+  small_qr(E, Uc, s, l, Tc);                      // U_c T_c := Xi_r^* Q_c
+  small_qr(E, Ur, s, l2, Tr);                     // U_r T_r := Xi_c^* Q_r
+  double* Tcp = E.alloc((int64_t)l * l);
+  double* Trp = E.alloc((int64_t)l2 * l2);
+  small_pinv(E, Tc, l, Tcp);
+  small_pinv(E, Tr, l2, Trp);
+  double* M1 = E.alloc((int64_t)l * s);
+  double* X = E.alloc((int64_t)l * l2);
+  double* C1 = E.alloc((int64_t)l * l2);
+  double* core = E.alloc((int64_t)l * l2);
+  double* scratch = E.alloc(2 * 512 * 512 + 4096);
+  double* Ux = E.alloc((int64_t)l2 * l);
+  double* Vx = E.alloc((int64_t)l * l);
+  double* sx = E.alloc(l);
+  double* A1 = E.alloc((int64_t)l * k);
+  double* B1 = E.alloc((int64_t)l2 * k);
+  double* Ul = E.alloc((int64_t)l2 * l);
+  double* Vr = E.alloc((int64_t)l * l);
+  double* lam = E.alloc(l);
+  if (E.live()) {
+    E.chk(launch_small_gemm(1, 0, l, s, s, Uc, s, Z, s, M1, l, E.st));         // U_c^* Z
+    E.chk(launch_small_gemm(0, 0, l, l2, s, M1, l, Ur, s, X, l, E.st));        // U_c^* Z U_r   (l x l2)
+    if (c.variant == RSVD_EXT_BWZ2) {
+      E.chk(launch_small_gemm(0, 0, l, l2, l, Tcp, l, X, l, C1, l, E.st));     // T_c^+ (.)
+      E.chk(launch_small_gemm(0, 1, l, l2, l2, C1, l, Trp, l2, core, l, E.st)); // (.) (T_r^*)^+
+    } else {
+      // [[X]]_k = Vx diag(sx) Ux^T from Jacobi on X^T (l2 x l): X^T = Ux S Vx^T
+      E.chk(launch_jacobi_t(X, l, 1, l2, l, Ux, sx, Vx, scratch, E.ctx->dstat, E.st, 0));
+      E.chk(launch_small_gemm(0, 0, l, k, l, Tcp, l, Vx, l, A1, l, E.st));      // T_c^+ U_x
+      E.chk(launch_scale_cols(A1, l, l, k, sx, E.st));                           //   diag(sigma_x)
+      E.chk(launch_small_gemm(0, 0, l2, k, l2, Trp, l2, Ux, l2, B1, l2, E.st)); // T_r^+ V_x
+      E.chk(launch_small_gemm(0, 1, l, l2, k, A1, l, B1, l2, core, l, E.st));   // rank-k core
+    }
+    // tsvd(core, k): Jacobi on core^T (l2 x l): core^T = Ul S Vr^T  ->  core = Vr S Ul^T
+    E.chk(launch_jacobi_t(core, l, 1, l2, l, Ul, lam, Vr, scratch, E.ctx->dstat, E.st, 0));
+  }
+  write_outputs(E, SIDE_M, SIDE_N, Yc, Yr, Vr, Ul, lam, l, k);
 }
 
 // Alg. 3 QrQc on B = A (tr = false) or B = A^T (tr = true), v >= 0 views, starting
@@ -1114,6 +1232,7 @@ void run_alg(Exec& E) {
     case 2: alg_single_pass(E); break;
     case 3: alg_nystrom(E); break;
     case 4: alg_pinched(E); break;
+    case 5: alg_extended(E); break;
     case 10: prim_view(E); break;
     case 11: prim_fused(E); break;
     case 12: prim_orth(E); break;
@@ -1125,10 +1244,13 @@ void run_alg(Exec& E) {
 
 std::string call_key(const Call& c, const Exec& E, const rsvd_ctx* ctx) {
   char buf[1024];
-  snprintf(buf, sizeof buf, "a%d k%d p%d v%d in%d l2%d lc%d t%d w%d r%lld c%d f%u A%p m%lld n%lld lda%lld U%d S%d V%d R%d ar%p nr%d",
+  snprintf(buf, sizeof buf,
+           "a%d k%d p%d v%d in%d l2%d lc%d t%d w%d r%lld c%d f%u A%p m%lld n%lld lda%lld U%d S%d V%d R%d ar%p nr%d "
+           "s%d x%d",
            c.alg, c.k, c.p, c.v, c.input, c.l2, c.lc, c.trans, c.w, (long long)c.rows, c.cols, c.flags,
            (const void*)E.A, (long long)E.m, (long long)E.n, (long long)E.lda, c.kU != PTR_NULL, c.kS != PTR_NULL,
-           c.kV != PTR_NULL, c.kR != PTR_NULL, (void*)ctx->arena, ctx->nranks + (ctx->comm ? 1000 : 0));
+           c.kV != PTR_NULL, c.kR != PTR_NULL, (void*)ctx->arena, ctx->nranks + (ctx->comm ? 1000 : 0), c.s,
+           c.variant);
   return std::string(buf);
 }
 
@@ -1169,6 +1291,8 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
   call.kS = ptr_kind(call.S, ctx->device);
   call.kV = ptr_kind(call.V, ctx->device);
   call.kR = ptr_kind(call.R, ctx->device);
+  call.kXr = ptr_kind(call.Xr, ctx->device);
+  call.kXc = ptr_kind(call.Xc, ctx->device);
   const bool profile = (call.flags & RSVD_PROFILE) != 0;
   if (ctx->pending) {
     set_err(ctx, "a RSVD_ASYNC call on this ctx has not been completed by rsvd_wait");
@@ -1297,6 +1421,7 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
   memset(&base_info, 0, sizeof(base_info));
   base_info.graph_replayed = replay ? 1 : 0;
   base_info.host_staged = (call.kA == PTR_HOST || call.kOm == PTR_HOST || call.kPhi == PTR_HOST ||
+                           call.kXr == PTR_HOST || call.kXc == PTR_HOST ||
                            call.kU == PTR_HOST || call.kV == PTR_HOST || call.kS == PTR_HOST)
                               ? 1
                               : 0;
@@ -1649,6 +1774,59 @@ int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int
     info->lc_used = lc;
     // MinVar: the choice is made on the device (complete now unless the call is RSVD_ASYNC)
     if (lc == RSVD_LC_MINVAR && r == RSVD_OK && !(flags & RSVD_ASYNC)) info->lc_used = ctx->hstat->minvar_lc;
+  }
+  return r;
+}
+
+int rsvd_single_pass_extended(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int s, const void* Omega,
+                              int64_t ld_omega, const void* Phi, int64_t ld_phi, const void* Xi_r, int64_t ld_xi_r,
+                              const void* Xi_c, int64_t ld_xi_c, int variant, void* U, int64_t ldu, void* S,
+                              void* V, int64_t ldv, unsigned flags, rsvd_info* info) {
+  int r = common_checks(ctx, A, k, p);
+  if (r == RSVD_OK) {
+    if (l2 < k + p) { set_err(ctx, "l2 >= k + p required (P:663)"); r = RSVD_E_ARG; }
+    else if (l2 > std::min<int64_t>(A->m, 512)) { set_err(ctx, "l2 exceeds min(m, 512)"); r = RSVD_E_ARG; }
+    else if (s < k + p || s > std::min<int64_t>(std::min(A->m, A->n), 512)) {
+      set_err(ctx, "k + p <= s <= min(m, n, 512) required (P:805)");
+      r = RSVD_E_ARG;
+    } else if (variant != RSVD_EXT_BWZ && variant != RSVD_EXT_BWZ2) { set_err(ctx, "unknown variant"); r = RSVD_E_ARG; }
+    else if (!Omega || !Phi || !Xi_r || !Xi_c) { set_err(ctx, "Omega/Phi/Xi_r/Xi_c NULL"); r = RSVD_E_ARG; }
+    else if (ld_omega < A->n || ld_phi < A->m_local || ld_xi_r < A->m_local || ld_xi_c < A->n) {
+      set_err(ctx, "ld_omega/ld_phi/ld_xi_r/ld_xi_c too small");
+      r = RSVD_E_ARG;
+    } else if ((U && ldu < A->m_local) || (V && ldv < A->n)) { set_err(ctx, "ldu/ldv too small"); r = RSVD_E_ARG; }
+  }
+  if (r != RSVD_OK) {
+    if (info) { memset(info, 0, sizeof(*info)); info->status = r; }
+    return r;
+  }
+  Call c;
+  c.alg = 5;
+  c.A = A;
+  c.k = k;
+  c.p = p;
+  c.l2 = l2;
+  c.s = s;
+  c.variant = variant;
+  c.Om = Omega;
+  c.ldom = ld_omega;
+  c.Phi = Phi;
+  c.ldphi = ld_phi;
+  c.Xr = Xi_r;
+  c.ldxr = ld_xi_r;
+  c.Xc = Xi_c;
+  c.ldxc = ld_xi_c;
+  c.U = U;
+  c.ldu = ldu;
+  c.S = S;
+  c.V = V;
+  c.ldv = ldv;
+  c.flags = flags;
+  r = execute(ctx, c, info);
+  if (info) {
+    info->status = r;
+    info->views = 1;
+    info->vectors = (int64_t)(k + p) + s + l2;   // A [Omega | Xi_c] and A^T Phi
   }
   return r;
 }

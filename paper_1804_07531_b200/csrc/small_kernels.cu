@@ -730,6 +730,42 @@ int launch_jacobi(const double* M, int64_t ldm, int r, int c, double* Ul, double
   return launch_jacobi_t(M, ldm, 0, r, c, Ul, S, Vr, scratch, status, st, 1);
 }
 
+// ------------------------------------------------------------------ pseudo-inverse / scaling
+// Tp (w x w) = V diag(s^+) U^T from T = U diag(s) V^T (U, V w x w col-major, s descending);
+// s_i <= rcut * s_0 is dropped.  One thread per output entry.
+__global__ void k_pinv_svd(const double* __restrict__ U, const double* __restrict__ s,
+                           const double* __restrict__ V, int w, double rcut, double* __restrict__ Tp) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= w * w) return;
+  const int i = e % w, j = e / w;
+  const double cut = rcut * s[0];
+  double acc = 0.0;
+  for (int t = 0; t < w; ++t) {
+    const double st = s[t];
+    if (st > cut && st > 0.0) acc = fma(V[(int64_t)t * w + i] / st, U[(int64_t)t * w + j], acc);
+  }
+  Tp[e] = acc;
+}
+
+int launch_pinv_svd(const double* U, const double* s, const double* V, int w, double rcut, double* Tp,
+                     cudaStream_t st) {
+  k_pinv_svd<<<(w * w + 255) / 256, 256, 0, st>>>(U, s, V, w, rcut, Tp);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+__global__ void k_scale_cols(double* __restrict__ X, int64_t ld, int rows, int cols, const double* __restrict__ d) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const int i = e % rows, j = e / rows;
+  X[(int64_t)j * ld + i] *= d[j];
+}
+
+int launch_scale_cols(double* X, int64_t ld, int rows, int cols, const double* d, cudaStream_t st) {
+  if (rows * cols == 0) return RSVD_OK;
+  k_scale_cols<<<(rows * cols + 255) / 256, 256, 0, st>>>(X, ld, rows, cols, d);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
 // ------------------------------------------------------------------ small dense helpers
 __global__ void k_small_gemm(int ta, int tb, int m, int n, int k, const double* __restrict__ A, int64_t lda_,
                              const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc) {

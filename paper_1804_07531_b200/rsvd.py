@@ -21,6 +21,7 @@ RSVD_INPUT_A, RSVD_INPUT_AT = 0, 1
 RSVD_GOAL_SVD, RSVD_GOAL_LEFT, RSVD_GOAL_RIGHT, RSVD_GOAL_NORMAL = 0, 1, 2, 3
 RSVD_SQUARED, RSVD_NO_GRAPH, RSVD_PROFILE, RSVD_CORE_NO_J, RSVD_ASYNC, RSVD_WOOLFE = 1, 2, 4, 16, 32, 64
 RSVD_LC_MINVAR = -2
+RSVD_EXT_BWZ, RSVD_EXT_BWZ2 = 0, 1
 RSVD_PLAN_FLAT, RSVD_PLAN_DECAY, RSVD_PLAN_RAPID, RSVD_PLAN_BALANCED = 0, 1, 2, 3
 ERR = {0: "RSVD_OK", -1: "RSVD_E_ARG", -2: "RSVD_E_DTYPE", -3: "RSVD_E_CUDA", -4: "RSVD_E_NCCL",
        -5: "RSVD_E_NOMEM", -6: "RSVD_E_NUMERIC", -7: "RSVD_E_STATE"}
@@ -28,7 +29,7 @@ ERR = {0: "RSVD_OK", -1: "RSVD_E_ARG", -2: "RSVD_E_DTYPE", -3: "RSVD_E_CUDA", -4
 EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_wait", "rsvd_strerror", "rsvd_last_error", "rsvd_version", "rsvd_sm_count",
            "rsvd_recommend_input", "rsvd_probe_peaks", "rsvd_get_unique_id", "rsvd_comm_init", "rsvd_comm_nranks", "rsvd_subspace",
            "rsvd_block_krylov", "rsvd_single_pass", "rsvd_nystrom", "rsvd_pinched", "rsvd_view", "rsvd_view_fused",
-           "rsvd_orth", "rsvd_core_svd", "rsvd_plan"]
+           "rsvd_orth", "rsvd_core_svd", "rsvd_plan", "rsvd_single_pass_extended"]
 
 
 class RsvdMat(ctypes.Structure):
@@ -87,6 +88,8 @@ def lib():
     L.rsvd_block_krylov.argtypes = alg
     L.rsvd_plan.argtypes = [i32, i32, i32, ctypes.c_double, ctypes.POINTER(i32), ctypes.POINTER(i32),
                             ctypes.POINTER(i32)]
+    L.rsvd_single_pass_extended.argtypes = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, i64, i32,
+                                            vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_single_pass.argtypes = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_nystrom.argtypes = [vp, pmat, i32, i32, i32, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_pinched.argtypes = [vp, pmat, i32, i32, i32, vp, i64, vp, vp, i64, u32, pinfo]
@@ -251,6 +254,25 @@ class Context:
                                     _ld(Ph), U.data_ptr(), _ld(U), S.data_ptr(), V.data_ptr(), _ld(V), flags,
                                     ctypes.byref(info))
         self._check(rc, "rsvd_single_pass")
+        return U, S, V, info
+
+    def single_pass_extended(self, A, k, p, l2, s, Omega, Phi, Xi_r, Xi_c, variant="bwz2", flags=0, m=None,
+                             row0=0, host_out=False):
+        """Extended 1-view sketch (P:797-846): Xi_r (m x s), Xi_c (n x s) are the SRFT test matrices;
+        variant "bwz" (Eq. bwz) or "bwz2" (Eq. bwzimproved)."""
+        var = {"bwz": RSVD_EXT_BWZ, "bwz2": RSVD_EXT_BWZ2}[variant] if isinstance(variant, str) else variant
+        Om, Ph, Xr, Xc = _colmajor(Omega), _colmajor(Phi), _colmajor(Xi_r), _colmajor(Xi_c)
+        M = self.mat(A, m, row0)
+        U = self._out_like(A, A.shape[0], k, host_out)
+        V = self._out_like(A, A.shape[1], k, host_out)
+        S = (torch.empty(k, dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
+             else torch.empty(k, dtype=A.dtype, device=A.device))
+        info = RsvdInfo()
+        rc = lib().rsvd_single_pass_extended(self._h, ctypes.byref(M), k, p, l2, s, Om.data_ptr(), _ld(Om),
+                                             Ph.data_ptr(), _ld(Ph), Xr.data_ptr(), _ld(Xr), Xc.data_ptr(), _ld(Xc),
+                                             var, U.data_ptr(), _ld(U), S.data_ptr(), V.data_ptr(), _ld(V), flags,
+                                             ctypes.byref(info))
+        self._check(rc, "rsvd_single_pass_extended")
         return U, S, V, info
 
     def _normal(self, fn, name, A, k, p, v, Omega, flags=0, m=None, row0=0, host_out=False):

@@ -112,3 +112,47 @@ def test_woolfe_parity(ctx, case, frac):
     # V has orthonormal columns by construction (line 9 d)
     Vh = host(V)
     assert np.abs(Vh.T @ Vh - np.eye(k)).max() <= 1e-12
+
+
+# ---------------------------------------------------------------- extended sketch (f4)
+EXT_CASES = [
+    ("C1", 200, 200, 10, 10, 20, 40),
+    ("C2", 1500, 1300, 20, 10, 30, 80),
+    ("C2", 777, 515, 5, 7, 12, 30),        # ragged
+    ("C3", 3000, 2000, 50, 20, 70, 140),
+]
+
+
+@pytest.mark.parametrize("case", EXT_CASES, ids=lambda c: f"{c[0]}-{c[1]}x{c[2]}-k{c[3]}p{c[4]}l2{c[5]}s{c[6]}")
+@pytest.mark.parametrize("variant", ["bwz", "bwz2"])
+def test_extended_parity(ctx, case, variant):
+    cfg_name, m, n, k, p, l2, s = case
+    cfg = S.CONFIGS[cfg_name]
+    A = S.make_matrix(cfg, m, n)
+    Om = S.gaussian_test_matrix(n, k + p, cfg, S.ROLE_OMEGA)
+    Phi = S.gaussian_test_matrix(m, l2, cfg, S.ROLE_PHI)
+    Xr, Xc = S.srft_matrix(m, s, 1), S.srft_matrix(n, s, 2)
+    U, sv, V, info = ctx.single_pass_extended(dev(A), k, p, l2, s, cm(Om), cm(Phi), cm(Xr), cm(Xc), variant=variant)
+    Uo, so, Vo = O.one_view_extended(A, k, p, l2 - k, Om, Phi, Xr, Xc, variant=variant)
+    assert info.views == 1
+    assert np.max(np.abs(host(sv) - so) / so) <= TOL_S
+    assert O.projector_distance(host(U), Uo) <= TOL_P and O.projector_distance(host(V), Vo) <= TOL_P
+
+
+def test_extended_exact_rank_and_errors(ctx):
+    from paper_1804_07531_b200 import rsvd
+
+    rng = np.random.default_rng(5)
+    m, n, k, p = 400, 300, 6, 4
+    X = np.linalg.qr(rng.standard_normal((m, 5)))[0]
+    Y = np.linalg.qr(rng.standard_normal((n, 5)))[0]
+    A = X @ np.diag([5.0, 4.0, 3.0, 2.0, 1.0]) @ Y.T
+    Om, Phi = rng.standard_normal((n, k + p)), rng.standard_normal((m, k + p))
+    Xr, Xc = S.srft_matrix(m, 30, 3), S.srft_matrix(n, 30, 4)
+    for variant in ("bwz", "bwz2"):
+        U, sv, V, info = ctx.single_pass_extended(dev(A), k, p, k + p, 30, cm(Om), cm(Phi), cm(Xr), cm(Xc),
+                                                  variant=variant)
+        np.testing.assert_allclose(host(sv)[:5], [5, 4, 3, 2, 1], rtol=1e-10)
+        assert np.all(np.abs(host(sv)[5:]) <= 1e-10)
+    with pytest.raises(rsvd.RsvdError):   # s < k + p
+        ctx.single_pass_extended(dev(A), k, p, k + p, 8, cm(Om), cm(Phi), cm(Xr[:, :8]), cm(Xc[:, :8]))
