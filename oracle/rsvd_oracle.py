@@ -35,6 +35,7 @@ __all__ = [
     "std_subspace_iteration", "gen_subspace_iteration", "qrqc", "one_view_tropp", "one_view_woolfe",
     "plan_flat", "plan_decay", "plan_rapid", "plan_balanced", "minvar_spectra", "minvar_select",
     "one_view_minvar", "one_view_extended", "plan_extended", "pinv",
+    "row_stream_qb",
     "gen_block_krylov", "normal_matrix_tevd", "nystrom_tevd", "pinched_tevd", "recommend_input", "svd_of",
     "views_and_vectors", "rel_frobenius_error", "rel_spectral_error", "projector_distance",
     "residual_fro", "half_power_lhs_rhs", "thm_bound",
@@ -451,6 +452,32 @@ def plan_extended(p, T, n_r, n_c):
     if s < p + l1:
         raise ValueError("budget leaves s < p + l_1")
     return l1, l1, s
+
+
+# ============================================================ single pass over the rows
+
+def row_stream_qb(A, p, l, Omega_r, panel_rows=1, order=None):
+    """Single pass over the rows of A: Y_c[i, :] = A[i, :] Omega_r and
+    Yhat_r = sum_i A[i, :]^* Y_c[i, :] accumulated row by row (rows visited once, in `order`);
+    [Q_c, R_c] = qr(Y_c); B^* R_c = Yhat_r solved with the TSVD pseudo-inverse of R_c (P:855:
+    'estimating a solution using a pseudoinverse'); then the rank-p SVD of Q_c B.  With R_c
+    invertible, B^* = A^* Q_c and this is Alg. 2 with v = 2 (P:853).  Returns (U, lambda, V)."""
+    A = _f64(A)
+    Omega_r = _f64(Omega_r)
+    n_r, n_c = A.shape
+    w = Omega_r.shape[1]
+    Yc = np.zeros((n_r, w))
+    Yr_hat = np.zeros((n_c, w))
+    rows = np.arange(n_r) if order is None else np.asarray(order)
+    for i0 in range(0, n_r, panel_rows):
+        idx = rows[i0:i0 + panel_rows]
+        Yc[idx] = A[idx] @ Omega_r                # Y_c[i, :] = A[i, :] Omega_r
+        Yr_hat += A[idx].T @ Yc[idx]              # Yhat_r += A[i, :]^* Y_c[i, :]
+    Qc, Rc = qr(Yc)
+    Bt = Yr_hat @ pinv(Rc)                        # B^* = Yhat_r R_c^+   (n_c x w)
+    Qb, Rb = qr(Bt)                               # Q_c B = Q_c R_b^* Q_b^*
+    Uh, lam, Vh = tsvd(Rb.T, p)
+    return Qc @ Uh, lam, Qb @ Vh
 
 
 # ============================================================ Algorithm 9 (P:900-928)

@@ -664,3 +664,42 @@ def test_extended_bwz2_at_least_as_accurate_on_average():
             U, lam, V = O.one_view_extended(A, p, l1, l1, Om_r, Om_c, Pr, Pc, variant=v)
             errs[v].append(np.linalg.norm(A - (U * lam) @ V.T) / np.linalg.norm(A))
     assert np.mean(errs["bwz2"]) <= np.mean(errs["bwz"]) * 1.0001
+
+
+# ---------------------------------------------------------------- f1: single pass over the rows
+
+def test_row_stream_equals_two_view_alg2():
+    """with R_c invertible, B^* = Yhat_r R_c^-1 = A^* Q_c, so the row-wise single pass gives
+    the basic 2-view approximation (Alg. 2, v = 2) — an independent route (Alg. 2's two views)."""
+    cfg = S.CONFIGS["C2"]
+    A = S.make_matrix(cfg, 700, 500)
+    Om = S.random_gaussian_matrix(500, 30, seed=41)
+    U, lam, V = O.row_stream_qb(A, 20, 10, Om, panel_rows=64)
+    Uo, lo, Vo = O.gen_subspace_iteration(A, 20, 10, 2, Om)
+    np.testing.assert_allclose(lam, lo, rtol=1e-10)
+    assert proj(U, Uo) <= 1e-9 and proj(V, Vo) <= 1e-9
+
+
+def test_row_stream_order_and_panels_invariant():
+    """Rows visited once in any order / any panel size: the sums are order-independent."""
+    cfg = S.CONFIGS["C1"]
+    A = S.make_matrix(cfg)
+    Om = S.random_gaussian_matrix(A.shape[1], 20, seed=42)
+    U1, l1, V1 = O.row_stream_qb(A, 10, 10, Om, panel_rows=1)
+    perm = np.random.default_rng(3).permutation(A.shape[0])
+    U2, l2, V2 = O.row_stream_qb(A, 10, 10, Om, panel_rows=7, order=perm)
+    np.testing.assert_allclose(l1, l2, rtol=1e-12)
+    assert proj(U1, U2) <= 1e-11 and proj(V1, V2) <= 1e-11
+
+
+def test_row_stream_exact_rank_and_single_row():
+    rng = np.random.default_rng(9)
+    X = np.linalg.qr(rng.standard_normal((120, 3)))[0]
+    Y = np.linalg.qr(rng.standard_normal((90, 3)))[0]
+    A = X @ np.diag([3.0, 2.0, 1.0]) @ Y.T
+    U, lam, V = O.row_stream_qb(A, 3, 4, rng.standard_normal((90, 7)), panel_rows=16)
+    np.testing.assert_allclose(lam, [3.0, 2.0, 1.0], rtol=1e-10)
+    assert np.linalg.norm(A - (U * lam) @ V.T) <= 1e-10 * np.linalg.norm(A)
+    a = rng.standard_normal((1, 40))                      # single-row matrix: rank-1 exact (S:393)
+    U, lam, V = O.row_stream_qb(a, 1, 0, rng.standard_normal((40, 1)))
+    np.testing.assert_allclose(lam[0], np.linalg.norm(a), rtol=1e-13)
