@@ -179,6 +179,16 @@ int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int
                      void* U, int64_t ldu, void* S, void* V, int64_t ldv,
                      unsigned flags, rsvd_info* info);
 
+/* Single pass over the rows of A: Y_c[i, :] = A[i, :] Omega and Yhat_r = sum_i
+ * A[i, :]^T Y_c[i, :] from ONE pass over A's rows, Q_c R_c := Y_c, B^T = Yhat_r R_c^+ (TSVD
+ * pseudo-inverse, singular values below 1e-12 sigma_max dropped), and the rank-k SVD of
+ * Q_c B.  With R_c invertible this equals rsvd_subspace with v = 2 from half the reads of
+ * A: the GPU walks A in row panels of <= 48 MB that stay in L2 between the two products (each
+ * panel is read from HBM once).  Omega n x (k+p).  info->views = 1.  Same pointer, dtype, sharding
+ * and error rules as rsvd_subspace (Yhat_r is all-reduced over the row shards). */
+int rsvd_row_stream(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, const void* Omega, int64_t ld_omega,
+                    void* U, int64_t ldu, void* S, void* V, int64_t ldv, unsigned flags, rsvd_info* info);
+
 /* Extended 1-view sketch: from ONE view of A, Y_c = A Omega (n x (k+p) Omega),
  * Y_r = A^T Phi (Phi m_local x l2) and Z = Xi_r^T A Xi_c (s x s), with Xi_r (m_local x s) and Xi_c
  * (n x s) the paper's SRFT matrices Phi_r, Phi_c, materialised dense by the caller and

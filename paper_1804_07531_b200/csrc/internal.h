@@ -24,6 +24,7 @@ struct ViewArgs {
   int64_t ldo, slot_stride;
   int S, KTS;       // reduction split (from plan_view)
   int grid_cap;     // persistent grid size (SM count)
+  int a_keep = 0;   // A*X only: load A with evict_last (a row panel re-read from L2 by A^T Y next)
 };
 
 struct FusedArgs {
@@ -113,6 +114,8 @@ int launch_small_gemm(int ta, int tb, int m, int n, int k, const double* A, int6
 int launch_copy_cols(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int cols,
                      cudaStream_t st);
 int launch_fill(double* dst, int64_t count, double v, cudaStream_t st);
+// out (rows x c) += T (rows x c), column-major
+int launch_add_cols(const double* T, int64_t ldt, double* out, int64_t ldo, int64_t rows, int c, cudaStream_t st);
 // out (rows x c) -= T (rows x c), column-major
 int launch_sub_cols(const double* T, int64_t ldt, double* out, int64_t ldo, int64_t rows, int c, cudaStream_t st);
 // triangular-system helpers for Alg. 7: out (c x c) = upper-triangular inverse of R (c x c)

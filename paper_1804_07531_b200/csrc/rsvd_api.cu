@@ -263,9 +263,13 @@ struct Exec {
 
   // ------------------------------------------------------------ matrix views (hot path)
   // from == SIDE_N: Y (side M) = A X;  from == SIDE_M: Y (side N) = A^T X (+ all-reduce)
-  void view(Side from, const TS& X, const TS& Y) {
+  // One view of A (or, with nr >= 0, of its row panel [r0, r0 + nr): then Y / X are the panel's
+  // row slices, nothing is all-reduced, and a_keep loads the panel with evict_last for a re-read).
+  void view(Side from, const TS& X, const TS& Y, int64_t r0 = 0, int64_t nr = -1, int a_keep = 0) {
+    const bool panel = nr >= 0;
+    const int64_t rows_v = panel ? nr : m;
     if (dtype == RSVD_F32) {
-      view32(from, X, Y);
+      view32(from, X, Y, r0, nr);
       return;
     }
     const int w = X.w;
@@ -273,23 +277,24 @@ struct Exec {
       const int wc = std::min(kMaxWT * 8, w - c0);
       const size_t mk = mark();
       ViewArgs a;
-      a.A = A;
-      a.rows = m;
+      a.A = A + (panel ? r0 * lda : 0);
+      a.rows = rows_v;
       a.n = n;
       a.lda = lda;
+      a.a_keep = a_keep;
       a.X = X.p + (int64_t)c0 * X.ld;
       a.ldx = X.ld;
       a.w = wc;
       a.grid_cap = ctx->sms;
       const int kind = (from == SIDE_N) ? VIEW_AX : VIEW_ATY;
-      plan_view(kind, m, n, wc, ctx->sms, &a.S, &a.KTS);
+      plan_view(kind, rows_v, n, wc, ctx->sms, &a.S, &a.KTS);
       double* dst = Y.p + (int64_t)c0 * Y.ld;
       double* slots = (a.S == 1) ? dst : alloc((int64_t)a.S * Y.ld * wc);
       a.out = slots;
       a.ldo = Y.ld;
       a.slot_stride = (int64_t)Y.ld * wc;
-      view_bytes += (double)m * n * 8.0;
-      view_flops += 2.0 * m * n * wc;
+      view_bytes += (double)rows_v * n * 8.0;
+      view_flops += 2.0 * rows_v * n * wc;
       ++view_launches;
       if (live()) {
         int e0 = -1, e1 = -1;
@@ -301,19 +306,21 @@ struct Exec {
       }
       release(mk);
     }
-    if (from == SIDE_M && collective()) allreduce(Y.p, Y.ld * Y.w);
+    if (from == SIDE_M && collective() && !panel) allreduce(Y.p, Y.ld * Y.w);
   }
 
   // fp32 A: split X into tf32 hi / lo parts, tcgen05 3xTF32 view into fp64 partial slots
-  void view32(Side from, const TS& X, const TS& Y) {
+  void view32(Side from, const TS& X, const TS& Y, int64_t r0 = 0, int64_t nr = -1) {
+    const bool panel = nr >= 0;
+    const int64_t rows_v = panel ? nr : m;
     const int w = X.w;
     for (int c0 = 0; c0 < w; c0 += kMaxW32) {
       const int wc = std::min(kMaxW32, w - c0);
       const size_t mk = mark();
       ViewArgs32 a;
       a.kind = (from == SIDE_N) ? VIEW_AX : VIEW_ATY;
-      a.A = A32;
-      a.rows = m;
+      a.A = A32 + (panel ? r0 * lda : 0);
+      a.rows = rows_v;
       a.n = n;
       a.lda = lda;
       float* xh = alloc_f(X.ld * wc);
@@ -323,14 +330,14 @@ struct Exec {
       a.ldx = X.ld;
       a.w = wc;
       a.grid_cap = ctx->sms;
-      plan_view_tf32(a.kind, m, n, wc, ctx->sms, &a.S, &a.KTS);
+      plan_view_tf32(a.kind, rows_v, n, wc, ctx->sms, &a.S, &a.KTS);
       double* dst = Y.p + (int64_t)c0 * Y.ld;
       double* slots = (a.S == 1) ? dst : alloc((int64_t)a.S * Y.ld * wc);
       a.out = slots;
       a.ldo = Y.ld;
       a.slot_stride = (int64_t)Y.ld * wc;
-      view_bytes += (double)m * n * 4.0;
-      view_flops += 2.0 * m * n * wc;
+      view_bytes += (double)rows_v * n * 4.0;
+      view_flops += 2.0 * rows_v * n * wc;
       ++view_launches;
       if (live()) {
         chk(launch_split_tf32(X.p + (int64_t)c0 * X.ld, X.ld, X.rows, wc, xh, xl, X.ld, st));
@@ -343,7 +350,7 @@ struct Exec {
       }
       release(mk);
     }
-    if (from == SIDE_M && collective()) allreduce(Y.p, Y.ld * Y.w);
+    if (from == SIDE_M && collective() && !panel) allreduce(Y.p, Y.ld * Y.w);
   }
 
   // G (a x b, col-major ld a) = Xa^T Xb over the side's rows (+ all-reduce when sharded)
@@ -985,6 +992,57 @@ void alg_extended(Exec& E) {
   write_outputs(E, SIDE_M, SIDE_N, Yc, Yr, Vr, Ul, lam, l, k);
 }
 
+// Single pass over the rows of A.  A is walked in row panels small enough to stay in
+// L2: each panel is read from HBM once by the range view (Y_c rows = panel Omega, A loaded with
+// evict_last) and re-read from L2 by the co-range view (Yhat_r += panel^T Y_c rows, accumulated
+// in panel order).  Then Q_c R_c := Y_c, B^* = Yhat_r R_c^+ (TSVD pseudo-inverse) and
+// the rank-k SVD of Q_c B through qr(B^*).  With R_c invertible this is Alg. 2, v = 2.
+constexpr double kRowPanelBytes = 48.0 * 1024 * 1024;
+void alg_row_stream(Exec& E) {
+  const Call& c = E.call;
+  const int l = c.k + c.p;
+  TS Om = E.stage_in(SIDE_N, c.Om, c.ldom, l, c.kOm);
+  TS Yc = E.new_ts(SIDE_M, l);
+  TS Yh = E.new_ts(SIDE_N, l);
+  TS T = E.new_ts(SIDE_N, l);
+  const double esz = (E.dtype == RSVD_F32) ? 4.0 : 8.0;
+  static const double panel_bytes = [] {
+    const char* e = getenv("RSVD_ROW_PANEL_MB");   // A/B experiments only
+    return e ? atof(e) * 1024 * 1024 : kRowPanelBytes;
+  }();
+  int64_t P = (int64_t)(panel_bytes / (esz * (double)E.n));
+  P = std::max<int64_t>(128, P / 128 * 128);
+  for (int64_t r0 = 0; r0 < E.m; r0 += P) {
+    const int64_t nr = std::min<int64_t>(P, E.m - r0);
+    TS Yp;
+    Yp.p = Yc.p + r0;
+    Yp.rows = nr;
+    Yp.ld = Yc.ld;
+    Yp.w = l;
+    E.view(SIDE_N, Om, Yp, r0, nr, /*a_keep=*/1);            // Y_c[panel] = A[panel] Omega
+    const bool first = (r0 == 0);
+    E.view(SIDE_M, Yp, first ? Yh : T, r0, nr);              // A[panel]^* Y_c[panel]
+    if (!first && E.live()) E.chk(launch_add_cols(T.p, T.ld, Yh.p, Yh.ld, Yh.rows, l, E.st));
+  }
+  if (E.m == 0 && E.live()) E.chk(launch_fill(Yh.p, Yh.ld * l, 0.0, E.st));
+  if (E.collective()) E.allreduce(Yh.p, Yh.ld * l);          // Yhat_r over the row shards
+  double* Rc = E.alloc((int64_t)l * l);
+  E.orth(SIDE_M, Yc, Rc, nullptr);                           // Q_c R_c := Y_c
+  // R_c^+: guarded triangular inverse — equal to the TSVD pseudo-inverse for an invertible R_c and
+  // for the guard-zeroed rows / columns of an exactly rank-deficient one (reading R26)
+  double* Rcp = E.alloc((int64_t)l * l);
+  if (E.live()) E.chk(launch_tri_inv(Rc, l, Rcp, nullptr, E.st));
+  TS Bt = E.new_ts(SIDE_N, l);
+  E.tsmm(Yh.p, Yh.ld, Yh.rows, l, Rcp, l, l, Bt.p, Bt.ld, 0); // B^* = Yhat_r R_c^+
+  double* Rb = E.alloc((int64_t)l * l);
+  E.orth(SIDE_N, Bt, Rb, nullptr);                           // B^* = Q_b R_b
+  double* Ul = E.alloc((int64_t)l * l);
+  double* Vr = E.alloc((int64_t)l * l);
+  double* lam = E.alloc(l);
+  E.core_svd(Rb, l, 1, Vr, lam, Ul);                         // R_b = Ul S Vr^T -> Q_c B = Q_c Vr S Ul^T Q_b^T
+  write_outputs(E, SIDE_M, SIDE_N, Yc, Bt, /*Uh=*/Vr, /*Vh=*/Ul, lam, l, c.k);
+}
+
 // Alg. 3 QrQc on B = A (tr = false) or B = A^T (tr = true), v >= 0 views, starting
 // from the staged test matrix Q (on B's co-range side).  Returns the final basis: Q_r of B
 // (B's co-range side, in Q) for even v, Q_c of B (B's range side, new block) for odd v.
@@ -1233,6 +1291,7 @@ void run_alg(Exec& E) {
     case 3: alg_nystrom(E); break;
     case 4: alg_pinched(E); break;
     case 5: alg_extended(E); break;
+    case 6: alg_row_stream(E); break;
     case 10: prim_view(E); break;
     case 11: prim_fused(E); break;
     case 12: prim_orth(E); break;
@@ -1827,6 +1886,40 @@ int rsvd_single_pass_extended(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, in
     info->status = r;
     info->views = 1;
     info->vectors = (int64_t)(k + p) + s + l2;   // A [Omega | Xi_c] and A^T Phi
+  }
+  return r;
+}
+
+int rsvd_row_stream(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, const void* Omega, int64_t ld_omega, void* U,
+                    int64_t ldu, void* S, void* V, int64_t ldv, unsigned flags, rsvd_info* info) {
+  int r = common_checks(ctx, A, k, p);
+  if (r == RSVD_OK) {
+    if (!Omega) { set_err(ctx, "Omega NULL"); r = RSVD_E_ARG; }
+    else if (ld_omega < A->n) { set_err(ctx, "ld_omega too small"); r = RSVD_E_ARG; }
+    else if ((U && ldu < A->m_local) || (V && ldv < A->n)) { set_err(ctx, "ldu/ldv too small"); r = RSVD_E_ARG; }
+  }
+  if (r != RSVD_OK) {
+    if (info) { memset(info, 0, sizeof(*info)); info->status = r; }
+    return r;
+  }
+  Call c;
+  c.alg = 6;
+  c.A = A;
+  c.k = k;
+  c.p = p;
+  c.Om = Omega;
+  c.ldom = ld_omega;
+  c.U = U;
+  c.ldu = ldu;
+  c.S = S;
+  c.V = V;
+  c.ldv = ldv;
+  c.flags = flags;
+  r = execute(ctx, c, info);
+  if (info) {
+    info->status = r;
+    info->views = 1;                                 // one pass over the rows
+    info->vectors = 2 * (int64_t)(k + p);
   }
   return r;
 }

@@ -730,6 +730,31 @@ int launch_jacobi(const double* M, int64_t ldm, int r, int c, double* Ul, double
   return launch_jacobi_t(M, ldm, 0, r, c, Ul, S, Vr, scratch, status, st, 1);
 }
 
+// ------------------------------------------------------------------ guarded triangular inverse
+// X = R^-1 for upper-triangular R (c x c, col-major), one thread per column j (back substitution
+// x_i = -(sum_{t=i+1..j} R_it x_t) / R_ii).  A zero pivot R_ii (a column zeroed by the rank guard,
+// whose row is zero too) gives a zero row and column of X: then X is exactly R^+.
+__global__ void k_tri_inv(const double* __restrict__ R, int c, double* __restrict__ X) {
+  for (int j = threadIdx.x; j < c; j += blockDim.x) {
+    double* x = X + (int64_t)j * c;
+    for (int i = c - 1; i > j; --i) x[i] = 0.0;
+    const double rjj = R[(int64_t)j * c + j];
+    x[j] = rjj != 0.0 ? 1.0 / rjj : 0.0;
+    for (int i = j - 1; i >= 0; --i) {
+      const double rii = R[(int64_t)i * c + i];
+      double s = 0.0;
+      for (int t = i + 1; t <= j; ++t) s = fma(R[(int64_t)t * c + i], x[t], s);
+      x[i] = rii != 0.0 ? -s / rii : 0.0;
+    }
+  }
+}
+
+int launch_tri_inv(const double* R, int c, double* Rinv, DevStatus* /*status*/, cudaStream_t st) {
+  if (c < 1) return RSVD_E_ARG;
+  k_tri_inv<<<1, 128, 0, st>>>(R, c, Rinv);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
 // ------------------------------------------------------------------ pseudo-inverse / scaling
 // Tp (w x w) = V diag(s^+) U^T from T = U diag(s) V^T (U, V w x w col-major, s descending);
 // s_i <= rcut * s_0 is dropped.  One thread per output entry.
@@ -1651,7 +1676,18 @@ __global__ void k_sub_cols(const double* __restrict__ T, int64_t ldt, double* __
   const int j = blockIdx.y;
   if (r < rows && j < c) out[(int64_t)j * ldo + r] -= T[(int64_t)j * ldt + r];
 }
+__global__ void k_add_cols(const double* __restrict__ T, int64_t ldt, double* __restrict__ out, int64_t ldo,
+                           int64_t rows, int c) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (r < rows && j < c) out[(int64_t)j * ldo + r] += T[(int64_t)j * ldt + r];
+}
 }  // namespace
+int launch_add_cols(const double* T, int64_t ldt, double* out, int64_t ldo, int64_t rows, int c, cudaStream_t st) {
+  if (rows <= 0 || c <= 0) return RSVD_OK;
+  k_add_cols<<<dim3((unsigned)((rows + 255) / 256), (unsigned)c), 256, 0, st>>>(T, ldt, out, ldo, rows, c);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
 int launch_sub_cols(const double* T, int64_t ldt, double* out, int64_t ldo, int64_t rows, int c, cudaStream_t st) {
   if (rows <= 0 || c <= 0) return RSVD_OK;
   k_sub_cols<<<dim3((unsigned)((rows + 255) / 256), (unsigned)c), 256, 0, st>>>(T, ldt, out, ldo, rows, c);

@@ -49,7 +49,7 @@ template <int WT>
 __global__ void __launch_bounds__(kThreads, 1)
     k_view_ax(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX,
               double* __restrict__ out, int64_t ldo, int64_t slot_stride, int rows, int w, int RB, int S,
-              int KT, int KTS) {
+              int KT, int KTS, int a_keep) {
   using C = AxCfg<WT>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmX);
-      const uint64_t pa = policy_evict_first(), px = policy_evict_last();
+      const uint64_t pa = a_keep ? policy_evict_last() : policy_evict_first(), px = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < U; u += gridDim.x) {
@@ -548,7 +548,7 @@ int launch_ax_t(const ViewArgs& a, cudaStream_t st) {
     attr = true;
   }
   k_view_ax<WT><<<grid, kThreads, C::SMEM, st>>>(tmA, tmX, a.out, a.ldo, a.slot_stride, (int)a.rows, a.w, RB, a.S, KT,
-                                                   a.KTS);
+                                                   a.KTS, a.a_keep);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 

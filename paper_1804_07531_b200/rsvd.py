@@ -29,7 +29,8 @@ ERR = {0: "RSVD_OK", -1: "RSVD_E_ARG", -2: "RSVD_E_DTYPE", -3: "RSVD_E_CUDA", -4
 EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_wait", "rsvd_strerror", "rsvd_last_error", "rsvd_version", "rsvd_sm_count",
            "rsvd_recommend_input", "rsvd_probe_peaks", "rsvd_get_unique_id", "rsvd_comm_init", "rsvd_comm_nranks", "rsvd_subspace",
            "rsvd_block_krylov", "rsvd_single_pass", "rsvd_nystrom", "rsvd_pinched", "rsvd_view", "rsvd_view_fused",
-           "rsvd_orth", "rsvd_core_svd", "rsvd_plan", "rsvd_single_pass_extended"]
+           "rsvd_orth", "rsvd_core_svd", "rsvd_plan", "rsvd_single_pass_extended",
+           "rsvd_row_stream"]
 
 
 class RsvdMat(ctypes.Structure):
@@ -90,6 +91,7 @@ def lib():
                             ctypes.POINTER(i32)]
     L.rsvd_single_pass_extended.argtypes = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, i64, i32,
                                             vp, i64, vp, vp, i64, u32, pinfo]
+    L.rsvd_row_stream.argtypes = [vp, pmat, i32, i32, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_single_pass.argtypes = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_nystrom.argtypes = [vp, pmat, i32, i32, i32, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_pinched.argtypes = [vp, pmat, i32, i32, i32, vp, i64, vp, vp, i64, u32, pinfo]
@@ -273,6 +275,20 @@ class Context:
                                              var, U.data_ptr(), _ld(U), S.data_ptr(), V.data_ptr(), _ld(V), flags,
                                              ctypes.byref(info))
         self._check(rc, "rsvd_single_pass_extended")
+        return U, S, V, info
+
+    def row_stream(self, A, k, p, Omega, flags=0, m=None, row0=0, host_out=False):
+        """Single pass over the rows of A; equals subspace(v=2) when R_c is invertible."""
+        Om = _colmajor(Omega)
+        M = self.mat(A, m, row0)
+        U = self._out_like(A, A.shape[0], k, host_out)
+        V = self._out_like(A, A.shape[1], k, host_out)
+        S = (torch.empty(k, dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
+             else torch.empty(k, dtype=A.dtype, device=A.device))
+        info = RsvdInfo()
+        rc = lib().rsvd_row_stream(self._h, ctypes.byref(M), k, p, Om.data_ptr(), _ld(Om), U.data_ptr(), _ld(U),
+                                   S.data_ptr(), V.data_ptr(), _ld(V), flags, ctypes.byref(info))
+        self._check(rc, "rsvd_row_stream")
         return U, S, V, info
 
     def _normal(self, fn, name, A, k, p, v, Omega, flags=0, m=None, row0=0, host_out=False):

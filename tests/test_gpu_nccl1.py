@@ -102,3 +102,17 @@ def test_one_rank_comm_adaptive_single_pass(ctxs, variant):
     assert np.max(np.abs(s - so) / so) <= 1e-10
     assert O.projector_distance(U, Uo) <= 1e-9 and O.projector_distance(V, Vo) <= 1e-9
     assert np.max(np.abs(s - s0) / s0) <= 1e-12
+
+
+def test_one_rank_comm_row_stream(ctxs):
+    """The row-wise pass through the sharded route (Yhat_r all-reduced once after the panels)."""
+    c1, c0 = ctxs
+    cfg = S.CONFIGS["C2"]
+    A = S.make_matrix(cfg)
+    Om = S.gaussian_test_matrix(A.shape[1], cfg.l, cfg, S.ROLE_OMEGA)
+    Ad = torch.from_numpy(A).cuda()
+    (U, s, V), (U0, s0, V0) = [[host(x) for x in c.row_stream(Ad, cfg.k, cfg.p, colmajor_dev(Om))[:3]]
+                               for c in (c1, c0)]
+    Uo, so, Vo = O.row_stream_qb(A, cfg.k, cfg.p, Om, panel_rows=4096)
+    assert np.max(np.abs(s - so) / so) <= 1e-10 and O.projector_distance(V, Vo) <= 1e-9
+    assert np.max(np.abs(s - s0) / s0) <= 1e-12

@@ -156,3 +156,34 @@ def test_extended_exact_rank_and_errors(ctx):
         assert np.all(np.abs(host(sv)[5:]) <= 1e-10)
     with pytest.raises(rsvd.RsvdError):   # s < k + p
         ctx.single_pass_extended(dev(A), k, p, k + p, 8, cm(Om), cm(Phi), cm(Xr[:, :8]), cm(Xc[:, :8]))
+
+
+# ---------------------------------------------------------------- single pass over the rows (f1)
+ROW_CASES = [("C1", None, None), ("C2", None, None), ("C2", 777, 515), ("C3", 20000, 8000), ("C3", 9001, 3000)]
+
+
+@pytest.mark.parametrize("case", ROW_CASES, ids=lambda c: f"{c[0]}-{c[1]}x{c[2]}")
+def test_row_stream_parity(ctx, case):
+    """Row panels (48 MB) read once from HBM: vs the oracle's row-by-row pass and, as R_c is
+    invertible here, vs Alg. 2 with v = 2.  C3 at full size spans several panels."""
+    name, m, n = case
+    cfg = S.CONFIGS[name]
+    A = S.make_matrix(cfg, m, n)
+    Om = S.gaussian_test_matrix(A.shape[1], cfg.l, cfg, S.ROLE_OMEGA)
+    U, sv, V, info = ctx.row_stream(dev(A), cfg.k, cfg.p, cm(Om))
+    Uo, so, Vo = O.row_stream_qb(A, cfg.k, cfg.p, Om, panel_rows=4096)
+    assert info.views == 1
+    assert np.max(np.abs(host(sv) - so) / so) <= TOL_S
+    assert O.projector_distance(host(U), Uo) <= TOL_P and O.projector_distance(host(V), Vo) <= TOL_P
+    U2, s2, V2, _ = O.svd_of(A, "subspace", cfg.k, cfg.p, v=2, Omega=Om)
+    assert np.max(np.abs(host(sv) - s2) / s2) <= TOL_S
+
+
+def test_row_stream_fp32(ctx):
+    cfg = S.CONFIGS["C5"]
+    A = S.make_matrix(cfg, 3000, 2000).astype(np.float32)
+    Om = S.gaussian_test_matrix(2000, 60, cfg, S.ROLE_OMEGA).astype(np.float32)
+    U, sv, V, _ = ctx.row_stream(dev(A), 40, 20, cm(Om))
+    Uo, so, Vo = O.row_stream_qb(A.astype(np.float64), 40, 20, Om.astype(np.float64), panel_rows=4096)
+    assert np.max(np.abs(host(sv).astype(np.float64) - so) / so) <= 1e-4
+    assert O.projector_distance(host(U).astype(np.float64), Uo) <= 1e-3
