@@ -530,9 +530,12 @@ struct Exec {
   }
 
   // block classical Gram-Schmidt, twice, over blocks of width bw, then CholeskyQR2 per block
-  void bcgs2(Side s, const TS& K, int bw) {
+  // first_orthonormal: block 0 is already the Q of an orth (an intermediate Krylov block), so its
+  // own CholeskyQR2 would return it unchanged to rounding (R = I) and is skipped
+  void bcgs2(Side s, const TS& K, int bw, bool first_orthonormal = false) {
     const int nb = (K.w + bw - 1) / bw;
     for (int b = 0; b < nb; ++b) {
+      if (b == 0 && first_orthonormal) continue;
       const int c0 = b * bw, wc = std::min(bw, K.w - c0);
       TS Wb = slice(K, c0, wc);
       const size_t mk = mark();
@@ -702,7 +705,9 @@ void alg_krylov(Exec& E) {
     prev = dst;
   }
   if (v == 1) return;
-  E.bcgs2(side_K, K, l);                                  // qr(K_c) / qr(K_r)  (lines 9 / 14)
+  // block 0 of K is Q^1 (v even) or Q^2 (v odd): orthonormalised already unless it is the raw last block
+  const bool first_orth = even ? (1 < v - 1) : (2 < v - 1);
+  E.bcgs2(side_K, K, l, first_orth);                      // qr(K_c) / qr(K_r)  (lines 9 / 14)
   TS Qo = E.new_ts(even ? side_r : side_c, W);
   double* Rw = E.alloc((int64_t)W * W);
   E.view(side_K, K, Qo);                                  // one more view (lines 10 / 15)
