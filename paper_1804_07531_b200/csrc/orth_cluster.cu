@@ -240,6 +240,21 @@ __device__ __forceinline__ void gram_tiles(const double* Yc, int rpc, double* G,
   __syncthreads();
 }
 
+// (upper-triangular A B)(i, k) = sum_{q=i..k} A(i, q) B(q, k), col-major w x w, four named
+// accumulators (an accumulator array indexed by q & 3 lives in local memory)
+__device__ __forceinline__ double triu_dot(const double* A, const double* B, int w, int i, int k) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int q = i;
+  for (; q + 3 <= k; q += 4) {
+    s0 = fma(A[q * w + i], B[k * w + q], s0);
+    s1 = fma(A[(q + 1) * w + i], B[k * w + q + 1], s1);
+    s2 = fma(A[(q + 2) * w + i], B[k * w + q + 2], s2);
+    s3 = fma(A[(q + 3) * w + i], B[k * w + q + 3], s3);
+  }
+  for (; q <= k; ++q) s0 = fma(A[q * w + i], B[k * w + q], s0);
+  return (s0 + s1) + (s2 + s3);
+}
+
 template <int W>
 __global__ void __launch_bounds__(kThreads, 1)
     k_orth_cluster(double* __restrict__ Y, int64_t ldy, int64_t rows, int w, int rpc, int shifted, double shift_coef,
@@ -386,30 +401,42 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     apply_rinv<W>(Yc, Ri, rpc, warp, g, t4, Y + r0, ldy, nr, w);
   }
+  OT(28);
   // R_out = R_2 R_1 (R_2 R_1 R_0 when shifted; upper triangular products), CTA 0
   if (Rout && crank == 0) {
     __syncthreads();
+    OT(29);
+    // both factors in shared memory: G is free on CTA 0 now, and so is the row buffer Yc after the
+    // final apply when it holds w*w doubles (a dependent loop over global loads costs an L2 round
+    // trip per step: ~50k cycles at W = 64); tiny blocks keep the second factor in global memory
+    const bool yc_fits = (int64_t)rpc * ld >= (int64_t)w * w;
     if (shifted) {
-      // R_1 <- R_1 R_0: stage R_1 in shared memory (G is free on CTA 0 now), R_0 from global
+      // R_1 <- R_1 R_0
       for (int e = tid; e < w * w; e += kThreads) G[e] = R1[e];
+      const double* R0s = R0;
+      if (yc_fits) {
+        for (int e = tid; e < w * w; e += kThreads) Yc[e] = R0[e];
+        R0s = Yc;
+      }
       __syncthreads();
       for (int e = tid; e < w * w; e += kThreads) {
         const int i = e % w, k = e / w;
-        double sa[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int q = i; q <= k; ++q) sa[q & 3] = fma(G[q * w + i], R0[k * w + q], sa[q & 3]);
-        R1[e] = (i <= k) ? (sa[0] + sa[1]) + (sa[2] + sa[3]) : 0.0;
+        R1[e] = (i <= k) ? triu_dot(G, R0s, w, i, k) : 0.0;
       }
       __syncthreads();
     }
-    // stage R_2 in shared memory, R_1 is read from global (L1/L2)
+    // R_out = R_2 R_1
     const double* R1s = R1;
     for (int e = tid; e < w * w; e += kThreads) G[e] = Rc[e];
+    if (yc_fits) {
+      for (int e = tid; e < w * w; e += kThreads) Yc[e] = R1[e];
+      R1s = Yc;
+    }
     __syncthreads();
+    OT(30);
     for (int e = tid; e < w * w; e += kThreads) {
       const int i = e % w, k = e / w;
-      double sa[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int q = i; q <= k; ++q) sa[q & 3] = fma(G[q * w + i], R1s[k * w + q], sa[q & 3]);
-      Rout[e] = (i <= k) ? (sa[0] + sa[1]) + (sa[2] + sa[3]) : 0.0;
+      Rout[e] = (i <= k) ? triu_dot(G, R1s, w, i, k) : 0.0;
     }
   }
   OT(21);

@@ -30,6 +30,7 @@ int main(int argc, char** argv) {
            rc, cudaGetErrorString(cudaGetLastError()), ms * 1e3, t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3],
            t[5] - t[4], t[6] - t[5], t[8] - t[6], t[9] - t[8], t[10] - t[9], t[11] - t[10], t[12] - t[11],
            t[21] - t[20], t[22] - t[21], t[23] - t[1], t[24] - t[23], t[2] - t[24], t[15] - t[4], t[16] - t[15], t[13] - t[16], t[14] - t[13]);
+    printf("   final split: apply %lld, sync %lld, stage %lld, product %lld\n", t[28] - t[20], t[29] - t[28], t[30] - t[29], t[21] - t[30]);
   }
 }
 // ---- standalone timing of the factorisation (single CTA, no cluster)
@@ -61,7 +62,7 @@ int chol_alone_main() {
 }
 namespace rsvd { namespace {
 template <int W>
-__global__ void k_gram_alone(int rpc, long long* t, double* out) {
+__global__ void k_gram_alone(int rpc, long long* t, double* out, double* gout, int64_t ldo) {
   extern __shared__ double sm[];
   double* G = sm;
   double* Yc = sm + W * W;
@@ -75,17 +76,25 @@ __global__ void k_gram_alone(int rpc, long long* t, double* out) {
   apply_rinv<W>(Yc, G, rpc, warp, lane >> 2, lane & 3, nullptr, 0, 0, 0);
   __syncthreads();
   long long t2 = clock64();
-  if (threadIdx.x == 0) { t[0] = t1 - t0; t[1] = t2 - t1; out[0] = G[5] + Yc[7]; }
+  apply_rinv<W>(Yc, G, rpc, warp, lane >> 2, lane & 3, gout, ldo, rpc, W);
+  __syncthreads();
+  long long t3 = clock64();
+  if (threadIdx.x == 0) { t[0] = t1 - t0; t[1] = t2 - t1; t[2] = t3 - t2; out[0] = G[5] + Yc[7]; }
 }
 } }
-int gram_alone_main() {
-  long long* t; double* o; cudaMalloc(&t, 16); cudaMalloc(&o, 8);
+template <int W>
+void gram_alone_w() {
+  long long* t; double* o; double* go; cudaMalloc(&t, 24); cudaMalloc(&o, 8); cudaMalloc(&go, 4032 * 64 * 8);
   const int rpc = 256;
-  size_t smem = (32 * 32 + rpc * oc_ld(32)) * 8;
-  cudaFuncSetAttribute(k_gram_alone<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+  size_t smem = (W * W + rpc * oc_ld(W)) * 8;
+  cudaFuncSetAttribute(k_gram_alone<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
   for (int rep = 0; rep < 3; ++rep) {
-    k_gram_alone<32><<<1, 256, smem>>>(rpc, t, o); long long ht[2]; cudaMemcpy(ht, t, 16, cudaMemcpyDeviceToHost);
-    printf("standalone W=32 rpc=256: gram %lld cycles, apply %lld cycles (%s)\n", ht[0], ht[1], cudaGetErrorString(cudaGetLastError()));
+    k_gram_alone<W><<<1, 256, smem>>>(rpc, t, o, go, 4032); long long ht[3]; cudaMemcpy(ht, t, 24, cudaMemcpyDeviceToHost);
+    printf("standalone W=%d rpc=256: gram %lld cycles, apply %lld cycles, apply->global %lld cycles (%s)\n", W, ht[0], ht[1], ht[2], cudaGetErrorString(cudaGetLastError()));
   }
+}
+int gram_alone_main() {
+  gram_alone_w<32>();
+  gram_alone_w<64>();
   return 0;
 }
