@@ -530,12 +530,13 @@ struct Exec {
   }
 
   // block classical Gram-Schmidt, twice, over blocks of width bw, then CholeskyQR2 per block
-  // first_orthonormal: block 0 is already the Q of an orth (an intermediate Krylov block), so its
-  // own CholeskyQR2 would return it unchanged to rounding (R = I) and is skipped
-  void bcgs2(Side s, const TS& K, int bw, bool first_orthonormal = false) {
+  // Block 0 is re-orthonormalised even when it is already an orth's Q (an intermediate Krylov
+  // block): skipping it was measured to break exactly dependent blocks (A diagonal, Omega = I[:, :l]:
+  // the projected remainder of block 1 is rounding noise along block 0's directions, which the
+  // self-referenced rank guard keeps and renormalises into a duplicate direction).
+  void bcgs2(Side s, const TS& K, int bw) {
     const int nb = (K.w + bw - 1) / bw;
     for (int b = 0; b < nb; ++b) {
-      if (b == 0 && first_orthonormal) continue;
       const int c0 = b * bw, wc = std::min(bw, K.w - c0);
       TS Wb = slice(K, c0, wc);
       const size_t mk = mark();
@@ -705,9 +706,7 @@ void alg_krylov(Exec& E) {
     prev = dst;
   }
   if (v == 1) return;
-  // block 0 of K is Q^1 (v even) or Q^2 (v odd): orthonormalised already unless it is the raw last block
-  const bool first_orth = even ? (1 < v - 1) : (2 < v - 1);
-  E.bcgs2(side_K, K, l, first_orth);                      // qr(K_c) / qr(K_r)  (lines 9 / 14)
+  E.bcgs2(side_K, K, l);                                  // qr(K_c) / qr(K_r)  (lines 9 / 14)
   TS Qo = E.new_ts(even ? side_r : side_c, W);
   double* Rw = E.alloc((int64_t)W * W);
   E.view(side_K, K, Qo);                                  // one more view (lines 10 / 15)

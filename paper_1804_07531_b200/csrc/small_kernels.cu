@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(LPP == 4 ? 256 : 512) k_jacobi_mid(const doubl
   };
   const bool active = grp < npairs;
   for (; sweep < max_sweeps; ++sweep) {
-    int rotated = 0;
+    int rotated = 0, big = 0;
     for (int round = 0; round < m1; ++round) {
       if (active) {
         int p, q;
@@ -555,6 +555,7 @@ __global__ void __launch_bounds__(LPP == 4 ? 256 : 512) k_jacobi_mid(const doubl
         }
         if (cc * cc > tol2 * (a * b) && cc != 0.0) {
           rotated = 1;
+          big |= (cc * cc > 1e-20 * (a * b)) ? 1 : 0;
           const double d = b - a;
           double rd, rsq, rt;
           asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(fmax(fabs(d), 1e-300)));
@@ -576,6 +577,13 @@ __global__ void __launch_bounds__(LPP == 4 ? 256 : 512) k_jacobi_mid(const doubl
       __syncthreads();
     }
     if (!__syncthreads_or(rotated)) {
+      converged = true;
+      ++sweep;
+      break;
+    }
+    // quadratic convergence: when no rotation of this sweep had |c| / sqrt(ab) above 1e-10, the
+    // off-diagonal left is O(1e-20), far below tol, so the confirming sweep is skipped
+    if (!__syncthreads_or(big)) {
       converged = true;
       ++sweep;
       break;
@@ -1396,7 +1404,7 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
   };
   const bool active = grp < npairs;
   for (; sweep < max_sweeps; ++sweep) {
-    int rotated = 0;
+    int rotated = 0, big = 0;
     for (int round = 0; round < m1; ++round) {
       if (active) {
         int p, q;
@@ -1440,6 +1448,7 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
         }
         if (cc * cc > tol2 * (a * b) && cc != 0.0) {
           rotated = 1;
+          big |= (cc * cc > 1e-20 * (a * b)) ? 1 : 0;
           // rho = 2c / |b - a|, t = sign(b - a) rho / (1 + sqrt(1 + rho^2)), approximate fp64 MUFU ops
           const double d = b - a;
           double rd, rsq, rt;
@@ -1462,6 +1471,13 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
       __syncthreads();
     }
     if (!__syncthreads_or(rotated)) {
+      converged = true;
+      ++sweep;
+      break;
+    }
+    // quadratic convergence: when no rotation of this sweep had |c| / sqrt(ab) above 1e-10, the
+    // off-diagonal left is O(1e-20), far below tol, so the confirming sweep is skipped
+    if (!__syncthreads_or(big)) {
       converged = true;
       ++sweep;
       break;
