@@ -187,3 +187,31 @@ def test_row_stream_fp32(ctx):
     Uo, so, Vo = O.row_stream_qb(A.astype(np.float64), 40, 20, Om.astype(np.float64), panel_rows=4096)
     assert np.max(np.abs(host(sv).astype(np.float64) - so) / so) <= 1e-4
     assert O.projector_distance(host(U).astype(np.float64), Uo) <= 1e-3
+
+
+@pytest.mark.parametrize("variant", ["minvar", "woolfe", "bwz", "bwz2"])
+def test_adaptive_and_extended_fp32(ctx, variant):
+    """The new single-pass variants on an fp32 A (tcgen05 views, fp64 in between): fp32 tolerances
+    against the oracle on the same fp32 bytes."""
+    from paper_1804_07531_b200 import rsvd
+
+    cfg = S.CONFIGS["C5"]
+    m, n, k, p, l2, s = 2000, 1500, 20, 10, 60, 60
+    A = S.make_matrix(cfg, m, n).astype(np.float32)
+    Om = S.gaussian_test_matrix(n, k + p, cfg, S.ROLE_OMEGA).astype(np.float32)
+    Phi = S.gaussian_test_matrix(m, l2, cfg, S.ROLE_PHI).astype(np.float32)
+    A64, Om64, Phi64 = A.astype(np.float64), Om.astype(np.float64), Phi.astype(np.float64)
+    if variant in ("bwz", "bwz2"):
+        Xr, Xc = S.srft_matrix(m, s, 5).astype(np.float32), S.srft_matrix(n, s, 6).astype(np.float32)
+        U, sv, V, _ = ctx.single_pass_extended(dev(A), k, p, l2, s, cm(Om), cm(Phi), cm(Xr), cm(Xc), variant=variant)
+        Uo, so, Vo = O.one_view_extended(A64, k, p, l2 - k, Om64, Phi64, Xr.astype(np.float64),
+                                         Xc.astype(np.float64), variant=variant)
+    elif variant == "minvar":
+        U, sv, V, info = ctx.single_pass(dev(A), k, p, l2, cm(Om), cm(Phi), lc="minvar")
+        Uo, so, Vo = O.one_view_tropp(A64, k, p, l2 - k, info.lc_used, Om64, Phi64)
+    else:
+        U, sv, V, _ = ctx.single_pass(dev(A), k, p, l2, cm(Om), cm(Phi), lc=p // 2, flags=rsvd.RSVD_WOOLFE)
+        Uo, so, Vo = O.one_view_woolfe(A64, k, p, l2 - k, p // 2, Om64, Phi64)
+    assert np.max(np.abs(host(sv).astype(np.float64) - so) / so) <= 1e-4
+    assert O.projector_distance(host(U).astype(np.float64), Uo) <= 1e-3
+    assert O.projector_distance(host(V).astype(np.float64), Vo) <= 1e-3
