@@ -30,6 +30,14 @@ constexpr int kNG = 4;             // n-tiles per B-fragment group
 template <int WT>
 struct KUnroll { static constexpr int v = WT <= 4 ? 4 : (WT <= 6 ? 2 : 1); };
 
+// 1024-byte aligned base of the dynamic shared memory (128B-swizzled TMA tiles need it), formed by
+// pointer arithmetic on the __shared__ array: an integer round trip (uintptr_t) would lose the
+// address space and turn every operand load into a generic LD.E with 64-bit address math.
+__device__ __forceinline__ uint8_t* smem_base_1024(uint8_t* raw) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(raw));
+  return raw + ((1024u - (a & 1023u)) & 1023u);
+}
+
 // =====================================================================================
 // Y = A X     (M = rows of A, K = n, N = w)
 // =====================================================================================
@@ -53,7 +61,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = AxCfg<WT>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_base_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
   uint64_t* empty = full + STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -181,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = AtyCfg<WT>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_base_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
   uint64_t* empty = full + STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = FusedCfg<L2T>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_base_1024(smem_raw);
   uint8_t* om = smem + STAGES * C::STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(om + C::OM_BYTES);
   uint64_t* empty = full + STAGES;

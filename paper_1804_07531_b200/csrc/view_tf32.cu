@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   G.init(MT, w);
   const int WP = G.WP, NW = G.NW;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // aligned by pointer arithmetic on the __shared__ array (keeps the shared address space)
+  uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G.stages * G.stage_bytes);
   uint64_t* conv = full + kMaxStages;
   uint64_t* empty = conv + kMaxStages;
