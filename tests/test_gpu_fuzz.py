@@ -101,3 +101,26 @@ def test_random_parity(ctx, seed):
     # north_star tolerances (fp64): sigma 1e-10 relative, projectors 1e-9
     assert np.max(np.abs(s - so) / np.maximum(so, 1e-300)) <= 1e-10, (alg, m, n, k, p, v)
     assert O.projector_distance(U, Uo) <= 1e-9 and O.projector_distance(V, Vo) <= 1e-9, (alg, m, n, k, p, v)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_parity_fp32(ctx, seed):
+    """fp32 A (tcgen05 3xTF32 views): the oracle runs in fp64 on the same fp32 bytes; north_star
+    fp32 tolerances (sigma 1e-4, projectors 1e-3).  Gentle decay keeps the top-k well separated."""
+    g, m, n, k, p, alg, v, decay = draw(seed)
+    A = matrix(g, m, n, min(decay, 0.2)).astype(np.float32)
+    l = k + p
+    Om = g.standard_normal((n, l)).astype(np.float32)
+    A64, Om64 = A.astype(np.float64), Om.astype(np.float64)
+    if seed % 3 == 0:
+        U, s, V, _ = ctx.subspace(dev(A), k, p, v, cm(Om))
+        Uo, so, Vo, _ = O.svd_of(A64, "subspace", k, p, v=v, Omega=Om64)
+    elif seed % 3 == 1:
+        U, s, V, _ = ctx.block_krylov(dev(A), k, p, v, cm(Om))
+        Uo, so, Vo, _ = O.svd_of(A64, "krylov", k, p, v=v, Omega=Om64)
+    else:
+        U, s, V, _ = ctx.row_stream(dev(A), k, p, cm(Om))
+        Uo, so, Vo = O.row_stream_qb(A64, k, p, Om64, panel_rows=64)
+    s, U, V = (host(x).astype(np.float64) for x in (s, U, V))
+    assert np.max(np.abs(s - so) / so) <= 1e-4
+    assert O.projector_distance(U, Uo) <= 1e-3 and O.projector_distance(V, Vo) <= 1e-3
