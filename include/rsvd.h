@@ -72,6 +72,13 @@ enum {
   RSVD_E_NUMERIC = -6,   /* numerical failure (Jacobi not converged, singular R-hat in Alg. 7) */
   RSVD_E_STATE = -7      /* ctx misuse (e.g. comm already initialised)                       */
 };
+/* ENVIRONMENT.  A/B measurement switches, read once per process; the defaults are the tuned
+ * paths and no switch changes results beyond rounding:
+ *   RSVD_NO_ORTH_CLUSTER=1        CholeskyQR without the 16-CTA cluster kernel (w <= 64)
+ *   RSVD_CHOL_BIG_FROM=w          blocked Cholesky (k_chol_big) from this width (default 161)
+ *   RSVD_JACOBI_CLUSTER_FROM=c    cluster block Jacobi from this core width (default 129)
+ *   RSVD_JACOBI_OLD_MID=1         previous 65..128-column Jacobi kernel
+ *   RSVD_ROW_PANEL_MB=x           row-panel size of rsvd_row_stream (default 48)          */
 /* flags */
 #define RSVD_SQUARED      1u   /* S := sigma^2  (normal-matrix estimate A^T A ~ V S V^T) */
 #define RSVD_NO_GRAPH     2u   /* enqueue kernels directly instead of replaying a CUDA graph    */
