@@ -478,7 +478,10 @@ __global__ void __launch_bounds__(LPP == 4 ? 256 : 512) k_jacobi_mid(const doubl
   extern __shared__ double jm_dyn[];
   const int ce = c + (c & 1);
   double* W = jm_dyn;                                 // ce x RS
-  double* J = j_in_smem ? jm_dyn + (int64_t)ce * RS : gJ;   // ce x ce
+  // WJ = 2: J in shared memory (a compile-time choice keeps the shared address space: LDS, not
+  // generic loads); WJ = 1: J in the global scratch
+  double* J = (WJ == 2) ? jm_dyn + (int64_t)ce * RS : gJ;   // ce x ce
+  (void)j_in_smem;
   __shared__ double sval[128];
   __shared__ int srank[128];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -694,6 +697,7 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
     static bool mattr = false;
     if (!mattr) {
       cudaFuncSetAttribute(k_jacobi_mid<8, 16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      cudaFuncSetAttribute(k_jacobi_mid<8, 16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       cudaFuncSetAttribute(k_jacobi_mid<4, 32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       mattr = true;
     }
@@ -702,8 +706,11 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
       const size_t wb = (size_t)ce * (8 * 16 + 4) * 8, jb = (size_t)ce * ce * 8;
       const int j_in = (wb + jb) <= 220 * 1024 ? 1 : 0;
       const int threads = ((8 * (ce / 2)) + 31) / 32 * 32;
-      k_jacobi_mid<8, 16, 1><<<1, threads, wb + (j_in ? jb : 0), st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, j_in,
-                                                                       tolm, 60, status);
+      if (j_in)
+        k_jacobi_mid<8, 16, 2><<<1, threads, wb + jb, st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, 1, tolm, 60,
+                                                            status);
+      else
+        k_jacobi_mid<8, 16, 1><<<1, threads, wb, st>>>(M, ldm, trans, r, c, Ul, S, Vr, scratch, 0, tolm, 60, status);
     } else {
       const size_t wb = (size_t)ce * (4 * 32 + 4) * 8;
       const int threads = ((4 * (ce / 2)) + 31) / 32 * 32;
