@@ -131,3 +131,29 @@ def test_fp32_zero_and_rank_one(ctx, alg, v):
     s, U, V = host(s).astype(np.float64), host(U).astype(np.float64), host(V).astype(np.float64)
     assert abs(s[0] - 3.0) <= 1e-5 * 3.0 and np.all(np.abs(s[1:]) <= 1e-5)
     assert abs(abs(U[123, 0]) - 1.0) <= 1e-5 and abs(abs(V[45, 0]) - 1.0) <= 1e-5
+
+
+@pytest.mark.parametrize("variant", ["row", "bwz", "bwz2"])
+def test_new_paths_zero_and_rank_one(ctx, variant):
+    """The row-wise pass and the extended sketch on A = 0 (sigma = 0 exactly, finite vectors) and on
+    a rank-1 spike (sigma = (3, 0, ...), U_1 = +-e_i, V_1 = +-e_j)."""
+    m, n, k, p = 300, 200, 5, 5
+    Om = S.random_gaussian_matrix(n, k + p, seed=51)
+    Phi = S.random_gaussian_matrix(m, 2 * (k + p), seed=52)
+    Xr, Xc = S.srft_matrix(m, 30, 53), S.srft_matrix(n, 30, 54)
+
+    def call(A):
+        if variant == "row":
+            return ctx.row_stream(dev(A), k, p, cm(Om))
+        return ctx.single_pass_extended(dev(A), k, p, 2 * (k + p), 30, cm(Om), cm(Phi), cm(Xr), cm(Xc),
+                                        variant=variant)
+
+    A = np.zeros((m, n))
+    U, s, V, _ = call(A)
+    assert np.all(host(s) == 0.0) and np.all(np.isfinite(host(U))) and np.all(np.isfinite(host(V)))
+    A[77, 123] = 3.0
+    U, s, V, _ = call(A)
+    s, U, V = host(s), host(U), host(V)
+    np.testing.assert_allclose(s[0], 3.0, rtol=1e-14)
+    assert np.all(np.abs(s[1:]) <= 1e-13)
+    assert abs(abs(U[77, 0]) - 1.0) <= 1e-13 and abs(abs(V[123, 0]) - 1.0) <= 1e-13
