@@ -127,6 +127,11 @@ const char* rsvd_strerror(int code);
 const char* rsvd_last_error(const rsvd_ctx* ctx);
 int  rsvd_version(void);                                /* 100 * major + minor               */
 int  rsvd_sm_count(const rsvd_ctx* ctx);
+/* Caps the SMs this ctx's persistent kernels are sized for (1 <= n; n >= the device's SM count
+ * restores the default).  For several contexts running concurrently on one GPU: a smaller budget
+ * for the off-critical-path calls leaves SMs to the critical one.  Results do not depend on it
+ * beyond rounding (the reduction splits change).  Returns RSVD_E_ARG for n < 1. */
+int  rsvd_set_sm_limit(rsvd_ctx* ctx, int n);
 /* Completes a call made with RSVD_ASYNC on this ctx: synchronises the ctx stream, fills the
  * device-side fields of info (rank-deficient columns, Jacobi sweeps) and returns the call's
  * numerical status.  Until then the caller must not read the outputs nor modify the inputs,

@@ -1309,11 +1309,11 @@ std::string call_key(const Call& c, const Exec& E, const rsvd_ctx* ctx) {
   char buf[1024];
   snprintf(buf, sizeof buf,
            "a%d k%d p%d v%d in%d l2%d lc%d t%d w%d r%lld c%d f%u A%p m%lld n%lld lda%lld U%d S%d V%d R%d ar%p nr%d "
-           "s%d x%d",
+           "s%d x%d sm%d",
            c.alg, c.k, c.p, c.v, c.input, c.l2, c.lc, c.trans, c.w, (long long)c.rows, c.cols, c.flags,
            (const void*)E.A, (long long)E.m, (long long)E.n, (long long)E.lda, c.kU != PTR_NULL, c.kS != PTR_NULL,
            c.kV != PTR_NULL, c.kR != PTR_NULL, (void*)ctx->arena, ctx->nranks + (ctx->comm ? 1000 : 0), c.s,
-           c.variant);
+           c.variant, ctx->sms);
   return std::string(buf);
 }
 
@@ -1647,6 +1647,14 @@ int rsvd_destroy(rsvd_ctx* c) {
 }
 
 int rsvd_sm_count(const rsvd_ctx* c) { return c ? c->sms : 0; }
+
+int rsvd_set_sm_limit(rsvd_ctx* c, int n) {
+  if (!c || n < 1) return RSVD_E_ARG;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, c->device) != cudaSuccess) return RSVD_E_CUDA;
+  c->sms = std::min(n, prop.multiProcessorCount);
+  return RSVD_OK;
+}
 
 int rsvd_wait(rsvd_ctx* c, rsvd_info* info) {
   if (!c) return RSVD_E_ARG;

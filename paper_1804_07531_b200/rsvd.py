@@ -30,7 +30,7 @@ EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_wait", "rsvd_strerror", "rsvd_la
            "rsvd_recommend_input", "rsvd_probe_peaks", "rsvd_get_unique_id", "rsvd_comm_init", "rsvd_comm_nranks", "rsvd_subspace",
            "rsvd_block_krylov", "rsvd_single_pass", "rsvd_nystrom", "rsvd_pinched", "rsvd_view", "rsvd_view_fused",
            "rsvd_orth", "rsvd_core_svd", "rsvd_plan", "rsvd_single_pass_extended",
-           "rsvd_row_stream"]
+           "rsvd_row_stream", "rsvd_set_sm_limit"]
 
 
 class RsvdMat(ctypes.Structure):
@@ -78,6 +78,7 @@ def lib():
     L.rsvd_last_error.argtypes = [vp]
     L.rsvd_last_error.restype = ctypes.c_char_p
     L.rsvd_sm_count.argtypes = [vp]
+    L.rsvd_set_sm_limit.argtypes = [vp, i32]
     L.rsvd_wait.argtypes = [vp, pinfo]
     L.rsvd_recommend_input.argtypes = [i32, i32]
     L.rsvd_get_unique_id.argtypes = [vp]
@@ -175,6 +176,10 @@ class Context:
     @property
     def sm_count(self) -> int:
         return lib().rsvd_sm_count(self._h)
+
+    def set_sm_limit(self, n: int):
+        """Cap the SMs this context's persistent kernels are sized for (rsvd_set_sm_limit)."""
+        self._check(lib().rsvd_set_sm_limit(self._h, n), "rsvd_set_sm_limit")
 
     def probe_peaks(self):
         """(FP64 DMMA TFLOP/s, HBM read GB/s) measured on this device."""
