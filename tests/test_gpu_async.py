@@ -47,3 +47,36 @@ def test_async_concurrent_equals_sync():
     ctxs[0].wait(o[3])
     for c in ctxs:
         c.close()
+
+
+def test_sm_limit_same_results():
+    """rsvd_set_sm_limit only resizes the persistent grids (reduction splits): results agree with the
+    full-GPU context to rounding and with the oracle; n < 1 is an argument error."""
+    import numpy as np
+    import torch
+
+    import oracle as O
+    import synth as S
+    from paper_1804_07531_b200 import build, rsvd
+
+    build.build()
+    cfg = S.CONFIGS["C2"]
+    A = torch.from_numpy(S.make_matrix(cfg)).cuda()
+    Om_h = S.gaussian_test_matrix(cfg.n, cfg.l, cfg, S.ROLE_OMEGA)
+    Om = torch.from_numpy(np.ascontiguousarray(Om_h.T)).cuda().t()
+    full, capped = rsvd.Context(0), rsvd.Context(0)
+    capped.set_sm_limit(20)
+    assert capped.sm_count == 20
+    U0, s0, V0, _ = full.block_krylov(A, cfg.k, cfg.p, 4, Om)
+    U1, s1, V1, _ = capped.block_krylov(A, cfg.k, cfg.p, 4, Om)
+    s0, s1 = s0.cpu().numpy(), s1.cpu().numpy()
+    assert np.max(np.abs(s1 - s0) / s0) <= 1e-12
+    assert O.projector_distance(U1.cpu().numpy(), U0.cpu().numpy()) <= 1e-11
+    Uo, so, Vo, _ = O.svd_of(A.cpu().numpy(), "krylov", cfg.k, cfg.p, v=4, Omega=Om_h)
+    assert np.max(np.abs(s1 - so) / so) <= 1e-10
+    with pytest.raises(rsvd.RsvdError):
+        capped.set_sm_limit(0)
+    capped.set_sm_limit(10_000)
+    assert capped.sm_count == full.sm_count
+    full.close()
+    capped.close()
