@@ -216,6 +216,8 @@ class Context:
         return RsvdMat(dt, 0, m if m is not None else ml, n, ml, row0, A.stride(0), A.data_ptr())
 
     def _out_like(self, A, rows, cols, host_out):
+        # at least one column: an invalid k must reach the C ABI, which reports RSVD_E_ARG
+        cols = max(cols, 1)
         if host_out or not A.is_cuda:
             return _new_colmajor(rows, cols, A.cpu() if A.is_cuda else A, pin=True)
         return _new_colmajor(rows, cols, A)
@@ -227,8 +229,8 @@ class Context:
         M = self.mat(A, m, row0)
         U = self._out_like(A, A.shape[0], k, host_out) if want_u else None
         V = self._out_like(A, A.shape[1], k, host_out) if want_v else None
-        S = (torch.empty(k, dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
-             else torch.empty(k, dtype=A.dtype, device=A.device))
+        S = (torch.empty(max(k, 1), dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
+             else torch.empty(max(k, 1), dtype=A.dtype, device=A.device))
         info = RsvdInfo()
         rc = fn(self._h, ctypes.byref(M), k, p, v, input, Om.data_ptr(), _ld(Om),
                 U.data_ptr() if U is not None else None, _ld(U) if U is not None else 0, S.data_ptr(),
@@ -254,8 +256,8 @@ class Context:
         M = self.mat(A, m, row0)
         U = self._out_like(A, A.shape[0], k, host_out)
         V = self._out_like(A, A.shape[1], k, host_out)
-        S = (torch.empty(k, dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
-             else torch.empty(k, dtype=A.dtype, device=A.device))
+        S = (torch.empty(max(k, 1), dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
+             else torch.empty(max(k, 1), dtype=A.dtype, device=A.device))
         info = RsvdInfo()
         rc = lib().rsvd_single_pass(self._h, ctypes.byref(M), k, p, l2, lc, Om.data_ptr(), _ld(Om), Ph.data_ptr(),
                                     _ld(Ph), U.data_ptr(), _ld(U), S.data_ptr(), V.data_ptr(), _ld(V), flags,
@@ -272,8 +274,8 @@ class Context:
         M = self.mat(A, m, row0)
         U = self._out_like(A, A.shape[0], k, host_out)
         V = self._out_like(A, A.shape[1], k, host_out)
-        S = (torch.empty(k, dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
-             else torch.empty(k, dtype=A.dtype, device=A.device))
+        S = (torch.empty(max(k, 1), dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
+             else torch.empty(max(k, 1), dtype=A.dtype, device=A.device))
         info = RsvdInfo()
         rc = lib().rsvd_single_pass_extended(self._h, ctypes.byref(M), k, p, l2, s, Om.data_ptr(), _ld(Om),
                                              Ph.data_ptr(), _ld(Ph), Xr.data_ptr(), _ld(Xr), Xc.data_ptr(), _ld(Xc),
@@ -288,8 +290,8 @@ class Context:
         M = self.mat(A, m, row0)
         U = self._out_like(A, A.shape[0], k, host_out)
         V = self._out_like(A, A.shape[1], k, host_out)
-        S = (torch.empty(k, dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
-             else torch.empty(k, dtype=A.dtype, device=A.device))
+        S = (torch.empty(max(k, 1), dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
+             else torch.empty(max(k, 1), dtype=A.dtype, device=A.device))
         info = RsvdInfo()
         rc = lib().rsvd_row_stream(self._h, ctypes.byref(M), k, p, Om.data_ptr(), _ld(Om), U.data_ptr(), _ld(U),
                                    S.data_ptr(), V.data_ptr(), _ld(V), flags, ctypes.byref(info))
@@ -300,8 +302,8 @@ class Context:
         Om = _colmajor(Omega)
         M = self.mat(A, m, row0)
         V = self._out_like(A, A.shape[1], k, host_out)
-        S = (torch.empty(k, dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
-             else torch.empty(k, dtype=A.dtype, device=A.device))
+        S = (torch.empty(max(k, 1), dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
+             else torch.empty(max(k, 1), dtype=A.dtype, device=A.device))
         info = RsvdInfo()
         self._check(fn(self._h, ctypes.byref(M), k, p, v, Om.data_ptr(), _ld(Om), S.data_ptr(), V.data_ptr(), _ld(V),
                        flags, ctypes.byref(info)), name)

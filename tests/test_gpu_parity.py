@@ -324,3 +324,34 @@ def test_normal_matrix_parity(ctx, alg, name, m, n, v):
     assert info.views == v
     assert np.max(np.abs(s2 - s2o) / s2o) <= 2 * TOL_S  # eigenvalues = sigma^2: twice sigma's relative error
     assert O.projector_distance(host(V), Vo) <= TOL_P
+
+
+@pytest.mark.parametrize("shape", [(0, 40), (50, 0), (0, 0)])
+def test_empty_matrix_rejected(ctx, shape):
+    """An empty A is an argument error (RSVD_E_ARG, -1) for every entry point, never a crash."""
+    from paper_1804_07531_b200 import rsvd
+
+    m, n = shape
+    A = torch.zeros(m, n, dtype=torch.float64, device="cuda")
+    Om = colmajor_dev(np.zeros((max(n, 1), 2)))
+    Phi = colmajor_dev(np.zeros((max(m, 1), 4)))
+    Xi = colmajor_dev(np.zeros((max(m, n, 1), 4)))
+    calls = [lambda: ctx.subspace(A, 1, 1, 2, Om), lambda: ctx.block_krylov(A, 1, 1, 3, Om),
+             lambda: ctx.single_pass(A, 1, 1, 4, Om, Phi), lambda: ctx.row_stream(A, 1, 1, Om),
+             lambda: ctx.single_pass_extended(A, 1, 1, 2, 4, Om, Phi, Xi, Xi),
+             lambda: ctx.nystrom(A, 1, 1, 2, Om)]
+    for fn in calls:
+        with pytest.raises(rsvd.RsvdError) as e:
+            fn()
+        assert e.value.code == -1
+
+
+def test_invalid_rank_rejected(ctx):
+    from paper_1804_07531_b200 import rsvd
+
+    A = dev(np.ones((50, 40)))
+    Om = colmajor_dev(np.zeros((40, 10)))
+    for k, p in ((0, 5), (-1, 5), (5, -1)):
+        with pytest.raises(rsvd.RsvdError) as e:
+            ctx.subspace(A, k, p, 2, Om)
+        assert e.value.code == -1
