@@ -60,6 +60,10 @@ for name in names:
         nb = v // 2 if v % 2 == 0 else (v - 1) // 2
         floor = (v - 1) * view_floor(l) + view_floor(nb * l)
         runs.append(("krylov", v, lambda v=v: ctx.block_krylov(A, cfg.k, cfg.p, v, Om), floor))
+    for v in cfg.runs.get("normal", []):
+        # A^T A ~ V diag(S) V^T by Alg. 4 (Nystrom): Omega on the m side for odd v, n side for even v
+        Omn = Om if v % 2 == 0 else S.gaussian_test_matrix_torch(m, l, cfg, S.ROLE_OMEGA_M, dev)
+        runs.append(("nystrom", v, lambda v=v, Omn=Omn: ctx.nystrom(A, cfg.k, cfg.p, v, Omn), v * view_floor(l)))
     if cfg.runs.get("single_pass"):
         runs.append(("single_pass", 1, lambda: ctx.single_pass(A, cfg.k, cfg.p, cfg.l2, Om, Phi),
                      max(m * n * es / HBM, 2.0 * m * n * (l + cfg.l2) / peak)))
