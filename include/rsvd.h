@@ -7,7 +7,12 @@
  *
  *   rsvd_subspace      Alg. 2, generalized subspace iteration, any v >= 2
  *   rsvd_block_krylov  Alg. 9, generalized block Krylov, any v >= 2
- *   rsvd_single_pass   Alg. 7, 1-view Tropp variant with l_c
+ *   rsvd_single_pass   Alg. 7, 1-view Tropp variant with l_c;
+ *                      minimum-variance l_c; Alg. 8 Woolfe variant
+ *   rsvd_single_pass_extended  extended 1-view sketch, bwz / bwz2
+ *   rsvd_row_stream    single pass over the rows of A
+ *   rsvd_nystrom, rsvd_pinched  normal-matrix TEVDs, Alg. 4 / Alg. 5
+ *   rsvd_plan          single-pass oversampling plans (host only)
  *
  * plus the primitives they are built from, exported for unit-level parity tests:
  *   rsvd_view          Y = A X  or  Z = A^T Y        (one matrix view)
@@ -29,18 +34,20 @@
  *   library detects the kind with cudaPointerGetAttributes and stages host data through its own
  *   device workspace (host<->device copies then happen inside the call).  Device pointers must
  *   be on the ctx's device.
- * DTYPE.  All arrays of one call share A's dtype.  RSVD_F64 is fully supported.  RSVD_F32 is
- *   not implemented in this release and returns RSVD_E_DTYPE.
+ * DTYPE.  All arrays of one call share A's dtype, RSVD_F64 or RSVD_F32.  fp32 views run on the
+ *   tcgen05 tensor cores in 3xTF32; everything between views is computed in fp64 and the
+ *   outputs are rounded to fp32.  Other dtypes return RSVD_E_DTYPE.
  * OWNERSHIP.  The caller owns every array; nothing is retained after return.  The ctx owns its
  *   workspace (grown on demand, freed by rsvd_destroy) and its CUDA-graph cache.
  * SYNCHRONISATION.  Calls are synchronous: one stream synchronisation at the end; no host
  *   round trip between views (the whole algorithm is one CUDA graph launch after the first call
- *   with a given signature).
+ *   with a given signature).  With RSVD_ASYNC a call only enqueues; rsvd_wait completes it.
  * MULTI-GPU.  After rsvd_comm_init every algorithm call is a collective over the ranks: A is
  *   row-sharded (rank r holds rows [row0, row0 + m_local)); U is returned row-sharded like A;
  *   S and V are replicated and bitwise identical on all ranks.  Gram matrices and the partial
  *   co-range views A^T Y are summed with NCCL all-reduce.
- * DETERMINISM.  Bitwise run-to-run reproducible for fixed inputs and rank count, except the
+ * DETERMINISM.  Bitwise run-to-run reproducible for fixed inputs, rank count and SM budget
+ *   (rsvd_set_sm_limit changes the reduction splits, i.e. the rounding), except the
  *   single-pass Y_c accumulation when the deterministic partial buffers would exceed the memory
  *   budget (info->nondeterministic = 1; never for the BASELINE configs C1-C3).
  * ERRORS.  Every function returns an int status (RSVD_OK = 0 or a negative RSVD_E_*); no C++
@@ -92,7 +99,7 @@ enum {
 #define RSVD_SIM_SHARDS_SHIFT 8 /* debug: bits 8..15 = number of virtual row shards (loopback) */
 
 typedef struct {
-  int32_t dtype;          /* RSVD_F64 (RSVD_F32 reserved)                                */
+  int32_t dtype;          /* RSVD_F64 or RSVD_F32                                         */
   int32_t reserved;
   int64_t m, n;           /* global shape of A                                            */
   int64_t m_local, row0;  /* this rank's rows [row0, row0 + m_local); single GPU: m, 0    */
@@ -230,7 +237,6 @@ int rsvd_single_pass_extended(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, in
 enum { RSVD_PLAN_FLAT = 0, RSVD_PLAN_DECAY = 1, RSVD_PLAN_RAPID = 2, RSVD_PLAN_BALANCED = 3 };
 int rsvd_plan(int scheme, int k, int T, double alpha, int* p, int* l2, int* lc);
 
-/* ---- primitives (single GPU; for unit tests and the benchmark's kernel timing) -------------- */
 /* ---------------------------------------------------------------------------------------------
  * Normal-matrix estimates A^T A ~ V diag(S) V^T (S = eigenvalues, descending), v >= 2 views.
  *
@@ -250,6 +256,8 @@ int rsvd_nystrom(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, const vo
                  void* V, int64_t ldv, unsigned flags, rsvd_info* info);
 int rsvd_pinched(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, const void* Omega, int64_t ld_omega, void* S,
                  void* V, int64_t ldv, unsigned flags, rsvd_info* info);
+
+/* ---- primitives (single GPU; for unit tests and the benchmark's kernel timing) -------------- */
 
 /* trans == 0: Y (m_local x w) = A X with X n x w;  trans == 1: Y (n x w) = A^T X with X m_local x w.
  * 1 <= w <= 1024 (wider views run as column chunks of 128 (fp64) / 512 (fp32) columns). */
