@@ -84,7 +84,9 @@ __global__ void __launch_bounds__(256) k_cross_gram(const double* __restrict__ X
 }
 
 int gram_slots(int64_t rows) {
-  int64_t s = (rows + 255) / 256;
+  // 64 rows per slot: the per-slot loop over rows is a dependent latency chain, so more, shorter
+  // slots finish sooner (C2's 4000-row Grams: 16 -> 63 CTAs); the slots are summed in order
+  int64_t s = (rows + 63) / 64;
   if (s < 1) s = 1;
   if (s > 148) s = 148;
   return (int)s;
@@ -102,9 +104,18 @@ int launch_cross_gram(const double* Xa, int64_t lda_, int a, const double* Xb, i
 __global__ void k_slots_reduce_small(const double* __restrict__ slots, int nslots, int64_t count, double* __restrict__ G) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
-  double s = slots[i];
-  for (int k = 1; k < nslots; ++k) s += slots[(int64_t)k * count + i];
-  G[i] = s;
+  // four interleaved partial sums (slot k goes to sum k % 4), combined in a fixed order: the loads
+  // of a group are independent, so they are in flight together (deterministic: the order is fixed)
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int k = 0;
+  for (; k + 3 < nslots; k += 4) {
+    s0 += slots[(int64_t)k * count + i];
+    s1 += slots[(int64_t)(k + 1) * count + i];
+    s2 += slots[(int64_t)(k + 2) * count + i];
+    s3 += slots[(int64_t)(k + 3) * count + i];
+  }
+  for (; k < nslots; ++k) s0 += slots[(int64_t)k * count + i];
+  G[i] = (s0 + s1) + (s2 + s3);
 }
 
 int launch_slots_reduce_small(const double* slots, int nslots, int64_t count, double* G, cudaStream_t st) {
