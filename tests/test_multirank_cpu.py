@@ -3,7 +3,8 @@
 * shard planning, unique-id broadcast and max-over-ranks timing (paper_1804_07531_b200.sharding);
 * the library's row-sharded schedule (include/rsvd.h MULTI-GPU) emulated in NumPy
   with gloo all-reduces: A X local, A^T Y and every Gram / cross product of a row-sharded block
-  all-reduced, column-side blocks replicated.  Each rank runs Alg. 2 / 9 / 7 on its row block;
+  all-reduced, column-side blocks replicated.  Each rank runs Alg. 2 / 9 / 7 / 8, the extended
+  sketch and the row-wise single pass on its row block;
   the gathered result must equal the single-process oracle (the schedule is exact algebra, so the
   same 1e-10 / 1e-9 tolerances as GPU parity apply).
 """
@@ -85,6 +86,7 @@ class ShardedOps:
             G = G + 11.0 * (rows * w + w * (w + 1)) * 1.1102230246251565e-16 * np.trace(G) * np.eye(w)
             L = np.linalg.cholesky(G)
             Y = np.linalg.solve(L, Y.T).T
+            R = L.T                            # R0 folded into R (Y_in = Q R2 R1 R0)
         for _ in range(2):
             G = self.cross(side, Y, Y)
             L = np.linalg.cholesky(G)
@@ -149,10 +151,61 @@ def _alg7_sharded(ops, k, p, Om, Phi_local):
     return Qc @ Uw[:, :k], lam[:k], Vwt[:k].T
 
 
+def _row_sharded(ops, k, p, Om):
+    """Single pass over the rows: the local panels give Y_c rows and a partial
+    A_local^T Y_c; Yhat_r is all-reduced once (include/rsvd.h rsvd_row_stream)."""
+    Yc = ops.view("N", Om)
+    Yh = ops.allreduce(ops.A.T @ Yc)
+    Qc, Rc = ops.orth("M", Yc)
+    Bt = Yh @ np.linalg.pinv(Rc, rcond=1e-12)
+    Qb, Rb = ops.orth("N", Bt)
+    Uh, lam, Vht = np.linalg.svd(Rb.T)
+    return Qc @ Uh[:, :k], lam[:k], Qb @ Vht.T[:, :k]
+
+
+def _woolfe_sharded(ops, k, p, lc, Om, Phi_local):
+    """Alg. 8: Y_r all-reduced, Phi^T Q_c all-reduced, everything on side N replicated."""
+    Yc = ops.view("N", Om)
+    Yr = ops.view("M", Phi_local)
+    Qc, Rc = ops.orth("M", Yc)
+    Qr, Rr = ops.orth("N", Yr, shifted=True)
+    w = k + lc
+    Qc = Qc @ np.linalg.svd(Rc)[0][:, :w]
+    Ur = np.linalg.svd(Rr)[0][:, :w]
+    Qr = Qr @ Ur
+    Qh, Rh = np.linalg.qr(ops.cross("M", Phi_local, Qc))
+    Xh = np.linalg.solve(Rh, Qh.T @ (Yr.T @ Qr))
+    Ux, lam, Vxt = np.linalg.svd(Xh)
+    return Qc @ Ux[:, :k], lam[:k], Qr @ Vxt.T[:, :k]
+
+
+def _extended_sharded(ops, k, p, Om, Phi_local, Xr_local, Xc, variant):
+    """Extended sketch: [A Omega | A Xi_c] local, Y_r all-reduced, Z = Xi_r^T (A Xi_c)
+    and Xi_r^T Q_c all-reduced; the small algebra replicated."""
+    Yc = ops.view("N", Om)
+    W = ops.view("N", Xc)
+    Yr = ops.view("M", Phi_local)
+    Z = ops.cross("M", Xr_local, W)
+    Qc, _ = ops.orth("M", Yc)
+    Qr, _ = ops.orth("N", Yr, shifted=True)
+    Uc, Tc = np.linalg.qr(ops.cross("M", Xr_local, Qc))
+    Ur, Tr = np.linalg.qr(Xc.T @ Qr)
+    Tcp, Trp = np.linalg.pinv(Tc, rcond=1e-12), np.linalg.pinv(Tr, rcond=1e-12)
+    X = Uc.T @ Z @ Ur
+    if variant == "bwz2":
+        core = Tcp @ X @ Trp.T
+    else:
+        Ux, sx, Vxt = np.linalg.svd(X)
+        core = (Tcp @ Ux[:, :k]) @ np.diag(sx[:k]) @ (Trp @ Vxt.T[:, :k]).T
+    Uk, lam, Vkt = np.linalg.svd(core)
+    return Qc @ Uk[:, :k], lam[:k], Qr @ Vkt.T[:, :k]
+
+
 CASES = [("subspace", "C1", 2, None, None), ("subspace", "C1", 3, None, None),
          ("subspace", "C2", 4, 1200, 900), ("krylov", "C1", 4, None, None),
          ("krylov", "C2", 5, 1200, 900), ("single_pass", "C1", 1, None, None),
-         ("single_pass", "C3", 1, 1500, 700)]
+         ("single_pass", "C3", 1, 1500, 700), ("row", "C2", 1, 1200, 900), ("row", "C1", 1, None, None),
+         ("woolfe", "C2", 1, 1200, 900), ("bwz", "C1", 1, None, None), ("bwz2", "C2", 1, 1200, 900)]
 
 
 def _one_case(rank, world, case):
@@ -163,18 +216,35 @@ def _one_case(rank, world, case):
     Phi = S.gaussian_test_matrix(A.shape[0], cfg.l2, cfg, S.ROLE_PHI)
     sh = shard_rows(A.shape[0], world, rank)
     ops = ShardedOps(A[sh.row0:sh.row0 + sh.m_local])
+    Phi_l = Phi[sh.row0:sh.row0 + sh.m_local]
+    s_ext = min(A.shape[0], A.shape[1], 2 * cfg.l)
+    Xr, Xc = S.srft_matrix(A.shape[0], s_ext, 7), S.srft_matrix(A.shape[1], s_ext, 8)
+    lc = cfg.p // 2
     if alg == "subspace":
         U, s, V = _alg2_sharded(ops, cfg.k, cfg.p, v, Om)
     elif alg == "krylov":
         U, s, V = _alg9_sharded(ops, cfg.k, cfg.p, v, Om)
+    elif alg == "row":
+        U, s, V = _row_sharded(ops, cfg.k, cfg.p, Om)
+    elif alg == "woolfe":
+        U, s, V = _woolfe_sharded(ops, cfg.k, cfg.p, lc, Om, Phi_l)
+    elif alg in ("bwz", "bwz2"):
+        U, s, V = _extended_sharded(ops, cfg.k, cfg.p, Om, Phi_l, Xr[sh.row0:sh.row0 + sh.m_local], Xc, alg)
     else:
-        U, s, V = _alg7_sharded(ops, cfg.k, cfg.p, Om, Phi[sh.row0:sh.row0 + sh.m_local])
+        U, s, V = _alg7_sharded(ops, cfg.k, cfg.p, Om, Phi_l)
     parts = [None] * world
     dist.all_gather_object(parts, U)
     res = {}
     if rank == 0:
         Ug = np.vstack(parts)
-        Uo, so, Vo, _ = O.svd_of(A, alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi)
+        if alg == "row":
+            Uo, so, Vo = O.row_stream_qb(A, cfg.k, cfg.p, Om, panel_rows=256)
+        elif alg == "woolfe":
+            Uo, so, Vo = O.one_view_woolfe(A, cfg.k, cfg.p, cfg.l2 - cfg.k, lc, Om, Phi)
+        elif alg in ("bwz", "bwz2"):
+            Uo, so, Vo = O.one_view_extended(A, cfg.k, cfg.p, cfg.l2 - cfg.k, Om, Phi, Xr, Xc, variant=alg)
+        else:
+            Uo, so, Vo, _ = O.svd_of(A, alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi)
         res["sig"] = float(np.max(np.abs(s - so) / so))
         res["pu"] = O.projector_distance(Ug, Uo)
         res["pv"] = O.projector_distance(V, Vo)
