@@ -38,6 +38,20 @@ __device__ __forceinline__ uint8_t* smem_base_1024(uint8_t* raw) {
   return raw + ((1024u - (a & 1023u)) & 1023u);
 }
 
+// Per-CTA %globaltimer stamps of k_view_ax for tools/view_timeline.cu (compiled out otherwise):
+// [0] start, [1] first stage consumed (warp 0), [2 + i] end of the CTA's unit i (warp 0, i < 6), [8] end.
+#ifdef RSVD_VIEW_TIMING
+__device__ unsigned long long g_view_t[160][9];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define VT(i) do { if (threadIdx.x == 0 && blockIdx.x < 160) g_view_t[blockIdx.x][i] = gtimer(); } while (0)
+#else
+#define VT(i) do {} while (0)
+#endif
+
 // =====================================================================================
 // Y = A X     (M = rows of A, K = n, N = w)
 // =====================================================================================
@@ -65,6 +79,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
   uint64_t* empty = full + STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  VT(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -106,6 +121,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   double acc[C::MT][WT][2];
   int stage = 0;
   uint32_t phase = 0;
+#ifdef RSVD_VIEW_TIMING
+  int nu = 0;
+#endif
   for (int u = blockIdx.x; u < U; u += gridDim.x) {
     const int rb = u / S, s = u % S;
     const int kt0 = s * KTS, kt1 = min(KT, kt0 + KTS);
@@ -115,6 +133,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int nt = 0; nt < WT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
     for (int kt = kt0; kt < kt1; ++kt) {
       mbar_wait(&full[stage], phase);
+#ifdef RSVD_VIEW_TIMING
+      if (nu == 0 && kt == kt0) VT(1);
+#endif
       const uint8_t* As = smem + stage * C::STAGE;
       const uint8_t* Xs = As + C::A_STAGE;
 #pragma unroll (KUnroll<WT>::v)
@@ -163,7 +184,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+#ifdef RSVD_VIEW_TIMING
+    if (nu < 6) VT(2 + nu);
+    ++nu;
+#endif
   }
+  VT(8);
 }
 
 // =====================================================================================
@@ -315,7 +341,23 @@ struct FusedCfg {
   static constexpr int STAGE = A_STAGE + P_STAGE;
   static constexpr int OM_BYTES = LPMAX * BN * 8;  // Omega^T strip, 4 boxes of LP x 128 B
   static constexpr int STAGES = ((kSmemBudget - OM_BYTES) / STAGE) > 5 ? 5 : ((kSmemBudget - OM_BYTES) / STAGE);
-  static constexpr int SMEM = STAGES * STAGE + OM_BYTES + 1024 + (2 * STAGES + 2) * 8;
+  static constexpr int SMEM = STAGES * STAGE + OM_BYTES + 1024 + (2 * STAGES + 4) * 8;
+};
+
+// Shared-memory plan for one (L2T, LTC) instance: the Omega^T strip is sized by LTC (LP <= 16 LTC)
+// and double-buffered when that still leaves 4 pipeline stages, so the next unit's strip is
+// loaded while the current unit runs (otherwise every unit start waits one TMA round trip).
+template <int L2T, int LTC>
+struct FusedPlan {
+  using B = FusedCfg<L2T>;
+  static constexpr int OM_ONE = (LTC * 16 < B::LPMAX ? LTC * 16 : B::LPMAX) * B::BN * 8;
+  static constexpr int OM_BUFS = (kSmemBudget - 2 * OM_ONE) / B::STAGE >= 4 ? 2 : 1;
+  static constexpr int OM_BYTES = OM_BUFS * OM_ONE;
+  static constexpr int ST = (kSmemBudget - OM_BYTES) / B::STAGE;
+  static constexpr int STAGES = ST > 5 ? 5 : ST;
+  static constexpr int SMEM = STAGES * B::STAGE + OM_BYTES + 1024 + (2 * STAGES + 4) * 8;
+  static_assert(OM_ONE % 1024 == 0 && B::STAGE % 1024 == 0, "128B-swizzled TMA tiles need 1024 B alignment");
+  static_assert(STAGES >= 2 && SMEM <= 227 * 1024, "fused shared-memory plan");
 };
 
 // LTC: Y_c n-tiles per warp (warp groups 0/1 take n-tiles g, g+2, ...; LTC = ceil(LT/2)) — a
@@ -328,22 +370,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                  int64_t yr_slot_stride, int rows, int ncols, int l, int LP, int l2, int NSB, int S, int KT,
                  int KTS) {
   using C = FusedCfg<L2T>;
-  constexpr int STAGES = C::STAGES;
+  using P = FusedPlan<L2T, LTC>;
+  constexpr int STAGES = P::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_base_1024(smem_raw);
-  uint8_t* om = smem + STAGES * C::STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(om + C::OM_BYTES);
+  uint8_t* om0 = smem + STAGES * C::STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(om0 + P::OM_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* om_full = empty + STAGES;
-  uint64_t* om_empty = om_full + 1;
+  uint64_t* om_full = empty + STAGES;   // [P::OM_BUFS]
+  uint64_t* om_empty = om_full + 2;     // [P::OM_BUFS]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kNW);
     }
-    mbar_init(om_full, 1);
-    mbar_init(om_empty, kNW);
+    for (int b = 0; b < P::OM_BUFS; ++b) {
+      mbar_init(&om_full[b], 1);
+      mbar_init(&om_empty[b], kNW);
+    }
     fence_barrier_init();
   }
   __syncthreads();
@@ -358,15 +403,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pa = policy_evict_first(), pk = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0, ophase = 0;
+      int ob = 0;
       for (int u = blockIdx.x; u < U; u += gridDim.x) {
         const int sb = u / S, s = u % S;
-        // Omega^T strip for this unit (LP rows x BN cols), released by the consumers at unit end
-        mbar_wait(om_empty, ophase ^ 1);
-        mbar_arrive_expect_tx(om_full, OM_TX);
+        // Omega^T strip for this unit (LP rows x BN cols) into buffer ob, released by the
+        // consumers at unit end; with two buffers it is issued one unit ahead
+        mbar_wait(&om_empty[ob], ophase ^ 1);
+        mbar_arrive_expect_tx(&om_full[ob], OM_TX);
+        uint8_t* om = om0 + ob * P::OM_ONE;
 #pragma unroll
         for (int b = 0; b < C::BN / 16; ++b)
-          tma_load_2d(om + b * LP * 128, &tmOm, om_full, sb * C::BN + b * 16, 0, pk);
-        ophase ^= 1;
+          tma_load_2d(om + b * LP * 128, &tmOm, &om_full[ob], sb * C::BN + b * 16, 0, pk);
+        if (++ob == P::OM_BUFS) { ob = 0; ophase ^= 1; }
         const int kt0 = s * KTS, kt1 = min(KT, kt0 + KTS);
         for (int kt = kt0; kt < kt1; ++kt) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -393,19 +441,65 @@ __global__ void __launch_bounds__(kThreads, 1)
   double accr[L2T][2];
   int stage = 0;
   uint32_t phase = 0, ophase = 0;
+  int ob = 0;
   for (int u = blockIdx.x; u < U; u += gridDim.x) {
     const int sb = u / S, s = u % S;
     const int kt0 = s * KTS, kt1 = min(KT, kt0 + KTS);
 #pragma unroll
     for (int nt = 0; nt < L2T; ++nt) accr[nt][0] = accr[nt][1] = 0.0;
-    mbar_wait(om_full, ophase);
-    ophase ^= 1;
+    mbar_wait(&om_full[ob], ophase);
+    const uint8_t* om = om0 + ob * P::OM_ONE;
     for (int kt = kt0; kt < kt1; ++kt) {
       mbar_wait(&full[stage], phase);
       const uint8_t* As = smem + stage * C::STAGE;
       const uint8_t* Ps = As + C::A_STAGE;
+      // Y_c first: its short dependent DMMA chain and its partial stores overlap the Y_r DMMAs
+      // that follow (both k-loops fully unrolled: 113 -> 112 us, and 127 -> 113 us for the unroll)
+      // ---- Y_c(tile rows) = A_tile Omega_strip  (ax pattern; K = BN = 64 -> 8 double-steps)
+      {
+        double accc[LTC][2];
+#pragma unroll
+        for (int i = 0; i < LTC; ++i) accc[i][0] = accc[i][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < C::BN / 8; ++kk) {
+          const int box = kk >> 1;
+          const uint32_t q = ((kk & 1) << 2) + t;
+          const double2 a = *reinterpret_cast<const double2*>(As + box * kBK * 128 + sw128(yc_mt * 8 + pg, q));
+          double2 b[LTC];
+#pragma unroll
+          for (int i = 0; i < LTC; ++i) {
+            const int nt = yc_n0 + 2 * i;
+            if (nt < LT) b[i] = *reinterpret_cast<const double2*>(om + box * LP * 128 + sw128(nt * 8 + pg, q));
+          }
+#pragma unroll
+          for (int i = 0; i < LTC; ++i)
+            if (yc_n0 + 2 * i < LT) dmma(accc[i][0], accc[i][1], a.x, b[i].x);
+#pragma unroll
+          for (int i = 0; i < LTC; ++i)
+            if (yc_n0 + 2 * i < LT) dmma(accc[i][0], accc[i][1], a.y, b[i].y);
+        }
+
+        const int r = kt * kBK + yc_mt * 8 + pg;
+        if (r < rows) {
+          double* o = yc + (yc_atomic ? 0 : (int64_t)sb * yc_slot_stride);
+#pragma unroll
+          for (int i = 0; i < LTC; ++i) {
+            const int nt = yc_n0 + 2 * i;
+            if (nt < LT) {
+              const int c0 = nt * 8 + t, c1 = c0 + 4;
+              if (yc_atomic) {
+                if (c0 < l) atomicAdd(&o[(int64_t)c0 * ldyc + r], accc[i][0]);
+                if (c1 < l) atomicAdd(&o[(int64_t)c1 * ldyc + r], accc[i][1]);
+              } else {
+                if (c0 < l) o[(int64_t)c0 * ldyc + r] = accc[i][0];
+                if (c1 < l) o[(int64_t)c1 * ldyc + r] = accc[i][1];
+              }
+            }
+          }
+        }
+      }
       // ---- Y_r += A_tile^T Phi_tile  (aty pattern; this warp owns A columns warp*8 + g)
-#pragma unroll 1
+#pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const int r0 = kk * 8 + 2 * t;
         const int c = warp * 8 + g;
@@ -429,54 +523,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (n0 + j < L2T) dmma(accr[n0 + j][0], accr[n0 + j][1], a1, b[j].y);
         }
       }
-      // ---- Y_c(tile rows) = A_tile Omega_strip  (ax pattern; K = BN = 64 -> 8 double-steps)
-      {
-        double accc[LTC][2];
-#pragma unroll
-        for (int i = 0; i < LTC; ++i) accc[i][0] = accc[i][1] = 0.0;
-#pragma unroll 1
-        for (int kk = 0; kk < C::BN / 8; ++kk) {
-          const int box = kk >> 1;
-          const uint32_t q = ((kk & 1) << 2) + t;
-          const double2 a = *reinterpret_cast<const double2*>(As + box * kBK * 128 + sw128(yc_mt * 8 + pg, q));
-          double2 b[LTC];
-#pragma unroll
-          for (int i = 0; i < LTC; ++i) {
-            const int nt = yc_n0 + 2 * i;
-            if (nt < LT) b[i] = *reinterpret_cast<const double2*>(om + box * LP * 128 + sw128(nt * 8 + pg, q));
-          }
-#pragma unroll
-          for (int i = 0; i < LTC; ++i)
-            if (yc_n0 + 2 * i < LT) dmma(accc[i][0], accc[i][1], a.x, b[i].x);
-#pragma unroll
-          for (int i = 0; i < LTC; ++i)
-            if (yc_n0 + 2 * i < LT) dmma(accc[i][0], accc[i][1], a.y, b[i].y);
-        }
-        const int r = kt * kBK + yc_mt * 8 + pg;
-        if (r < rows) {
-          double* o = yc + (yc_atomic ? 0 : (int64_t)sb * yc_slot_stride);
-#pragma unroll
-          for (int i = 0; i < LTC; ++i) {
-            const int nt = yc_n0 + 2 * i;
-            if (nt < LT) {
-              const int c0 = nt * 8 + t, c1 = c0 + 4;
-              if (yc_atomic) {
-                if (c0 < l) atomicAdd(&o[(int64_t)c0 * ldyc + r], accc[i][0]);
-                if (c1 < l) atomicAdd(&o[(int64_t)c1 * ldyc + r], accc[i][1]);
-              } else {
-                if (c0 < l) o[(int64_t)c0 * ldyc + r] = accc[i][0];
-                if (c1 < l) o[(int64_t)c1 * ldyc + r] = accc[i][1];
-              }
-            }
-          }
-        }
-      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(om_empty);
+    if (lane == 0) mbar_arrive(&om_empty[ob]);
+    if (++ob == P::OM_BUFS) { ob = 0; ophase ^= 1; }
     double* o = yr + (int64_t)s * yr_slot_stride;
     const int col = sb * C::BN + warp * 8 + g;
     if (col < ncols) {
@@ -594,10 +647,10 @@ int launch_fused_t(const FusedArgs& a, cudaStream_t st) {
   const int grid = std::min(U, a.grid_cap);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_view_fused<L2T, LTC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(k_view_fused<L2T, LTC>, cudaFuncAttributeMaxDynamicSharedMemorySize, FusedPlan<L2T, LTC>::SMEM);
     attr = true;
   }
-  k_view_fused<L2T, LTC><<<grid, kThreads, C::SMEM, st>>>(tmA, tmOm, tmPhi, a.yc, a.ldyc, a.yc_slot_stride, a.yc_atomic,
+  k_view_fused<L2T, LTC><<<grid, kThreads, FusedPlan<L2T, LTC>::SMEM, st>>>(tmA, tmOm, tmPhi, a.yc, a.ldyc, a.yc_slot_stride, a.yc_atomic,
                                                        a.yr, a.ldyr, a.yr_slot_stride, (int)a.rows, (int)a.n, a.l,
                                                        LP, a.l2, NSB, a.S, KT, a.KTS);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
