@@ -25,10 +25,12 @@ constexpr int kThreads = (kNW + 1) * 32;
 constexpr int kBK = 32;            // reduction-dimension elements per pipeline stage
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kNG = 4;             // n-tiles per B-fragment group
-// k-loop unroll by width: narrow tiles have registers to spare, so unrolling lets the next
-// step's fragment loads overlap the current DMMAs; wide tiles stay rolled (register budget 168)
+// k-loop unroll (of the 4 k-steps per stage) by width: unrolling lets the next step's fragment
+// loads overlap the current DMMAs.  4 everywhere except WT 9..12, where two 8-row m-tiles per warp
+// (MT = 2) double the accumulators and a full unroll spills.  Measured against the earlier
+// 4/2/1 policy (tools/view_probe_ab.py): C3 20000 x 8000 w = 140 views -5%, C2 w = 60/120 -2/-3%.
 template <int WT>
-struct KUnroll { static constexpr int v = WT <= 4 ? 4 : (WT <= 6 ? 2 : 1); };
+struct KUnroll { static constexpr int v = (WT >= 9 && WT <= 12) ? 2 : 4; };
 
 // 1024-byte aligned base of the dynamic shared memory (128B-swizzled TMA tiles need it), formed by
 // pointer arithmetic on the __shared__ array: an integer round trip (uintptr_t) would lose the
