@@ -17,8 +17,17 @@ __global__ void k_slot_sum(const double* __restrict__ in, int64_t ldi, int64_t s
   const int c = blockIdx.y;
   if (r >= rows || c >= w) return;
   const double* p = in + (int64_t)c * ldi + r;
+  // loads in groups of 4 (in flight together), summed in slot order: same bits as a plain loop
   double s = p[0];
-  for (int k = 1; k < S; ++k) s += p[(int64_t)k * slot_stride];
+  int k = 1;
+  for (; k + 4 <= S; k += 4) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = p[(int64_t)(k + u) * slot_stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s += v[u];
+  }
+  for (; k < S; ++k) s += p[(int64_t)k * slot_stride];
   out[(int64_t)c * ldo + r] = s;
 }
 
@@ -824,7 +833,19 @@ __global__ void k_small_gemm(int ta, int tb, int m, int n, int k, const double* 
   const int j = blockIdx.y;
   if (i >= m || j >= n) return;
   double s = 0.0;
-  for (int p = 0; p < k; ++p) {
+  // operands loaded 8 k at a time (in flight together), accumulated in k order
+  int p = 0;
+  for (; p + 8 <= k; p += 8) {
+    double a[8], b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      a[u] = ta ? A[(int64_t)i * lda_ + p + u] : A[(int64_t)(p + u) * lda_ + i];
+      b[u] = tb ? B[(int64_t)(p + u) * ldb + j] : B[(int64_t)j * ldb + p + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = fma(a[u], b[u], s);
+  }
+  for (; p < k; ++p) {
     const double a = ta ? A[(int64_t)i * lda_ + p] : A[(int64_t)p * lda_ + i];
     const double b = tb ? B[(int64_t)p * ldb + j] : B[(int64_t)j * ldb + p];
     s = fma(a, b, s);
