@@ -35,7 +35,7 @@ __host__ __device__ constexpr int oc_ld(int W) { return W + ((4 - W % 16) + 16) 
 // fixed smem (doubles): Ri (W x ld), G (W x W), broadcast / pivot scratch
 __host__ __device__ constexpr int oc_fixed(int W) { return W * oc_ld(W) + W * W + 4 * 64; }
 __host__ __device__ constexpr int oc_rows_max(int W) {
-  return ((kSmemMax / 8 - oc_fixed(W)) / oc_ld(W)) / 8 * 8;
+  return ((kSmemMax / 8 - oc_fixed(W)) / oc_ld(W)) / 16 * 16;
 }
 
 enum { PASS_SHIFT = 0, PASS_GUARD = 1, PASS_SECOND = 2 };
@@ -125,9 +125,10 @@ __device__ int chol_inv_cols(double* G, int w, double shift, double tol, double*
 // O = Yc Ri for this warp's 8-row tiles (mt = warp, warp + 8, ...), up to 4 tiles at once
 // (4 * W/8 independent DMMA chains).  In place (out == nullptr) or to global column-major out.
 template <int W>
-__device__ __forceinline__ void apply_rinv(double* Yc, const double* Ri, int rpc, int warp, int g, int t4,
+__device__ __forceinline__ void apply_rinv(double* Yc, const double* Ri, int rpc, int warp_in, int g, int t4,
                                            double* out, int64_t ldo, int nr, int w) {
   constexpr int NT = W / 8, ld = oc_ld(W);
+  const int warp = __shfl_sync(0xffffffffu, warp_in, 0);  // uniform: the tile predicates need no WARPSYNC
   const int nmt = rpc / 8;
   for (int mt0 = warp; mt0 < nmt; mt0 += 32) {
     double oc[4][NT][2];
@@ -197,8 +198,11 @@ __device__ __forceinline__ void solve_rows(double* Yc, const double* Rm, int rpc
 }
 
 template <int W>
-__device__ __forceinline__ void gram_tiles(const double* Yc, int rpc, double* G, int warp, int g, int t4) {
+__device__ __forceinline__ void gram_tiles(const double* Yc, int rpc, double* G, int warp_in, int g, int t4) {
   constexpr int NT = W / 8, NTILES = NT * (NT + 1) / 2, ld = oc_ld(W);
+  // a provably warp-uniform warp index: a tile predicate on it needs no WARPSYNC before the
+  // predicated mma.sync (rpc is a multiple of 16, so the k-steps need no predicate at all)
+  const int warp = __shfl_sync(0xffffffffu, warp_in, 0);
   constexpr int TPW = (NTILES + 7) / 8;  // tiles per warp (max)
   int tbi[TPW], tbj[TPW];
 #pragma unroll
@@ -218,12 +222,10 @@ __device__ __forceinline__ void gram_tiles(const double* Yc, int rpc, double* G,
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int kr = k0 + 4 * r + t4;
-      if (k0 + 4 * r < rpc) {
 #pragma unroll
-        for (int q = 0; q < TPW; ++q)
-          if (warp + 8 * q < NTILES)
-            dmma(ga[q][r][0], ga[q][r][1], Yc[kr * ld + tbi[q] * 8 + g], Yc[kr * ld + tbj[q] * 8 + g]);
-      }
+      for (int q = 0; q < TPW; ++q)
+        if (warp + 8 * q < NTILES)
+          dmma(ga[q][r][0], ga[q][r][1], Yc[kr * ld + tbi[q] * 8 + g], Yc[kr * ld + tbj[q] * 8 + g]);
     }
   }
 #pragma unroll
@@ -303,6 +305,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     gram_tiles<W>(Yc, rpc, G, warp, g, t4);
     OT(2 + 6 * ps);
+#ifdef RSVD_ORTH_GRAM_TWICE  // probe only: the same Gram again (warm instruction cache)
+    if (ps == 0) {
+      gram_tiles<W>(Yc, rpc, G, warp, g, t4);
+      OT(31);
+    }
+#endif
     cluster.sync();
     OT(3 + 6 * ps);
     // reduce-scatter over the whole cluster: upper-triangle entry e is summed (partials of CTA
@@ -449,7 +457,7 @@ template <int W>
 int launch_w(double* Y, int64_t ldy, int64_t rows, int w, int shifted, double shift_coef, double* Rout, double* Rw,
              DevStatus* status, cudaStream_t st) {
   int rpc = (int)((rows + kCluster - 1) / kCluster);
-  rpc = (rpc + 7) / 8 * 8;
+  rpc = (rpc + 15) / 16 * 16;  // gram_tiles steps 16 rows at a time without a bounds predicate
   if (rpc > oc_rows_max(W)) return RSVD_E_ARG;
   const size_t smem = (size_t)(oc_fixed(W) + rpc * oc_ld(W)) * 8;
   static bool attr = false;

@@ -438,8 +438,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int g = lane >> 2, t = lane & 3, pg = perm8(g);
   const int LT = LP >> 3;
   // Y_c work split per stage: warp -> m-tile (warp & 3) of the 4 row tiles, n-tiles j = (warp>>2) + 2i
-  const int yc_mt = warp & 3;
-  const int yc_n0 = warp >> 2;
+  // from a provably warp-uniform warp index, so the Y_c tile predicate below (nt < LT) is uniform
+  // and the predicated mma.sync needs no WARPSYNC
+  const int warp_u = __shfl_sync(0xffffffffu, warp, 0);
+  const int yc_mt = warp_u & 3;
+  const int yc_n0 = warp_u >> 2;
   double accr[L2T][2];
   int stage = 0;
   uint32_t phase = 0, ophase = 0;

@@ -31,6 +31,9 @@ int main(int argc, char** argv) {
            t[5] - t[4], t[6] - t[5], t[8] - t[6], t[9] - t[8], t[10] - t[9], t[11] - t[10], t[12] - t[11],
            t[21] - t[20], t[22] - t[21], t[23] - t[1], t[24] - t[23], t[2] - t[24], t[15] - t[4], t[16] - t[15], t[13] - t[16], t[14] - t[13]);
     printf("   final split: apply %lld, sync %lld, stage %lld, product %lld\n", t[28] - t[20], t[29] - t[28], t[30] - t[29], t[21] - t[30]);
+#ifdef RSVD_ORTH_GRAM_TWICE
+    printf("   gram0 again (warm i-cache): %lld\n", t[31] - t[2]);
+#endif
   }
 }
 // ---- standalone timing of the factorisation (single CTA, no cluster)
