@@ -114,7 +114,7 @@ __device__ int chol_inv_cols(double* G, int w, double shift, double tol, double*
   if (act) {
     for (int i = 0; i < W; ++i) {
       const double r = (i <= j) ? G[j * W + i] : 0.0;
-      if (i < w && j < w) R[j * w + i] = r;
+      if (R && i < w && j < w) R[j * w + i] = r;
       Ri[i * ld + j] = (i == j) ? invd[j] : r;
     }
   }
@@ -313,27 +313,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     cluster.sync();
     OT(3 + 6 * ps);
-    // reduce-scatter over the whole cluster: upper-triangle entry e is summed (partials of CTA
-    // 0..C-1, in that order) by one thread of one CTA and written into CTA 0's G over DSMEM; the
-    // thread reads CTA 0's partial of e before overwriting it and no other thread touches e
+    // all-reduce over the whole cluster: upper-triangle entry e (W*W <= C * kThreads, so at most
+    // one per thread) is summed by one thread of one CTA (partials of CTA 0..C-1, in that order),
+    // and after a barrier (every partial read) written into the G of EVERY CTA.  Each CTA then
+    // factors the same bits with the same code, so R and R^-1 are identical on all CTAs and no
+    // CTA copies R^-1 from CTA 0 (that DSMEM broadcast through one SM's port cost 7.7k / 25k
+    // cycles per pass at W = 32 / 64).
     {
-      double* G0 = cluster.map_shared_rank(G, 0);
-      for (int e = crank * kThreads + tid; e < W * W; e += C * kThreads) {
-        const int i = e % W, jj = e / W;
-        if (i <= jj) {
-          double v[kCluster];
+      static_assert(W * W <= kCluster * kThreads, "one Gram entry per thread");
+      const int e = crank * kThreads + tid;
+      const int i = e % W, jj = e / W;
+      const bool own = e < W * W && i <= jj;
+      double sum = 0.0;
+      if (own) {
+        double v[kCluster];
 #pragma unroll
-          for (int k = 0; k < kCluster; ++k) v[k] = (k < C) ? cluster.map_shared_rank(G, k)[e] : 0.0;
-          double sum = v[0];
+        for (int k = 0; k < kCluster; ++k) v[k] = (k < C) ? cluster.map_shared_rank(G, k)[e] : 0.0;
+        sum = v[0];
 #pragma unroll
-          for (int k = 1; k < kCluster; ++k) sum += v[k];
-          if (jj >= w) sum = (i == jj) ? 1.0 : 0.0;
-          G0[e] = sum;
-        }
+        for (int k = 1; k < kCluster; ++k) sum += v[k];
+        if (jj >= w) sum = (i == jj) ? 1.0 : 0.0;
       }
+      cluster.sync();  // every partial has been read
+      if (own)
+        for (int k = 0; k < C; ++k) cluster.map_shared_rank(G, k)[e] = sum;
     }
-    cluster.sync();
-    if (crank == 0) {
+    cluster.sync();    // every sum has landed
+    {
       // bookkeeping warps (>= CW): mirror, second-pass test; factorisation warps (< CW) wait
       constexpr int CW = chol_warps<W>();
       const int bt = tid - 32 * CW, nbt = kThreads - 32 * CW;
@@ -371,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               r = (i == k) ? 1.0 + 0.5 * E : E;
               ri = (i == k) ? 1.0 - 0.5 * E : -E;
             }
-            if (i < w && k < w) Rc[k * w + i] = r;
+            if (crank == 0 && i < w && k < w) Rc[k * w + i] = r;
             Ri[k * ld + i] = ri;
           }
       } else if (warp < CW) {
@@ -382,21 +388,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           shift = shift_coef * tr;
         }
         const double tol = (kind == PASS_SHIFT) ? 0.0 : 1e-12;
-        double* Rdst = (kind == PASS_GUARD) ? R1 : (kind == PASS_SHIFT) ? R0 : Rc;
+        double* Rdst = crank != 0 ? nullptr : (kind == PASS_GUARD) ? R1 : (kind == PASS_SHIFT) ? R0 : Rc;
         const int cnt = chol_inv_cols<W>(G, w, shift, tol, Rdst, Ri, ld, bc);
         if (tid == 0) mode = 1;
-        if (tid == 0 && kind == PASS_GUARD && cnt && status) atomicAdd(&status->deficient, cnt);
+        if (tid == 0 && crank == 0 && kind == PASS_GUARD && cnt && status) atomicAdd(&status->deficient, cnt);
       }
       __syncthreads();
       OT(5 + 6 * ps);
     }
-    cluster.sync();
     OT(6 + 6 * ps);
-    if (crank != 0) {
-      const double* src = cluster.map_shared_rank(Ri, 0);
-      for (int e = tid; e < W * ld; e += kThreads) Ri[e] = src[e];
-      if (tid == 0) mode = *cluster.map_shared_rank(&mode, 0);
-    }
     __syncthreads();
   }
   OT(20);
@@ -448,8 +448,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   OT(21);
-  // keep every CTA's shared memory alive until the DSMEM reads of CTA 0's Ri are done
-  cluster.sync();
+  // no trailing cluster barrier: the last remote (DSMEM) accesses are the Gram-sum writes of the
+  // last pass, which complete before that pass's cluster.sync
   OT(22);
 }
 
