@@ -84,11 +84,12 @@ __device__ int chol_inv_cols(double* G, int w, double shift, double tol, double*
   int ndef = 0;
   OT(25);
   // rrow has 2W slots so that rrow[p + i] (i < W) never needs clamping; pivot values are
-  // broadcast through shared memory (immediate-offset loads, no shuffles)
-  for (int p = 0; p < W; ++p) {
+  // broadcast through shared memory (immediate-offset loads, no shuffles).  One pivot: the
+  // column shifts from cs into cd.
+  auto pivot = [&](int p, double (&cs)[W], double (&cd)[W]) {
     if (j == p) {
-      c[0] += sj;
-      bc[192] = c[0];
+      cs[0] += sj;
+      bc[192] = cs[0];
       bc[193] = refj;
     }
     csync<W>();
@@ -96,16 +97,27 @@ __device__ int chol_inv_cols(double* G, int w, double shift, double tol, double*
     const bool def = !(d > tol * rf) || !(rf > 0.0);
     ndef += (def && p < w) ? 1 : 0;
     const double inv = def ? 0.0 : rsqrt(d);
-    const double rpj = (j > p) ? c[0] * inv : ((j == p) ? d * inv : 0.0);
+    const double rpj = (j > p) ? cs[0] * inv : ((j == p) ? d * inv : 0.0);
     if (act && j >= p) G[j * W + p] = def ? 0.0 : rpj;  // R(p, j)
     if (j == p) invd[p] = inv;
     if (act) rrow[j] = rpj;
     csync<W>();
     const double* rp = rrow + p;
 #pragma unroll
-    for (int i = 1; i < W; ++i) c[i - 1] = def ? c[i] : fma(-rp[i], rpj, c[i]);
-    c[W - 1] = 0.0;
+    for (int i = 1; i < W; ++i) cd[i - 1] = def ? cs[i] : fma(-rp[i], rpj, cs[i]);
+    cd[W - 1] = 0.0;
     csync<W>();
+  };
+  if constexpr (W <= 32) {
+    // two pivots per iteration, c -> t -> c: every shifted value is written straight into its
+    // final register (a one-pivot runtime loop has to copy the whole column down each pivot)
+    double t[W];
+    for (int p = 0; p < W; p += 2) {
+      pivot(p, c, t);
+      pivot(p + 1, t, c);
+    }
+  } else {
+    for (int p = 0; p < W; ++p) pivot(p, c, c);
   }
   csync<W>();
   OT(26);
