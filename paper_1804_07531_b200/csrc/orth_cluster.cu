@@ -198,13 +198,23 @@ __device__ __forceinline__ void solve_rows(double* Yc, const double* Rm, int rpc
     double y[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) y[i] = yr[i];
-    for (int j = 0; j < W; ++j) {
+    // one column: solve entry j and shift the rest from ys into yd
+    auto step = [&](int j, double (&ys)[W], double (&yd)[W]) {
       const double* rj = Rm + j * ld + j;  // R(j, j + i) at rj[i]
-      const double q = y[0] * rj[0];
+      const double q = ys[0] * rj[0];
       yr[j] = q;
 #pragma unroll
-      for (int i = 1; i < W; ++i) y[i - 1] = fma(-q, rj[i], y[i]);
-      y[W - 1] = 0.0;
+      for (int i = 1; i < W; ++i) yd[i - 1] = fma(-q, rj[i], ys[i]);
+      yd[W - 1] = 0.0;
+    };
+    if constexpr (W <= 32) {
+      double t[W];  // two columns per iteration: no register copies for the shift (as in the Cholesky)
+      for (int j = 0; j < W; j += 2) {
+        step(j, y, t);
+        step(j + 1, t, y);
+      }
+    } else {
+      for (int j = 0; j < W; ++j) step(j, y, y);
     }
   }
 }
