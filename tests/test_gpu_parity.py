@@ -90,7 +90,10 @@ def test_fused_view_bit_exact(ctx, shape, l, l2):
 # ------------------------------------------------------------------ orth and core SVD
 
 @pytest.mark.parametrize("rows,w", [(4000, 30), (1037, 20), (200000, 8), (777, 128), (5000, 160), (40, 40),
-                                    (3000, 200), (5000, 250), (2000, 500)])
+                                    (3000, 200), (5000, 250), (2000, 500),
+                                    # cluster path: ragged rows (16-row chunks padded), the largest
+                                    # W = 64 block it holds (16 x 272 rows) and one row more (other path)
+                                    (3001, 30), (4000, 60), (4352, 64), (4353, 64)])
 def test_orth_cholqr2(ctx, rows, w):
     Y = S.random_gaussian_matrix(rows, w, seed=rows + w) * np.logspace(0, -3, w)
     Q, R, info = ctx.orth(colmajor_dev(Y))
@@ -103,7 +106,7 @@ def test_orth_cholqr2(ctx, rows, w):
     assert info.rank_deficient_cols == 0
 
 
-@pytest.mark.parametrize("w,r", [(24, 17), (250, 201)])
+@pytest.mark.parametrize("w,r", [(24, 17), (30, 21), (60, 43), (250, 201)])
 def test_orth_rank_deficient(ctx, w, r):
     """Exactly rank-r input: the guarded Cholesky zeroes l - r columns; the kept Q spans range(Y)."""
     rows = 3000
