@@ -117,7 +117,38 @@ __device__ int chol_inv_cols(double* G, int w, double shift, double tol, double*
       pivot(p + 1, t, c);
     }
   } else {
-    for (int p = 0; p < W; ++p) pivot(p, c, c);
+    // W > 32 (a second array would not fit the registers): 8 pivots per iteration with c indexed
+    // from the window base p0, updated in place (compile-time offsets k, i), and the window
+    // shifted once per 8 pivots (7 register copies per pivot instead of W - 1)
+    for (int p0 = 0; p0 < W; p0 += 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int p = p0 + k;
+        if (j == p) {
+          c[k] += sj;
+          bc[192] = c[k];
+          bc[193] = refj;
+        }
+        csync<W>();
+        const double d = bc[192], rf = bc[193];
+        const bool def = !(d > tol * rf) || !(rf > 0.0);
+        ndef += (def && p < w) ? 1 : 0;
+        const double inv = def ? 0.0 : rsqrt(d);
+        const double rpj = (j > p) ? c[k] * inv : ((j == p) ? d * inv : 0.0);
+        if (act && j >= p) G[j * W + p] = def ? 0.0 : rpj;  // R(p, j)
+        if (j == p) invd[p] = inv;
+        if (act) rrow[j] = rpj;
+        csync<W>();
+        const double* rp = rrow + p0;  // rp[i] = R(p, p0 + i)
+#pragma unroll
+        for (int i = k + 1; i < W; ++i) c[i] = def ? c[i] : fma(-rp[i], rpj, c[i]);
+        csync<W>();
+      }
+#pragma unroll
+      for (int i = 0; i < W - 8; ++i) c[i] = c[i + 8];
+#pragma unroll
+      for (int i = W - 8; i < W; ++i) c[i] = 0.0;
+    }
   }
   csync<W>();
   OT(26);
@@ -214,7 +245,22 @@ __device__ __forceinline__ void solve_rows(double* Yc, const double* Rm, int rpc
         step(j + 1, t, y);
       }
     } else {
-      for (int j = 0; j < W; ++j) step(j, y, y);
+      // W > 32: 8 columns per iteration, y indexed from the window base j0 and solved in place,
+      // the window shifted once per 8 columns (as in the Cholesky)
+      for (int j0 = 0; j0 < W; j0 += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double* rj = Rm + (j0 + k) * ld + j0;  // R(j0 + k, j0 + i) at rj[i]
+          const double q = y[k] * rj[k];
+          yr[j0 + k] = q;
+#pragma unroll
+          for (int i = k + 1; i < W; ++i) y[i] = fma(-q, rj[i], y[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < W - 8; ++i) y[i] = y[i + 8];
+#pragma unroll
+        for (int i = W - 8; i < W; ++i) y[i] = 0.0;
+      }
     }
   }
 }
