@@ -84,42 +84,11 @@ __device__ int chol_inv_cols(double* G, int w, double shift, double tol, double*
   int ndef = 0;
   OT(25);
   // rrow has 2W slots so that rrow[p + i] (i < W) never needs clamping; pivot values are
-  // broadcast through shared memory (immediate-offset loads, no shuffles).  One pivot: the
-  // column shifts from cs into cd.
-  auto pivot = [&](int p, double (&cs)[W], double (&cd)[W]) {
-    if (j == p) {
-      cs[0] += sj;
-      bc[192] = cs[0];
-      bc[193] = refj;
-    }
-    csync<W>();
-    const double d = bc[192], rf = bc[193];
-    const bool def = !(d > tol * rf) || !(rf > 0.0);
-    ndef += (def && p < w) ? 1 : 0;
-    const double inv = def ? 0.0 : rsqrt(d);
-    const double rpj = (j > p) ? cs[0] * inv : ((j == p) ? d * inv : 0.0);
-    if (act && j >= p) G[j * W + p] = def ? 0.0 : rpj;  // R(p, j)
-    if (j == p) invd[p] = inv;
-    if (act) rrow[j] = rpj;
-    csync<W>();
-    const double* rp = rrow + p;
-#pragma unroll
-    for (int i = 1; i < W; ++i) cd[i - 1] = def ? cs[i] : fma(-rp[i], rpj, cs[i]);
-    cd[W - 1] = 0.0;
-    csync<W>();
-  };
-  if constexpr (W <= 32) {
-    // two pivots per iteration, c -> t -> c: every shifted value is written straight into its
-    // final register (a one-pivot runtime loop has to copy the whole column down each pivot)
-    double t[W];
-    for (int p = 0; p < W; p += 2) {
-      pivot(p, c, t);
-      pivot(p + 1, t, c);
-    }
-  } else {
-    // W > 32 (a second array would not fit the registers): 8 pivots per iteration with c indexed
-    // from the window base p0, updated in place (compile-time offsets k, i), and the window
-    // shifted once per 8 pivots (7 register copies per pivot instead of W - 1)
+  // broadcast through shared memory (immediate-offset loads, no shuffles).  8 pivots per iteration
+  // with c indexed from the window base p0 and updated in place at compile-time offsets (k, i);
+  // the window shifts once per 8 pivots.  (A one-pivot runtime loop over a shift register made
+  // the compiler copy the whole column every pivot: W = 64 74k -> 46k cycles, W = 32 24k -> 18k.)
+  {
     for (int p0 = 0; p0 < W; p0 += 8) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -218,9 +187,10 @@ __device__ __forceinline__ void apply_rinv(double* Yc, const double* Ri, int rpc
 // owns upper 8x8 tiles q, q+8, ... over all rows, with 4 DMMA chains per tile (k-steps
 // interleaved) summed in a fixed order: no cross-warp reduction.
 // Yc <- Yc R^-1 by forward substitution, one thread per row (q R = y): Rm is R row-major
-// (Rm[i*ld + k] = R(i, k)) with 1/R_jj on the diagonal.  The row lives in registers as a shift
-// register (y[0] = the entry being solved), so the column loop stays compact.  Reads past
-// row W-1 of Rm land in G (the next buffer): those values multiply padding entries only.
+// (Rm[i*ld + k] = R(i, k)) with 1/R_jj on the diagonal.  The row lives in registers, indexed
+// from an 8-column window that shifts once per 8 columns, so the column loop stays compact.
+// Reads past column W-1 of a row of Rm (its padding, the next row, or G after the last row)
+// only ever multiply into entries beyond the row, which are never solved or stored.
 template <int W>
 __device__ __forceinline__ void solve_rows(double* Yc, const double* Rm, int rpc, int tid) {
   constexpr int ld = oc_ld(W);
@@ -229,24 +199,9 @@ __device__ __forceinline__ void solve_rows(double* Yc, const double* Rm, int rpc
     double y[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) y[i] = yr[i];
-    // one column: solve entry j and shift the rest from ys into yd
-    auto step = [&](int j, double (&ys)[W], double (&yd)[W]) {
-      const double* rj = Rm + j * ld + j;  // R(j, j + i) at rj[i]
-      const double q = ys[0] * rj[0];
-      yr[j] = q;
-#pragma unroll
-      for (int i = 1; i < W; ++i) yd[i - 1] = fma(-q, rj[i], ys[i]);
-      yd[W - 1] = 0.0;
-    };
-    if constexpr (W <= 32) {
-      double t[W];  // two columns per iteration: no register copies for the shift (as in the Cholesky)
-      for (int j = 0; j < W; j += 2) {
-        step(j, y, t);
-        step(j + 1, t, y);
-      }
-    } else {
-      // W > 32: 8 columns per iteration, y indexed from the window base j0 and solved in place,
-      // the window shifted once per 8 columns (as in the Cholesky)
+    // 8 columns per iteration, y indexed from the window base j0 and solved in place at
+    // compile-time offsets, the window shifted once per 8 columns (as in the Cholesky)
+    {
       for (int j0 = 0; j0 < W; j0 += 8) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
