@@ -265,6 +265,33 @@ __device__ __forceinline__ void gram_tiles(const double* Yc, int rpc, double* G,
   __syncthreads();
 }
 
+// out = A B for upper-triangular A, B (col-major W x W in shared memory, zero outside w x w) on
+// FP64 DMMA: warp q owns the upper 8x8 output tiles q, q+8, ...; tile (bi, bj) sums the k-blocks
+// bi..bj (the only non-zero contributions) in k order.  out is col-major w x w (global), lower
+// triangle zero.  The warp index is shuffled to make the loop bounds provably warp-uniform.
+template <int W>
+__device__ __forceinline__ void triu_product_dmma(const double* As, const double* Bs, int w, double* out, int warp_in,
+                                                  int g, int t4) {
+  constexpr int NT = W / 8, NTILES = NT * (NT + 1) / 2;
+  const int warp = __shfl_sync(0xffffffffu, warp_in, 0);
+  // the strictly lower triangle (the tiles below the diagonal are not computed); the lower
+  // entries of the diagonal tiles are also written as 0 below, the same value
+  for (int e = threadIdx.x; e < w * w; e += kThreads)
+    if (e % w > e / w) out[e] = 0.0;
+  for (int u0 = warp; u0 < NTILES; u0 += 8) {
+    int u = u0, bi = 0;
+    while (u >= NT - bi) { u -= NT - bi; ++bi; }
+    const int bj = bi + u;
+    double d0 = 0.0, d1 = 0.0;
+    for (int k0 = bi * 8; k0 < bj * 8 + 8; k0 += 4)
+      dmma(d0, d1, As[(k0 + t4) * W + bi * 8 + g], Bs[(bj * 8 + g) * W + k0 + t4]);
+    const int i = bi * 8 + g;
+    const int k = bj * 8 + 2 * t4;
+    if (i < w && k < w) out[k * w + i] = (i <= k) ? d0 : 0.0;
+    if (i < w && k + 1 < w) out[(k + 1) * w + i] = (i <= k + 1) ? d1 : 0.0;
+  }
+}
+
 // (upper-triangular A B)(i, k) = sum_{q=i..k} A(i, q) B(q, k), col-major w x w, four named
 // accumulators (an accumulator array indexed by q & 3 lives in local memory)
 __device__ __forceinline__ double triu_dot(const double* A, const double* B, int w, int i, int k) {
@@ -438,36 +465,58 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     OT(29);
     // both factors in shared memory: G is free on CTA 0 now, and so is the row buffer Yc after the
-    // final apply when it holds w*w doubles (a dependent loop over global loads costs an L2 round
-    // trip per step: ~50k cycles at W = 64); tiny blocks keep the second factor in global memory
-    const bool yc_fits = (int64_t)rpc * ld >= (int64_t)w * w;
-    if (shifted) {
-      // R_1 <- R_1 R_0
-      for (int e = tid; e < w * w; e += kThreads) G[e] = R1[e];
-      const double* R0s = R0;
-      if (yc_fits) {
-        for (int e = tid; e < w * w; e += kThreads) Yc[e] = R0[e];
-        R0s = Yc;
+    // final apply.  When Yc holds a W x W block the products run on DMMA (W-padded, zero outside
+    // w x w); tiny blocks keep the scalar dot products with the second factor in global memory
+    // (a dependent loop over global loads costs an L2 round trip per step).
+    if ((int64_t)rpc * ld >= (int64_t)W * W) {
+      auto stage = [&](double* dst, const double* src) {
+        // 8 independent L2 loads in flight per thread (a load -> store loop pays one round trip
+        // per element)
+        for (int e0 = tid; e0 < W * W; e0 += 8 * kThreads) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * kThreads, i = e % W, k = e / W;
+            v[u] = (e < W * W && i < w && k < w) ? src[k * w + i] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * kThreads;
+            if (e < W * W) dst[e] = v[u];
+          }
+        }
+      };
+      if (shifted) {  // R_1 <- R_1 R_0
+        stage(G, R1);
+        stage(Yc, R0);
+        __syncthreads();
+        triu_product_dmma<W>(G, Yc, w, R1, warp, g, t4);
+        __syncthreads();
       }
+      stage(G, Rc);   // R_out = R_2 R_1
+      stage(Yc, R1);
       __syncthreads();
+      OT(30);
+      triu_product_dmma<W>(G, Yc, w, Rout, warp, g, t4);
+    } else {
+      if (shifted) {
+        // R_1 <- R_1 R_0
+        for (int e = tid; e < w * w; e += kThreads) G[e] = R1[e];
+        __syncthreads();
+        for (int e = tid; e < w * w; e += kThreads) {
+          const int i = e % w, k = e / w;
+          R1[e] = (i <= k) ? triu_dot(G, R0, w, i, k) : 0.0;
+        }
+        __syncthreads();
+      }
+      // R_out = R_2 R_1
+      for (int e = tid; e < w * w; e += kThreads) G[e] = Rc[e];
+      __syncthreads();
+      OT(30);
       for (int e = tid; e < w * w; e += kThreads) {
         const int i = e % w, k = e / w;
-        R1[e] = (i <= k) ? triu_dot(G, R0s, w, i, k) : 0.0;
+        Rout[e] = (i <= k) ? triu_dot(G, R1, w, i, k) : 0.0;
       }
-      __syncthreads();
-    }
-    // R_out = R_2 R_1
-    const double* R1s = R1;
-    for (int e = tid; e < w * w; e += kThreads) G[e] = Rc[e];
-    if (yc_fits) {
-      for (int e = tid; e < w * w; e += kThreads) Yc[e] = R1[e];
-      R1s = Yc;
-    }
-    __syncthreads();
-    OT(30);
-    for (int e = tid; e < w * w; e += kThreads) {
-      const int i = e % w, k = e / w;
-      Rout[e] = (i <= k) ? triu_dot(G, R1s, w, i, k) : 0.0;
     }
   }
   OT(21);
