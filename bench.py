@@ -335,10 +335,12 @@ def main():
         torch.cuda.Stream(dev, priority=(-5 if alg == "krylov" else 0)) for alg, _ in STEP_PLAN[1:]]
     ctxs = [rsvd.Context(local, stream=s_) for s_ in streams]
     ctx = ctxs[0]
-    # SM budget of the two calls off the critical path (rsvd_set_sm_limit): their persistent view
-    # kernels then leave SMs to the Krylov chain; measured 1.31-1.33 -> 1.29 ms per step with 64
-    # (48: 1.33, 32: 1.6).  RSVD_BENCH_SIDE_SMS=0 disables it.
-    side_sms = int(os.environ.get("RSVD_BENCH_SIDE_SMS", "64"))
+    # Optional SM budget of the two calls off the critical path (rsvd_set_sm_limit), so that their
+    # persistent view kernels leave SMs to the Krylov chain.  It paid while that chain was longer
+    # (1.31-1.33 -> 1.29 ms per step with 64); with the current kernels it no longer does (mean of
+    # 4 runs: no limit 1.111 ms, 64 SMs 1.125, 48: 1.176, 80: 1.131, 96: 1.147), so the default is
+    # off.  RSVD_BENCH_SIDE_SMS=<n> re-enables it for A/B runs.
+    side_sms = int(os.environ.get("RSVD_BENCH_SIDE_SMS", "0"))
 
     def limit_side(on):
         # only around the concurrent step; every sequential measurement (per-algorithm SVD times,
