@@ -197,17 +197,25 @@ __device__ __forceinline__ void solve_rows(double* Yc, const double* Rm, int rpc
   for (int r = tid; r < rpc; r += kThreads) {
     double* yr = Yc + r * ld;
     double y[W];
+    // 16-byte accesses (ld is even and Yc 16-byte aligned): a row per thread at stride ld hits
+    // only a few banks, so half as many accesses means half the conflicted wavefronts
 #pragma unroll
-    for (int i = 0; i < W; ++i) y[i] = yr[i];
+    for (int i = 0; i < W; i += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(yr + i);
+      y[i] = v.x;
+      y[i + 1] = v.y;
+    }
     // 8 columns per iteration, y indexed from the window base j0 and solved in place at
     // compile-time offsets, the window shifted once per 8 columns (as in the Cholesky)
     {
       for (int j0 = 0; j0 < W; j0 += 8) {
+        double qe = 0.0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const double* rj = Rm + (j0 + k) * ld + j0;  // R(j0 + k, j0 + i) at rj[i]
           const double q = y[k] * rj[k];
-          yr[j0 + k] = q;
+          if (k & 1) *reinterpret_cast<double2*>(yr + j0 + k - 1) = make_double2(qe, q);
+          else qe = q;
 #pragma unroll
           for (int i = k + 1; i < W; ++i) y[i] = fma(-q, rj[i], y[i]);
         }
