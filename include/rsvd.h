@@ -93,6 +93,8 @@ enum {
 #define RSVD_CORE_NO_J    16u  /* rsvd_core_svd: V = M^T U S^-1 instead of accumulated rotations  */
 #define RSVD_ASYNC        32u  /* enqueue only: outputs and info complete after rsvd_wait(ctx) */
 #define RSVD_WOOLFE       64u  /* rsvd_single_pass: Alg. 8 (Woolfe variant) instead of Alg. 7   */
+#define RSVD_ORTH_SHIFTED 128u /* rsvd_orth: shifted CholeskyQR3 (a shift pass before the two
+                                  CholeskyQR passes; what Alg. 9's projected Krylov blocks use) */
 #define RSVD_LC_MINVAR    (-2) /* rsvd_single_pass lc: minimum-variance l_c          */
 #define RSVD_EXT_BWZ      0    /* rsvd_single_pass_extended: Eq. (bwz)               */
 #define RSVD_EXT_BWZ2     1    /* rsvd_single_pass_extended: Eq. (bwzimproved)       */
@@ -269,7 +271,9 @@ int rsvd_view_fused(rsvd_ctx* ctx, const rsvd_mat* A, const void* Omega, int64_t
                     void* Yr, int64_t ld_yr, unsigned flags, rsvd_info* info);
 /* In place: Y (rows x w) <- Q with Q^T Q = I, and R (w x w, column-major, may be NULL) with
  * Y_in = Q R, diag(R) >= 0.  Columns whose Cholesky pivot falls below the rank guard are set to
- * zero in Q (and their row of R is zero); their count is info->rank_deficient_cols. */
+ * zero in Q (and their row of R is zero); their count is info->rank_deficient_cols.
+ * flags | RSVD_ORTH_SHIFTED: shifted CholeskyQR3 (R = R_2 R_1 R_0), for blocks whose condition
+ * number is too large for CholeskyQR2. */
 int rsvd_orth(rsvd_ctx* ctx, int64_t rows, int w, void* Y, int64_t ldy, void* R, unsigned flags,
               rsvd_info* info);
 /* M (r x c, column-major, ldm >= r, r >= c): M = U diag(S) V^T with U r x c, S c (descending),

@@ -1195,7 +1195,7 @@ void prim_orth(Exec& E) {
   double* R = E.alloc((int64_t)c.w * c.w);
   const int64_t n_save = E.n;
   E.n = c.rows;
-  E.orth(SIDE_N, Y, R, nullptr);  // SIDE_N: never all-reduced
+  E.orth(SIDE_N, Y, R, nullptr, (c.flags & RSVD_ORTH_SHIFTED) != 0);  // SIDE_N: never all-reduced
   E.n = n_save;
   int64_t ld;
   double* o = E.out_ptr(c.U, c.ldu, Y.rows, c.w, c.kU, &ld);

@@ -20,6 +20,7 @@ RSVD_F32, RSVD_F64 = 1, 2
 RSVD_INPUT_A, RSVD_INPUT_AT = 0, 1
 RSVD_GOAL_SVD, RSVD_GOAL_LEFT, RSVD_GOAL_RIGHT, RSVD_GOAL_NORMAL = 0, 1, 2, 3
 RSVD_SQUARED, RSVD_NO_GRAPH, RSVD_PROFILE, RSVD_CORE_NO_J, RSVD_ASYNC, RSVD_WOOLFE = 1, 2, 4, 16, 32, 64
+RSVD_ORTH_SHIFTED = 128
 RSVD_LC_MINVAR = -2
 RSVD_EXT_BWZ, RSVD_EXT_BWZ2 = 0, 1
 RSVD_PLAN_FLAT, RSVD_PLAN_DECAY, RSVD_PLAN_RAPID, RSVD_PLAN_BALANCED = 0, 1, 2, 3
@@ -340,7 +341,8 @@ class Context:
         return Yc, Yr, info
 
     def orth(self, Y, flags=0):
-        """CholeskyQR2 (returns a new Q and R; the input is not modified)."""
+        """CholeskyQR2, or shifted CholeskyQR3 with flags | RSVD_ORTH_SHIFTED (returns a new Q and
+        R; the input is not modified)."""
         Q = _colmajor(Y).clone() if _colmajor(Y).data_ptr() == Y.data_ptr() else _colmajor(Y)
         Q = Q.t().contiguous().t()
         w = Q.shape[1]

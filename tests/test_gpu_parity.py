@@ -106,6 +106,25 @@ def test_orth_cholqr2(ctx, rows, w):
     assert info.rank_deficient_cols == 0
 
 
+@pytest.mark.parametrize("rows,w", [(4000, 30), (4000, 60), (3001, 20), (777, 128), (5000, 250)])
+def test_orth_shifted_cholqr3(ctx, rows, w):
+    """Shifted CholeskyQR3 (the Krylov blocks' orthonormalisation) on an ill-conditioned block
+    (kappa ~ 1e10, beyond CholeskyQR2): Q orthonormal, Y = Q R, and R upper triangular with exact
+    zeros below the diagonal (R = R_2 R_1 R_0 is formed by a tiled product in the cluster kernel)."""
+    from paper_1804_07531_b200 import rsvd
+
+    Y = S.random_gaussian_matrix(rows, w, seed=rows + 3 * w) * np.logspace(0, -10, w)
+    Q, R, info = ctx.orth(colmajor_dev(Y), flags=rsvd.RSVD_ORTH_SHIFTED)
+    Q, R = host(Q), host(R)
+    np.testing.assert_allclose(Q.T @ Q, np.eye(w), atol=5e-14 * np.sqrt(w))
+    assert np.all(np.tril(R, -1) == 0) and np.all(np.diag(R) >= 0)
+    assert np.linalg.norm(Q @ R - Y) <= 1e-13 * np.linalg.norm(Y)
+    Qo, Ro = O.qr(Y)
+    # the trailing columns of an ill-conditioned block carry R entries known only to u * kappa
+    # relative to ||Y||: compare R column by column against the oracle's Householder R
+    assert np.linalg.norm(R - Ro) <= 1e-12 * np.linalg.norm(Ro)
+
+
 @pytest.mark.parametrize("w,r", [(24, 17), (30, 21), (60, 43), (250, 201)])
 def test_orth_rank_deficient(ctx, w, r):
     """Exactly rank-r input: the guarded Cholesky zeroes l - r columns; the kept Q spans range(Y)."""
