@@ -320,7 +320,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_orth_cluster(double* __restrict__ Y, int64_t ldy, int64_t rows, int w, int rpc, int shifted, double shift_coef,
                    double* __restrict__ Rout, double* __restrict__ Rw /* 3 w*w global scratch */,
                    DevStatus* status) {
-  constexpr int NT = W / 8, NTILES = NT * (NT + 1) / 2;
   constexpr int ld = oc_ld(W);
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();

@@ -124,7 +124,6 @@ struct TS {  // column-major tall-skinny block: w columns of `rows`, leading dim
   double* p = nullptr;
   int64_t rows = 0, ld = 0;
   int w = 0;
-  double* col(int j) const { return p + (int64_t)j * ld; }
 };
 
 enum PtrKind { PTR_NULL = 0, PTR_DEVICE = 1, PTR_HOST = 2 };

@@ -488,7 +488,6 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
 // accumulated (stride ce; in shared memory when W and J fit, else in the global scratch).
 // WJ = 0: no J; right vectors B^T U S^-1 from the input in global memory (leading triplets only,
 // as k_jacobi_small); 4 lanes x 32 rows per pair was the fastest no-J layout (tools/jac_small_probe).
-constexpr int kMidLPP = 8, kMidRW = 16, kMidRS = kMidLPP * kMidRW + 4;
 template <int LPP, int RW, int WJ>
 __global__ void __launch_bounds__(LPP == 4 ? 256 : 512) k_jacobi_mid(const double* __restrict__ M, int64_t ldm, int trans, int r, int c,
                                                     double* __restrict__ Ul, double* __restrict__ Sv,
@@ -1018,8 +1017,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define PHASE_MIN(i) do {} while (0)
 #endif
 constexpr int kFW = 64;          // max width of the fused path
-constexpr int kFRows = 32;       // rows per smem tile
-constexpr int kFLd = kFW + 1;    // padded tile row
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
