@@ -2,20 +2,24 @@
 """Benchmark of the pass-efficient randomized SVD hot path on B200 (BASELINE.json metric
 "A-view HBM GB/s (fraction of roofline) and rank-k SVD time per view budget").
 
-A STEP is one pass of the whole hot path over one synthetic matrix:
-    rsvd_subspace (Alg. 2, v=3)  +  rsvd_block_krylov (Alg. 9, v=4)  +  rsvd_single_pass (Alg. 7)
-= 3 + 4 + 1 = 8 views of A.  Workload at N=1: BASELINE.json configs[1] = C2 (fp64 4000x4000,
-k=20, p=10, l2=60).  At N GPUs (weak scaling) every rank holds a C2-sized row block of an
-(N*4000) x 4000 matrix with the same spectrum and the step is ONE distributed SVD (NCCL all-reduce
-of the Gram matrices and of the co-range views).
+A STEP is one pass of the whole hot path over one synthetic matrix.
+Default workload (N = 1): BASELINE C4, the largest single-GPU config — fp64 50000 x 200000 (80 GB),
+X diag(i^-1.5) Y^T (rank 500) + 1e-8 G, k = 100, p = 20 — with BASELINE C4's three runs:
+    rsvd_block_krylov v = 3                            (3 views, Alg. 9 == Alg. 2 at v = 3)
+    rsvd_single_pass l2 = 240                          (1 view, Alg. 7)
+    rsvd_subspace v = 3, input = A^T, RSVD_SQUARED     (3 views, the A^T A normal-matrix estimate)
+= 7 views of A per step.  A (80 GB) is far larger than L2 (126 MB): every view streams it from HBM,
+no flush is needed (stated in `config`).
 
-value = A-view bytes of all ranks / step time (GB/s); L2 is flushed (256 MiB write) before every
-timed step, outside the timed events.  `e2e` = the same step end to end from pinned HOST memory
-on a stream of K matrices: A, Omega, Phi copied to the device per step (double-buffered on a copy
-stream, overlapping the previous step's calls), the three API calls, every U, S, V copied back —
-all host<->device copies inside the timed region.
+value = A bytes of all views of the step / step time (GB/s); the three calls run concurrently on
+three contexts / streams (RSVD_ASYNC) at N = 1, sequentially on one communicator at N > 1.
+N > 1 (torchrun, one process per GPU): the SAME matrix row-sharded over the N GPUs
+(shard_rows, 128-row aligned; strong scaling), NCCL all-reduce of the A^T Y partials and Grams.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C2]
+Secondary records: C5 (fp32 100000^2, 40 GB; tcgen05 3xTF32 views) SVD times and view fractions
+(3xTF32 and strict 1x-flop), and the C2 per-call latencies.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C4|C5|C2|C3]
 """
 from __future__ import annotations
 
@@ -34,27 +38,45 @@ import numpy as np  # noqa: E402
 
 import synth as S  # noqa: E402
 
-STEP_PLAN = [("subspace", 3), ("krylov", 4), ("single_pass", 1)]
 METRIC = "A-view HBM GB/s (fraction of roofline) and rank-k SVD time per view budget"
+SQUARED = 1
+# (algorithm, views, input (0 = A, 1 = A^T), flags) per config
+PLANS = {
+    "C4": [("krylov", 3, 0, 0), ("single_pass", 1, 0, 0), ("subspace", 3, 1, SQUARED)],
+    "C5": [("subspace", 2, 0, 0), ("krylov", 4, 0, 0)],
+    "C3": [("subspace", 3, 0, 0), ("krylov", 4, 0, 0), ("single_pass", 1, 0, 0)],
+    "C2": [("subspace", 3, 0, 0), ("krylov", 4, 0, 0), ("single_pass", 1, 0, 0)],
+}
+DMMA_NOMINAL_TF, BF16_NOMINAL_TF, TF32_NOMINAL_TF = 40.0, 2250.0, 1100.0
 
 
-def step_views():
-    return sum(v for _, v in STEP_PLAN)
+def plan_views(plan):
+    return sum(v for _, v, _, _ in plan)
+
+
+def plan_name(plan):
+    return " + ".join(f"{a} v={v}" + (" input=A^T" if i else "") + (" S^2" if f & SQUARED else "") for a, v, i, f in plan)
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-steps", type=int, default=3)
-    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (multi-GB configs)")
-    ap.add_argument("--no-secondary", action="store_true", help="skip the C5 fp32 (tcgen05) view measurement")
+    ap.add_argument("--profile-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--sequential", action="store_true", help="N = 1: run the step's calls one after another")
     return ap.parse_args()
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(path)) if os.path.exists(path) else {}
 
 
 # ------------------------------------------------------------------ clocks during the timed region
@@ -66,18 +88,18 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.lines = []
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
         return self
 
     def __exit__(self, *a):
-        self.lines = []
         if self.proc:
             self.proc.terminate()
             try:
@@ -90,7 +112,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
+        for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -106,205 +128,102 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ------------------------------------------------------------------ CPU oracle baseline (reference arm)
-def run_oracle_step(A, cfg, Om, Phi):
+# ------------------------------------------------------------------ CPU oracle (cpu_baseline / reference arm)
+def oracle_step(A, cfg, plan, Om, Omm, Phi):
     import oracle as O
 
-    for alg, v in STEP_PLAN:
-        O.svd_of(A, alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi)
+    for alg, v, inp, _ in plan:
+        O.svd_of(A, alg, cfg.k, cfg.p, v=v, Omega=Omm if inp else Om, l2=cfg.l2, Phi=Phi, transpose=bool(inp))
 
 
-def oracle_baseline(cfg, steps=1, budget_s=30.0, warmup=1):
-    """Time the oracle, as it stands, on this host's cores on the same workload (C2 step), after
-    `warmup` untimed steps."""
-    A = S.make_matrix(cfg)
-    Om = S.gaussian_test_matrix(cfg.n, cfg.l, cfg, S.ROLE_OMEGA)
-    Phi = S.gaussian_test_matrix(cfg.m, cfg.l2, cfg, S.ROLE_PHI)
+def oracle_sample_inputs(cfg, rows):
+    """The config's recipe at a bounded row sample (rows x n), NumPy generator (host only)."""
+    A = S.make_matrix(cfg, rows, cfg.n).astype(np.float64)
+    Om = S.gaussian_test_matrix(cfg.n, cfg.l, cfg, S.ROLE_OMEGA).astype(np.float64)
+    Omm = S.gaussian_test_matrix(rows, cfg.l, cfg, S.ROLE_OMEGA_M).astype(np.float64)
+    Phi = S.gaussian_test_matrix(rows, cfg.l2, cfg, S.ROLE_PHI).astype(np.float64)
+    return A, Om, Omm, Phi
+
+
+SAMPLE_ROWS = {"C4": 12000, "C5": 8000, "C3": 20000, "C2": 4000}
+
+
+def time_oracle(A, cfg, plan, Om, Omm, Phi, steps, warmup, budget_s):
     for _ in range(max(0, warmup)):
-        run_oracle_step(A, cfg, Om, Phi)
-    times = []
+        oracle_step(A, cfg, plan, Om, Omm, Phi)
+    ts = []
     t_all = time.perf_counter()
     for _ in range(max(1, steps)):
         t0 = time.perf_counter()
-        run_oracle_step(A, cfg, Om, Phi)
-        times.append(time.perf_counter() - t0)
+        oracle_step(A, cfg, plan, Om, Omm, Phi)
+        ts.append(time.perf_counter() - t0)
         if time.perf_counter() - t_all > budget_s:
             break
-    step_s = statistics.median(times)
-    bytes_step = step_views() * cfg.m * cfg.n * cfg.itemsize
+    step_s = statistics.median(ts)
+    gbs = plan_views(plan) * A.shape[0] * A.shape[1] * cfg.itemsize / step_s / 1e9
     cores = len(os.sched_getaffinity(0))
-    return {"value": bytes_step / step_s / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
-            "sample": f"{len(times)} full step(s) of {cfg.name} ({'+'.join(f'{a}(v={v})' for a, v in STEP_PLAN)}), "
-                      f"NumPy/OpenBLAS fp64, median step {step_s:.3f} s",
-            "step_s": step_s}
+    sample = (f"{len(ts)} oracle step(s) ({plan_name(plan)}) on a {A.shape[0]} x {A.shape[1]} row sample of "
+              f"{cfg.name}'s recipe (the full matrix is {cfg.m} x {cfg.n}); NumPy/OpenBLAS fp64 on {cores} cores, "
+              f"median step {step_s:.3f} s; value = A-view bytes of the sample / step time")
+    return {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample, "step_s": step_s}
 
 
 def reference_main(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     cfg = S.CONFIGS[args.config]
+    plan = PLANS[args.config]
+    rows = SAMPLE_ROWS.get(cfg.name, cfg.m)
+    A, Om, Omm, Phi = oracle_sample_inputs(cfg, rows)
     steps = max(1, min(args.steps, 3))
-    warm = max(3, args.warmup)
-    base = oracle_baseline(cfg, steps=steps, budget_s=120.0, warmup=warm)
+    warm = max(1, min(args.warmup, 3))
+    base = time_oracle(A, cfg, plan, Om, Omm, Phi, steps, warm, budget_s=120.0)
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "GB/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": warm, "ms_per_step": base["step_s"] * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: fp64 {cfg.m}x{cfg.n} Haar-spectrum matrix, k={cfg.k}, p={cfg.p}, "
-                                   f"l2={cfg.l2}; step = subspace v=3 + block Krylov v=4 + single pass (8 views)"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} ({cfg.m}x{cfg.n} {cfg.dtype}, k={cfg.k}, p={cfg.p}, l2={cfg.l2}); "
+                                   f"step = {plan_name(plan)}; bounded row sample {rows} x {cfg.n}"},
             "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def run_e2e(args, cfg, A, Om, Phi, step, barrier, flush, stream, dev, max_over_ranks, world, m, n, bytes_step_rank):
-    """End to end through the public API on a stream of host matrices, the way a PyTorch user
-    pipelines it: every step's inputs (A, Omega, Phi) are copied from pinned host memory into one
-    of two device buffer sets on a copy stream, overlapped with the previous step's three calls on
-    the other set; every output (U, S, V of each call) is copied back into pinned host memory.
-    The timed region spans all K steps (first copy to last output copy); ms_per_step = total / K.
-    Byte counts come from the copied tensors."""
-    import torch
-    Ah = A.cpu().pin_memory()
-    Omh = Om.t().contiguous().cpu().pin_memory().t()
-    Phih = Phi.t().contiguous().cpu().pin_memory().t()
-    bufs = [(A, Om, Phi), (torch.empty_like(A), Om.clone(), Phi.clone())]
-    copy_stream = torch.cuda.Stream(dev)
-    host_outs = None
-
-    def run(K):
-        nonlocal host_outs
-        ready = [torch.cuda.Event(), torch.cuda.Event()]
-        free = [torch.cuda.Event(), torch.cuda.Event()]
-
-        def upload(k):
-            Ad, Omd, Phid = bufs[k % 2]
-            with torch.cuda.stream(copy_stream):
-                if k >= 2:
-                    copy_stream.wait_event(free[k % 2])     # step k-2 has finished with this set
-                Ad.copy_(Ah, non_blocking=True)
-                Omd.copy_(Omh, non_blocking=True)
-                Phid.copy_(Phih, non_blocking=True)
-                ready[k % 2].record(copy_stream)
-
-        upload(0)
-        outs = None
-        for k in range(K):
-            if k + 1 < K:
-                upload(k + 1)
-            stream.wait_event(ready[k % 2])
-            Ad, Omd, Phid = bufs[k % 2]
-            outs = []
-            step(Ax=Ad, Omx=Omd, Phix=Phid, outs=outs)
-            free[k % 2].record(stream)
-            if host_outs is None:
-                host_outs = [[torch.empty_like(t, device="cpu").pin_memory() for t in o] for o in outs]
-            for ho, o in zip(host_outs, outs):
-                for h, t in zip(ho, o):
-                    h.copy_(t, non_blocking=True)
-        return outs
-
-    run(2)
-    torch.cuda.synchronize(dev)
-    K = max(2, args.e2e_steps)
-    flush.zero_()
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    copy_stream.wait_stream(stream)
-    outs = run(K)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    e2e_step_ms = max_over_ranks(e0.elapsed_time(e1) / K)
-    h2d = sum(t.numel() * t.element_size() for t in (Ah, Omh, Phih))
-    d2h = sum(t.numel() * t.element_size() for o in outs for t in o)
-    e2e = {"value": world * bytes_step_rank / (e2e_step_ms * 1e-3) / 1e9, "unit": "GB/s",
-           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step_ms, "steps": K,
-           "how": "stream of K host matrices: pinned-host -> device copy of A, Omega, Phi per step on a copy "
-                  "stream, double-buffered so it overlaps the previous step's three API calls; "
-                  "device -> pinned-host copy of every U, S, V; ms_per_step = (first copy .. last output) / K"}
-    return e2e
-
-
-def fp64_large_secondary(ctx, dev, dmma_peak, reps=3):
-    """The fp64 DMMA view kernels at a size where the per-launch fixed cost is amortised: a
-    50000 x 40000 fp64 A (16 GB, a C4-like row block) at w = 30 (C2's width) and w = 120 (C4's);
-    device time of the view kernels (RSVD_PROFILE events), fraction of the measured DMMA peak."""
-    import torch
-    from paper_1804_07531_b200 import rsvd
-
-    m, n = 50000, 40000
-    A = torch.empty(m, n, dtype=torch.float64, device=dev)
-    for r0 in range(0, m, 8192):
-        A[r0:r0 + 8192].normal_()
-    out = {"workload": "fp64 50000x40000 (16 GB), views A*X and A^T*Y at w = 30 and 120",
-           "dmma_peak_tflops": dmma_peak}
-    for w in (30, 120):
-        for trans in (0, 1):
-            X = torch.randn(w, m if trans else n, dtype=torch.float64, device=dev).t()
-            ctx.view(A, X, trans=bool(trans), flags=rsvd.RSVD_PROFILE)
-            ts = []
-            for _ in range(reps):
-                _, info = ctx.view(A, X, trans=bool(trans), flags=rsvd.RSVD_PROFILE)
-                ts.append(info.view_ms)
-            t = statistics.median(ts)
-            tf = 2.0 * m * n * w / t / 1e9
-            out[f"{'aty' if trans else 'ax'}_w{w}"] = {"ms": t, "tflops": tf,
-                                                       "frac_tensor": tf / dmma_peak if dmma_peak else None,
-                                                       "hbm_gbs": m * n * 8 / t / 1e6}
-            del X
-    del A
-    torch.cuda.empty_cache()
-    return out
-
-
-def c5_secondary(ctx, dev, reps=3):
-    """C5-shaped fp32 views (tcgen05 kind::tf32, 3xTF32) on a 100000 x 100000 fp32 A (40 GB),
-    w = l = 250: device time of the view kernels (RSVD_PROFILE events), roofline against the
-    tf32 tensor peak (measured bf16 burst x nominal tf32/bf16 ratio) at 3x the flops."""
-    import torch
-    from paper_1804_07531_b200 import rsvd
-
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    bf16 = peaks.get("bf16_tflops", 1590.0)
-    tf32_peak = bf16 * 1.1 / 2.25
-    m = n = 100000
-    w = 250
-    A = torch.empty(m, n, dtype=torch.float32, device=dev)
-    for r0 in range(0, m, 8192):
-        A[r0:r0 + 8192].normal_()
-    out = {"workload": "C5 fp32 100000x100000, views A*X and A^T*Y at w = k+p = 250",
-           "tf32_peak_tflops": tf32_peak,
-           "tf32_peak_source": f"MEASURED_PEAKS bf16 burst {bf16:.1f} TF x nominal tf32/bf16 1.1/2.25"}
-    for trans in (0, 1):
-        X = torch.randn(w, m if trans else n, dtype=torch.float32, device=dev).t()
-        ctx.view(A, X, trans=bool(trans), flags=rsvd.RSVD_PROFILE)
-        ts = []
-        for _ in range(reps):
-            _, info = ctx.view(A, X, trans=bool(trans), flags=rsvd.RSVD_PROFILE)
-            ts.append(info.view_ms)
-        t = statistics.median(ts)
-        fl = 2.0 * m * n * w
-        out["aty" if trans else "ax"] = {"ms": t, "tflops_3xtf32": 3 * fl / t / 1e9,
-                                         "frac_tensor": 3 * fl / t / 1e9 / tf32_peak,
-                                         "hbm_gbs": m * n * 4 / t / 1e6}
-        del X
-    Om = torch.randn(250, n, dtype=torch.float32, device=dev).t()
-    ctx.subspace(A, 200, 50, 2, Om)
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    ctx.subspace(A, 200, 50, 2, Om)
-    e1.record()
-    torch.cuda.synchronize(dev)
-    out["subspace_v2_k200_p50_ms"] = e0.elapsed_time(e1)
-    del A
-    torch.cuda.empty_cache()
-    return out
-
-
 # ------------------------------------------------------------------ our arm
+def call(ctx, alg, v, inp, fl, A, Om, Omm, Phi, cfg, m, row0, host_out=False):
+    if alg == "subspace":
+        return ctx.subspace(A, cfg.k, cfg.p, v, Omm if inp else Om, input=inp, flags=fl, m=m, row0=row0,
+                            host_out=host_out)
+    if alg == "krylov":
+        return ctx.block_krylov(A, cfg.k, cfg.p, v, Omm if inp else Om, input=inp, flags=fl, m=m, row0=row0,
+                                host_out=host_out)
+    return ctx.single_pass(A, cfg.k, cfg.p, cfg.l2, Om, Phi, flags=fl, m=m, row0=row0, host_out=host_out)
+
+
+def view_roofline(infos_per_call, peak_tf, alt_peak_tf, dtype):
+    """Dominant kernels = the view kernels: algorithmic flops per launch / average launch duration
+    (CUDA events on the ctx stream around every view launch, RSVD_PROFILE)."""
+    vms = sum(i.view_ms for i in infos_per_call)
+    vfl = sum(i.view_flops for i in infos_per_call)
+    vby = sum(i.view_bytes for i in infos_per_call)
+    n = sum(i.view_launches for i in infos_per_call)
+    tot = sum(i.total_ms for i in infos_per_call)
+    mult = 3.0 if dtype == "f32" else 1.0       # 3xTF32 executes three tensor products per flop
+    ach = mult * vfl / (vms * 1e-3) / 1e12 if vms > 0 else None
+    out = {"bound": "tensor", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
+           "frac": ach / peak_tf if ach and peak_tf else None,
+           "view_launches": n, "avg_view_ms": vms / max(n, 1),
+           "flops_per_launch": vfl / max(n, 1), "bytes_per_launch": vby / max(n, 1),
+           "hbm_gbs_during_views": vby / (vms * 1e-3) / 1e9 if vms > 0 else None,
+           "view_share_of_calls": vms / tot if tot > 0 else None}
+    if alt_peak_tf:
+        out["peak_alt"] = alt_peak_tf
+        out["frac_alt"] = ach / alt_peak_tf if ach else None
+    if dtype == "f32" and ach:
+        out["achieved_1x_flops"] = ach / 3.0
+        out["frac_strict_1x"] = ach / 3.0 / peak_tf if peak_tf else None
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -314,7 +233,7 @@ def main():
     import torch.distributed as dist
 
     from paper_1804_07531_b200 import rsvd
-    from paper_1804_07531_b200.sharding import broadcast_uid, max_over_ranks as _mor, weak_scaled
+    from paper_1804_07531_b200.sharding import broadcast_uid, max_over_ranks as _mor, shard_rows
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -322,76 +241,51 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=dev)
     cfg = S.CONFIGS[args.config]
-    # the step's three SVD calls are independent: one context (own stream, own communicator)
-    # per call, enqueued with RSVD_ASYNC and run concurrently; `ctx` (the first) also serves the
-    # sequential per-algorithm timings
-    # the first context keeps torch's current stream (ordered with the inputs' producers)
-    # the block Krylov call is the step's critical path (the longest dependent chain of kernels):
-    # its stream gets the highest priority so that its blocks are scheduled first whenever the
-    # concurrent calls compete for SMs; the other two calls fill the gaps
-    streams = [torch.cuda.current_stream(dev)] + [
-        torch.cuda.Stream(dev, priority=(-5 if alg == "krylov" else 0)) for alg, _ in STEP_PLAN[1:]]
+    plan = PLANS[args.config]
+    esz = cfg.itemsize
+    peaks_file = measured_peaks()
+
+    # ---- inputs: the whole matrix, row-sharded over the ranks (strong scaling, 128-row aligned)
+    m, n = cfg.m, cfg.n
+    sh = shard_rows(m, world, rank, align=128)
+    A = S.make_matrix_torch(cfg, dev, row0=sh.row0, rows=sh.m_local)
+    Om = S.gaussian_test_matrix_torch(n, cfg.l, cfg, S.ROLE_OMEGA, dev)                       # replicated
+    Omm_full = S.gaussian_test_matrix_torch(m, cfg.l, cfg, S.ROLE_OMEGA_M, dev)
+    Omm = Omm_full[sh.row0:sh.row0 + sh.m_local]                                            # A^T input: shard
+    Phi_full = S.gaussian_test_matrix_torch(m, cfg.l2, cfg, S.ROLE_PHI, dev)
+    Phi = Phi_full[sh.row0:sh.row0 + sh.m_local]
+    torch.cuda.synchronize(dev)
+
+    concurrent = world == 1 and not args.sequential
+    if concurrent:
+        streams = [torch.cuda.current_stream(dev)] + [torch.cuda.Stream(dev) for _ in plan[1:]]
+    else:
+        streams = [torch.cuda.current_stream(dev)]
     ctxs = [rsvd.Context(local, stream=s_) for s_ in streams]
     ctx = ctxs[0]
-    # Optional SM budget of the two calls off the critical path (rsvd_set_sm_limit), so that their
-    # persistent view kernels leave SMs to the Krylov chain.  It paid while that chain was longer
-    # (1.31-1.33 -> 1.29 ms per step with 64); with the current kernels it no longer does (mean of
-    # 4 runs: no limit 1.111 ms, 64 SMs 1.125, 48: 1.176, 80: 1.131, 96: 1.147), so the default is
-    # off.  RSVD_BENCH_SIDE_SMS=<n> re-enables it for A/B runs.
-    side_sms = int(os.environ.get("RSVD_BENCH_SIDE_SMS", "0"))
-
-    def limit_side(on):
-        # only around the concurrent step; every sequential measurement (per-algorithm SVD times,
-        # view profiling, peak probe, secondaries) runs with the full GPU
-        if side_sms > 0:
-            for (alg, _), c_ in zip(STEP_PLAN, ctxs):
-                if alg != "krylov":
-                    c_.set_sm_limit(side_sms if on else 1 << 20)
-
-    limit_side(True)
     if world > 1:
-        for c_ in ctxs:
-            uid = broadcast_uid(rsvd.get_unique_id() if rank == 0 else None, rank)
-            c_.comm_init(world, rank, uid)
+        uid = broadcast_uid(rsvd.get_unique_id() if rank == 0 else None, rank)
+        ctx.comm_init(world, rank, uid)             # ONE communicator per rank; calls in a fixed order
 
-    # ---- inputs: rank r holds rows [r*m, (r+1)*m) of A_global = [U_1;..;U_N] diag(sigma) V^T / sqrt(N)
-    m, n = cfg.m, cfg.n
-    A = S.make_matrix_torch(cfg, dev, m, n, seed_offset=rank)
-    if world > 1:
-        A.mul_(1.0 / np.sqrt(world))
-    Om = S.gaussian_test_matrix_torch(n, cfg.l, cfg, S.ROLE_OMEGA, dev)          # replicated
-    Phi = S.gaussian_test_matrix_torch(m, cfg.l2, cfg, S.ROLE_PHI, dev, seed_offset=rank)
-    shard = weak_scaled(m, world, rank)
-    M_glob, row0 = shard.m, shard.row0
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)     # 256 MiB > L2 (126 MB)
-    stream = torch.cuda.current_stream(dev)
-
-    def step(flags=0, Ax=A, Omx=Om, Phix=Phi, host_out=False, outs=None):
-        concurrent = not (flags & rsvd.RSVD_PROFILE)
+    def step(flags=0):
         cur = torch.cuda.current_stream(dev)
         infos = []
-        outs = [] if outs is None else outs
-        for (alg, v), c_, s_ in zip(STEP_PLAN, ctxs, streams):
-            c = c_ if concurrent else ctx
-            fl = flags | (rsvd.RSVD_ASYNC if concurrent else 0)
-            if concurrent and s_ != cur:
-                s_.wait_stream(cur)   # after the L2 flush / start event on the current stream
-            if alg == "subspace":
-                r = c.subspace(Ax, cfg.k, cfg.p, v, Omx, flags=fl, m=M_glob, row0=row0, host_out=host_out)
-            elif alg == "krylov":
-                r = c.block_krylov(Ax, cfg.k, cfg.p, v, Omx, flags=fl, m=M_glob, row0=row0, host_out=host_out)
-            else:
-                r = c.single_pass(Ax, cfg.k, cfg.p, cfg.l2, Omx, Phix, flags=fl, m=M_glob, row0=row0,
-                                  host_out=host_out)
+        conc = concurrent and not (flags & rsvd.RSVD_PROFILE)
+        for i, (alg, v, inp, fl) in enumerate(plan):
+            c = ctxs[i] if conc else ctx
+            s_ = streams[i] if conc else cur
+            if conc and s_ != cur:
+                s_.wait_stream(cur)
+            r = call(c, alg, v, inp, fl | flags | (rsvd.RSVD_ASYNC if conc else 0), A, Om, Omm, Phi, cfg, m, sh.row0)
             infos.append(r[3])
-            outs.append(r[:3])
-        if concurrent:
-            for c_, s_, inf in zip(ctxs, streams, infos):
-                c_.wait(inf)
+        if conc:
+            for c, s_, inf in zip(ctxs, streams, infos):
+                c.wait(inf)
                 if s_ != cur:
-                    cur.wait_stream(s_)   # the end event follows all three calls
+                    cur.wait_stream(s_)
         return infos
 
     def barrier():
@@ -403,127 +297,208 @@ def main():
     def max_over_ranks(x):
         return _mor(x, device=dev)
 
-    # ---- warm-up (also captures the CUDA graphs)
+    stream = torch.cuda.current_stream(dev)
     for _ in range(max(3, args.warmup)):
         step()
     barrier()
 
-    # ---- timed region: device events per step, L2 flushed before each step (outside the events)
+    # ---- timed region: CUDA events on the launching stream, A >> L2 (no flush needed)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
-        # keep the GPU busy (untimed steps) while nvidia-smi starts sampling, so that the samples
-        # bracket the timed region under load
         t_busy = time.perf_counter()
-        while time.perf_counter() - t_busy < 1.0:
+        while time.perf_counter() - t_busy < 0.5:        # samples start under load
             step()
             torch.cuda.synchronize(dev)
         barrier()
         for i in range(args.steps):
-            flush.zero_()
             evs[i][0].record(stream)
             infos = step()
             evs[i][1].record(stream)
         barrier()
-        t_busy = time.perf_counter()
-        while time.perf_counter() - t_busy < 0.4:      # a few more samples under load
-            step()
-            torch.cuda.synchronize(dev)
-    limit_side(False)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = max_over_ranks(sum(step_ms))
     ms_per_step = total_ms / args.steps
-    bytes_step_rank = step_views() * m * n * 8
-    value = world * bytes_step_rank * args.steps / (total_ms * 1e-3) / 1e9
+    a_bytes = m * n * esz                                   # the whole matrix (all ranks)
+    bytes_step = plan_views(plan) * a_bytes
+    value = bytes_step * args.steps / (total_ms * 1e-3) / 1e9
     launches_per_step = sum(inf.kernel_launches for inf in infos)
 
-    # ---- per-algorithm SVD time (graph replay, device events, L2 flushed)
-    alg_ms = {}
-    for idx, (alg, v) in enumerate(STEP_PLAN):
+    # ---- per-call SVD time (sequential, graph replay, device events)
+    svd_ms = {}
+    for alg, v, inp, fl in plan:
         ts = []
-        for _ in range(max(3, args.steps // 2)):
-            flush.zero_()
+        for _ in range(3):
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            if alg == "subspace":
-                ctx.subspace(A, cfg.k, cfg.p, v, Om, m=M_glob, row0=row0)
-            elif alg == "krylov":
-                ctx.block_krylov(A, cfg.k, cfg.p, v, Om, m=M_glob, row0=row0)
-            else:
-                ctx.single_pass(A, cfg.k, cfg.p, cfg.l2, Om, Phi, m=M_glob, row0=row0)
+            call(ctx, alg, v, inp, fl, A, Om, Omm, Phi, cfg, m, sh.row0)
             e1.record(stream)
             torch.cuda.synchronize(dev)
             ts.append(e0.elapsed_time(e1))
-        alg_ms[f"{alg}_v{v}"] = max_over_ranks(statistics.median(ts))
-
-    # ---- view-kernel durations (RSVD_PROFILE: events around every view kernel, same stream)
-    vms, vfl, vby, vcount, tot = 0.0, 0.0, 0.0, 0, 0.0
+        key = f"{alg}_v{v}" + ("_AT" if inp else "") + ("_sq" if fl & SQUARED else "")
+        svd_ms[key] = max_over_ranks(statistics.median(ts))
+    # ---- view-kernel durations (RSVD_PROFILE: events around every view kernel on the ctx stream)
+    prof = []
     for _ in range(args.profile_steps):
-        flush.zero_()
         barrier()
-        for inf in step(flags=rsvd.RSVD_PROFILE):
-            vms += inf.view_ms
-            vfl += inf.view_flops
-            vby += inf.view_bytes
-            vcount += inf.view_launches
-            tot += inf.total_ms
-    peaks = {}
+        prof += step(flags=rsvd.RSVD_PROFILE)
     try:
         t_dmma, g_read = ctx.probe_peaks()
-        peaks = {"dmma_fp64_tflops": t_dmma, "hbm_read_gbs": g_read}
+        probed = {"dmma_fp64_tflops": t_dmma, "hbm_read_gbs": g_read}
     except Exception as e:  # pragma: no cover
-        peaks = {"error": str(e)}
-    achieved_tf = vfl / (vms * 1e-3) / 1e12 if vms > 0 else None
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
+        probed = {"error": str(e)}
+    bf16 = peaks_file.get("bf16_tflops")
+    if cfg.dtype == "f64":
+        peak = probed.get("dmma_fp64_tflops")
+        alt = bf16 * DMMA_NOMINAL_TF / BF16_NOMINAL_TF if bf16 else None
+        roof = view_roofline(prof, peak, alt, "f64")
+        roof["kernel"] = "view kernels k_view_ax / k_view_aty / k_view_fused (FP64 DMMA m8n8k4, TMA-fed)"
+        roof["peak_source"] = ("FP64 DMMA throughput measured on this GPU by rsvd_probe_peaks (mma.sync m8n8k4, "
+                               "all SMs); peak_alt = MEASURED_PEAKS bf16 burst x nominal fp64/bf16 40/2250")
+    else:
+        peak = bf16 * TF32_NOMINAL_TF / BF16_NOMINAL_TF if bf16 else None
+        roof = view_roofline(prof, peak, None, "f32")
+        roof["kernel"] = "k_view_tf32 (tcgen05 kind::tf32, 3xTF32, TMEM accumulators)"
+        roof["peak_source"] = "MEASURED_PEAKS bf16 burst x nominal tf32/bf16 1100/2250"
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")
+    roof["traffic"] = None
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(cfg.name)
+            roof["traffic"] = json.load(open(tpath)).get(cfg.name)
+            roof["traffic_source"] = "profiles/ncu_traffic_r02.json (ncu dram__bytes_read.sum + write.sum per launch)"
         except Exception:
-            traffic = None
-    roofline = {"bound": "tensor", "kernel": "view kernels (k_view_ax / k_view_aty / k_view_fused), FP64 DMMA",
-                "achieved": achieved_tf, "peak": peaks.get("dmma_fp64_tflops"), "unit": "TFLOP/s",
-                "frac": (achieved_tf / peaks["dmma_fp64_tflops"]) if achieved_tf and peaks.get("dmma_fp64_tflops") else None,
-                "traffic": traffic,
-                "peak_source": "measured on this GPU by rsvd_probe_peaks (FP64 DMMA m8n8k4, all SMs); "
-                               "nominal-ratio alternative 1652.7 TF bf16 x 40/2250 = 29.4 TF",
-                "view_share_of_step": (vms / tot) if tot > 0 else None,
-                "hbm_gbs_during_views": (vby / (vms * 1e-3) / 1e9) if vms > 0 else None,
-                "hbm_read_peak_gbs": peaks.get("hbm_read_gbs"),
-                "avg_view_ms": vms / max(vcount, 1)}
+            pass
+    view_roof_ms = {}
+    for alg, v, inp, fl in plan:
+        vb = v * a_bytes
+        key = f"{alg}_v{v}" + ("_AT" if inp else "") + ("_sq" if fl & SQUARED else "")
+        w = cfg.l + (cfg.l2 if alg == "single_pass" else 0)
+        nvec = (v * cfg.l if alg == "subspace" else (v + v // 2 - 1) * cfg.l if alg == "krylov" else w)
+        flops = 2.0 * m * n * nvec * (3.0 if cfg.dtype == "f32" else 1.0)
+        t_roof = max(vb / (peaks_file.get("hbm_gbs", 6456.8) * 1e9), flops / ((peak or 1) * 1e12)) * 1e3
+        view_roof_ms[key] = {"roofline_ms": t_roof, "frac_of_view_roofline": t_roof / svd_ms[key]}
 
-    # ---- e2e: pinned host buffers through the C ABI, copies inside the timed region
-    if args.no_e2e:
-        e2e = None
-    else:
-        limit_side(True)
-        e2e = run_e2e(args, cfg, A, Om, Phi, step, barrier, flush, stream, dev, max_over_ranks, world, m, n,
-                      bytes_step_rank)
-        limit_side(False)
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: fp64 {m * world}x{n} (row block {m}x{n} per GPU), Haar factors, "
-                                   f"sigma_i=1 (i<=20) then 10^(-0.25(i-20)); k={cfg.k}, p={cfg.p}, l2={cfg.l2}; "
-                                   "step = subspace v=3 + block Krylov v=4 + single pass (8 views of A), "
-                                   "the three independent calls concurrent on three streams (RSVD_ASYNC)",
-                       "l2_flush": "256 MiB write before every timed step (outside the events)",
-                       "parallelism": f"row-sharded A over {world} GPU(s), NCCL all-reduce" if world > 1 else "1 GPU"},
-            "views_per_s": world * step_views() * args.steps / (total_ms * 1e-3) / world,
-            "svd_ms": alg_ms, "roofline": roofline, "peaks_measured": peaks, "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary()}
-    if rank == 0 and world == 1 and not args.no_secondary:
-        line["secondary_fp64_large"] = fp64_large_secondary(ctx, dev, peaks.get("dmma_fp64_tflops"))
-        line["secondary_c5_fp32"] = c5_secondary(ctx, dev)
+            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
+            "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.dtype} {m}x{n} ({a_bytes / 1e9:.0f} GB) "
+                                   f"{'X diag(i^-1.5) Y^T rank 500 + 1e-8 G' if cfg.name == 'C4' else cfg.kind}, "
+                                   f"k={cfg.k}, p={cfg.p}, l2={cfg.l2}; step = {plan_name(plan)} "
+                                   f"({plan_views(plan)} views of A)",
+                       "l2_flush": "none needed: A is larger than L2 and every view streams it from HBM",
+                       "calls": "concurrent on %d streams (RSVD_ASYNC)" % len(plan) if concurrent else "sequential",
+                       "parallelism": (f"A row-sharded over {world} GPUs (128-row aligned), NCCL all-reduce; the "
+                                       f"same matrix at every N (strong scaling)") if world > 1 else "1 GPU"},
+            "views_per_s": plan_views(plan) * args.steps / (total_ms * 1e-3),
+            "svd_ms": svd_ms, "view_roofline_per_call": view_roof_ms, "roofline": roof, "peaks_probed": probed,
+            "gpu_launches": launches_per_step * args.steps}
+
+    # ---- CPU oracle on a bounded row sample of the same bytes (rank 0, N = 1)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        base = oracle_baseline(cfg, steps=1, budget_s=30.0)
+        rows = SAMPLE_ROWS.get(cfg.name, m)
+        As = A[:rows].double().cpu().numpy()
+        base = time_oracle(As, cfg, plan, Om.double().cpu().numpy(), Omm_full[:rows].double().cpu().numpy(),
+                           Phi_full[:rows].double().cpu().numpy(), steps=1, warmup=0, budget_s=30.0)
         line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        del As
+
+    # ---- e2e: the same step through the C ABI with HOST buffers (pinned), copies inside the timed
+    # region: every call stages A (and Omega / Phi) host -> device itself and returns U, S, V to host
+    for c_ in ctxs[1:]:
+        c_.close()
+    if not args.no_e2e:
+        Ah = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
+        Ah.copy_(A)
+        Omh = Om.t().contiguous().cpu().pin_memory().t()
+        Ommh = Omm.t().contiguous().cpu().pin_memory().t()
+        Phih = Phi.t().contiguous().cpu().pin_memory().t()
+        del A, Omm_full, Phi_full
+        ctx.close()
+        torch.cuda.empty_cache()
+        ctx = rsvd.Context(local)
+        if world > 1:
+            uid = broadcast_uid(rsvd.get_unique_id() if rank == 0 else None, rank)
+            ctx.comm_init(world, rank, uid)
+
+        def e2e_step():
+            outs = []
+            for alg, v, inp, fl in plan:
+                outs.append(call(ctx, alg, v, inp, fl, Ah, Omh, Ommh, Phih, cfg, m, sh.row0, host_out=True))
+            return outs
+
+        e2e_step()                                       # warm-up (graph capture, workspace)
+        barrier()
+        K = max(2, args.e2e_steps)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(K):
+            outs = e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / K)
+        h2d = sum(Ah.numel() * esz + (Ommh if inp else Omh).numel() * esz + (Phih.numel() * esz if alg == "single_pass" else 0)
+                  for alg, v, inp, fl in plan)
+        d2h = sum(t.numel() * t.element_size() for o in outs for t in o[:3] if t is not None)
+        line["e2e"] = {"value": bytes_step / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": K,
+                       "how": "the step's calls through the C ABI with pinned HOST A / Omega / Phi and host U, S, V: "
+                              "each call stages A (80 GB for C4) host -> device in its own workspace and returns "
+                              "U, S, V to host; synchronous calls, CUDA events around K steps; bound by the host "
+                              "link (one A transfer per call)"}
+        del Ah
+    ctx.close()
+    torch.cuda.empty_cache()
+
+    if rank == 0 and world == 1 and not args.no_secondary and cfg.name == "C4":
+        line["secondary_c5"] = secondary(rsvd, torch, dev, "C5", peaks_file)
+        line["secondary_c2"] = secondary(rsvd, torch, dev, "C2", peaks_file, reps=10)
+    line["clocks"] = clk.summary()
     if rank == 0:
         print(json.dumps(line), flush=True)
-    for c_ in ctxs:
-        c_.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def secondary(rsvd, torch, dev, name, peaks_file, reps=3):
+    """Per-call SVD times of another config (sequential, graph replay, device events) and its view
+    kernels' roofline fraction (RSVD_PROFILE)."""
+    cfg = S.CONFIGS[name]
+    A = S.make_matrix_torch(cfg, dev)
+    Om = S.gaussian_test_matrix_torch(cfg.n, cfg.l, cfg, S.ROLE_OMEGA, dev)
+    Phi = S.gaussian_test_matrix_torch(cfg.m, cfg.l2, cfg, S.ROLE_PHI, dev)
+    torch.cuda.synchronize(dev)
+    ctx = rsvd.Context(dev.index)
+    runs = {"C5": [("subspace", 2), ("subspace", 3), ("krylov", 3), ("krylov", 4)],
+            "C2": [("subspace", 3), ("krylov", 4), ("single_pass", 1)]}[name]
+    out = {"workload": f"{name}: {cfg.dtype} {cfg.m}x{cfg.n}, k={cfg.k}, p={cfg.p}", "svd_ms": {}}
+    stream = torch.cuda.current_stream(dev)
+    prof = []
+    bf16 = peaks_file.get("bf16_tflops")
+    for alg, v in runs:
+        call(ctx, alg, v, 0, 0, A, Om, None, Phi, cfg, cfg.m, 0)
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            call(ctx, alg, v, 0, 0, A, Om, None, Phi, cfg, cfg.m, 0)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ts.append(e0.elapsed_time(e1))
+        out["svd_ms"][f"{alg}_v{v}"] = statistics.median(ts)
+        prof.append(call(ctx, alg, v, 0, rsvd.RSVD_PROFILE, A, Om, None, Phi, cfg, cfg.m, 0)[3])
+    if cfg.dtype == "f32":
+        peak = bf16 * TF32_NOMINAL_TF / BF16_NOMINAL_TF if bf16 else None
+        out["roofline"] = view_roofline(prof, peak, None, "f32")
+        out["roofline"]["peak_source"] = "MEASURED_PEAKS bf16 burst x nominal tf32/bf16 1100/2250"
+    else:
+        t, _ = ctx.probe_peaks()
+        out["roofline"] = view_roofline(prof, t, None, "f64")
+    ctx.close()
+    del A
+    torch.cuda.empty_cache()
+    return out
 
 
 if __name__ == "__main__":

@@ -43,9 +43,12 @@
  *   round trip between views (the whole algorithm is one CUDA graph launch after the first call
  *   with a given signature).  With RSVD_ASYNC a call only enqueues; rsvd_wait completes it.
  * MULTI-GPU.  After rsvd_comm_init every algorithm call is a collective over the ranks: A is
- *   row-sharded (rank r holds rows [row0, row0 + m_local)); U is returned row-sharded like A;
- *   S and V are replicated and bitwise identical on all ranks.  Gram matrices and the partial
- *   co-range views A^T Y are summed with NCCL all-reduce.
+ *   row-sharded (rank r holds rows [row0, row0 + m_local), the shards tiling [0, m) in rank
+ *   order); U is returned row-sharded like A; S and V are replicated and bitwise identical on
+ *   all ranks.  Gram matrices and the partial co-range views A^T Y are summed with NCCL
+ *   all-reduce.  A call waits for its collectives by polling ncclCommGetAsyncError: an
+ *   asynchronous NCCL error, or no completion within RSVD_COMM_TIMEOUT_S seconds (environment,
+ *   default 600), aborts the communicator and returns RSVD_E_NCCL (the ctx then needs a new one).
  * DETERMINISM.  Bitwise run-to-run reproducible for fixed inputs, rank count and SM budget
  *   (rsvd_set_sm_limit changes the reduction splits, i.e. the rounding), except the
  *   single-pass Y_c accumulation when the deterministic partial buffers would exceed the memory
@@ -98,7 +101,6 @@ enum {
 #define RSVD_LC_MINVAR    (-2) /* rsvd_single_pass lc: minimum-variance l_c          */
 #define RSVD_EXT_BWZ      0    /* rsvd_single_pass_extended: Eq. (bwz)               */
 #define RSVD_EXT_BWZ2     1    /* rsvd_single_pass_extended: Eq. (bwzimproved)       */
-#define RSVD_SIM_SHARDS_SHIFT 8 /* debug: bits 8..15 = number of virtual row shards (loopback) */
 
 typedef struct {
   int32_t dtype;          /* RSVD_F64 or RSVD_F32                                         */
@@ -130,7 +132,13 @@ typedef struct {
 } rsvd_info;
 
 /* ---- context ------------------------------------------------------------------------------- */
-int  rsvd_create(rsvd_ctx** ctx, int cuda_device, void* cuda_stream /* NULL: private stream */);
+/* cuda_stream: the stream every call of this ctx is enqueued on.  NULL: the ctx creates its own
+ * BLOCKING stream (cudaStreamDefault flags), which is ordered in both directions with the legacy
+ * default stream (handle 0), so work queued there before a call (e.g. a PyTorch producer on the
+ * default stream) completes before the call starts, and default-stream work queued after the
+ * call waits for it.  A non-NULL stream is used as is: ordering against other streams is then
+ * the caller's responsibility. */
+int  rsvd_create(rsvd_ctx** ctx, int cuda_device, void* cuda_stream);
 int  rsvd_destroy(rsvd_ctx* ctx);
 const char* rsvd_strerror(int code);
 const char* rsvd_last_error(const rsvd_ctx* ctx);
@@ -163,6 +171,20 @@ int  rsvd_get_unique_id(void* id128);                  /* rank 0: fills 128 byte
  * A^T Y partials, NCCL inside the CUDA graph) on a single GPU.  RSVD_E_STATE if already set. */
 int  rsvd_comm_init(rsvd_ctx* ctx, int nranks, int rank, const void* id128);
 int  rsvd_comm_nranks(const rsvd_ctx* ctx);
+/* Loopback communicator: N virtual row shards of one A on ONE GPU (tests of the sharded path
+ * without N GPUs).  rsvd_loop_create makes a group of 1 <= nranks <= 16 virtual ranks
+ * (timeout_s <= 0: 120 s); each of N contexts joins it with rsvd_comm_init_loopback(ctx, loop, r)
+ * and is then driven by ITS OWN host thread (every rank must make the same sequence of calls
+ * with the same scalars, as with NCCL).  A collective is a host barrier of the N threads plus
+ * cross-stream event waits, and sums the ranks' buffers in rank order 0..N-1 (identical bits on
+ * every rank); no kernel waits on another kernel.  Loopback calls enqueue directly (no CUDA
+ * graph).  A rank whose call fails aborts the group: peers blocked in a collective return
+ * RSVD_E_NCCL (also after timeout_s without all ranks arriving).  rsvd_loop_destroy may be called
+ * once every ctx has joined; the group lives until its last ctx is destroyed. */
+typedef struct rsvd_loop rsvd_loop;
+int  rsvd_loop_create(int nranks, double timeout_s, rsvd_loop** loop);
+int  rsvd_loop_destroy(rsvd_loop* loop);
+int  rsvd_comm_init_loopback(rsvd_ctx* ctx, rsvd_loop* loop, int rank);
 
 /* ---- algorithms ----------------------------------------------------------------------------- */
 /* Alg. 2.  k >= 1, p >= 0, l = k + p <= min(m, n), v >= 2.

@@ -37,7 +37,7 @@ __all__ = [
     "one_view_minvar", "one_view_extended", "plan_extended", "pinv",
     "row_stream_qb",
     "gen_block_krylov", "normal_matrix_tevd", "nystrom_tevd", "pinched_tevd", "recommend_input", "svd_of",
-    "views_and_vectors", "rel_frobenius_error", "rel_spectral_error", "projector_distance",
+    "views_and_vectors", "PanelOp", "rel_frobenius_error", "rel_spectral_error", "projector_distance",
     "residual_fro", "half_power_lhs_rhs", "thm_bound",
     "GOAL_SVD", "GOAL_LEFT", "GOAL_RIGHT", "GOAL_NORMAL",
 ]
@@ -165,6 +165,54 @@ class _Op:
         self.views += 1
         self.vectors += Y.shape[1]
         return (self.A @ Y) if self.T else (self.A.T @ Y)
+
+
+class PanelOp(_Op):
+    """The same operator as _Op, with every view evaluated one row panel of A at a time
+    ("views as BLAS A[panel] @ X / A[panel].T @ Y over row panels", so that an
+    80 GB A never has to be held in fp64 at once).  ``A`` is any row-sliceable array (ndarray or
+    memmap) of any float dtype; each panel is upcast to fp64 on its own.
+
+        (A X)[panel]  = A[panel] X                      (rows are independent: same numbers as _Op)
+        A^* Y         = sum over panels, in row order, of A[panel]^* Y[panel]
+
+    Only the summation order of A^* Y differs from the dense product (the definition of the view,
+    P:100); the algorithms above are unchanged."""
+
+    def __init__(self, A, transpose=False, panel_rows=4096):
+        self.A = A
+        self.T = bool(transpose)
+        self.views = 0
+        self.vectors = 0
+        self.panel_rows = int(panel_rows)
+
+    def _rows(self, X):                           # A X
+        X = _f64(X)
+        m = self.A.shape[0]
+        Y = np.empty((m, X.shape[1]))
+        for r0 in range(0, m, self.panel_rows):
+            r1 = min(m, r0 + self.panel_rows)
+            Y[r0:r1] = _f64(self.A[r0:r1]) @ X
+        return Y
+
+    def _cols(self, Y):                           # A^* Y
+        Y = _f64(Y)
+        m, n = self.A.shape
+        Z = np.zeros((n, Y.shape[1]))
+        for r0 in range(0, m, self.panel_rows):
+            r1 = min(m, r0 + self.panel_rows)
+            Z += _f64(self.A[r0:r1]).T @ Y[r0:r1]
+        return Z
+
+    def apply(self, X):
+        self.views += 1
+        self.vectors += X.shape[1]
+        return self._cols(X) if self.T else self._rows(X)
+
+    def adjoint(self, Y):
+        self.views += 1
+        self.vectors += Y.shape[1]
+        return self._rows(Y) if self.T else self._cols(Y)
 
 
 # ============================================================ Algorithm 1 (P:81-98)
@@ -530,11 +578,12 @@ def recommend_input(goal, v):
     return 0
 
 
-def svd_of(A, algorithm, k, p, v=None, Omega=None, l2=None, lc=None, Phi=None, transpose=False):
+def svd_of(A, algorithm, k, p, v=None, Omega=None, l2=None, lc=None, Phi=None, transpose=False, panel_rows=None):
     """Run an algorithm on A (transpose=False) or on A^* (transpose=True) and return the TSVD
     of A itself: (U, sigma, V) with A ~ U diag(sigma) V^T.  When the algorithm ran on A^*, its
-    (U, V) are A's (V, U) (reading R6)."""
-    op = _Op(A, transpose)
+    (U, V) are A's (V, U) (reading R6).  panel_rows: evaluate every view over
+    row panels of that many rows (PanelOp; for matrices too large to upcast at once)."""
+    op = _Op(A, transpose) if panel_rows is None else PanelOp(A, transpose, panel_rows)
     if algorithm == "subspace":
         U, s, V = gen_subspace_iteration(None, k, p, v, Omega, _op=op)
     elif algorithm == "krylov":

@@ -10,6 +10,7 @@
 //   panel:      R12 = R11^-T G12 (one thread per trailing column)
 //   update:     G22 -= R12^T R12 on the upper triangle (4x4 register tiles)
 // then R^-1 by blocked back substitution, bottom block row first.
+#include <atomic>
 #include "common.cuh"
 #include "internal.h"
 
@@ -241,7 +242,7 @@ int launch_chol_big(const double* G, const double* ref, int w, double tol, doubl
                     DevStatus* status, cudaStream_t st, double shift_coef) {
   if (w < 1 || w > kMaxW) return RSVD_E_ARG;
   const size_t smem = (size_t)(kNB * kMaxW + 2 * kNB * 33 + kMaxW) * 8 + kMaxW * 4;
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_chol_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;

@@ -13,6 +13,7 @@
 // Deterministic: fixed pairing and summation order, independent of timing.
 // Outputs as the other Jacobi kernels: sigma_j = |W_j| sorted descending, Ul = W_j / sigma_j,
 // Vr = J (want_j, rotations accumulated in global memory) or Vr = B^T Ul S^-1.
+#include <atomic>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -267,7 +268,7 @@ int launch_jacobi_cluster(const double* M, int64_t ldm, int trans, int r, int c,
   double* sval = J + (int64_t)kMaxC * kMaxC;
   int* flags = reinterpret_cast<int*>(sval + 2 * kMaxC);
   const size_t smem = (size_t)2 * b * r * 8;
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_jacobi_cluster<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16 * kMaxC * 8);
     cudaFuncSetAttribute(k_jacobi_cluster<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -11,6 +11,7 @@
 // with 0/0 = 1 and a/0 = inf (reading R20) -> an int in device memory.
 // k_mask_cols: zero the columns j >= k + l_c of Q_c and C, so that the rest of Alg. 7 runs at
 // the fixed width l with exact zero trailing columns (same result as truncating to k + l_c).
+#include <atomic>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -178,7 +179,7 @@ int launch_minvar_trials(const double* Z, int l2, int l, const double* Rhi, int 
   if (l > kMaxW32 || k < 1 || p < 0 || l2 < l) return RSVD_E_ARG;
   const size_t bytes = (size_t)l2 * l * 8;
   const int use_smem = bytes <= 200 * 1024 ? 1 : 0;
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_minvar_trials, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;

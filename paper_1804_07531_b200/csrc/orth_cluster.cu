@@ -16,6 +16,7 @@
 // columns of Y are zero and the padding block of G is set to the identity, so they factor
 // trivially, never count as deficient and never mix with the real columns.
 // Deterministic (fixed summation orders).
+#include <atomic>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -539,7 +540,7 @@ int launch_w(double* Y, int64_t ldy, int64_t rows, int w, int shifted, double sh
   rpc = (rpc + 15) / 16 * 16;  // gram_tiles steps 16 rows at a time without a bounds predicate
   if (rpc > oc_rows_max(W)) return RSVD_E_ARG;
   const size_t smem = (size_t)(oc_fixed(W) + rpc * oc_ld(W)) * 8;
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_orth_cluster<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
     cudaFuncSetAttribute(k_orth_cluster<W>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "internal.h"
 
 namespace rsvd {
@@ -40,50 +41,13 @@ int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo
 
 using namespace rsvd;
 
-// ================================================================ NCCL (dlopen)
-namespace {
-typedef int nccl_res_t;
-typedef void* nccl_comm_t;
-struct nccl_uid_t { char internal[128]; };
-typedef nccl_res_t (*pf_get_uid)(nccl_uid_t*);
-typedef nccl_res_t (*pf_init_rank)(nccl_comm_t*, int, nccl_uid_t, int);
-typedef nccl_res_t (*pf_allreduce)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t);
-typedef nccl_res_t (*pf_destroy)(nccl_comm_t);
-typedef const char* (*pf_errstr)(nccl_res_t);
-struct NcclApi {
-  void* h = nullptr;
-  pf_get_uid get_uid = nullptr;
-  pf_init_rank init_rank = nullptr;
-  pf_allreduce allreduce = nullptr;
-  pf_destroy destroy = nullptr;
-  pf_errstr errstr = nullptr;
-  bool load() {
-    if (h) return true;
-    const char* names[] = {"libnccl.so.2", "libnccl.so"};
-    for (const char* nm : names) {
-      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
-      if (h) break;
-    }
-    if (!h) return false;
-    get_uid = (pf_get_uid)dlsym(h, "ncclGetUniqueId");
-    init_rank = (pf_init_rank)dlsym(h, "ncclCommInitRank");
-    allreduce = (pf_allreduce)dlsym(h, "ncclAllReduce");
-    destroy = (pf_destroy)dlsym(h, "ncclCommDestroy");
-    errstr = (pf_errstr)dlsym(h, "ncclGetErrorString");
-    return get_uid && init_rank && allreduce && destroy;
-  }
-};
-NcclApi g_nccl;
-constexpr int kNcclFloat64 = 8, kNcclSum = 0;
-}  // namespace
-
 // ================================================================ context
 struct rsvd_ctx {
   int device = 0;
   int sms = 148;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  nccl_comm_t comm = nullptr;
+  Comm* comm = nullptr;        // rsvd_comm_init (NCCL) or rsvd_comm_init_loopback; null: single GPU
   int nranks = 1, rank = 0;
   char* arena = nullptr;
   size_t arena_size = 0;
@@ -164,6 +128,9 @@ struct Call {
   int64_t ldxr = 0;
   const void* Xc = nullptr;
   int64_t ldxc = 0;
+  // info fields known at enqueue time (also what rsvd_wait reports for RSVD_ASYNC calls)
+  int info_views = 0, info_lc = 0;
+  int64_t info_vectors = 0;
   // resolved kinds
   PtrKind kA = PTR_NULL, kOm = PTR_NULL, kPhi = PTR_NULL, kU = PTR_NULL, kS = PTR_NULL, kV = PTR_NULL,
           kR = PTR_NULL, kXr = PTR_NULL, kXc = PTR_NULL;
@@ -192,6 +159,7 @@ struct Exec {
   const float* A32 = nullptr;   // dtype == RSVD_F32: A itself (every internal block stays fp64)
   int dtype = RSVD_F64;
   int64_t lda = 0, m = 0, n = 0;
+  int64_t m_glob = 0;   // global row count of A (m = this rank's rows)
   // host-transfer plan (executed outside the graph); esz = element bytes (8, or 4 for fp32)
   struct H2D { void* dst; int64_t ldd; const void* src; int64_t lds; int64_t rows; int64_t cols; int esz = 8; };
   struct D2H { void* dst; int64_t ldd; const void* src; int64_t lds; int64_t rows; int64_t cols; int esz = 8; };
@@ -243,10 +211,11 @@ struct Exec {
 
   void allreduce(double* p, int64_t count) {
     if (!live()) return;
-    nccl_res_t r = g_nccl.allreduce(p, p, (size_t)count, kNcclFloat64, kNcclSum, ctx->comm, st);
-    if (r != 0) {
-      set_err(ctx, "ncclAllReduce failed: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
-      chk(RSVD_E_NCCL);
+    std::string e;
+    const int r = ctx->comm->allreduce(p, (size_t)count, st, &e);
+    if (r != RSVD_OK) {
+      set_err(ctx, "%s", e.c_str());
+      chk(r);
     }
   }
   void ev_record(int* idx) {
@@ -454,7 +423,8 @@ struct Exec {
       double* R0 = alloc((int64_t)w * w);
       R0s = R0;
       double* R0i = alloc((int64_t)w * w);
-      const double rows_all = (double)(s == SIDE_M ? m * ctx->nranks : Y.rows);
+      // the shift must be identical on every rank: the GLOBAL row count of a sharded side
+      const double rows_all = (double)(sharded(s) ? m_glob : Y.rows);
       const double coef = 11.0 * (rows_all * w + (double)w * (w + 1)) * 1.1102230246251565e-16;
       cross(s, Y, Y, G);
       if (live()) chk(launch_chol_ref(G, nullptr, w, 0.0, R0, R0i, nullptr, st, coef));
@@ -1307,10 +1277,12 @@ void run_alg(Exec& E) {
 std::string call_key(const Call& c, const Exec& E, const rsvd_ctx* ctx) {
   char buf[1024];
   snprintf(buf, sizeof buf,
-           "a%d k%d p%d v%d in%d l2%d lc%d t%d w%d r%lld c%d f%u A%p m%lld n%lld lda%lld U%d S%d V%d R%d ar%p nr%d "
+           "a%d k%d p%d v%d in%d l2%d lc%d t%d w%d r%lld c%d f%u dt%d A%p m%lld n%lld lda%lld U%d S%d V%d R%d ar%p nr%d "
            "s%d x%d sm%d",
-           c.alg, c.k, c.p, c.v, c.input, c.l2, c.lc, c.trans, c.w, (long long)c.rows, c.cols, c.flags,
-           (const void*)E.A, (long long)E.m, (long long)E.n, (long long)E.lda, c.kU != PTR_NULL, c.kS != PTR_NULL,
+           c.alg, c.k, c.p, c.v, c.input, c.l2, c.lc, c.trans, c.w, (long long)c.rows, c.cols, c.flags, E.dtype,
+           // the captured graph reads A in place: the device A (fp64 or fp32) is part of the key
+           E.dtype == RSVD_F32 ? (const void*)E.A32 : (const void*)E.A, (long long)E.m, (long long)E.n,
+           (long long)E.lda, c.kU != PTR_NULL, c.kS != PTR_NULL,
            c.kV != PTR_NULL, c.kR != PTR_NULL, (void*)ctx->arena, ctx->nranks + (ctx->comm ? 1000 : 0), c.s,
            c.variant, ctx->sms);
   return std::string(buf);
@@ -1320,6 +1292,7 @@ std::string call_key(const Call& c, const Exec& E, const rsvd_ctx* ctx) {
 void bind_A(Exec& E, const Call& call) {
   if (!call.A) return;
   E.m = call.A->m_local;
+  E.m_glob = call.A->m;
   E.n = call.A->n;
   E.lda = call.A->lda;
   E.dtype = call.A->dtype;
@@ -1343,7 +1316,38 @@ void bind_A(Exec& E, const Call& call) {
   }
 }
 
+// Wait for the ctx stream.  With a communicator: its wait (NCCL polls ncclCommGetAsyncError and
+// aborts after RSVD_COMM_TIMEOUT_S seconds, default 600, instead of hanging on a dead peer).
+int wait_stream(rsvd_ctx* ctx) {
+  std::string e;
+  int r;
+  if (ctx->comm) {
+    static const double timeout_s = [] {
+      const char* v = getenv("RSVD_COMM_TIMEOUT_S");
+      return v ? atof(v) : 600.0;
+    }();
+    r = ctx->comm->wait(ctx->stream, timeout_s, &e);
+  } else {
+    cudaError_t se = cudaStreamSynchronize(ctx->stream);
+    r = se == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+    if (r) e = std::string("CUDA error: ") + cudaGetErrorString(se);
+  }
+  if (r) set_err(ctx, "%s", e.c_str());
+  return r;
+}
+
+int execute_impl(rsvd_ctx* ctx, Call& call, rsvd_info* info);
+
+// A rank whose call fails before its collectives complete would leave its peers blocked in them:
+// abort the communicator (loopback: release the peers' host barriers; NCCL: ncclCommAbort).
+// Numerical failures are detected after the whole call completed and leave the comm intact.
 int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
+  const int r = execute_impl(ctx, call, info);
+  if (r != RSVD_OK && r != RSVD_E_NUMERIC && ctx->comm) ctx->comm->abort();
+  return r;
+}
+
+int execute_impl(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
   if (info) memset(info, 0, sizeof(*info));
   cudaSetDevice(ctx->device);
   call.kA = call.A ? ptr_kind(call.A->data, ctx->device) : PTR_NULL;
@@ -1394,7 +1398,8 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
   E.profile = profile;
   bind_A(E, call);
   cudaStream_t st = ctx->stream;
-  const bool use_graph = !(call.flags & RSVD_NO_GRAPH) && !profile;
+  // the loopback communicator synchronises ranks on the host: not capturable, enqueue directly
+  const bool use_graph = !(call.flags & RSVD_NO_GRAPH) && !profile && (!ctx->comm || ctx->comm->graph_ok());
   const std::string key = call_key(call, E, ctx);
   auto it = use_graph ? ctx->graphs.find(key) : ctx->graphs.end();
   const bool replay = use_graph && it != ctx->graphs.end();
@@ -1493,6 +1498,9 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
   base_info.view_bytes = sz.view_bytes;
   base_info.view_flops = sz.view_flops;
   base_info.nondeterministic = sz.nondet;
+  base_info.views = call.info_views;
+  base_info.vectors = call.info_vectors;
+  base_info.lc_used = call.info_lc;
   if ((call.flags & RSVD_ASYNC) && rc == RSVD_OK) {
     // enqueued only: rsvd_wait synchronises the stream and completes the info
     ctx->pending = true;
@@ -1500,10 +1508,9 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
     if (info) *info = base_info;
     return RSVD_OK;
   }
-  cudaError_t se = cudaStreamSynchronize(st);
-  if (se != cudaSuccess) {
-    set_err(ctx, "CUDA error: %s", cudaGetErrorString(se));
-    return RSVD_E_CUDA;
+  {
+    const int wr = wait_stream(ctx);
+    if (wr != RSVD_OK) return wr;
   }
   if (rc != RSVD_OK) {
     cudaError_t le = cudaGetLastError();
@@ -1517,6 +1524,7 @@ int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
     info->status = st0;
     info->rank_deficient_cols = hs.deficient;
     info->jacobi_sweeps = hs.jacobi_sweeps;
+    if (call.info_lc == RSVD_LC_MINVAR) info->lc_used = hs.minvar_lc;
     if (profile && !E.ev_pairs.empty()) {
       double vm = 0;
       for (size_t i = 1; i < E.ev_pairs.size(); ++i) {
@@ -1613,7 +1621,10 @@ int rsvd_create(rsvd_ctx** out, int device, void* stream) {
   if (stream) {
     c->stream = static_cast<cudaStream_t>(stream);
   } else {
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    // a BLOCKING stream: it is ordered with the legacy default stream (handle 0, torch's default)
+    // in both directions, so the work a caller queued there before the call (inputs produced,
+    // buffers reused by a caching allocator) completes first, and later default-stream work waits
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamDefault) != cudaSuccess) {
       delete c;
       return RSVD_E_CUDA;
     }
@@ -1639,7 +1650,7 @@ int rsvd_destroy(rsvd_ctx* c) {
   if (c->dstat) cudaFree(c->dstat);
   if (c->counter) cudaFree(c->counter);
   if (c->hstat) cudaFreeHost(c->hstat);
-  if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
+  delete c->comm;
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return RSVD_OK;
@@ -1660,21 +1671,16 @@ int rsvd_wait(rsvd_ctx* c, rsvd_info* info) {
   if (!c->pending) return RSVD_OK;
   cudaSetDevice(c->device);
   c->pending = false;
-  cudaError_t se = cudaStreamSynchronize(c->stream);
-  if (se != cudaSuccess) {
-    set_err(c, "CUDA error: %s", cudaGetErrorString(se));
-    if (info) info->status = RSVD_E_CUDA;
-    return RSVD_E_CUDA;
+  const int wr = wait_stream(c);
+  if (wr != RSVD_OK) {
+    if (info) info->status = wr;
+    return wr;
   }
   const DevStatus hs = *c->hstat;
   if (info) {
-    const int32_t views = info->views;
-    const int64_t vectors = info->vectors;
-    const int32_t lc = info->lc_used;
+    // everything known at enqueue time comes from the ctx (the caller's struct may be fresh)
     *info = c->pending_info;
-    info->views = views;
-    info->vectors = vectors;
-    info->lc_used = (lc == RSVD_LC_MINVAR) ? hs.minvar_lc : lc;
+    if (info->lc_used == RSVD_LC_MINVAR) info->lc_used = hs.minvar_lc;
     info->rank_deficient_cols = hs.deficient;
     info->jacobi_sweeps = hs.jacobi_sweeps;
     info->status = RSVD_OK;
@@ -1695,35 +1701,63 @@ int rsvd_probe_peaks(rsvd_ctx* c, double* dmma_tflops, double* read_gbs) {
 
 int rsvd_get_unique_id(void* id128) {
   if (!id128) return RSVD_E_ARG;
-  if (!g_nccl.load()) return RSVD_E_NCCL;
-  nccl_uid_t uid;
-  if (g_nccl.get_uid(&uid) != 0) return RSVD_E_NCCL;
-  memcpy(id128, &uid, 128);
-  return RSVD_OK;
+  return nccl_unique_id(id128);
+}
+
+static void install_comm(rsvd_ctx* c, Comm* comm) {
+  c->comm = comm;
+  c->nranks = comm->nranks;
+  c->rank = comm->rank;
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  c->graphs.clear();
+  c->graph_kernels.clear();
 }
 
 int rsvd_comm_init(rsvd_ctx* c, int nranks, int rank, const void* id128) {
   if (!c || nranks < 1 || rank < 0 || rank >= nranks || !id128) return RSVD_E_ARG;
   if (c->comm) return RSVD_E_STATE;
   // nranks == 1 also creates a (1-rank) communicator: the sharded code path then runs on one GPU
-  if (!g_nccl.load()) {
-    set_err(c, "libnccl.so.2 not loadable");
-    return RSVD_E_NCCL;
-  }
   cudaSetDevice(c->device);
-  nccl_uid_t uid;
-  memcpy(&uid, id128, 128);
-  nccl_comm_t comm = nullptr;
-  nccl_res_t r = g_nccl.init_rank(&comm, nranks, uid, rank);
-  if (r != 0) {
-    set_err(c, "ncclCommInitRank failed: %s", g_nccl.errstr ? g_nccl.errstr(r) : "?");
+  std::string e;
+  Comm* comm = nccl_comm_create(nranks, rank, id128, &e);
+  if (!comm) {
+    set_err(c, "%s", e.c_str());
     return RSVD_E_NCCL;
   }
-  c->comm = comm;
-  c->nranks = nranks;
-  c->rank = rank;
-  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
-  c->graphs.clear();
+  install_comm(c, comm);
+  return RSVD_OK;
+}
+
+struct rsvd_loop {
+  LoopGroup* g;
+};
+
+int rsvd_loop_create(int nranks, double timeout_s, rsvd_loop** out) {
+  if (!out) return RSVD_E_ARG;
+  *out = nullptr;
+  LoopGroup* g = loop_group_create(nranks, timeout_s);
+  if (!g) return RSVD_E_ARG;
+  *out = new rsvd_loop{g};
+  return RSVD_OK;
+}
+
+int rsvd_loop_destroy(rsvd_loop* lp) {
+  if (!lp) return RSVD_OK;
+  loop_group_release(lp->g);
+  delete lp;
+  return RSVD_OK;
+}
+
+int rsvd_comm_init_loopback(rsvd_ctx* c, rsvd_loop* lp, int rank) {
+  if (!c || !lp) return RSVD_E_ARG;
+  if (c->comm) return RSVD_E_STATE;
+  std::string e;
+  Comm* comm = loop_comm_create(lp->g, rank, c->device, &e);
+  if (!comm) {
+    set_err(c, "%s", e.c_str());
+    return RSVD_E_ARG;
+  }
+  install_comm(c, comm);
   return RSVD_OK;
 }
 
@@ -1743,9 +1777,6 @@ static int algo_entry(int alg, rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, i
       if (ld_omega < om_rows) { set_err(ctx, "ld_omega < rows of Omega"); r = RSVD_E_ARG; }
       if (U && ldu < A->m_local) { set_err(ctx, "ldu < m_local"); r = RSVD_E_ARG; }
       if (V && ldv < A->n) { set_err(ctx, "ldv < n"); r = RSVD_E_ARG; }
-      if (input == RSVD_INPUT_AT && ctx->nranks > 1 && alg == 1) {
-        // fine: sharded side handled by the same code path
-      }
       if (alg == 1 && r == RSVD_OK) {
         const int nb = (v % 2 == 0) ? v / 2 : (v - 1) / 2;
         const int64_t W = (int64_t)nb * l;
@@ -1779,13 +1810,10 @@ static int algo_entry(int alg, rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, i
   c.V = V;
   c.ldv = ldv;
   c.flags = flags;
+  c.info_views = v;
+  c.info_vectors = (alg == 0) ? (int64_t)v * (k + p) : (int64_t)(v + v / 2 - 1) * (k + p);
   r = execute(ctx, c, info);
-  if (info) {
-    info->status = r;
-    info->views = v;
-    const int l = k + p;
-    info->vectors = (alg == 0) ? (int64_t)v * l : (int64_t)(v + v / 2 - 1) * l;
-  }
+  if (info) info->status = r;
   return r;
 }
 
@@ -1836,15 +1864,11 @@ int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int
   c.V = V;
   c.ldv = ldv;
   c.flags = flags;
+  c.info_views = 1;
+  c.info_vectors = (int64_t)(k + p) + l2;
+  c.info_lc = lc;   // MinVar: replaced by the device's choice when the call completes
   r = execute(ctx, c, info);
-  if (info) {
-    info->status = r;
-    info->views = 1;
-    info->vectors = (int64_t)(k + p) + l2;
-    info->lc_used = lc;
-    // MinVar: the choice is made on the device (complete now unless the call is RSVD_ASYNC)
-    if (lc == RSVD_LC_MINVAR && r == RSVD_OK && !(flags & RSVD_ASYNC)) info->lc_used = ctx->hstat->minvar_lc;
-  }
+  if (info) info->status = r;
   return r;
 }
 
@@ -1892,12 +1916,10 @@ int rsvd_single_pass_extended(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, in
   c.V = V;
   c.ldv = ldv;
   c.flags = flags;
+  c.info_views = 1;
+  c.info_vectors = (int64_t)(k + p) + s + l2;   // A [Omega | Xi_c] and A^T Phi
   r = execute(ctx, c, info);
-  if (info) {
-    info->status = r;
-    info->views = 1;
-    info->vectors = (int64_t)(k + p) + s + l2;   // A [Omega | Xi_c] and A^T Phi
-  }
+  if (info) info->status = r;
   return r;
 }
 
@@ -1926,12 +1948,10 @@ int rsvd_row_stream(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, const void* 
   c.V = V;
   c.ldv = ldv;
   c.flags = flags;
+  c.info_views = 1;                                 // one pass over the rows
+  c.info_vectors = 2 * (int64_t)(k + p);
   r = execute(ctx, c, info);
-  if (info) {
-    info->status = r;
-    info->views = 1;                                 // one pass over the rows
-    info->vectors = 2 * (int64_t)(k + p);
-  }
+  if (info) info->status = r;
   return r;
 }
 
@@ -1987,12 +2007,10 @@ static int normal_entry(int alg, rsvd_ctx* ctx, const rsvd_mat* A, int k, int p,
   c.V = V;
   c.ldv = ldv;
   c.flags = flags;
+  c.info_views = v;
+  c.info_vectors = (int64_t)v * (k + p);
   r = execute(ctx, c, info);
-  if (info) {
-    info->status = r;
-    info->views = v;
-    info->vectors = (int64_t)v * (k + p);
-  }
+  if (info) info->status = r;
   return r;
 }
 

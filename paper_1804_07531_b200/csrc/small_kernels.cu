@@ -2,6 +2,7 @@
 //   slot sums (deterministic split-K reduction), Gram / cross products, guarded Cholesky with
 //   pseudo-inverse of R (CholeskyQR2 building block), tall-skinny x small GEMM, one-sided
 //   Jacobi SVD of the small core.  All fp64.
+#include <atomic>
 #include "common.cuh"
 #include "internal.h"
 
@@ -233,7 +234,7 @@ int launch_chol_ref(const double* G, const double* ref, int w, double tol, doubl
   if (w > kCholMaxW || w >= big_from) return launch_chol_big(G, ref, w, tol, R, Rinv, status, st, shift_coef);
   if (w < 1) return RSVD_E_ARG;
   const size_t smem = (size_t)w * w * 8 + (size_t)w * 4 + 16;
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholMaxW * kCholMaxW * 8 + kCholMaxW * 4 + 16);
     attr = true;
@@ -290,7 +291,7 @@ int launch_ts_gemm(const double* in, int64_t ldi, int64_t rows, int w, const dou
   if (w > 1024) return RSVD_E_ARG;
   dim3 grid((unsigned)((rows + 127) / 128), (unsigned)((c + kTsCC - 1) / kTsCC));
   const size_t smem = (size_t)w * kTsCC * 8;
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_ts_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * kTsCC * 8);
     attr = true;
@@ -713,7 +714,7 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
   want_j = want_j ? 1 : 0;
   const int ce = c + (c & 1);
   if (r <= 128 && !getenv_flag_jac("RSVD_JACOBI_OLD_MID")) {
-    static bool mattr = false;
+    static std::atomic<bool> mattr{false};
     if (!mattr) {
       cudaFuncSetAttribute(k_jacobi_mid<8, 16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       cudaFuncSetAttribute(k_jacobi_mid<8, 16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -743,7 +744,7 @@ int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, doubl
   int w_in = wbytes <= budget ? 1 : 0;
   int j_in = (w_in ? wbytes + jbytes : jbytes) <= budget ? 1 : 0;
   const size_t smem = (w_in ? wbytes : 0) + (j_in ? jbytes : 0);
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_jacobi<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
     cudaFuncSetAttribute(k_jacobi<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)budget);
@@ -1368,7 +1369,7 @@ int launch_cholqr_pass(const double* Yin, int64_t ldi, double* Yout, int64_t ldo
   const int G = cholqr_pass_ctas(rows);
   const int64_t rpc = (rows + G - 1) / G;
   const int smem = cholqr_smem_bytes(w);
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_cholqr_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
@@ -1602,7 +1603,7 @@ int launch_jacobi_small(const double* M, int64_t ldm, int trans, int r, int c, d
   const int ce = c + (c & 1);
   const double tol = 2.220446049250313e-16 * sqrt((double)r);
   const int smem = 2 * 64 * (64 + 4) * 8;  // W and J (or the staged input B), stride <= 68
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_jacobi_small<8, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k_jacobi_small<8, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -11,6 +11,7 @@
 // TMA; 8 consumer warps issue DMMA.  CTAs are persistent and walk "units" (a block of output
 // rows x a range of the reduction dimension); each unit writes its partial result to its own
 // slot so that the cross-unit sum is done later in a fixed order (bitwise deterministic).
+#include <atomic>
 #include "common.cuh"
 #include "internal.h"
 
@@ -608,7 +609,7 @@ int launch_ax_t(const ViewArgs& a, cudaStream_t st) {
   const int KT = (int)((a.n + kBK - 1) / kBK);
   const int U = RB * a.S;
   const int grid = std::min(U, a.grid_cap);
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_view_ax<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
@@ -628,7 +629,7 @@ int launch_aty_t(const ViewArgs& a, cudaStream_t st) {
   const int KT = (int)((a.rows + kBK - 1) / kBK);
   const int U = CB * a.S;
   const int grid = std::min(U, a.grid_cap);
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_view_aty<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
@@ -650,7 +651,7 @@ int launch_fused_t(const FusedArgs& a, cudaStream_t st) {
   const int KT = (int)((a.rows + kBK - 1) / kBK);
   const int U = NSB * a.S;
   const int grid = std::min(U, a.grid_cap);
-  static bool attr = false;
+  static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
     cudaFuncSetAttribute(k_view_fused<L2T, LTC>, cudaFuncAttributeMaxDynamicSharedMemorySize, FusedPlan<L2T, LTC>::SMEM);
     attr = true;

@@ -18,12 +18,14 @@
 //               smem descriptors and commits stage release / accumulator-ready to mbarriers
 // A x X: A tile is K-major (k contiguous).  A^T x Y: the A tile is read MN-major (the output
 // index, A's column, is the contiguous one) — tcgen05 accepts MN-major tf32 operands.
+#include <atomic>
 #include "common.cuh"
 #include "internal.h"
 
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace rsvd {
 namespace {
@@ -32,6 +34,13 @@ constexpr int kBK = 16;          // fp32 per 64-byte swizzled row = reduction el
 constexpr int kThreads = 192;    // 6 warps
 constexpr int kMaxStages = 8;
 constexpr int kSmemBudget = 200 * 1024;
+// Stages accumulated in one fp32 TMEM accumulator before it is drained into the fp64 partial
+// slot.  The tensor core's fp32 accumulation is not round-to-nearest: its error is biased toward
+// zero, so it grows with the number of accumulating MMAs (6 per stage).  Measured on the full C5
+// (100000^2, one accumulator over all 6250 stages): every singular value 2.1e-4 low, above the
+// fp32 parity tolerance 1e-4.  Chunks of kChunk stages bound the bias; the fp64 adds between
+// chunks round to nearest.
+constexpr int kChunkDefault = 256;   // RSVD_TF32_CHUNK=<stages> overrides (A/B experiments)
 
 __host__ __device__ constexpr int tmem_cols_for(int c) {
   return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
@@ -117,7 +126,7 @@ template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
     k_view_tf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
                 const __grid_constant__ CUtensorMap tmXl, double* __restrict__ out, int64_t ldo,
-                int64_t slot_stride, int out_rows, int w, int MT, int NB, int S, int KT, int KTS) {
+                int64_t slot_stride, int out_rows, int w, int MT, int NB, int S, int KT, int KTS, int kChunk) {
   Geo G;
   G.init(MT, w);
   const int WP = G.WP, NW = G.NW;
@@ -206,11 +215,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = blockIdx.x; u < U; u += gridDim.x) {
       const int s = u % S;
       const int kt0 = s * KTS, kt1 = min(KT, kt0 + KTS);
-      if (lane == 0) mbar_wait(tempty, tphase ^ 1);
-      tphase ^= 1;
-      __syncwarp();
-      tc_fence_after();
+      int kc0 = kt0;                         // first stage of the current accumulation chunk
       for (int kt = kt0; kt < kt1; ++kt) {
+        if (kt == kc0) {                     // a new chunk: TMEM must have been drained
+          if (lane == 0) mbar_wait(tempty, tphase ^ 1);
+          tphase ^= 1;
+          __syncwarp();
+          tc_fence_after();
+        }
+        const bool chunk_end = (kt == kt1 - 1) || (kt - kc0 == kChunk - 1);
         if (lane == 0) {
           mbar_wait(&conv[stage], phase);
           tc_fence_after();
@@ -226,16 +239,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t dxh = sdesc(xh + c * NW * 64 + ks * 32, 16, 512, 4);
                 const uint64_t dxl = sdesc(xl + c * NW * 64 + ks * 32, 16, 512, 4);
                 const uint32_t d = tbase + (uint32_t)(t * WP + c * NW);
-                mma_tf32(d, dah, dxh, id, (kt > kt0 || ks > 0) ? 1u : 0u);
+                mma_tf32(d, dah, dxh, id, (kt > kc0 || ks > 0) ? 1u : 0u);
                 mma_tf32(d, dah, dxl, id, 1u);
                 mma_tf32(d, dal, dxh, id, 1u);
               }
             }
           }
           mma_commit(&empty[stage]);
-          if (kt == kt1 - 1) mma_commit(tfull);
+          if (chunk_end) mma_commit(tfull);
         }
         __syncwarp();
+        if (chunk_end) kc0 = kt + 1;
         if (++stage == G.stages) { stage = 0; phase ^= 1; }
       }
     }
@@ -248,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = blockIdx.x; u < U; u += gridDim.x) {
       const int blk = u / S, s = u % S;
       const int kt0 = s * KTS, kt1 = min(KT, kt0 + KTS);
+      int kc0 = kt0;
       for (int kt = kt0; kt < kt1; ++kt) {
         mbar_wait(&full[stage], phase);
         uint8_t* st = smem + stage * G.stage_bytes;
@@ -268,28 +283,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[stage]);
         if (++stage == G.stages) { stage = 0; phase ^= 1; }
-      }
-      // epilogue: TMEM lane = output row inside the 128-row tile, column = output column
-      mbar_wait(tfull, tphase);
-      tphase ^= 1;
-      tc_fence_after();
-      double* o = out + (int64_t)s * slot_stride;
-      for (int t = 0; t < MT; ++t) {
-        const int r = blk * BM + t * 128 + q * 32 + lane;
-        for (int c0 = 0; c0 < WP; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(t * WP + c0), v);
-          tmem_ld_wait();
-          if (r < out_rows) {
+        if (kt != kt1 - 1 && kt - kc0 != kChunk - 1) continue;
+        // end of an accumulation chunk: drain TMEM (lane = output row inside the 128-row tile,
+        // column = output column) into the fp64 partial slot — stored by the unit's first chunk,
+        // added (fp64, round to nearest, fixed order) by the later ones
+        const bool first = (kc0 == kt0);
+        kc0 = kt + 1;
+        mbar_wait(tfull, tphase);
+        tphase ^= 1;
+        tc_fence_after();
+        double* o = out + (int64_t)s * slot_stride;
+        for (int t = 0; t < MT; ++t) {
+          const int r = blk * BM + t * 128 + q * 32 + lane;
+          for (int c0 = 0; c0 < WP; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(t * WP + c0), v);
+            tmem_ld_wait();
+            if (r < out_rows) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (c0 + j < w) o[(int64_t)(c0 + j) * ldo + r] = (double)__uint_as_float(v[j]);
+              for (int j = 0; j < 16; ++j)
+                if (c0 + j < w) {
+                  double* dst = &o[(int64_t)(c0 + j) * ldo + r];
+                  const double x = (double)__uint_as_float(v[j]);
+                  *dst = first ? x : *dst + x;
+                }
+            }
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
     }
   }
   tc_fence_before();
@@ -393,7 +417,12 @@ int launch_view_tf32(const ViewArgs32& a, cudaStream_t st) {
   const int U = NB * a.S;
   const int grid = std::min(U, a.grid_cap);
   const int smem = G.smem();
-  static bool attr[2] = {false, false};
+  static const int chunk = [] {
+    const char* e = getenv("RSVD_TF32_CHUNK");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : kChunkDefault;
+  }();
+  static std::atomic<bool> attr[2] = {{false}, {false}};
   if (!attr[ax ? 0 : 1]) {
     if (ax)
       cudaFuncSetAttribute(k_view_tf32<VIEW_AX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
@@ -403,10 +432,10 @@ int launch_view_tf32(const ViewArgs32& a, cudaStream_t st) {
   }
   if (ax)
     k_view_tf32<VIEW_AX><<<grid, kThreads, smem, st>>>(tmA, tmXh, tmXl, a.out, a.ldo, a.slot_stride, (int)out_rows,
-                                                        a.w, MT, NB, a.S, KT, a.KTS);
+                                                        a.w, MT, NB, a.S, KT, a.KTS, chunk);
   else
     k_view_tf32<VIEW_ATY><<<grid, kThreads, smem, st>>>(tmA, tmXh, tmXl, a.out, a.ldo, a.slot_stride, (int)out_rows,
-                                                         a.w, MT, NB, a.S, KT, a.KTS);
+                                                         a.w, MT, NB, a.S, KT, a.KTS, chunk);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 

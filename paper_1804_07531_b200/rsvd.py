@@ -31,7 +31,8 @@ EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_wait", "rsvd_strerror", "rsvd_la
            "rsvd_recommend_input", "rsvd_probe_peaks", "rsvd_get_unique_id", "rsvd_comm_init", "rsvd_comm_nranks", "rsvd_subspace",
            "rsvd_block_krylov", "rsvd_single_pass", "rsvd_nystrom", "rsvd_pinched", "rsvd_view", "rsvd_view_fused",
            "rsvd_orth", "rsvd_core_svd", "rsvd_plan", "rsvd_single_pass_extended",
-           "rsvd_row_stream", "rsvd_set_sm_limit"]
+           "rsvd_row_stream", "rsvd_set_sm_limit", "rsvd_loop_create", "rsvd_loop_destroy",
+           "rsvd_comm_init_loopback"]
 
 
 class RsvdMat(ctypes.Structure):
@@ -86,6 +87,9 @@ def lib():
     L.rsvd_probe_peaks.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
     L.rsvd_comm_init.argtypes = [vp, i32, i32, vp]
     L.rsvd_comm_nranks.argtypes = [vp]
+    L.rsvd_loop_create.argtypes = [i32, ctypes.c_double, ctypes.POINTER(vp)]
+    L.rsvd_loop_destroy.argtypes = [vp]
+    L.rsvd_comm_init_loopback.argtypes = [vp, vp, i32]
     alg = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_subspace.argtypes = alg
     L.rsvd_block_krylov.argtypes = alg
@@ -146,8 +150,39 @@ def _new_colmajor(rows, cols, like: torch.Tensor, pin=False):
     return torch.empty((cols, rows), dtype=like.dtype, pin_memory=pin).t()
 
 
+class LoopGroup:
+    """rsvd_loop: N virtual row shards of one A on one GPU (the sharded path without N GPUs).
+    Each member Context joins with ``ctx.comm_init_loopback(group, rank)`` and must be driven by
+    its own thread (every rank makes the same calls, as with NCCL)."""
+
+    def __init__(self, nranks: int, timeout_s: float = 120.0):
+        h = ctypes.c_void_p()
+        rc = lib().rsvd_loop_create(nranks, timeout_s, ctypes.byref(h))
+        if rc:
+            raise RsvdError(rc, "rsvd_loop_create: 1 <= nranks <= 16")
+        self._h = h
+        self.nranks = nranks
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().rsvd_loop_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
-    """One rsvd_ctx bound to a CUDA device and (by default) torch's current stream."""
+    """One rsvd_ctx bound to a CUDA device and a stream.
+
+    By default the stream is torch's current stream.  When that is the legacy default stream
+    (handle 0), the library creates its own BLOCKING stream, which the CUDA runtime orders with
+    the default stream in both directions (rsvd_create), so inputs produced on torch's default
+    stream are complete before a call starts and later default-stream work waits for the call.
+    With an explicit torch stream the caller orders it (``wait_stream``) against producers."""
 
     def __init__(self, device: int | None = None, stream: torch.cuda.Stream | None = None):
         L = lib()
@@ -197,6 +232,11 @@ class Context:
     def _check(self, rc, what):
         if rc:
             raise RsvdError(rc, f"{what}: {lib().rsvd_last_error(self._h).decode()}")
+
+    def comm_init_loopback(self, group: LoopGroup, rank: int):
+        """Join a loopback group as virtual rank `rank` (rsvd_comm_init_loopback)."""
+        self._check(lib().rsvd_comm_init_loopback(self._h, group._h, rank), "rsvd_comm_init_loopback")
+        self.nranks, self.rank = group.nranks, rank
 
     def comm_init(self, nranks: int, rank: int, uid: bytes):
         """Collective: all ranks pass the same 128-byte id (rank 0's get_unique_id())."""

@@ -237,22 +237,31 @@ def srft_matrix(n: int, s: int, seed: int) -> np.ndarray:
     return (d[:, None] * F)[:, cols]
 
 
+NOISE_PANEL = 2048   # rows per seeded noise panel of the device-built matrices
+
+
 def make_matrix_torch(cfg: Config, device, m: int | None = None, n: int | None = None,
-                      panel_rows: int = 4096, seed_offset: int = 0):
+                      panel_rows: int = NOISE_PANEL, seed_offset: int = 0, row0: int = 0, rows: int | None = None):
     """Same recipe as ``make_matrix`` built on a CUDA device with torch's Philox generator
     (for the multi-GB configs).  Haar factors use torch.linalg.qr of a Gaussian; this is input
-    construction, not the method.  Returns a row-major torch tensor of cfg's dtype."""
+    construction, not the method.  Returns a row-major torch tensor of cfg's dtype.
+
+    row0 / rows select a row block [row0, row0 + rows) of the m x n matrix (a rank's shard): the
+    noise is drawn in fixed panels of NOISE_PANEL rows, each from its own seed, and the factors are
+    built whole, so the block's bytes equal those rows of the full matrix for any sharding.
+    (panel_rows is accepted for compatibility; the noise panel grid is fixed.)"""
     import torch
 
     m = cfg.m if m is None else m
     n = cfg.n if n is None else n
+    rows = m - row0 if rows is None else rows
     tdt = torch.float64 if cfg.dtype == "f64" else torch.float32
     gen = torch.Generator(device=device)
     base = (SEED_BASE[0] * 1_000_003 + SEED_BASE[1]) * 101 + cfg.cid * 7 + seed_offset
 
-    def orth(rows, cols, role):
+    def orth(nrows, cols, role):
         gen.manual_seed(base * 13 + role)
-        g = torch.randn(rows, cols, generator=gen, device=device, dtype=torch.float64)
+        g = torch.randn(nrows, cols, generator=gen, device=device, dtype=torch.float64)
         q, r = torch.linalg.qr(g)
         s = torch.sign(torch.diagonal(r))
         s[s == 0] = 1.0
@@ -260,23 +269,23 @@ def make_matrix_torch(cfg: Config, device, m: int | None = None, n: int | None =
 
     if cfg.kind == "haar":
         N = min(m, n)
-        U = orth(m, N, ROLE_U)
+        U = orth(m, N, ROLE_U)[row0:row0 + rows]
         V = orth(n, N, ROLE_V)
         sig = torch.as_tensor(config_sigma(cfg, N), device=device)
-        A = ((U * sig) @ V.T).to(tdt).contiguous()
-        return A
+        return ((U * sig) @ V.T).to(tdt).contiguous()
     R = min(cfg.rank, m, n)
-    X = orth(m, R, ROLE_U)
+    Xs = orth(m, R, ROLE_U)[row0:row0 + rows] * torch.as_tensor(config_sigma(cfg, R), device=device)
     Y = orth(n, R, ROLE_V)
-    Xs = X * torch.as_tensor(config_sigma(cfg, R), device=device)
-    A = torch.empty(m, n, dtype=tdt, device=device)
-    gen.manual_seed(base * 13 + ROLE_NOISE)
-    for r0 in range(0, m, panel_rows):
-        r1 = min(m, r0 + panel_rows)
-        blk = Xs[r0:r1] @ Y.T
-        blk += cfg.noise * torch.randn(r1 - r0, n, generator=gen, device=device, dtype=torch.float64)
-        A[r0:r1] = blk.to(tdt)
-        del blk
+    A = torch.empty(rows, n, dtype=tdt, device=device)
+    P = NOISE_PANEL
+    for p0 in range((row0 // P) * P, row0 + rows, P):       # global noise panels overlapping the block
+        gen.manual_seed(base * 13 + ROLE_NOISE + 1_000_003 * (p0 // P + 1))
+        G = torch.randn(min(P, m - p0), n, generator=gen, device=device, dtype=torch.float64)
+        a0, a1 = max(p0, row0), min(p0 + P, row0 + rows, m)
+        blk = Xs[a0 - row0:a1 - row0] @ Y.T
+        blk += cfg.noise * G[a0 - p0:a1 - p0]
+        A[a0 - row0:a1 - row0] = blk.to(tdt)
+        del blk, G
     return A
 
 

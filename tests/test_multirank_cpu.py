@@ -1,12 +1,15 @@
 """Multi-rank (N > 1) host logic on CPU: world_size-2 gloo process groups on 127.0.0.1.
 
 * shard planning, unique-id broadcast and max-over-ranks timing (paper_1804_07531_b200.sharding);
-* the library's row-sharded schedule (include/rsvd.h MULTI-GPU) emulated in NumPy
-  with gloo all-reduces: A X local, A^T Y and every Gram / cross product of a row-sharded block
+* the row-sharded SCHEDULE (include/rsvd.h MULTI-GPU) as a NumPy emulation with
+  gloo all-reduces: A X local, A^T Y and every Gram / cross product of a row-sharded block
   all-reduced, column-side blocks replicated.  Each rank runs Alg. 2 / 9 / 7 / 8, the extended
   sketch and the row-wise single pass on its row block;
   the gathered result must equal the single-process oracle (the schedule is exact algebra, so the
   same 1e-10 / 1e-9 tolerances as GPU parity apply).
+  This checks the decomposition, not librsvd: the library's own sharded code path (unequal shards,
+  row0 > 0, the CholeskyQR3 shift from the global row count) runs on one GPU with N virtual
+  ranks in tests/test_gpu_loopback.py.
 """
 import os
 import socket
@@ -56,7 +59,7 @@ def test_shard_rows_errors():
 
 # ------------------------------------------------------------------ the sharded schedule (emulated)
 class ShardedOps:
-    """Row-sharded executor mirroring librsvd's Exec: side M (rows of A) is sharded, side N is
+    """NumPy emulation of the row-sharded schedule: side M (rows of A) is sharded, side N is
     replicated.  All reductions go through dist.all_reduce (sum)."""
 
     def __init__(self, A_local):

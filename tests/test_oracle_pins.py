@@ -703,3 +703,93 @@ def test_row_stream_exact_rank_and_single_row():
     a = rng.standard_normal((1, 40))                      # single-row matrix: rank-1 exact
     U, lam, V = O.row_stream_qb(a, 1, 0, rng.standard_normal((40, 1)))
     np.testing.assert_allclose(lam[0], np.linalg.norm(a), rtol=1e-13)
+
+
+# ------------------------------------------------------------------ Krylov-specific closed form
+
+@pytest.mark.parametrize("v", [4, 5])
+def test_krylov_recovers_rank_between_l_and_2l_exactly(v):
+    """Exact rank r with l < r <= 2l and distinct sigma.  Alg. 9 at v = 4 builds
+    K_c = [A Omega, (A A^*) A Omega] (2l columns), which spans range(A) for r <= 2l, so
+    the final view and tsvd return the top-k triplets EXACTLY; at v = 5 K_r = [A^*A Omega,
+    (A^*A)^2 Omega] spans the row space.  Alg. 2 at the same v keeps only l columns
+    (< r), so it does NOT recover them: the test fails if the Krylov blocks are assembled wrongly
+    (a missing raw last block, a block repeated, K taken on the wrong side)."""
+    m, n, k, p = 150, 110, 6, 4
+    l = k + p
+    r = 2 * l - 3                                     # l < r <= 2l
+    sig = 1.0 / np.arange(1, r + 1) ** 0.7             # distinct, slowly decaying
+    A = S.exact_rank_matrix(m, n, sig, seed=77)
+    X, Y = S.exact_rank_factors(m, n, r, seed=77)
+    Om = S.gaussian((n, l), 77, S.ROLE_OMEGA, v)
+    U, s, V = O.gen_block_krylov(A, k, p, v, Om)
+    np.testing.assert_allclose(s, sig[:k], rtol=1e-11)
+    assert proj(U, X[:, :k]) < 1e-10 and proj(V, Y[:, :k]) < 1e-10
+    Us, ss, Vs = O.gen_subspace_iteration(A, k, p, v, Om)
+    assert np.max(np.abs(ss - sig[:k]) / sig[:k]) > 1e-6      # Alg. 2: not exact at width l < r
+
+
+# ------------------------------------------------------------------ error metrics (P:988-1001)
+
+def test_relative_error_metrics_closed_form():
+    """P:993-1001 on A = diag(d) with a known tail: the best rank-p approximation gives 0 for both
+    metrics, and dropping the p-th direction gives the closed forms
+    Frobenius: sqrt(sum_{i>=p} d_i^2) / sqrt(sum_{i>p} d_i^2) - 1,  spectral: d_p / d_{p+1} - 1."""
+    d = np.array([5.0, 4.0, 3.0, 2.0, 1.5, 1.0, 0.5, 0.25])
+    A = np.diag(d)
+    p = 3
+    best = np.diag(np.where(np.arange(8) < p, d, 0.0))
+    assert abs(O.rel_frobenius_error(A, best, p)) < 1e-15
+    assert abs(O.rel_spectral_error(A, best, p)) < 1e-15
+    worse = np.diag(np.where(np.arange(8) < p - 1, d, 0.0))   # rank p-1
+    tail_p, tail_p1 = np.sqrt(np.sum(d[p - 1:] ** 2)), np.sqrt(np.sum(d[p:] ** 2))
+    assert abs(O.rel_frobenius_error(A, worse, p) - (tail_p / tail_p1 - 1.0)) < 1e-14
+    assert abs(O.rel_spectral_error(A, worse, p) - (d[p - 1] / d[p] - 1.0)) < 1e-14
+    # a rotated A has the same singular values: the metrics are unitarily invariant
+    Q1, Q2 = O.qr(S.gaussian((8, 8), 5, S.ROLE_MISC))[0], O.qr(S.gaussian((8, 8), 6, S.ROLE_MISC))[0]
+    assert abs(O.rel_frobenius_error(Q1 @ A @ Q2.T, Q1 @ worse @ Q2.T, p) - (tail_p / tail_p1 - 1.0)) < 1e-13
+
+
+def test_thm_bound_limits():
+    """Thm 3.1 / 4.1 right-hand side: it is never below the unavoidable
+    error sigma_{p+1} (Eckart-Young), it tends to sigma_{p+1} as the exponent grows (the
+    (.)^{1/e} root of a sum dominated by sigma_{p+1}^e), it is 0 for an exactly rank-p spectrum,
+    and it grows with the tail."""
+    sig = 1.0 / np.arange(1, 201) ** 1.0
+    p, l = 10, 10
+    for e in (1, 2, 3, 5, 9):
+        assert O.thm_bound(sig, p, l, e) >= sig[p]
+    assert abs(O.thm_bound(sig, p, l, 100) / sig[p] - 1.0) < 0.02   # (2 + ...)^(1/100) ~ 1.012
+    assert O.thm_bound(np.r_[sig[:p], np.zeros(50)], p, l, 3) == 0.0
+    heavier = sig.copy()
+    heavier[p + 5:] *= 2.0
+    assert O.thm_bound(heavier, p, l, 3) > O.thm_bound(sig, p, l, 3)
+
+
+# ------------------------------------------------------------------ row-panel views (SURVEY §8(c))
+
+@pytest.mark.parametrize("alg,v,tr", [("subspace", 3, False), ("krylov", 4, False), ("krylov", 5, True),
+                                      ("single_pass", 1, False)])
+@pytest.mark.parametrize("panel", [7, 64, 10_000])
+def test_panel_views_equal_dense_views(alg, v, tr, panel):
+    """PanelOp evaluates A X panel by panel (same rows, same numbers) and A^* Y as a sum over
+    panels: the algorithms' outputs equal the dense-operator oracle to rounding, and bitwise when
+    one panel covers A (the full-size C4 / C5 parity tests use panels of a copied-back A)."""
+    cfg = S.CONFIGS["C2"]
+    A = S.make_matrix(cfg, 300, 220)
+    m, n = A.shape
+    Om = S.gaussian_test_matrix(m if tr else n, cfg.l, cfg, S.ROLE_OMEGA_M if tr else S.ROLE_OMEGA)
+    Phi = S.gaussian_test_matrix(m, cfg.l2, cfg, S.ROLE_PHI)
+    a = O.svd_of(A, alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi, transpose=tr)
+    b = O.svd_of(A, alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi, transpose=tr, panel_rows=panel)
+    if panel >= m:
+        for x, y in zip(a[:3], b[:3]):
+            assert np.array_equal(x, y)
+    np.testing.assert_allclose(b[1], a[1], rtol=1e-13)
+    assert proj(b[0], a[0]) < 1e-12 and proj(b[2], a[2]) < 1e-12
+    assert b[3].views == a[3].views and b[3].vectors == a[3].vectors
+    # fp32 input: panels are upcast one by one, the same as upcasting A once
+    A32 = A.astype(np.float32)
+    c = O.svd_of(A32, alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi, transpose=tr, panel_rows=panel)
+    d = O.svd_of(A32.astype(np.float64), alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi, transpose=tr)
+    np.testing.assert_allclose(c[1], d[1], rtol=1e-13)
