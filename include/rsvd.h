@@ -11,6 +11,7 @@
  *                      minimum-variance l_c; Alg. 8 Woolfe variant
  *   rsvd_single_pass_extended  extended 1-view sketch, bwz / bwz2
  *   rsvd_row_stream    single pass over the rows of A
+ *   rsvd_block_krylov_rows  block Krylov with A^T A X from one row pass
  *   rsvd_nystrom, rsvd_pinched  normal-matrix TEVDs, Alg. 4 / Alg. 5
  *   rsvd_plan          single-pass oversampling plans (host only)
  *
@@ -231,6 +232,22 @@ int rsvd_single_pass(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int l2, int
  * and error rules as rsvd_subspace (Yhat_r is all-reduced over the row shards). */
 int rsvd_row_stream(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, const void* Omega, int64_t ld_omega,
                     void* U, int64_t ldu, void* S, void* V, int64_t ldv, unsigned flags, rsvd_info* info);
+
+/* Block Krylov method for a matrix read row wise: A^T A X is evaluated in ONE pass
+ * over A's rows (Y[i, :] = A[i, :] X, Z = sum_i A[i, :]^T Y[i, :], the row panels staying in L2
+ * between the two products), so Alg. 9's Krylov blocks need about half the reads of A.
+ *   v odd : K_r = [A^TA Omega, (A^TA)^2 Omega, ...] from (v-1)/2 row passes, Q_r = qr(K_r),
+ *           Q_c R_c = A Q_r, tsvd(R_c): (v-1)/2 + 1 reads of A (Alg. 9: v views).
+ *   v even: the same passes also give the range blocks: K_c = [A Omega, A Q^1, ...], Q_c = qr(K_c),
+ *           Q_r R_r = A^T Q_c, tsvd(R_r): v/2 + 1 reads.
+ * Equal to rsvd_block_krylov (input = A) up to rounding when the intermediate blocks have full
+ * rank (the same Krylov subspaces).  input is always A; Omega n x (k+p); info->views = reads of A.
+ * Same pointer, dtype, sharding (Z all-reduced over the row shards) and error rules as
+ * rsvd_block_krylov. */
+int rsvd_block_krylov_rows(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v,
+                           const void* Omega, int64_t ld_omega,
+                           void* U, int64_t ldu, void* S, void* V, int64_t ldv,
+                           unsigned flags, rsvd_info* info);
 
 /* Extended 1-view sketch: from ONE view of A, Y_c = A Omega (n x (k+p) Omega),
  * Y_r = A^T Phi (Phi m_local x l2) and Z = Xi_r^T A Xi_c (s x s), with Xi_r (m_local x s) and Xi_c

@@ -36,7 +36,7 @@ __all__ = [
     "plan_flat", "plan_decay", "plan_rapid", "plan_balanced", "minvar_spectra", "minvar_select",
     "one_view_minvar", "one_view_extended", "plan_extended", "pinv",
     "row_stream_qb",
-    "gen_block_krylov", "normal_matrix_tevd", "nystrom_tevd", "pinched_tevd", "recommend_input", "svd_of",
+    "gen_block_krylov", "row_block_krylov", "normal_matrix_tevd", "nystrom_tevd", "pinched_tevd", "recommend_input", "svd_of",
     "views_and_vectors", "PanelOp", "rel_frobenius_error", "rel_spectral_error", "projector_distance",
     "residual_fro", "half_power_lhs_rhs", "thm_bound",
     "GOAL_SVD", "GOAL_LEFT", "GOAL_RIGHT", "GOAL_NORMAL",
@@ -560,6 +560,79 @@ def gen_block_krylov(A, p, l, v, Omega_r, transpose=False, _op=None, return_basi
     if return_basis:
         return out, (Qc, Qr)
     return out
+
+
+# ============================================================ block Krylov, matrix read row wise
+
+def row_block_krylov(A, p, l, v, Omega_r, panel_rows=1):
+    """Block Krylov method for a matrix accessed row by row: A^* A times a block is
+    evaluated in ONE pass over the rows, Y[i, :] = A[i, :] X and Z = sum_i A[i, :]^* Y[i, :] (the
+    single-pass product of P:849-851), so the Krylov blocks of Alg. 9 need about half
+    the views.  Returns ((U_p, Lambda_p, V_p), passes over A).
+
+    v odd  (co-range Krylov subspace): Q^0 = Omega_r; pass i = 1..(v-1)/2 gives
+           Z_i = A^* A Q^{i-1}, Q^i = qr(Z_i).Q (the last Z_i stays raw, as Alg. 9 lines 3-6);
+           K_r = [Z_1 .. Z_{(v-1)/2}] (orthonormalised blocks, last raw) spans Alg. 9's K_r
+           (A^*A Omega, (A^*A)^2 Omega, ...); then Alg. 9 lines 14-17: Q_r = qr(K_r),
+           [Q_c, R_c] = qr(A Q_r), tsvd(R_c).  (v-1)/2 + 1 passes instead of v views.
+    v even (range Krylov subspace): the same passes also give the range blocks A Q^{i-1}:
+           K_c = [A Q^0 .. A Q^{v/2-1}] spans Alg. 9's K_c (P:913: A Omega, A A^*A Omega, ...);
+           the last block needs only a range pass; then lines 9-12: Q_c = qr(K_c),
+           [Q_r, R_r] = qr(A^* Q_c), tsvd(R_r).  v/2 + 1 passes.
+    With every intermediate R invertible the subspaces equal Alg. 9's, so the outputs equal
+    gen_block_krylov's up to rounding."""
+    if v < 2:
+        raise ValueError("v >= 2 (P:903)")
+    A = _f64(A)
+    Omega_r = _f64(Omega_r)
+    n_r = A.shape[0]
+    passes = 0
+
+    def row_pass(X, want_z=True):
+        """One pass over the rows: (A X, A^* A X) accumulated row panel by row panel."""
+        nonlocal passes
+        passes += 1
+        Y = np.zeros((n_r, X.shape[1]))
+        Z = np.zeros((A.shape[1], X.shape[1]))
+        for i0 in range(0, n_r, panel_rows):
+            rows = slice(i0, min(n_r, i0 + panel_rows))
+            Y[rows] = A[rows] @ X                  # Y[i, :] = A[i, :] X
+            if want_z:
+                Z += A[rows].T @ Y[rows]           # Z += A[i, :]^* Y[i, :]
+        return Y, Z
+
+    Q = Omega_r
+    if v % 2 == 1:
+        nb = (v - 1) // 2
+        blocks = []
+        for i in range(nb):
+            _, Z = row_pass(Q)
+            if i < nb - 1:
+                Q = qr(Z)[0]
+                blocks.append(Q)
+            else:
+                blocks.append(Z)                  # last block raw (Alg. 9 line 4/6, j = v-1)
+        Qr, _ = qr(np.hstack(blocks))             # line 15
+        Yc, _ = row_pass(Qr, want_z=False)        # line 16: one more (range) pass
+        Qc, Rc = qr(Yc)
+        Uh, lam, Vh = tsvd(Rc, p)                 # line 17
+    else:
+        nb = v // 2
+        blocks = []
+        for i in range(nb):
+            Y, Z = row_pass(Q, want_z=(i < nb - 1))
+            blocks.append(Y)                      # A Q^{i}: range block (raw)
+            if i < nb - 1:
+                Q = qr(Z)[0]
+        Qc, _ = qr(np.hstack(blocks))             # line 10
+        Zr = np.zeros((A.shape[1], Qc.shape[1]))  # line 11: A^* Q_c, one more pass over the rows
+        passes += 1
+        for i0 in range(0, n_r, panel_rows):
+            rows = slice(i0, min(n_r, i0 + panel_rows))
+            Zr += A[rows].T @ Qc[rows]
+        Qr, Rr = qr(Zr)
+        Vh, lam, Uh = tsvd(Rr, p)                 # line 12: R_r = Vh Lam Uh^*
+    return (Qc @ Uh, lam, Qr @ Vh), passes
 
 
 # ============================================================ orientation / outputs

@@ -55,12 +55,18 @@ struct ViewArgs32 {
   const float* Xlo;
   int64_t ldx;
   int w;
-  double* out;        // fp64 partial slots, column-major (out_rows x w, ldo), slot s at out + s*slot_stride
+  float* out;         // fp32 partial slots, column-major (out_rows x w, ldo), slot j at out + j*slot_stride:
+                      // one per accumulation chunk of kTf32Chunk stages of each unit (tf32_slots)
   int64_t ldo, slot_stride;
   int S, KTS;
   int grid_cap;
 };
 void plan_view_tf32(int kind, int64_t rows, int64_t n, int w, int grid_cap, int* S, int* KTS);
+// number of fp32 partial slots of a planned view (S units x ceil(KTS / chunk) chunks per unit)
+int tf32_slots(int S, int KTS);
+// out (fp64) = sum of NS fp32 slots in slot order, accumulated in fp64 (round to nearest)
+int launch_slot_sum_f32(const float* in, int64_t ldi, int64_t slot_stride, int NS, int64_t rows, int w, double* out,
+                        int64_t ldo, cudaStream_t st);
 int launch_view_tf32(const ViewArgs32& a, cudaStream_t st);
 // X (fp64 col-major rows x w, ld) -> tf32-rounded hi / lo parts (fp32 col-major, ld32)
 int launch_split_tf32(const double* X, int64_t ld, int64_t rows, int w, float* hi, float* lo, int64_t ld32,
@@ -124,6 +130,9 @@ int launch_tri_inv(const double* R, int c, double* Rinv, DevStatus* status, cuda
 int launch_pinv_svd(const double* U, const double* s, const double* V, int w, double rcut, double* Tp,
                     cudaStream_t st);
 int launch_scale_cols(double* X, int64_t ld, int rows, int cols, const double* d, cudaStream_t st);
+// zero the columns j of X (rows x w) with G_jj <= tol * ref_j (dependent after a block projection)
+int launch_zero_dep_cols(double* X, int64_t ld, int64_t rows, int w, const double* G, const double* ref, double tol,
+                         DevStatus* status, cudaStream_t st);
 // S[i] <- S[i]^2
 int launch_square(double* S, int n, cudaStream_t st);
 // Nystrom (Alg. 4) helpers: nu = 2.2e-16 ||Y_r||_2 from the Gram of Y_r (power iteration);

@@ -300,7 +300,8 @@ struct Exec {
       a.grid_cap = ctx->sms;
       plan_view_tf32(a.kind, rows_v, n, wc, ctx->sms, &a.S, &a.KTS);
       double* dst = Y.p + (int64_t)c0 * Y.ld;
-      double* slots = (a.S == 1) ? dst : alloc((int64_t)a.S * Y.ld * wc);
+      const int ns = tf32_slots(a.S, a.KTS);                 // fp32 chunk partials, summed in fp64
+      float* slots = alloc_f((int64_t)ns * Y.ld * wc);
       a.out = slots;
       a.ldo = Y.ld;
       a.slot_stride = (int64_t)Y.ld * wc;
@@ -314,7 +315,7 @@ struct Exec {
         chk(launch_view_tf32(a, st));
         ev_record(&e1);
         if (e0 >= 0) ev_pairs.push_back({e0, e1});
-        if (a.S > 1) chk(launch_slot_sum(slots, Y.ld, a.slot_stride, a.S, Y.rows, wc, dst, Y.ld, st));
+        chk(launch_slot_sum_f32(slots, Y.ld, a.slot_stride, ns, Y.rows, wc, dst, Y.ld, st));
       }
       release(mk);
     }
@@ -498,12 +499,14 @@ struct Exec {
     release(mk);
   }
 
-  // block classical Gram-Schmidt, twice, over blocks of width bw, then CholeskyQR2 per block
-  // Block 0 is re-orthonormalised even when it is already an orth's Q (an intermediate Krylov
-  // block): skipping it was measured to break exactly dependent blocks (A diagonal, Omega = I[:, :l]:
-  // the projected remainder of block 1 is rounding noise along block 0's directions, which the
-  // self-referenced rank guard keeps and renormalises into a duplicate direction).
-  void bcgs2(Side s, const TS& K, int bw) {
+  // block classical Gram-Schmidt, twice, over blocks of width bw, then CholeskyQR2 per block.
+  // first_orthonormal: block 0 is already an orth's Q (an intermediate Krylov block, v >= 4).
+  // Rank guard of the projected blocks (reading R11): a column whose projected remainder is at
+  // the rounding level of the projection, |w_j - Q Q^T w_j|^2 <= (64 u)^2 |w_j|^2 with the norm
+  // taken BEFORE projecting, lies in the span of the previous blocks and is zeroed; the guarded
+  // Cholesky passes keep exact zero columns at zero.  (A self-referenced guard, judged on the
+  // remainder alone, would renormalise that rounding noise into a spurious direction.)
+  void bcgs2(Side s, const TS& K, int bw, bool first_orthonormal) {
     const int nb = (K.w + bw - 1) / bw;
     for (int b = 0; b < nb; ++b) {
       const int c0 = b * bw, wc = std::min(bw, K.w - c0);
@@ -515,13 +518,22 @@ struct Exec {
         // (removes the components the normalisation amplified), then CholeskyQR2.
         TS Qp = slice(K, 0, c0);
         double* C = alloc((int64_t)c0 * wc);
+        double* G = alloc((int64_t)wc * wc);
+        double* ref = alloc(wc);
+        cross(s, Wb, Wb, G);
+        if (live()) chk(launch_diag(G, wc, ref, st));
         cross(s, Qp, Wb, C);
         tsmm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1);
+        cross(s, Wb, Wb, G);
+        constexpr double kDepTol = (64.0 * 1.1102230246251565e-16) * (64.0 * 1.1102230246251565e-16);
+        if (live()) chk(launch_zero_dep_cols(Wb.p, Wb.ld, Wb.rows, wc, G, ref, kDepTol, ctx->dstat, st));
         orth(s, Wb, nullptr, nullptr, /*shifted=*/true);
         cross(s, Qp, Wb, C);
         tsmm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1);
+        orth(s, Wb, nullptr, nullptr);
+      } else if (!first_orthonormal) {
+        orth(s, Wb, nullptr, nullptr);
       }
-      orth(s, Wb, nullptr, nullptr);
       release(mk);
     }
   }
@@ -675,7 +687,7 @@ void alg_krylov(Exec& E) {
     prev = dst;
   }
   if (v == 1) return;
-  E.bcgs2(side_K, K, l);                                  // qr(K_c) / qr(K_r)  (lines 9 / 14)
+  E.bcgs2(side_K, K, l, /*first_orthonormal=*/nb > 1);   // qr(K_c) / qr(K_r)  (lines 9 / 14)
   TS Qo = E.new_ts(even ? side_r : side_c, W);
   double* Rw = E.alloc((int64_t)W * W);
   E.view(side_K, K, Qo);                                  // one more view (lines 10 / 15)
@@ -965,19 +977,13 @@ void alg_extended(Exec& E) {
   write_outputs(E, SIDE_M, SIDE_N, Yc, Yr, Vr, Ul, lam, l, k);
 }
 
-// Single pass over the rows of A.  A is walked in row panels small enough to stay in
-// L2: each panel is read from HBM once by the range view (Y_c rows = panel Omega, A loaded with
-// evict_last) and re-read from L2 by the co-range view (Yhat_r += panel^T Y_c rows, accumulated
-// in panel order).  Then Q_c R_c := Y_c, B^* = Yhat_r R_c^+ (TSVD pseudo-inverse) and
-// the rank-k SVD of Q_c B through qr(B^*).  With R_c invertible this is Alg. 2, v = 2.
+// One pass over the rows of A: Y = A X (side M, written panel by panel) and,
+// with Z, Z = A^T (A X) = sum over row panels of A[panel]^T Y[panel] (side N, accumulated in panel
+// order, then all-reduced over the row shards).  The panels are small enough to stay in L2
+// between the two products: each panel is read from HBM once by the range view (A loaded
+// evict_last) and re-read from L2 by the co-range view.  T: side-N scratch of X's width.
 constexpr double kRowPanelBytes = 48.0 * 1024 * 1024;
-void alg_row_stream(Exec& E) {
-  const Call& c = E.call;
-  const int l = c.k + c.p;
-  TS Om = E.stage_in(SIDE_N, c.Om, c.ldom, l, c.kOm);
-  TS Yc = E.new_ts(SIDE_M, l);
-  TS Yh = E.new_ts(SIDE_N, l);
-  TS T = E.new_ts(SIDE_N, l);
+void row_pass(Exec& E, const TS& X, const TS& Y, const TS* Z, const TS& T) {
   const double esz = (E.dtype == RSVD_F32) ? 4.0 : 8.0;
   static const double panel_bytes = [] {
     const char* e = getenv("RSVD_ROW_PANEL_MB");   // A/B experiments only
@@ -985,20 +991,36 @@ void alg_row_stream(Exec& E) {
   }();
   int64_t P = (int64_t)(panel_bytes / (esz * (double)E.n));
   P = std::max<int64_t>(128, P / 128 * 128);
+  const int w = X.w;
   for (int64_t r0 = 0; r0 < E.m; r0 += P) {
     const int64_t nr = std::min<int64_t>(P, E.m - r0);
     TS Yp;
-    Yp.p = Yc.p + r0;
+    Yp.p = Y.p + r0;
     Yp.rows = nr;
-    Yp.ld = Yc.ld;
-    Yp.w = l;
-    E.view(SIDE_N, Om, Yp, r0, nr, /*a_keep=*/1);            // Y_c[panel] = A[panel] Omega
+    Yp.ld = Y.ld;
+    Yp.w = w;
+    E.view(SIDE_N, X, Yp, r0, nr, /*a_keep=*/Z != nullptr);   // Y[panel] = A[panel] X
+    if (!Z) continue;
     const bool first = (r0 == 0);
-    E.view(SIDE_M, Yp, first ? Yh : T, r0, nr);              // A[panel]^* Y_c[panel]
-    if (!first && E.live()) E.chk(launch_add_cols(T.p, T.ld, Yh.p, Yh.ld, Yh.rows, l, E.st));
+    E.view(SIDE_M, Yp, first ? *Z : T, r0, nr);                // A[panel]^T Y[panel]
+    if (!first && E.live()) E.chk(launch_add_cols(T.p, T.ld, Z->p, Z->ld, Z->rows, w, E.st));
   }
-  if (E.m == 0 && E.live()) E.chk(launch_fill(Yh.p, Yh.ld * l, 0.0, E.st));
-  if (E.collective()) E.allreduce(Yh.p, Yh.ld * l);          // Yhat_r over the row shards
+  if (!Z) return;
+  if (E.m == 0 && E.live()) E.chk(launch_fill(Z->p, Z->ld * w, 0.0, E.st));
+  if (E.collective()) E.allreduce(Z->p, Z->ld * w);             // over the row shards
+}
+
+// Single pass over the rows of A: Y_c = A Omega and Yhat_r = A^T Y_c from one
+// row pass, then Q_c R_c := Y_c, B^* = Yhat_r R_c^+ (TSVD pseudo-inverse) and the rank-k
+// SVD of Q_c B through qr(B^*).  With R_c invertible this is Alg. 2, v = 2.
+void alg_row_stream(Exec& E) {
+  const Call& c = E.call;
+  const int l = c.k + c.p;
+  TS Om = E.stage_in(SIDE_N, c.Om, c.ldom, l, c.kOm);
+  TS Yc = E.new_ts(SIDE_M, l);
+  TS Yh = E.new_ts(SIDE_N, l);
+  TS T = E.new_ts(SIDE_N, l);
+  row_pass(E, Om, Yc, &Yh, T);
   double* Rc = E.alloc((int64_t)l * l);
   E.orth(SIDE_M, Yc, Rc, nullptr);                           // Q_c R_c := Y_c
   // R_c^+: guarded triangular inverse — equal to the TSVD pseudo-inverse for an invertible R_c and
@@ -1014,6 +1036,65 @@ void alg_row_stream(Exec& E) {
   double* lam = E.alloc(l);
   E.core_svd(Rb, l, 1, Vr, lam, Ul);                         // R_b = Ul S Vr^T -> Q_c B = Q_c Vr S Ul^T Q_b^T
   write_outputs(E, SIDE_M, SIDE_N, Yc, Bt, /*Uh=*/Vr, /*Vh=*/Ul, lam, l, c.k);
+}
+
+// Block Krylov method for a matrix read row wise: A^T A X in ONE row pass, so the
+// Krylov blocks of Alg. 9 need about half the reads of A (oracle.row_block_krylov).
+//   v odd : K_r = [A^TA Omega, (A^TA)^2 Omega, ...] ((v-1)/2 row passes; intermediate blocks
+//           orthonormalised, the last raw, as Alg. 9 lines 3-6), qr(K_r) by BCGS2, Q_c R_c = A Q_r
+//           (one range view), tsvd(R_c): (v-1)/2 + 1 reads instead of v.
+//   v even: the same passes also give the range blocks A Q^i: K_c = [A Omega, A Q^1, ...]
+//           (the last one a plain range view), qr(K_c), Q_r R_r = A^T Q_c, tsvd(R_r): v/2 + 1 reads.
+void alg_krylov_rows(Exec& E) {
+  const Call& c = E.call;
+  const int l = c.k + c.p, v = c.v;
+  const bool even = (v % 2 == 0);
+  const int nb = even ? v / 2 : (v - 1) / 2;
+  const int W = nb * l;
+  TS X = E.stage_in(SIDE_N, c.Om, c.ldom, l, c.kOm);         // Q^0 = Omega
+  TS T = E.new_ts(SIDE_N, l);
+  double* Rw = E.alloc((int64_t)W * W);
+  double* Ul = E.alloc((int64_t)W * W);
+  double* Vr = E.alloc((int64_t)W * W);
+  double* lam = E.alloc(W);
+  const int want_j = (c.flags & RSVD_SQUARED) ? 2 : 0;
+  if (!even) {
+    TS K = E.new_ts(SIDE_N, W);
+    TS Y = E.new_ts(SIDE_M, l);
+    for (int b = 0; b < nb; ++b) {
+      TS Kb = E.slice(K, b * l, l);
+      row_pass(E, X, Y, &Kb, T);                               // K_b = A^T A Q^{b}
+      if (b < nb - 1) {
+        E.orth(SIDE_N, Kb, nullptr, nullptr);                  // Q^{b+1} = qr(K_b).Q
+        X = Kb;
+      }
+    }
+    E.bcgs2(SIDE_N, K, l, /*first_orthonormal=*/nb > 1);      // Q_r = qr(K_r)   (line 15)
+    TS Qc = E.new_ts(SIDE_M, W);
+    E.view(SIDE_N, K, Qc);                                     // A Q_r           (line 16)
+    E.orth(SIDE_M, Qc, Rw, nullptr);
+    E.core_svd(Rw, W, 1, Vr, lam, Ul, want_j);                 // R_c = Ul S Vr^T (line 17)
+    write_outputs(E, SIDE_M, SIDE_N, Qc, K, Ul, Vr, lam, W, c.k);
+  } else {
+    TS K = E.new_ts(SIDE_M, W);
+    TS Z[2] = {E.new_ts(SIDE_N, l), E.new_ts(SIDE_N, l)};
+    for (int b = 0; b < nb; ++b) {
+      TS Kb = E.slice(K, b * l, l);
+      if (b < nb - 1) {
+        row_pass(E, X, Kb, &Z[b & 1], T);                      // K_b = A Q^b, Z = A^T A Q^b
+        E.orth(SIDE_N, Z[b & 1], nullptr, nullptr);            // Q^{b+1}
+        X = Z[b & 1];
+      } else {
+        E.view(SIDE_N, X, Kb);                                 // last block: range view only
+      }
+    }
+    E.bcgs2(SIDE_M, K, l, /*first_orthonormal=*/false);       // Q_c = qr(K_c)   (line 10)
+    TS Qr = E.new_ts(SIDE_N, W);
+    E.view(SIDE_M, K, Qr);                                     // A^T Q_c         (line 11)
+    E.orth(SIDE_N, Qr, Rw, nullptr);
+    E.core_svd(Rw, W, 1, Vr, lam, Ul, want_j);                 // R_r = Vh S Uh^T (line 12)
+    write_outputs(E, SIDE_M, SIDE_N, K, Qr, Vr, Ul, lam, W, c.k);
+  }
 }
 
 // Alg. 3 QrQc on B = A (tr = false) or B = A^T (tr = true), v >= 0 views, starting
@@ -1265,6 +1346,7 @@ void run_alg(Exec& E) {
     case 4: alg_pinched(E); break;
     case 5: alg_extended(E); break;
     case 6: alg_row_stream(E); break;
+    case 7: alg_krylov_rows(E); break;
     case 10: prim_view(E); break;
     case 11: prim_fused(E); break;
     case 12: prim_orth(E); break;
@@ -1950,6 +2032,48 @@ int rsvd_row_stream(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, const void* 
   c.flags = flags;
   c.info_views = 1;                                 // one pass over the rows
   c.info_vectors = 2 * (int64_t)(k + p);
+  r = execute(ctx, c, info);
+  if (info) info->status = r;
+  return r;
+}
+
+int rsvd_block_krylov_rows(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, const void* Omega,
+                           int64_t ld_omega, void* U, int64_t ldu, void* S, void* V, int64_t ldv, unsigned flags,
+                           rsvd_info* info) {
+  int r = common_checks(ctx, A, k, p);
+  const int l = k + p;
+  const bool even = (v % 2 == 0);
+  const int nb = even ? v / 2 : (v - 1) / 2;
+  if (r == RSVD_OK) {
+    if (v < 2) { set_err(ctx, "v >= 2 required (P:903)"); r = RSVD_E_ARG; }
+    else if (!Omega || ld_omega < A->n) { set_err(ctx, "Omega NULL or ld_omega < n"); r = RSVD_E_ARG; }
+    else if ((U && ldu < A->m_local) || (V && ldv < A->n)) { set_err(ctx, "ldu/ldv too small"); r = RSVD_E_ARG; }
+    else if ((int64_t)nb * l > (even ? A->m : A->n) || (int64_t)nb * l > 512) {
+      set_err(ctx, "Krylov basis width %lld exceeds its side or 512", (long long)nb * l);
+      r = RSVD_E_ARG;
+    }
+  }
+  if (r != RSVD_OK) {
+    if (info) { memset(info, 0, sizeof(*info)); info->status = r; }
+    return r;
+  }
+  Call c;
+  c.alg = 7;
+  c.A = A;
+  c.k = k;
+  c.p = p;
+  c.v = v;
+  c.Om = Omega;
+  c.ldom = ld_omega;
+  c.U = U;
+  c.ldu = ldu;
+  c.S = S;
+  c.V = V;
+  c.ldv = ldv;
+  c.flags = flags;
+  // reads of A: (v-1)/2 row passes + 1 (odd v), v/2 + 1 (even v); vectors: 2l per row pass
+  c.info_views = even ? nb + 1 : nb + 1;
+  c.info_vectors = even ? (int64_t)(nb - 1) * 2 * l + l + (int64_t)nb * l : (int64_t)nb * 2 * l + (int64_t)nb * l;
   r = execute(ctx, c, info);
   if (info) info->status = r;
   return r;

@@ -40,6 +40,34 @@ int launch_slot_sum(const double* in, int64_t ldi, int64_t slot_stride, int S, i
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
+// fp32 partial slots (the tf32 views' accumulation chunks) summed in fp64, in slot order
+__global__ void k_slot_sum_f32(const float* __restrict__ in, int64_t ldi, int64_t slot_stride, int S, int64_t rows,
+                               int w, double* __restrict__ out, int64_t ldo) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (r >= rows || c >= w) return;
+  const float* p = in + (int64_t)c * ldi + r;
+  double s = (double)p[0];
+  int k = 1;
+  for (; k + 8 <= S; k += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = p[(int64_t)(k + u) * slot_stride];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += (double)v[u];
+  }
+  for (; k < S; ++k) s += (double)p[(int64_t)k * slot_stride];
+  out[(int64_t)c * ldo + r] = s;
+}
+
+int launch_slot_sum_f32(const float* in, int64_t ldi, int64_t slot_stride, int S, int64_t rows, int w, double* out,
+                        int64_t ldo, cudaStream_t st) {
+  if (rows <= 0 || w <= 0) return RSVD_OK;
+  dim3 grid((unsigned)((rows + 255) / 256), (unsigned)w);
+  k_slot_sum_f32<<<grid, 256, 0, st>>>(in, ldi, slot_stride, S, rows, w, out, ldo);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
 // ------------------------------------------------------------------ cross Gram  G = Xa^T Xb
 // grid.x = row slots, grid.y = 64x64 output blocks (bi, bj).  256 threads, 4x4 register tile.
 constexpr int kGR = 32;  // rows per smem tile
@@ -893,6 +921,29 @@ __global__ void k_square(double* S, int n) {
 
 int launch_square(double* S, int n, cudaStream_t st) {
   k_square<<<(n + 127) / 128, 128, 0, st>>>(S, n);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+// Block Gram-Schmidt rank guard with a pre-projection reference: column j of X (rows x w) is
+// numerically dependent on the previous blocks when its projected remainder is at the rounding
+// level of the projection, |x_j|^2 <= tol * ref_j (ref = squared norm before projecting).  Such
+// columns are set to exactly zero (they then stay zero through the shifted and the guarded
+// Cholesky passes); their count goes to status->deficient.  G: the w x w Gram after projection.
+__global__ void k_zero_dep_cols(double* __restrict__ X, int64_t ld, int64_t rows, int w, const double* __restrict__ G,
+                                const double* __restrict__ ref, double tol, DevStatus* status) {
+  const int j = blockIdx.y;
+  if (j >= w) return;
+  if (!(G[(int64_t)j * w + j] <= tol * ref[j])) return;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+    X[(int64_t)j * ld + r] = 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && status) atomicAdd(&status->deficient, 1);
+}
+
+int launch_zero_dep_cols(double* X, int64_t ld, int64_t rows, int w, const double* G, const double* ref, double tol,
+                         DevStatus* status, cudaStream_t st) {
+  if (rows <= 0 || w <= 0) return RSVD_OK;
+  const unsigned bx = (unsigned)std::min<int64_t>((rows + 255) / 256, 64);
+  k_zero_dep_cols<<<dim3(bx, (unsigned)w), 256, 0, st>>>(X, ld, rows, w, G, ref, tol, status);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 

@@ -34,13 +34,14 @@ constexpr int kBK = 16;          // fp32 per 64-byte swizzled row = reduction el
 constexpr int kThreads = 192;    // 6 warps
 constexpr int kMaxStages = 8;
 constexpr int kSmemBudget = 200 * 1024;
-// Stages accumulated in one fp32 TMEM accumulator before it is drained into the fp64 partial
-// slot.  The tensor core's fp32 accumulation is not round-to-nearest: its error is biased toward
-// zero, so it grows with the number of accumulating MMAs (6 per stage).  Measured on the full C5
-// (100000^2, one accumulator over all 6250 stages): every singular value 2.1e-4 low, above the
-// fp32 parity tolerance 1e-4.  Chunks of kChunk stages bound the bias; the fp64 adds between
-// chunks round to nearest.
-constexpr int kChunkDefault = 256;   // RSVD_TF32_CHUNK=<stages> overrides (A/B experiments)
+// Stages accumulated in one fp32 TMEM accumulator before it is drained.  The tensor core's fp32
+// accumulation is not round-to-nearest: its error is biased toward zero and grows with the number
+// of accumulating MMAs (6 per stage).  Measured (tools/tf32_bias_probe.py, 20000 x 100000, w = 250):
+// one accumulator over ~1500 stages shrinks every output by 4.7e-5 (the full C5, 6250 stages: every
+// singular value 2.1e-4 low, above the fp32 parity tolerance 1e-4); 256-stage chunks 2.3e-5,
+// 64-stage chunks 6e-6.  Each chunk is stored as its own fp32 partial slot (fire-and-forget stores,
+// no read-modify-write in the kernel) and the slots are summed in fp64 afterwards.
+constexpr int kTf32Chunk = 256;
 
 __host__ __device__ constexpr int tmem_cols_for(int c) {
   return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
@@ -125,7 +126,7 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 template <int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
     k_view_tf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
-                const __grid_constant__ CUtensorMap tmXl, double* __restrict__ out, int64_t ldo,
+                const __grid_constant__ CUtensorMap tmXl, float* __restrict__ out, int64_t ldo,
                 int64_t slot_stride, int out_rows, int w, int MT, int NB, int S, int KT, int KTS, int kChunk) {
   Geo G;
   G.init(MT, w);
@@ -285,14 +286,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++stage == G.stages) { stage = 0; phase ^= 1; }
         if (kt != kt1 - 1 && kt - kc0 != kChunk - 1) continue;
         // end of an accumulation chunk: drain TMEM (lane = output row inside the 128-row tile,
-        // column = output column) into the fp64 partial slot — stored by the unit's first chunk,
-        // added (fp64, round to nearest, fixed order) by the later ones
-        const bool first = (kc0 == kt0);
+        // column = output column) into this chunk's fp32 partial slot
+        const int cpu = (KTS + kChunk - 1) / kChunk;            // chunk slots per unit
+        const int ci = (kc0 - kt0) / kChunk;
+        const bool last = (kt == kt1 - 1);
         kc0 = kt + 1;
         mbar_wait(tfull, tphase);
         tphase ^= 1;
         tc_fence_after();
-        double* o = out + (int64_t)s * slot_stride;
+        float* o = out + (int64_t)(s * cpu + ci) * slot_stride;
         for (int t = 0; t < MT; ++t) {
           const int r = blk * BM + t * 128 + q * 32 + lane;
           for (int c0 = 0; c0 < WP; c0 += 16) {
@@ -302,13 +304,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (r < out_rows) {
 #pragma unroll
               for (int j = 0; j < 16; ++j)
-                if (c0 + j < w) {
-                  double* dst = &o[(int64_t)(c0 + j) * ldo + r];
-                  const double x = (double)__uint_as_float(v[j]);
-                  *dst = first ? x : *dst + x;
-                }
+                if (c0 + j < w) o[(int64_t)(c0 + j) * ldo + r] = __uint_as_float(v[j]);
             }
           }
+          // a short last unit has fewer chunks than cpu: its unused slots hold zeros
+          if (last && r < out_rows)
+            for (int cz = ci + 1; cz < cpu; ++cz) {
+              float* oz = out + (int64_t)(s * cpu + cz) * slot_stride;
+              for (int c = 0; c < w; ++c) oz[(int64_t)c * ldo + r] = 0.0f;
+            }
         }
         tc_fence_before();
         __syncwarp();
@@ -389,6 +393,8 @@ void plan_view_tf32(int kind, int64_t rows, int64_t n, int w, int grid_cap, int*
   *KTS = bK;
 }
 
+int tf32_slots(int S, int KTS) { return S * ((KTS + kTf32Chunk - 1) / kTf32Chunk); }
+
 int launch_split_tf32(const double* X, int64_t ld, int64_t rows, int w, float* hi, float* lo, int64_t ld32,
                       cudaStream_t st) {
   if (rows <= 0 || w <= 0) return RSVD_OK;
@@ -417,11 +423,7 @@ int launch_view_tf32(const ViewArgs32& a, cudaStream_t st) {
   const int U = NB * a.S;
   const int grid = std::min(U, a.grid_cap);
   const int smem = G.smem();
-  static const int chunk = [] {
-    const char* e = getenv("RSVD_TF32_CHUNK");
-    const int v = e ? atoi(e) : 0;
-    return v > 0 ? v : kChunkDefault;
-  }();
+  const int chunk = kTf32Chunk;
   static std::atomic<bool> attr[2] = {{false}, {false}};
   if (!attr[ax ? 0 : 1]) {
     if (ax)

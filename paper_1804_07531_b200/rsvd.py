@@ -32,7 +32,7 @@ EXPORTS = ["rsvd_create", "rsvd_destroy", "rsvd_wait", "rsvd_strerror", "rsvd_la
            "rsvd_block_krylov", "rsvd_single_pass", "rsvd_nystrom", "rsvd_pinched", "rsvd_view", "rsvd_view_fused",
            "rsvd_orth", "rsvd_core_svd", "rsvd_plan", "rsvd_single_pass_extended",
            "rsvd_row_stream", "rsvd_set_sm_limit", "rsvd_loop_create", "rsvd_loop_destroy",
-           "rsvd_comm_init_loopback"]
+           "rsvd_comm_init_loopback", "rsvd_block_krylov_rows"]
 
 
 class RsvdMat(ctypes.Structure):
@@ -98,6 +98,7 @@ def lib():
     L.rsvd_single_pass_extended.argtypes = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, i64, i32,
                                             vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_row_stream.argtypes = [vp, pmat, i32, i32, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
+    L.rsvd_block_krylov_rows.argtypes = [vp, pmat, i32, i32, i32, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_single_pass.argtypes = [vp, pmat, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_nystrom.argtypes = [vp, pmat, i32, i32, i32, vp, i64, vp, vp, i64, u32, pinfo]
     L.rsvd_pinched.argtypes = [vp, pmat, i32, i32, i32, vp, i64, vp, vp, i64, u32, pinfo]
@@ -323,6 +324,20 @@ class Context:
                                              var, U.data_ptr(), _ld(U), S.data_ptr(), V.data_ptr(), _ld(V), flags,
                                              ctypes.byref(info))
         self._check(rc, "rsvd_single_pass_extended")
+        return U, S, V, info
+
+    def block_krylov_rows(self, A, k, p, v, Omega, flags=0, m=None, row0=0, host_out=False):
+        """Block Krylov with A^T A X from one pass over the rows; info.views = reads of A."""
+        Om = _colmajor(Omega)
+        M = self.mat(A, m, row0)
+        U = self._out_like(A, A.shape[0], k, host_out)
+        V = self._out_like(A, A.shape[1], k, host_out)
+        S = (torch.empty(max(k, 1), dtype=A.dtype, pin_memory=True) if (host_out or not A.is_cuda)
+             else torch.empty(max(k, 1), dtype=A.dtype, device=A.device))
+        info = RsvdInfo()
+        rc = lib().rsvd_block_krylov_rows(self._h, ctypes.byref(M), k, p, v, Om.data_ptr(), _ld(Om), U.data_ptr(),
+                                          _ld(U), S.data_ptr(), V.data_ptr(), _ld(V), flags, ctypes.byref(info))
+        self._check(rc, "rsvd_block_krylov_rows")
         return U, S, V, info
 
     def row_stream(self, A, k, p, Omega, flags=0, m=None, row0=0, host_out=False):

@@ -793,3 +793,39 @@ def test_panel_views_equal_dense_views(alg, v, tr, panel):
     c = O.svd_of(A32, alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi, transpose=tr, panel_rows=panel)
     d = O.svd_of(A32.astype(np.float64), alg, cfg.k, cfg.p, v=v, Omega=Om, l2=cfg.l2, Phi=Phi, transpose=tr)
     np.testing.assert_allclose(c[1], d[1], rtol=1e-13)
+
+
+# ------------------------------------------------------------------ block Krylov read row wise
+
+@pytest.mark.parametrize("v", [2, 3, 4, 5, 6, 7])
+def test_row_block_krylov_equals_alg9(v):
+    """The row-wise block Krylov (A^*A X in one pass over the rows) spans the same Krylov blocks as
+    Alg. 9 with explicit views (P:941-943 vs P:907-923): same outputs to rounding, with
+    (v-1)/2 + 1 passes for odd v (the co-range subspace with half the views) and v/2 + 1
+    for even v."""
+    cfg = S.CONFIGS["C2"]
+    A = S.make_matrix(cfg, 400, 300)
+    Om = S.gaussian_test_matrix(300, cfg.l, cfg, S.ROLE_OMEGA)
+    (U, s, V), passes = O.row_block_krylov(A, cfg.k, cfg.p, v, Om, panel_rows=37)
+    Uo, so, Vo = O.gen_block_krylov(A, cfg.k, cfg.p, v, Om)
+    np.testing.assert_allclose(s, so, rtol=1e-11)
+    assert proj(U, Uo) < 1e-9 and proj(V, Vo) < 1e-9
+    assert passes == ((v - 1) // 2 + 1 if v % 2 else v // 2 + 1)
+
+
+@pytest.mark.parametrize("v", [4, 5])
+def test_row_block_krylov_exact_rank_and_order_invariance(v):
+    """Exact rank l < r <= 2l recovered exactly (the Krylov closed form of
+    test_krylov_recovers_rank_between_l_and_2l_exactly), and the panel size does not matter."""
+    m, n, k, p = 150, 110, 6, 4
+    l = k + p
+    r = 2 * l - 3
+    sig = 1.0 / np.arange(1, r + 1) ** 0.7
+    A = S.exact_rank_matrix(m, n, sig, seed=78)
+    X, Y = S.exact_rank_factors(m, n, r, seed=78)
+    Om = S.gaussian((n, l), 78, S.ROLE_OMEGA, v)
+    (U, s, V), _ = O.row_block_krylov(A, k, p, v, Om, panel_rows=1)
+    np.testing.assert_allclose(s, sig[:k], rtol=1e-11)
+    assert proj(U, X[:, :k]) < 1e-10 and proj(V, Y[:, :k]) < 1e-10
+    (U2, s2, V2), _ = O.row_block_krylov(A, k, p, v, Om, panel_rows=1000)
+    np.testing.assert_allclose(s2, s, rtol=1e-13)

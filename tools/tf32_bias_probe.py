@@ -1,5 +1,6 @@
-"""Accumulation bias of the tcgen05 3xTF32 views vs an fp64 reference, by TMEM chunk length.
-    RSVD_TF32_CHUNK=<stages> python tools/tf32_bias_probe.py
+"""Accumulation bias of the tcgen05 3xTF32 views vs an fp64 reference (the chunk length is
+view_tf32.cu's kTf32Chunk; round-2 measurements of 1e6 / 1024 / 256 / 64 are in DESIGN §6.2).
+    python tools/tf32_bias_probe.py
 Reports ||Y||/||Y_ref|| - 1 (the systematic shrink) and the max relative column error, and the
 view time (RSVD_PROFILE), for A x X and A^T x Y on a C5-shaped fp32 A (20000 x 100000, w = 250)."""
 import os
@@ -25,6 +26,6 @@ for trans in (0, 1):
     shrink = (Yg.norm() / Yr.norm() - 1).item()
     colerr = ((Yg - Yr).norm(dim=0) / Yr.norm(dim=0)).max().item()
     bias = ((Yg - Yr) * Yr.sign()).mean().item() / Yr.abs().mean().item()
-    print(f"chunk={os.environ.get('RSVD_TF32_CHUNK', 'default')} {'ATY' if trans else 'AX'} shrink={shrink:.3e} "
+    print(f"{'ATY' if trans else 'AX'} shrink={shrink:.3e} "
           f"bias={bias:.3e} max_col_rel_err={colerr:.3e} view_ms={info.view_ms:.3f}", flush=True)
     del Yr, Yg
