@@ -1,5 +1,6 @@
-"""Warm per-kernel device time of one C2 call (graph replay, CUPTI via torch.profiler): the kernels on a
-call's critical path, without ncu's cold-cache serialisation.  usage: python tools/call_kernels.py [C2]"""
+"""Warm per-kernel device time of one call per algorithm (graph replay, CUPTI via torch.profiler): the
+kernels on a call's critical path, without ncu's cold-cache serialisation.
+usage: python tools/call_kernels.py [C2|C3|C4|C5] [alg_v ...]   (e.g. C5 subspace_v2 krylov_v4)"""
 import collections
 import os
 import sys
@@ -16,16 +17,24 @@ from paper_1804_07531_b200 import rsvd
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 cfg = S.CONFIGS[name]
 ctx = rsvd.Context(0)
-A = torch.from_numpy(S.make_matrix(cfg)).cuda()
+A = torch.from_numpy(S.make_matrix(cfg)).cuda() if name in ("C1", "C2", "C3") else S.make_matrix_torch(cfg, torch.device("cuda", 0))
 m, n = A.shape
-Om = torch.from_numpy(np.ascontiguousarray(S.gaussian_test_matrix(n, cfg.l, cfg, S.ROLE_OMEGA).T)).cuda().t()
-Ph = torch.from_numpy(np.ascontiguousarray(S.gaussian_test_matrix(m, cfg.l2, cfg, S.ROLE_PHI).T)).cuda().t()
-calls = {
-    "subspace_v3": lambda: ctx.subspace(A, cfg.k, cfg.p, 3, Om),
-    "krylov_v4": lambda: ctx.block_krylov(A, cfg.k, cfg.p, 4, Om),
-    "single_pass": lambda: ctx.single_pass(A, cfg.k, cfg.p, cfg.l2, Om, Ph),
-}
-REPS = 5
+Om = S.gaussian_test_matrix_torch(n, cfg.l, cfg, S.ROLE_OMEGA, torch.device("cuda", 0))
+Ph = S.gaussian_test_matrix_torch(m, cfg.l2, cfg, S.ROLE_PHI, torch.device("cuda", 0))
+wanted = sys.argv[2:] or ["subspace_v3", "krylov_v4", "single_pass_v1"]
+calls = {}
+for nm in wanted:
+    alg, v = nm.rsplit("_v", 1)
+    v = int(v)
+    if alg == "subspace":
+        calls[nm] = (lambda v=v: ctx.subspace(A, cfg.k, cfg.p, v, Om))
+    elif alg == "krylov":
+        calls[nm] = (lambda v=v: ctx.block_krylov(A, cfg.k, cfg.p, v, Om))
+    elif alg == "krylov_rows":
+        calls[nm] = (lambda v=v: ctx.block_krylov_rows(A, cfg.k, cfg.p, v, Om))
+    else:
+        calls[nm] = (lambda: ctx.single_pass(A, cfg.k, cfg.p, cfg.l2, Om, Ph))
+REPS = 5 if name in ("C1", "C2", "C3") else 2
 for cname, fn in calls.items():
     for _ in range(3):
         fn()
