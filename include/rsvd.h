@@ -99,6 +99,9 @@ enum {
 #define RSVD_WOOLFE       64u  /* rsvd_single_pass: Alg. 8 (Woolfe variant) instead of Alg. 7   */
 #define RSVD_ORTH_SHIFTED 128u /* rsvd_orth: shifted CholeskyQR3 (a shift pass before the two
                                   CholeskyQR passes; what Alg. 9's projected Krylov blocks use) */
+#define RSVD_ONE_READ     256u /* single pass (fp64, l > 72 or l2 > 144): Y_c and Y_r from ONE read
+                                  of A (thread-block-cluster kernel) instead of two view launches,
+                                  which are faster on device-resident A         */
 #define RSVD_LC_MINVAR    (-2) /* rsvd_single_pass lc: minimum-variance l_c          */
 #define RSVD_EXT_BWZ      0    /* rsvd_single_pass_extended: Eq. (bwz)               */
 #define RSVD_EXT_BWZ2     1    /* rsvd_single_pass_extended: Eq. (bwzimproved)       */
@@ -304,7 +307,9 @@ int rsvd_pinched(rsvd_ctx* ctx, const rsvd_mat* A, int k, int p, int v, const vo
  * 1 <= w <= 1024 (wider views run as column chunks of 128 (fp64) / 512 (fp32) columns). */
 int rsvd_view(rsvd_ctx* ctx, const rsvd_mat* A, int trans, const void* X, int64_t ldx, int w,
               void* Y, int64_t ldy, unsigned flags, rsvd_info* info);
-/* Y_c (m_local x l) = A Omega (Omega n x l) and Y_r (n x l2) = A^T Phi (Phi m_local x l2). */
+/* Y_c (m_local x l) = A Omega (Omega n x l) and Y_r (n x l2) = A^T Phi (Phi m_local x l2), from one
+ * read of A.  fp64: l <= 128 and l2 <= 256 (l > 72 or l2 > 144: the cluster kernel, whose Y_c
+ * partials are reduced across a 16- or 8-CTA thread-block cluster).  fp32: RSVD_E_DTYPE. */
 int rsvd_view_fused(rsvd_ctx* ctx, const rsvd_mat* A, const void* Omega, int64_t ld_omega, int l,
                     const void* Phi, int64_t ld_phi, int l2, void* Yc, int64_t ld_yc,
                     void* Yr, int64_t ld_yr, unsigned flags, rsvd_info* info);

@@ -45,6 +45,30 @@ struct FusedArgs {
   int grid_cap;
 };
 
+// Fused single pass for wide sketches (view_fused_cluster.cu): l <= 128, l2 <= 256, fp64, one read
+// of A, Y_c partials reduced across a 16- (or 8-) CTA cluster through distributed shared memory.
+struct FusedClArgs {
+  const double* A;
+  int64_t rows, n, lda;
+  const double* Om;   // Omega^T: l x n, ldom
+  int64_t ldom;
+  int l;
+  const double* Phi;  // Phi^T: l2 x rows, ldphi
+  int64_t ldphi;
+  int l2;
+  double* yc_slots;   // per strip group: row-major rows x ldys partial of Y_c
+  int64_t ldys, yc_slot_stride;
+  double* yr;         // per row split: column-major n x l2 (ldyr) partial of Y_r
+  int64_t ldyr, yr_slot_stride;
+  int CL, NG, S, KTS, nclusters;   // from plan_fused_cl
+};
+bool fused_cl_supported(int l, int l2);
+void plan_fused_cl(int64_t rows, int64_t n, int l, int l2, int sms, FusedClArgs* a);
+int launch_view_fused_cl(const FusedClArgs& a, cudaStream_t st);
+// out (column-major, ldo) = sum over NG row-major slots (rows x w, ld ldi) in slot order
+int launch_slot_sum_rows(const double* in, int64_t ldi, int64_t slot_stride, int NG, int64_t rows, int w, double* out,
+                         int64_t ldo, cudaStream_t st);
+
 // fp32 A (view_tf32.cu): tcgen05 kind::tf32 views with the 3xTF32 split of both operands
 constexpr int kMaxW32 = 512;      // widths per launch (wider -> column chunks)
 struct ViewArgs32 {

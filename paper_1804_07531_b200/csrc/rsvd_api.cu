@@ -707,8 +707,60 @@ constexpr double kYcSlotBudget = 4.0e9;  // bytes of deterministic Y_c partial s
 // One view of A for the 1-view methods (Alg. 7 line 3; the extended sketch):
 // Yc = A Om and Yr = A^* Phi from one read of every A tile (k_view_fused), or two view launches
 // when the widths exceed the fused kernel's register budget or A is fp32 (info.view_launches = 2).
+constexpr double kYcClusterSlotBudget = 24.0e9;  // bytes of the cluster kernel's Y_c group slots
+
+// Wide sketches (C4: l = 120, l2 = 240): k_view_fused_cl, one read of A with the Y_c partials
+// reduced across a thread-block cluster (view_fused_cluster.cu).  Returns false when not applicable.
+bool sketch_view_cluster(Exec& E, const TS& Om, const TS& Phi, const TS& Yc, const TS& Yr, bool wanted) {
+  const int l = Om.w, l2 = Phi.w;
+  const bool narrow = (l <= kFusedMaxL) && ((l2 + 7) / 8 <= kFusedMaxL2T);
+  if (!wanted || E.dtype != RSVD_F64 || !fused_cl_supported(l, l2) || narrow) return false;
+  FusedClArgs a;
+  plan_fused_cl(E.m, E.n, l, l2, E.ctx->sms, &a);
+  a.ldys = round_up(l, 8);
+  a.yc_slot_stride = round_up(std::max<int64_t>(E.m, 1), 32) * a.ldys;
+  if ((double)a.NG * a.yc_slot_stride * 8.0 > kYcClusterSlotBudget) return false;
+  const size_t mk = E.mark();
+  a.A = E.A;
+  a.rows = E.m;
+  a.n = E.n;
+  a.lda = E.lda;
+  a.Om = Om.p;
+  a.ldom = Om.ld;
+  a.l = l;
+  a.Phi = Phi.p;
+  a.ldphi = Phi.ld;
+  a.l2 = l2;
+  a.yc_slots = E.alloc((int64_t)a.NG * a.yc_slot_stride);
+  double* yrs = (a.S == 1) ? Yr.p : E.alloc((int64_t)a.S * Yr.ld * l2);
+  a.yr = yrs;
+  a.ldyr = Yr.ld;
+  a.yr_slot_stride = (int64_t)Yr.ld * l2;
+  E.view_bytes += (double)E.m * E.n * 8.0;
+  E.view_flops += 2.0 * E.m * E.n * (l + l2);
+  ++E.view_launches;
+  if (E.live()) {
+    int e0 = -1, e1 = -1;
+    E.ev_record(&e0);
+    E.chk(launch_view_fused_cl(a, E.st));
+    E.ev_record(&e1);
+    if (e0 >= 0) E.ev_pairs.push_back({e0, e1});
+    E.chk(launch_slot_sum_rows(a.yc_slots, a.ldys, a.yc_slot_stride, a.NG, Yc.rows, l, Yc.p, Yc.ld, E.st));
+    if (a.S > 1) E.chk(launch_slot_sum(yrs, Yr.ld, a.yr_slot_stride, a.S, Yr.rows, l2, Yr.p, Yr.ld, E.st));
+  }
+  if (E.collective()) E.allreduce(Yr.p, Yr.ld * l2);
+  E.release(mk);
+  return true;
+}
+
+// Sketch widths beyond the one-CTA fused kernel (C4: l = 120, l2 = 240) take two view launches by
+// default: on device-resident A both products are DMMA-bound, and the one-read cluster kernel runs
+// at 0.62 of the per-SM DMMA rate on the 112 SMs that seven 16-CTA clusters occupy (C4: 416 ms
+// against 204 ms for the two views).  flags & RSVD_ONE_READ selects the one-read path (A is read
+// from memory once: the paper's single-pass premise, for when reading A is the cost).
 void sketch_view(Exec& E, const TS& Om, const TS& Phi, const TS& Yc, const TS& Yr) {
   const int l = Om.w, l2 = Phi.w;
+  if (sketch_view_cluster(E, Om, Phi, Yc, Yr, (E.call.flags & RSVD_ONE_READ) != 0)) return;
   const bool fused_ok = (E.dtype == RSVD_F64) && (l <= kFusedMaxL) && ((l2 + 7) / 8 <= kFusedMaxL2T);
   if (fused_ok) {
     const size_t mk = E.mark();
@@ -1267,7 +1319,16 @@ void prim_fused(Exec& E) {
   TS Phi = E.stage_in(SIDE_M, c.Phi, c.ldphi, l2, c.kPhi);
   TS Yc = E.new_ts(SIDE_M, l), Yr = E.new_ts(SIDE_N, l2);
   if (l > kFusedMaxL || (l2 + 7) / 8 > kFusedMaxL2T) {
-    E.chk(RSVD_E_ARG);
+    // wide sketches: the cluster kernel (one read of A)
+    if (!sketch_view_cluster(E, Om, Phi, Yc, Yr, true)) {
+      E.chk(RSVD_E_ARG);
+      return;
+    }
+    int64_t ld;
+    double* o1 = E.out_ptr(c.U, c.ldu, Yc.rows, l, c.kU, &ld);
+    if (E.live()) E.chk(launch_copy_cols(Yc.p, Yc.ld, o1, ld, Yc.rows, l, E.st));
+    double* o2 = E.out_ptr(c.V, c.ldv, Yr.rows, l2, c.kV, &ld);
+    if (E.live()) E.chk(launch_copy_cols(Yr.p, Yr.ld, o2, ld, Yr.rows, l2, E.st));
     return;
   }
   FusedArgs a;
@@ -2176,9 +2237,11 @@ int rsvd_view_fused(rsvd_ctx* ctx, const rsvd_mat* A, const void* Omega, int64_t
   if (!ctx) return RSVD_E_ARG;
   int r = check_mat(ctx, A);
   if (r == RSVD_OK) {
-    if (l < 1 || l > kFusedMaxL || l2 < 1 || (l2 + 7) / 8 > kFusedMaxL2T || !Omega || !Phi || !Yc || !Yr ||
+    const bool narrow = l >= 1 && l <= kFusedMaxL && l2 >= 1 && (l2 + 7) / 8 <= kFusedMaxL2T;
+    const bool wide = A->dtype == RSVD_F64 && fused_cl_supported(l, l2);
+    if (!(narrow || wide) || !Omega || !Phi || !Yc || !Yr ||
         ld_omega < A->n || ld_phi < A->m_local || ld_yc < A->m_local || ld_yr < A->n) {
-      set_err(ctx, "bad fused-view arguments (l <= %d, l2 <= %d)", kFusedMaxL, kFusedMaxL2T * 8);
+      set_err(ctx, "bad fused-view arguments (fp64: l <= 128, l2 <= 256)");
       r = RSVD_E_ARG;
     }
   }

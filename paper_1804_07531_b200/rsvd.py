@@ -21,6 +21,7 @@ RSVD_INPUT_A, RSVD_INPUT_AT = 0, 1
 RSVD_GOAL_SVD, RSVD_GOAL_LEFT, RSVD_GOAL_RIGHT, RSVD_GOAL_NORMAL = 0, 1, 2, 3
 RSVD_SQUARED, RSVD_NO_GRAPH, RSVD_PROFILE, RSVD_CORE_NO_J, RSVD_ASYNC, RSVD_WOOLFE = 1, 2, 4, 16, 32, 64
 RSVD_ORTH_SHIFTED = 128
+RSVD_ONE_READ = 256
 RSVD_LC_MINVAR = -2
 RSVD_EXT_BWZ, RSVD_EXT_BWZ2 = 0, 1
 RSVD_PLAN_FLAT, RSVD_PLAN_DECAY, RSVD_PLAN_RAPID, RSVD_PLAN_BALANCED = 0, 1, 2, 3

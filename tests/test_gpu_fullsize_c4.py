@@ -125,3 +125,17 @@ def test_c4_normal_mode_vs_oracle(ctx, c4):
     s = np.sqrt(s2)
     cols = [0, 7, 100000, cfg.n - 1]
     assert np.max(np.abs(Ah[:, cols].T @ U - V[cols] * s) / s[0]) <= 1e-12
+
+
+def test_c4_single_pass_one_read_vs_oracle(ctx, c4):
+    """The same single pass from ONE read of the 80 GB A (RSVD_ONE_READ: the cluster kernel, a3)."""
+    from paper_1804_07531_b200 import rsvd
+
+    cfg, A, Ah, Om, _, Phi = c4
+    U, s, V, info = ctx.single_pass(A, cfg.k, cfg.p, cfg.l2, Om, Phi, flags=rsvd.RSVD_ONE_READ)
+    assert info.views == 1 and info.view_launches == 1
+    assert info.view_bytes == cfg.m * cfg.n * 8.0
+    U, s, V = host(U), host(s), host(V)
+    Uo, so, Vo, _ = O.svd_of(Ah, "single_pass", cfg.k, cfg.p, Omega=host(Om), l2=cfg.l2, Phi=host(Phi),
+                             panel_rows=PANEL)
+    _compare(Ah, U, s, V, Uo, so, Vo)
