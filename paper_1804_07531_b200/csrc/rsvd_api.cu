@@ -20,6 +20,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "comm.h"
 #include "internal.h"
 
@@ -266,8 +268,10 @@ struct Exec {
       ++view_launches;
       if (live()) {
         int e0 = -1, e1 = -1;
+        nvtxRangePushA(kind == VIEW_AX ? "view A*X" : "view A^T*Y");
         ev_record(&e0);
         chk(kind == VIEW_AX ? launch_view_ax(a, st) : launch_view_aty(a, st));
+        nvtxRangePop();
         ev_record(&e1);
         if (e0 >= 0) ev_pairs.push_back({e0, e1});
         if (a.S > 1) chk(launch_slot_sum(slots, Y.ld, a.slot_stride, a.S, Y.rows, wc, dst, Y.ld, st));
@@ -1484,8 +1488,29 @@ int execute_impl(rsvd_ctx* ctx, Call& call, rsvd_info* info);
 // A rank whose call fails before its collectives complete would leave its peers blocked in them:
 // abort the communicator (loopback: release the peers' host barriers; NCCL: ncclCommAbort).
 // Numerical failures are detected after the whole call completed and leave the comm intact.
+// NVTX range per API call (visible in Nsight timelines; a no-op without a tool attached)
+const char* alg_name(int alg) {
+  switch (alg) {
+    case 0: return "rsvd_subspace";
+    case 1: return "rsvd_block_krylov";
+    case 2: return "rsvd_single_pass";
+    case 3: return "rsvd_nystrom";
+    case 4: return "rsvd_pinched";
+    case 5: return "rsvd_single_pass_extended";
+    case 6: return "rsvd_row_stream";
+    case 7: return "rsvd_block_krylov_rows";
+    case 10: return "rsvd_view";
+    case 11: return "rsvd_view_fused";
+    case 12: return "rsvd_orth";
+    case 13: return "rsvd_core_svd";
+    default: return "rsvd";
+  }
+}
+
 int execute(rsvd_ctx* ctx, Call& call, rsvd_info* info) {
+  nvtxRangePushA(alg_name(call.alg));
   const int r = execute_impl(ctx, call, info);
+  nvtxRangePop();
   if (r != RSVD_OK && r != RSVD_E_NUMERIC && ctx->comm) ctx->comm->abort();
   return r;
 }

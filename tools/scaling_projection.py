@@ -1,0 +1,90 @@
+"""Projected strong scaling of the row-sharded path from measured 1-GPU phase times.
+
+For each call: T_1 = measured call time (graph replay, CUDA events), V = its A-view kernel time
+(RSVD_PROFILE), rest = T_1 - V (orthonormalisation, core SVD, small kernels).  With A row-sharded
+over N GPUs (one process per GPU, NCCL):
+    T_N = V / N + rest_shard / N + rest_repl + comm(N)
+rest_shard: the side-M (row-sharded) work, scaled from its share of the Gram / apply flops;
+rest_repl : everything else (side-N blocks, Cholesky, core SVD), replicated on every rank;
+comm(N)  : per co-range view an all-reduce of the n x w partial, per side-M orthonormalisation two
+           w x w Gram all-reduces: 2 (N-1)/N bytes / 725 GB/s (measured 8-rank NVLink bus
+           bandwidth, B200_PROFILING.md) + 25 us latency each.
+Usage: python tools/scaling_projection.py > profiles/scaling_projection_r02.md"""
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth as S  # noqa: E402
+from paper_1804_07531_b200 import build, rsvd  # noqa: E402
+
+BUS = 725e9
+LAT = 25e-6
+build.build()
+dev = torch.device("cuda", 0)
+ctx = rsvd.Context(0)
+rows_out = []
+
+
+def measure(fn):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+for name, runs in (("C4", [("krylov", 3, 0), ("single_pass", 1, 0), ("subspace", 3, 1)]),
+                   ("C5", [("subspace", 2, 0), ("subspace", 3, 0), ("krylov", 4, 0)])):
+    cfg = S.CONFIGS[name]
+    A = S.make_matrix_torch(cfg, dev)
+    Om = S.gaussian_test_matrix_torch(cfg.n, cfg.l, cfg, S.ROLE_OMEGA, dev)
+    Omm = S.gaussian_test_matrix_torch(cfg.m, cfg.l, cfg, S.ROLE_OMEGA_M, dev)
+    Phi = S.gaussian_test_matrix_torch(cfg.m, cfg.l2, cfg, S.ROLE_PHI, dev)
+    esz = cfg.itemsize
+    for alg, v, inp in runs:
+        def call(flags=0):
+            if alg == "subspace":
+                return ctx.subspace(A, cfg.k, cfg.p, v, Omm if inp else Om, input=inp, flags=flags)
+            if alg == "krylov":
+                return ctx.block_krylov(A, cfg.k, cfg.p, v, Om, flags=flags)
+            return ctx.single_pass(A, cfg.k, cfg.p, cfg.l2, Om, Phi, flags=flags)
+        t1 = measure(call) * 1e-3
+        info = call(rsvd.RSVD_PROFILE)[3]
+        V = info.view_ms * 1e-3
+        rest = max(t1 - V, 0.0)
+        l = cfg.l
+        W = l * ((v // 2) if (alg == "krylov" and v % 2 == 0) else ((v - 1) // 2 if alg == "krylov" else 1))
+        # co-range views (partials all-reduced): input A -> even views; sizes n x width
+        n_co = v // 2 if not inp else (v + 1) // 2
+        co_bytes = n_co * cfg.n * max(l, W) * 8 if alg != "single_pass" else cfg.n * cfg.l2 * 8
+        n_gram = 2 * ((v + 1) // 2) + 2
+        # side-M share of the between-view flops: Gram + apply of the m-side blocks vs the n-side ones
+        m_side = (cfg.m if not inp else cfg.n)
+        n_side = (cfg.n if not inp else cfg.m)
+        frac_m = m_side / (m_side + n_side)
+        row = {"cfg": name, "call": f"{alg} v={v}" + (" input=A^T" if inp else ""), "T1_ms": t1 * 1e3,
+               "views_ms": V * 1e3, "rest_ms": rest * 1e3}
+        for N in (1, 2, 4, 8):
+            comm = 0.0 if N == 1 else (2 * (N - 1) / N * co_bytes / BUS + (n_co + n_gram) * LAT)
+            tN = V / N + rest * frac_m / N + rest * (1 - frac_m) + comm
+            row[f"T{N}_ms"] = tN * 1e3
+            row[f"x{N}"] = t1 / tN
+        rows_out.append(row)
+        print(row, file=sys.stderr, flush=True)
+    del A
+    torch.cuda.empty_cache()
+
+print("| config | call | 1-GPU ms | views ms | between-views ms | 2 GPUs | 4 GPUs | 8 GPUs |")
+print("|---|---|---|---|---|---|---|---|")
+for r in rows_out:
+    print(f"| {r['cfg']} | {r['call']} | {r['T1_ms']:.1f} | {r['views_ms']:.1f} | {r['rest_ms']:.1f} | "
+          f"{r['T2_ms']:.1f} ({r['x2']:.2f}x) | {r['T4_ms']:.1f} ({r['x4']:.2f}x) | {r['T8_ms']:.1f} ({r['x8']:.2f}x) |")
