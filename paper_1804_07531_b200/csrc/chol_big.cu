@@ -19,53 +19,75 @@ namespace {
 
 constexpr int kNB = 32;
 constexpr int kMaxW = 512;
-constexpr int kThr = 512;      // 128 registers per thread (32-entry column solves in registers)
+constexpr int kThr = 256;      // up to 255 registers per thread (32-entry column solves in registers)
 
 // unblocked guarded factorisation of the jb x jb diagonal block D (smem, col-major ld 33),
-// executed by warp 0; writes defi[] for the block's columns
+// executed by warp 0; writes defi[] for the block's columns and dinv[] = 1 / R_pp (0 for a
+// deficient pivot).  Per pivot one reciprocal (shared by every lane); the trailing update of
+// column `lane` reads row p of R once (broadcast loads, issued together) before it writes.
 __device__ void factor_diag(double* D, int jb, const double* gdiag, const double* ref, int j0, double tol,
-                            double shift, int* defi) {
+                            double shift, int* defi, double* dinv) {
   const int lane = threadIdx.x & 31;
   for (int p = 0; p < jb; ++p) {
     const double d = D[p * 33 + p];
     const double rf = ref ? ref[j0 + p] : (gdiag[j0 + p] + shift);
     const bool def = !(d > tol * rf) || !(rf > 0.0);
     const double rjj = def ? 0.0 : sqrt(d);
+    const double inv = def ? 0.0 : 1.0 / rjj;
     __syncwarp();
-    if (lane > p && lane < jb) D[lane * 33 + p] = def ? 0.0 : D[lane * 33 + p] / rjj;
+    double rpc = 0.0;
+    if (lane > p && lane < jb) {
+      rpc = D[lane * 33 + p] * inv;
+      D[lane * 33 + p] = rpc;
+    }
     if (lane == 0) {
       D[p * 33 + p] = rjj;
       defi[j0 + p] = def ? 1 : 0;
+      dinv[p] = inv;
     }
     __syncwarp();
     // trailing in-block update of column `lane`: D(i, lane) -= R(p, i) R(p, lane), p < i <= lane
     if (!def && lane > p && lane < jb) {
-      const double rpl = D[lane * 33 + p];
-      for (int i = p + 1; i <= lane; ++i) D[lane * 33 + i] -= D[i * 33 + p] * rpl;
+      double v[kNB];
+#pragma unroll
+      for (int i = 0; i < kNB; ++i) v[i] = (i > p && i <= lane) ? D[i * 33 + p] : 0.0;
+#pragma unroll
+      for (int i = 0; i < kNB; ++i)
+        if (i > p && i <= lane) D[lane * 33 + i] = fma(-v[i], rpc, D[lane * 33 + i]);
     }
     __syncwarp();
   }
 }
 
 // upper-triangular inverse of the jb x jb block D (rows of deficient pivots -> 0), warp 0,
-// result in X (smem col-major ld 33)
-__device__ void invert_diag(const double* D, int jb, const int* defi, int j0, double* X) {
+// result in X (smem col-major ld 33).  Column `lane` of X is held in registers (compile-time
+// indices) and solved from the bottom; 1 / D_ii comes from dinv (0 for a deficient pivot).
+__device__ void invert_diag(const double* D, int jb, const int* defi, int j0, const double* dinv, double* X) {
   const int lane = threadIdx.x & 31;
-  // column `lane` of X: back substitution from the bottom
-  for (int i = jb - 1; i >= 0; --i) {
+  double x[kNB];
+#pragma unroll
+  for (int i = kNB - 1; i >= 0; --i) {
     double v = 0.0;
-    if (lane < jb && lane >= i && !defi[j0 + i]) {
+    if (i < jb && lane < jb && lane >= i && !defi[j0 + i]) {
       if (lane == i) {
-        v = 1.0 / D[i * 33 + i];
+        v = dinv[i];
       } else {
-        double s = 0.0;
-        for (int k = i + 1; k <= lane; ++k) s = fma(D[k * 33 + i], X[lane * 33 + k], s);
-        v = -s / D[i * 33 + i];
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int k = i + 1; k < kNB; k += 2) {
+          if (k <= lane) s0 = fma(D[k * 33 + i], x[k], s0);
+          if (k + 1 < kNB && k + 1 <= lane) s1 = fma(D[(k + 1) * 33 + i], x[k + 1], s1);
+        }
+        v = -(s0 + s1) * dinv[i];
       }
     }
-    if (lane < jb) X[lane * 33 + i] = (lane >= i) ? v : 0.0;
-    __syncwarp();
+    x[i] = (i < jb && lane >= i) ? v : 0.0;
   }
+  if (lane < jb)
+#pragma unroll
+    for (int i = 0; i < kNB; ++i)
+      if (i < jb) X[lane * 33 + i] = x[i];
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(kThr, 1) k_chol_big(const double* __restrict__ G, const double* __restrict__ ref,
@@ -77,6 +99,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chol_big(const double* __restrict__
   double* Xd = D + kNB * 33;            // 32 x 33
   double* gdiag = Xd + kNB * 33;        // w (diagonal of G, the default rank-guard reference)
   int* defi = reinterpret_cast<int*>(gdiag + kMaxW);
+  __shared__ double s_dinv[kMaxW];      // 1 / R_jj (0 for a deficient pivot)
   __shared__ double s_shift;
   __shared__ int s_fast;
   const int tid = threadIdx.x;
@@ -106,36 +129,35 @@ __global__ void __launch_bounds__(kThr, 1) k_chol_big(const double* __restrict__
       D[c * 33 + i] = (i <= c) ? R[(int64_t)(j0 + c) * w + j0 + i] : 0.0;
     }
     __syncthreads();
-    if (tid < 32) factor_diag(D, jb, gdiag, ref, j0, tol, shift, defi);
+    if (tid < 32) factor_diag(D, jb, gdiag, ref, j0, tol, shift, defi, s_dinv + j0);
     __syncthreads();
     for (int e = tid; e < jb * jb; e += kThr) {
       const int i = e % jb, c = e / jb;
       R[(int64_t)(j0 + c) * w + j0 + i] = (i <= c) ? D[c * 33 + i] : 0.0;
     }
-    // panel: for trailing column c solve R11^T y = x (forward substitution), y -> P and R
-    if (tid < T) {
-      const int c = t0 + tid;
+    // panel: for trailing column c solve R11^T y = x (forward substitution, column oriented:
+    // y_p = y_p / R_pp, then y_k -= R(p, k) y_p for every k > p — independent updates, so the
+    // dependent chain is one multiply and one FMA per pivot), y -> P and R
+    for (int cc0 = tid; cc0 < T; cc0 += kThr) {
+      const int c = t0 + cc0;
       double y[kNB];
 #pragma unroll
       for (int k = 0; k < kNB; ++k) y[k] = (k < jb) ? R[(int64_t)c * w + j0 + k] : 0.0;
 #pragma unroll
       for (int p = 0; p < kNB; ++p) {
         if (p < jb) {
-          double v = 0.0;
-          if (!defi[j0 + p]) {
-            double s = y[p];
+          const double yp = y[p] * s_dinv[j0 + p];   // 0 for a deficient pivot
+          y[p] = yp;
 #pragma unroll
-            for (int k = 0; k < p; ++k) s = fma(-D[p * 33 + k], y[k], s);
-            v = s / D[p * 33 + p];
-          }
-          y[p] = v;
+          for (int k = p + 1; k < kNB; ++k)
+            if (k < jb) y[k] = fma(-D[k * 33 + p], yp, y[k]);
         }
       }
 #pragma unroll
       for (int k = 0; k < kNB; ++k)
         if (k < jb) {
           R[(int64_t)c * w + j0 + k] = y[k];
-          P[k * kMaxW + tid] = y[k];
+          P[k * kMaxW + cc0] = y[k];
         }
     }
     __syncthreads();
@@ -197,20 +219,30 @@ __global__ void __launch_bounds__(kThr, 1) k_chol_big(const double* __restrict__
       P[k * kMaxW + cc] = R[(int64_t)(t0 + cc) * w + i0 + k];
     }
     __syncthreads();
-    if (tid < 32) invert_diag(D, ib, defi, i0, Xd);
+    if (tid < 32) invert_diag(D, ib, defi, i0, s_dinv + i0, Xd);
     __syncthreads();
     // X(i0.., j) = -Dinv * sum_{k = t0..j} R(i0.., k) X(k, j)   for j >= t0
-    if (tid < T) {
-      const int j = t0 + tid;
+    for (int jj = tid; jj < T; jj += kThr) {
+      const int j = t0 + jj;
       double acc[kNB];
 #pragma unroll
       for (int r = 0; r < kNB; ++r) acc[r] = 0.0;
-      for (int k = t0; k <= j; ++k) {
-        const double x = Rinv[(int64_t)j * w + k];
-        if (x != 0.0) {
+      // the already-computed rows of column j of R^-1 (L2): 4 loads in flight per batch
+      const double* xj = Rinv + (int64_t)j * w;
+      int k = t0;
+      for (; k + 4 <= j + 1; k += 4) {
+        double xv[4];
 #pragma unroll
-          for (int r = 0; r < kNB; ++r) acc[r] = fma(P[r * kMaxW + (k - t0)], x, acc[r]);
-        }
+        for (int u = 0; u < 4; ++u) xv[u] = xj[k + u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int r = 0; r < kNB; ++r) acc[r] = fma(P[r * kMaxW + (k + u - t0)], xv[u], acc[r]);
+      }
+      for (; k <= j; ++k) {
+        const double x = xj[k];
+#pragma unroll
+        for (int r = 0; r < kNB; ++r) acc[r] = fma(P[r * kMaxW + (k - t0)], x, acc[r]);
       }
 #pragma unroll
       for (int r = 0; r < kNB; ++r) {
