@@ -99,9 +99,11 @@ enum {
 #define RSVD_WOOLFE       64u  /* rsvd_single_pass: Alg. 8 (Woolfe variant) instead of Alg. 7   */
 #define RSVD_ORTH_SHIFTED 128u /* rsvd_orth: shifted CholeskyQR3 (a shift pass before the two
                                   CholeskyQR passes; what Alg. 9's projected Krylov blocks use) */
-#define RSVD_ONE_READ     256u /* single pass (fp64, l > 72 or l2 > 144): Y_c and Y_r from ONE read
-                                  of A (thread-block-cluster kernel) instead of two view launches,
-                                  which are faster on device-resident A         */
+#define RSVD_ONE_READ     256u /* single pass, fp64, l <= 128, l2 <= 256: Y_c and Y_r from ONE read
+                                  of A on the thread-block-cluster kernel, whose partial traffic is
+                                  the lowest (l / (64 CL) of A's bytes).  Without it: the one-CTA
+                                  fused kernel for l <= 72, l2 <= 144 and two view launches above,
+                                  faster on device-resident A                    */
 #define RSVD_LC_MINVAR    (-2) /* rsvd_single_pass lc: minimum-variance l_c          */
 #define RSVD_EXT_BWZ      0    /* rsvd_single_pass_extended: Eq. (bwz)               */
 #define RSVD_EXT_BWZ2     1    /* rsvd_single_pass_extended: Eq. (bwzimproved)       */

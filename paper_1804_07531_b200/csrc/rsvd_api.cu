@@ -722,8 +722,10 @@ constexpr double kYcClusterSlotBudget = 24.0e9;  // bytes of the cluster kernel'
 // reduced across a thread-block cluster (view_fused_cluster.cu).  Returns false when not applicable.
 bool sketch_view_cluster(Exec& E, const TS& Om, const TS& Phi, const TS& Yc, const TS& Yr, bool wanted) {
   const int l = Om.w, l2 = Phi.w;
-  const bool narrow = (l <= kFusedMaxL) && ((l2 + 7) / 8 <= kFusedMaxL2T);
-  if (!wanted || E.dtype != RSVD_F64 || !fused_cl_supported(l, l2) || narrow) return false;
+  // with RSVD_ONE_READ the cluster kernel also takes the narrow widths: its Y_c partial traffic is
+  // l / (64 CL) of A's bytes against l / 64 for the one-CTA kernel (C3, l = 70: 3.2x A's bytes of
+  // DRAM traffic in all with the one-CTA kernel)
+  if (!wanted || E.dtype != RSVD_F64 || !fused_cl_supported(l, l2)) return false;
   FusedClArgs a;
   plan_fused_cl(E.m, E.n, l, l2, E.ctx->sms, &a);
   a.ldys = round_up(l, 8);
@@ -1327,8 +1329,8 @@ void prim_fused(Exec& E) {
   TS Om = E.stage_in(SIDE_N, c.Om, c.ldom, l, c.kOm);
   TS Phi = E.stage_in(SIDE_M, c.Phi, c.ldphi, l2, c.kPhi);
   TS Yc = E.new_ts(SIDE_M, l), Yr = E.new_ts(SIDE_N, l2);
-  if (l > kFusedMaxL || (l2 + 7) / 8 > kFusedMaxL2T) {
-    // wide sketches: the cluster kernel (one read of A)
+  if (l > kFusedMaxL || (l2 + 7) / 8 > kFusedMaxL2T || (c.flags & RSVD_ONE_READ)) {
+    // wide sketches (or RSVD_ONE_READ): the cluster kernel (one read of A)
     if (!sketch_view_cluster(E, Om, Phi, Yc, Yr, true)) {
       E.chk(RSVD_E_ARG);
       return;

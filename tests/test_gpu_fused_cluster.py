@@ -34,7 +34,9 @@ def host(t):
 
 @pytest.mark.parametrize("m,n,k,p,l2", [(3000, 4000, 100, 20, 240), (2503, 1100, 80, 20, 203),
                                         (1777, 5003, 60, 20, 170), (4100, 2200, 120, 8, 256),
-                                        (999, 777, 90, 10, 100)])
+                                        (999, 777, 90, 10, 100),
+                                        # narrow widths (C2's 30 / 60, C3's 70 / 140) on the cluster kernel
+                                        (4000, 4000, 20, 10, 60), (6001, 2999, 50, 20, 140)])
 def test_fused_cluster_single_pass_vs_oracle(ctx, m, n, k, p, l2):
     cfg = S.CONFIGS["C4"]
     A = S.make_matrix(cfg, m, n)
