@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "librsvd.so")
-SOURCES = ["view_kernels.cu", "view_tf32.cu", "small_kernels.cu", "chol_big.cu", "jacobi_cluster.cu", "orth_cluster.cu",
+SOURCES = ["view_kernels.cu", "view_tf32.cu", "small_kernels.cu", "chol_big.cu", "jacobi_cluster.cu", "jacobi_gcl.cu", "orth_cluster.cu",
            "minvar.cu", "comm.cu", "view_fused_cluster.cu", "rsvd_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

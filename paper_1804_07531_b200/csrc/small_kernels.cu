@@ -566,17 +566,19 @@ __global__ void __launch_bounds__(LPP == 4 ? 256 : 512) k_jacobi_mid(const doubl
   for (; sweep < max_sweeps; ++sweep) {
     int rotated = 0, big = 0;
     for (int round = 0; round < m1; ++round) {
-      if (active) {
+      {
+        // every lane of every warp runs the round (inactive groups read column 0 and never
+        // store): a warp that reaches the group shuffles diverged takes the serialised BRA.DIV
+        // path (tools/jac_small_probe.cu: thousands of cycles per round instead of ~100)
         int p, q;
-        if (grp == 0) {
-          p = round;
-          q = m1;
-        } else {
-          p = round + grp;
-          if (p >= m1) p -= m1;
-          q = round - grp;
-          if (q < 0) q += m1;
-          if (p > q) { const int tt = p; p = q; q = tt; }
+        {
+          int pp = round + grp;
+          if (pp >= m1) pp -= m1;
+          int qq = round - grp;
+          if (qq < 0) qq += m1;
+          p = grp == 0 ? round : min(pp, qq);
+          q = grp == 0 ? m1 : max(pp, qq);
+          if (!active) p = q = 0;
         }
         double* wp = W + p * RS;
         double* wq = W + q * RS;
@@ -597,14 +599,15 @@ __global__ void __launch_bounds__(LPP == 4 ? 256 : 512) k_jacobi_mid(const doubl
           c1 = fma(x[t + 1], y[t + 1], c1);
         }
         double a = a0 + a1, b = b0 + b1, cc = c0 + c1;
-        apply_pending_j();
+        __syncwarp();
 #pragma unroll
         for (int o = LPP / 2; o > 0; o >>= 1) {
-          a += __shfl_xor_sync(gmask, a, o, LPP);
-          b += __shfl_xor_sync(gmask, b, o, LPP);
-          cc += __shfl_xor_sync(gmask, cc, o, LPP);
+          a += __shfl_xor_sync(0xffffffffu, a, o, LPP);
+          b += __shfl_xor_sync(0xffffffffu, b, o, LPP);
+          cc += __shfl_xor_sync(0xffffffffu, cc, o, LPP);
         }
-        if (cc * cc > tol2 * (a * b) && cc != 0.0) {
+        apply_pending_j();
+        if (active && cc * cc > tol2 * (a * b) && cc != 0.0) {
           rotated = 1;
           big |= (cc * cc > 1e-20 * (a * b)) ? 1 : 0;
           const double d = b - a;
@@ -724,12 +727,29 @@ int launch_jacobi_small(const double* M, int64_t ldm, int trans, int r, int c, d
                         DevStatus* status, cudaStream_t st, int want_j);
 int launch_jacobi_cluster(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
                           double* scratch, DevStatus* status, cudaStream_t st, int want_j);
+int launch_jacobi_gcl(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
+                      double* scratch, DevStatus* status, cudaStream_t st, int want_j);
 
 // want_j = 0: right vectors formed as B^T U S^-1 at the end (leading triplets only accurate)
 int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
                     double* scratch, DevStatus* status, cudaStream_t st, int want_j) {
   if (c < 1 || c > kJacMaxC || r < c || r > kJacMaxC) return RSVD_E_ARG;
   // want_j: 0 = no J, 1 = J everywhere, 2 = J in the 64 < c <= 128 path only
+  // block Jacobi with the Gram inner solver on a cluster (jacobi_gcl.cu) for c > 64, and for
+  // c > 32 when J is accumulated (measured, tools/core_probe.py: w = 60 with J 0.58 vs 0.81 ms,
+  // w = 120 1.15 vs 2.03 ms, w = 250 2.9 vs 8.1 ms); RSVD_JACOBI_GCL_FROM overrides the width,
+  // RSVD_JACOBI_OLD_CLUSTER=1 keeps the one-CTA / plane-rotation cluster kernels
+  static const int gcl_from = [] {
+    const char* e = getenv("RSVD_JACOBI_GCL_FROM");
+    return e ? atoi(e) : 0;
+  }();
+  static const bool old_cluster = getenv_flag_jac("RSVD_JACOBI_OLD_CLUSTER");
+  const bool use_gcl = gcl_from > 0 ? c >= gcl_from : (c > 64 || (c > 32 && want_j == 1));
+  // the Gram-block kernel always accumulates J (+20% at w = 250): both factors then stay
+  // orthonormal to ~1e-14 (B^T U S^-1 loses u sigma_1 / sigma_j on the trailing triplets, which the
+  // full-size C4 Krylov check, k = 100 of l = 120, sees at the 1e-12 level)
+  if (use_gcl && !old_cluster)
+    return launch_jacobi_gcl(M, ldm, trans, r, c, Ul, S, Vr, scratch, status, st, 1);
   if (r <= 64) return launch_jacobi_small(M, ldm, trans, r, c, Ul, S, Vr, status, st, want_j == 1);
   static const int cl_from = [] {
     const char* e = getenv("RSVD_JACOBI_CLUSTER_FROM");
@@ -1494,17 +1514,19 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
   for (; sweep < max_sweeps; ++sweep) {
     int rotated = 0, big = 0;
     for (int round = 0; round < m1; ++round) {
-      if (active) {
+      {
+        // every lane of every warp runs the round (inactive groups read column 0 and never
+        // store): a warp that reaches the group shuffles diverged takes the serialised BRA.DIV
+        // path (tools/jac_small_probe.cu: thousands of cycles per round instead of ~100)
         int p, q;
-        if (grp == 0) {
-          p = round;
-          q = m1;
-        } else {
-          p = round + grp;
-          if (p >= m1) p -= m1;
-          q = round - grp;
-          if (q < 0) q += m1;
-          if (p > q) { const int tt = p; p = q; q = tt; }
+        {
+          int pp = round + grp;
+          if (pp >= m1) pp -= m1;
+          int qq = round - grp;
+          if (qq < 0) qq += m1;
+          p = grp == 0 ? round : min(pp, qq);
+          q = grp == 0 ? m1 : max(pp, qq);
+          if (!active) p = q = 0;
         }
         double* wp = W + p * RS;
         double* wq = W + q * RS;
@@ -1527,14 +1549,15 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
           }
         }
         double a = a0 + a1, b = b0 + b1, cc = c0 + c1;
-        apply_pending_j();
+        __syncwarp();
 #pragma unroll
         for (int o = LPP / 2; o > 0; o >>= 1) {
-          a += __shfl_xor_sync(gmask, a, o, LPP);
-          b += __shfl_xor_sync(gmask, b, o, LPP);
-          cc += __shfl_xor_sync(gmask, cc, o, LPP);
+          a += __shfl_xor_sync(0xffffffffu, a, o, LPP);
+          b += __shfl_xor_sync(0xffffffffu, b, o, LPP);
+          cc += __shfl_xor_sync(0xffffffffu, cc, o, LPP);
         }
-        if (cc * cc > tol2 * (a * b) && cc != 0.0) {
+        apply_pending_j();
+        if (active && cc * cc > tol2 * (a * b) && cc != 0.0) {
           rotated = 1;
           big |= (cc * cc > 1e-20 * (a * b)) ? 1 : 0;
           // rho = 2c / |b - a|, t = sign(b - a) rho / (1 + sqrt(1 + rho^2)), approximate fp64 MUFU ops

@@ -15,7 +15,11 @@ __global__ void __launch_bounds__(256) k_jac(const double* __restrict__ M, int r
                                              int* sweeps_out, double tol) {
   unsigned long long ph[7] = {0, 0, 0, 0, 0, 0, 0};
   long long tA = 0;
+#ifdef TIMING
+#define TS(i) { if (tid == 0) { const long long _t = clock64(); ph[i] += _t - tA; tA = _t; } }
+#else
 #define TS(i) {}
+#endif
   constexpr int RS = LPP * RW + 4;  // padded column stride (bank spread)
   extern __shared__ double W[];     // 128 x RS
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -34,12 +38,15 @@ __global__ void __launch_bounds__(256) k_jac(const double* __restrict__ M, int r
   for (; sweep < 60; ++sweep) {
     int rotated = 0;
     for (int round = 0; round < m1; ++round) {
-      if (active) {
+      if (tid == 0) tA = clock64();
+      {
         int p, q;
-        if (grp == 0) { p = round; q = m1; }
-        else {
-          p = round + grp; if (p >= m1) p -= m1;
-          q = round - grp; if (q < 0) q += m1;
+        {
+          int pp = round + grp; if (pp >= m1) pp -= m1;
+          int qq = round - grp; if (qq < 0) qq += m1;
+          p = grp == 0 ? round : min(pp, qq);
+          q = grp == 0 ? m1 : max(pp, qq);
+          if (!active) p = q = 0;
         }
         double* wp = W + p * RS;
         double* wq = W + q * RS;
@@ -65,27 +72,28 @@ __global__ void __launch_bounds__(256) k_jac(const double* __restrict__ M, int r
         double a = aa[0], b = bb[0], cc = cv[0];
         asm volatile("" :: "d"(a), "d"(b), "d"(cc));
         TS(1);
+        __syncwarp();
         if (FAST >= 3) {
           // column norms only steer the test and the angle: reduce them in fp32
           float af = (float)a, bf = (float)b;
 #pragma unroll
           for (int o = LPP / 2; o > 0; o >>= 1) {
-            af += __shfl_xor_sync(gmask, af, o, LPP);
-            bf += __shfl_xor_sync(gmask, bf, o, LPP);
-            cc += __shfl_xor_sync(gmask, cc, o, LPP);
+            af += __shfl_xor_sync(0xffffffffu, af, o, LPP);
+            bf += __shfl_xor_sync(0xffffffffu, bf, o, LPP);
+            cc += __shfl_xor_sync(0xffffffffu, cc, o, LPP);
           }
           a = af; b = bf;
         } else {
 #pragma unroll
           for (int o = LPP / 2; o > 0; o >>= 1) {
-            a += __shfl_xor_sync(gmask, a, o, LPP);
-            b += __shfl_xor_sync(gmask, b, o, LPP);
-            cc += __shfl_xor_sync(gmask, cc, o, LPP);
+            a += __shfl_xor_sync(0xffffffffu, a, o, LPP);
+            b += __shfl_xor_sync(0xffffffffu, b, o, LPP);
+            cc += __shfl_xor_sync(0xffffffffu, cc, o, LPP);
           }
         }
         asm volatile("" :: "d"(a), "d"(b), "d"(cc));
         TS(2);
-        if (cc * cc > tol2 * (a * b) && cc != 0.0) {
+        if (active && cc * cc > tol2 * (a * b) && cc != 0.0) {
           rotated = 1;
           const double d = b - a, e2 = 2.0 * cc;
           double t;
