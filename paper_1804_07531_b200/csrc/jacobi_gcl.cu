@@ -39,8 +39,8 @@ namespace {
 constexpr int kGThreads = 512;   // 16 warps
 constexpr int kGWarps = kGThreads / 32;
 constexpr int kGMaxC = 512;
-constexpr int kGDsmMaxR = 256;   // DSM pair buffers (two per CTA) up to r = 256 rows
 constexpr int kGMaxRS = kGMaxC + 8 + 4;
+constexpr int kGSmemMax = 225 * 1024;   // dynamic shared memory opt-in (227 KB less the static arrays)
 
 // phase timers (tools/gcl_probe.cu builds this file with RSVD_GCL_TIMING): cycles seen by thread 0
 // of cluster rank 0 per phase of the block round
@@ -175,8 +175,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
                  int max_sweeps, int want_j, int once, int flags_mode, DevStatus* status) {
   constexpr int b = B2 / 2;
   constexpr int NT = B2 / 8;
-  constexpr int T = NT * NT;                       // 8 x 8 Gram tiles
-  constexpr int S = (kGWarps / T) > 0 ? kGWarps / T : 1;   // k-slices per tile
+  constexpr int T = NT * (NT + 1) / 2;             // 8 x 8 Gram tiles on and above the diagonal
+  constexpr int S = kGWarps / T > 0 ? kGWarps / T : 1;   // k-slices per tile (one item per warp)
   constexpr int LG = B2 + 1;                       // G row stride
   constexpr int LJ = B2 + 4;                       // J_l column stride
   constexpr int kInner = ((b * b + 31) / 32) * 32; // threads of the inner sweep (named barrier 1)
@@ -194,6 +194,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
   const int g8 = lane >> 2, t4 = lane & 3;
   const int ncol = nb * b;                         // padded column count (a multiple of 8)
   const int r4 = (r + 3) & ~3, r8 = (r + 7) & ~7;
+  // DSM with J: the pair's J columns (ncol rows) travel below its W columns (rows r8..r8+ncol),
+  // so J_P <- J_P J_l is part of the same DMMA product and push
+  const bool jw = DSM && want_j;
+  const int rows8 = r8 + (jw ? ncol : 0);
   const double tol2 = tol * tol;
   // ---- W = B (B = M or M^T), zero-padded; J = I
   for (int64_t e = (int64_t)rank * kGThreads + tid; e < (int64_t)r * ncol; e += (int64_t)C * kGThreads) {
@@ -202,7 +206,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     if (j < c) v = trans ? M[(int64_t)i * ldm + j] : M[(int64_t)j * ldm + i];
     W[e] = v;
   }
-  if (want_j)
+  if (want_j && !DSM)
     for (int64_t e = (int64_t)rank * kGThreads + tid; e < (int64_t)ncol * ncol; e += (int64_t)C * kGThreads) {
       const int i = (int)(e % ncol), j = (int)(e / ncol);
       J[e] = (i == j) ? 1.0 : 0.0;
@@ -222,27 +226,27 @@ __global__ void __launch_bounds__(kGThreads, 1)
       // 1. block pair -> shared memory (rows r..r8-1 zero), 8 loads in flight per thread; in DSM
       // mode only for the first block round (later pairs are pushed in by the previous owners)
       if (!DSM || first) {
+        // 16 threads per column (B2 <= 32), rows sub, sub + 16, ...: no index division
         constexpr int U = 8;
-        const int tot = B2 * r8;
         double* dst = Wbuf + (DSM ? cur : 0) * (size_t)B2 * RS;
-        for (int e0 = tid; e0 < tot; e0 += U * kGThreads) {
-          double v[U];
-          int at[U];
+        const int lj = tid >> 4, sub = tid & 15;
+        if (lj < B2) {
+          const int X = lj < b ? P : Q, jb = lj < b ? lj : lj - b;
+          const double* srcc = W + (int64_t)(X * b + jb) * r;
+          double* dstc = dst + lj * RS;
+          for (int i0 = sub; i0 < r8; i0 += 16 * U) {
+            double v[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int e = e0 + u * kGThreads;
-            v[u] = 0.0;
-            at[u] = -1;
-            if (e < tot) {
-              const int lj = e / r8, i = e - lj * r8;
-              const int X = lj < b ? P : Q, jb = lj < b ? lj : lj - b;
-              at[u] = lj * RS + i;
-              if (i < r) v[u] = __ldcg(W + (int64_t)(X * b + jb) * r + i);
+            for (int u = 0; u < U; ++u) {
+              const int i = i0 + 16 * u;
+              v[u] = (i < r) ? __ldcg(srcc + i) : 0.0;
             }
-          }
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (at[u] >= 0) dst[at[u]] = v[u];
+            for (int u = 0; u < U; ++u)
+              if (i0 + 16 * u < r8) dstc[i0 + 16 * u] = v[u];
+          }
+          if (jw)   // J = I: the pair's columns of the identity
+            for (int i = sub; i < ncol; i += 16) dstc[r8 + i] = (i == X * b + jb) ? 1.0 : 0.0;
         }
       }
       first = false;
@@ -260,7 +264,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
       // 2. Gram partials on the tensor cores: item = (tile, k-slice)
       for (int item = warp; item < T * S; item += kGWarps) {
         const int tile = item % T, sl = item / T;
-        const int I0 = (tile / NT) * 8, J0 = (tile % NT) * 8;
+        int ti = 0, rem = tile;                    // tile -> (ti <= tj), row-major upper triangle
+        while (rem >= NT - ti) { rem -= NT - ti; ++ti; }
+        const int I0 = ti * 8, J0 = (ti + rem) * 8;
         // four independent accumulators (the DMMA latency chain), loads of a group issued first
         double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         const double* ca = Wp + (I0 + g8) * RS + t4;
@@ -367,9 +373,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
         GCL_T(3);
         // 4. W_P <- W_P J_l: DSM into the next owners' buffers, else in place; V columns:
         // J_P <- J_P J_l from global memory, one row per thread
-        if (DSM) apply_jl_to<B2, LJ>(Wp, RS, r8, Jl, s_dst, warp, lane);
+        if (DSM) apply_jl_to<B2, LJ>(Wp, RS, rows8, Jl, s_dst, warp, lane);
         else apply_jl<B2, LJ>(Wp, RS, r8, Jl, warp, lane);
-        if (want_j) {
+        if (want_j && !DSM) {
           for (int i = tid; i < ncol; i += kGThreads) {
             double x[B2];
 #pragma unroll
@@ -390,22 +396,22 @@ __global__ void __launch_bounds__(kGThreads, 1)
         if (!DSM) {
           __syncthreads();
           GCL_T(4);
-          for (int e = tid; e < B2 * r; e += kGThreads) {
-            const int lj = e / r, i = e - lj * r;
+          const int lj = tid >> 4, sub = tid & 15;
+          if (lj < B2) {
             const int gj = lj < b ? P * b + lj : Q * b + (lj - b);
-            W[(int64_t)gj * r + i] = Wp[lj * RS + i];
+            for (int i = sub; i < r; i += 16) W[(int64_t)gj * r + i] = Wp[lj * RS + i];
           }
         }
         GCL_T(5);
       } else if (DSM) {
         // unchanged pair: 16-byte copies into the next owners' buffers
-        const int h8 = r8 >> 1;
+        const int h8 = rows8 >> 1;
         for (int e = tid; e < B2 * h8; e += kGThreads) {
           const int lj = e / h8, i2 = e - lj * h8;
           reinterpret_cast<double2*>(s_dst[lj])[i2] = reinterpret_cast<const double2*>(Wp + lj * RS)[i2];
         }
       }
-      if (!DSM || want_j) __threadfence();
+      if (!DSM) __threadfence();
       cluster.sync();
       if (DSM) cur ^= 1;
       GCL_T(6);
@@ -441,6 +447,12 @@ __global__ void __launch_bounds__(kGThreads, 1)
       const int gj = lj < b ? P * b + lj : Q * b + (lj - b);
       W[(int64_t)gj * r + i] = Wp[lj * RS + i];
     }
+    if (jw)
+      for (int e = tid; e < B2 * ncol; e += kGThreads) {
+        const int lj = e / ncol, i = e - lj * ncol;
+        const int gj = lj < b ? P * b + lj : Q * b + (lj - b);
+        J[(int64_t)gj * ncol + i] = Wp[lj * RS + r8 + i];
+      }
     __threadfence();
     cluster.sync();
   }
@@ -502,13 +514,13 @@ __global__ void __launch_bounds__(kGThreads, 1)
 }
 
 // inner rotations formed once per pair (b threads, one more barrier per round) or by every
-// updating thread (no extra barrier); measured: once from 2b = 24 (RSVD_GCL_ONCE=0/1 overrides)
+// updating thread (no extra barrier, the default: measured faster at every 2b; RSVD_GCL_ONCE=1)
 static int gcl_once(int B2) {
   static const int env = [] {
     const char* e = getenv("RSVD_GCL_ONCE");
     return e ? atoi(e) : -1;
   }();
-  return env >= 0 ? env : (B2 >= 24 ? 1 : 0);
+  return env >= 0 ? env : 0;
 }
 
 // bit 0: no early exit on small cosines (RSVD_GCL_MODE)
@@ -522,7 +534,7 @@ static int gcl_mode() {
 
 template <int B2, bool DSM>
 size_t gcl_smem(int RS) {
-  constexpr int NT = B2 / 8, T = NT * NT, S = (kGWarps / T) > 0 ? kGWarps / T : 1;
+  constexpr int NT = B2 / 8, T = NT * (NT + 1) / 2, S = kGWarps / T > 0 ? kGWarps / T : 1;
   return ((DSM ? 2 : 1) * (size_t)B2 * RS + 2 * B2 * (B2 + 1) + B2 * (B2 + 4) + (size_t)S * B2 * B2) * 8;
 }
 
@@ -533,8 +545,7 @@ int launch_gcl_t(int C, const double* M, int64_t ldm, int trans, int r, int c, d
   const size_t smem = gcl_smem<B2, DSM>(RS);
   static std::atomic<bool> attr{false};  // set once per process (calls may come from several threads)
   if (!attr) {
-    cudaFuncSetAttribute(k_jacobi_gcl<B2, DSM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)gcl_smem<B2, DSM>(DSM ? kGDsmMaxR + 12 : kGMaxRS));
+    cudaFuncSetAttribute(k_jacobi_gcl<B2, DSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGSmemMax);
     cudaFuncSetAttribute(k_jacobi_gcl<B2, DSM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
@@ -594,13 +605,15 @@ int launch_jacobi_gcl(const double* M, int64_t ldm, int trans, int r, int c, dou
   double* J = W + (int64_t)r * kGMaxC;              // ncol x ncol
   double* sval = J + (int64_t)kGMaxC * kGMaxC;      // 2 * kGMaxC
   int* flags = reinterpret_cast<int*>(sval + 2 * kGMaxC);
-  const int RS = ((r + 7) & ~7) + 4;
-  const bool dsm = r <= kGDsmMaxR;
-#define GCL_CASE(B2V)                                                                                          \
-  case B2V:                                                                                                    \
-    return dsm ? launch_gcl_t<B2V, true>(C, M, ldm, trans, r, c, Ul, S, Vr, W, J, sval, flags, RS, status, st, \
-                                         want_j)                                                               \
-               : launch_gcl_t<B2V, false>(C, M, ldm, trans, r, c, Ul, S, Vr, W, J, sval, flags, RS, status, st, \
+  // DSM (two pair buffers per CTA, J rows carried when wanted) when it fits in shared memory
+  const int r8 = (r + 7) & ~7;
+  const int RSd = r8 + (want_j ? ncol : 0) + 4, RSg = r8 + 4;
+#define GCL_CASE(B2V)                                                                                             \
+  case B2V:                                                                                                       \
+    return gcl_smem<B2V, true>(RSd) <= (size_t)kGSmemMax - 4096                                                   \
+               ? launch_gcl_t<B2V, true>(C, M, ldm, trans, r, c, Ul, S, Vr, W, J, sval, flags, RSd, status, st,    \
+                                         want_j)                                                                  \
+               : launch_gcl_t<B2V, false>(C, M, ldm, trans, r, c, Ul, S, Vr, W, J, sval, flags, RSg, status, st,   \
                                           want_j);
   switch (2 * b) {
     GCL_CASE(8)
