@@ -25,12 +25,12 @@ constexpr int kThr = 256;      // up to 255 registers per thread (32-entry colum
 // executed by warp 0; writes defi[] for the block's columns and dinv[] = 1 / R_pp (0 for a
 // deficient pivot).  Per pivot one reciprocal (shared by every lane); the trailing update of
 // column `lane` reads row p of R once (broadcast loads, issued together) before it writes.
-__device__ void factor_diag(double* D, int jb, const double* gdiag, const double* ref, int j0, double tol,
+__device__ void factor_diag(double* D, int jb, const double* gdiag, bool has_ref, int j0, double tol,
                             double shift, int* defi, double* dinv) {
   const int lane = threadIdx.x & 31;
   for (int p = 0; p < jb; ++p) {
     const double d = D[p * 33 + p];
-    const double rf = ref ? ref[j0 + p] : (gdiag[j0 + p] + shift);
+    const double rf = has_ref ? gdiag[j0 + p] : (gdiag[j0 + p] + shift);
     const bool def = !(d > tol * rf) || !(rf > 0.0);
     const double rjj = def ? 0.0 : sqrt(d);
     const double inv = def ? 0.0 : 1.0 / rjj;
@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(kThr, 1) k_chol_big(const double* __restrict__
     if (i == c) v += shift;
     R[e] = v;
   }
-  for (int j = tid; j < w; j += kThr) gdiag[j] = G[(int64_t)j * w + j];
+  // guard references in shared memory (ref, else diag(G)): no global load on the pivot chain
+  for (int j = tid; j < w; j += kThr) gdiag[j] = ref ? ref[j] : G[(int64_t)j * w + j];
   __syncthreads();
 
   for (int j0 = 0; j0 < w; j0 += kNB) {
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(kThr, 1) k_chol_big(const double* __restrict__
       D[c * 33 + i] = (i <= c) ? R[(int64_t)(j0 + c) * w + j0 + i] : 0.0;
     }
     __syncthreads();
-    if (tid < 32) factor_diag(D, jb, gdiag, ref, j0, tol, shift, defi, s_dinv + j0);
+    if (tid < 32) factor_diag(D, jb, gdiag, ref != nullptr, j0, tol, shift, defi, s_dinv + j0);
     __syncthreads();
     for (int e = tid; e < jb * jb; e += kThr) {
       const int i = e % jb, c = e / jb;

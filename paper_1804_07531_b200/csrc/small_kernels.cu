@@ -174,9 +174,12 @@ __global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, con
   int* defi = reinterpret_cast<int*>(S + w * w);
   __shared__ double s_shift;
   __shared__ int s_fast;
+  __shared__ double s_ref[kCholMaxW];   // guard references: a global load per pivot would sit on
+                                        // the pivot chain (an L2 round trip per column)
   const int tid = threadIdx.x, nt = blockDim.x;
   if (ref == nullptr && shift_coef == 0.0 && chol_near_identity(G, w, R, Rinv, status, &s_fast)) return;
   for (int e = tid; e < w * w; e += nt) S[e] = G[e];
+  for (int j = tid; j < w; j += nt) s_ref[j] = ref ? ref[j] : G[j * w + j];
   if (tid == 0) {
     // shifted CholeskyQR (Fukaya et al.): G + s I, s = shift_coef * ||Y||_F^2 >= shift_coef ||Y||_2^2
     double tr = 0.0;
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, con
   for (int j = 0; j < w; ++j) {
     // every thread derives the pivot itself (no broadcast barrier); rsqrt gives 1/R_jj and R_jj
     const double d = S[j * w + j];
-    const double rf = ref ? ref[j] : (G[j * w + j] + s_shift * (shift_coef > 0.0));
+    const double rf = ref ? s_ref[j] : (s_ref[j] + s_shift * (shift_coef > 0.0));
     const bool def = !(d > tol * rf) || !(rf > 0.0);
     const double inv = def ? 0.0 : rsqrt(d);
     // row j of R: R(j,i) = S(j,i) / R_jj, i > j  (S(j,i) at S[i*w + j])

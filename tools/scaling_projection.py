@@ -1,11 +1,14 @@
 """Projected strong scaling of the row-sharded path from measured 1-GPU phase times.
 
-For each call: T_1 = measured call time (graph replay, CUDA events), V = its A-view kernel time
-(RSVD_PROFILE), rest = T_1 - V (orthonormalisation, core SVD, small kernels).  With A row-sharded
-over N GPUs (one process per GPU, NCCL):
-    T_N = V / N + rest_shard / N + rest_repl + comm(N)
-rest_shard: the side-M (row-sharded) work, scaled from its share of the Gram / apply flops;
-rest_repl : everything else (side-N blocks, Cholesky, core SVD), replicated on every rank;
+For each call: T_1 = measured call time (graph replay, CUDA events); its kernels are timed with
+CUPTI (torch.profiler) and classified:
+  V     : the A-view kernels (the library's own RSVD_PROFILE view time), / N;
+  repl  : the w x w work every rank repeats (core Jacobi, Cholesky / triangular inverse, MinVar,
+          small products) plus the launch gaps (T_1 minus the summed kernel time);
+  tall  : everything else, including the view kernels that run the Grams / applies of wide
+          tall-skinny blocks (profiled k_view_* time minus V), slot sums, copies; split by the side-M
+          share of the rows (side-M blocks are row-sharded: / N; side-N blocks replicated).
+    T_N = V / N + tall_M / N + tall_N + repl + comm(N)
 comm(N)  : per co-range view an all-reduce of the n x w partial, per side-M orthonormalisation two
            w x w Gram all-reduces: 2 (N-1)/N bytes / 725 GB/s (measured 8-rank NVLink bus
            bandwidth, B200_PROFILING.md) + 25 us latency each.
@@ -42,6 +45,34 @@ def measure(fn):
     return statistics.median(ts)
 
 
+REPL = ("k_jacobi", "k_chol", "k_minvar", "k_small_gemm", "k_diag", "k_tri_inv", "k_pinv_svd", "k_nys",
+        "k_symmetrize", "k_mask_cols", "k_square")
+
+
+def kernel_split(fn, reps=2):
+    """(view_s, repl_s, tall_s) kernel time per call"""
+    from torch.profiler import ProfilerActivity, profile
+    fn()
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+    v = r = t = 0.0
+    for ev in prof.events():
+        if ev.device_type != torch.autograd.DeviceType.CUDA:
+            continue
+        us = ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
+        nm = ev.name.replace("(anonymous namespace)::", "").replace("rsvd::", "").replace("void ", "")
+        if "k_view" in nm:
+            v += us
+        elif any(k in nm for k in REPL):
+            r += us
+        else:
+            t += us
+    return v * 1e-6 / reps, r * 1e-6 / reps, t * 1e-6 / reps
+
+
 for name, runs in (("C4", [("krylov", 3, 0), ("single_pass", 1, 0), ("subspace", 3, 1)]),
                    ("C5", [("subspace", 2, 0), ("subspace", 3, 0), ("krylov", 4, 0)])):
     cfg = S.CONFIGS[name]
@@ -58,8 +89,10 @@ for name, runs in (("C4", [("krylov", 3, 0), ("single_pass", 1, 0), ("subspace",
                 return ctx.block_krylov(A, cfg.k, cfg.p, v, Om, flags=flags)
             return ctx.single_pass(A, cfg.k, cfg.p, cfg.l2, Om, Phi, flags=flags)
         t1 = measure(call) * 1e-3
-        info = call(rsvd.RSVD_PROFILE)[3]
-        V = info.view_ms * 1e-3
+        Vall, repl, tall = kernel_split(call)
+        V = call(rsvd.RSVD_PROFILE)[3].view_ms * 1e-3      # the A views alone
+        tall += max(Vall - V, 0.0)                           # view kernels on tall-skinny blocks
+        gaps = max(t1 - (V + repl + tall), 0.0)              # launch gaps: replicated
         rest = max(t1 - V, 0.0)
         l = cfg.l
         W = l * ((v // 2) if (alg == "krylov" and v % 2 == 0) else ((v - 1) // 2 if alg == "krylov" else 1))
@@ -67,15 +100,15 @@ for name, runs in (("C4", [("krylov", 3, 0), ("single_pass", 1, 0), ("subspace",
         n_co = v // 2 if not inp else (v + 1) // 2
         co_bytes = n_co * cfg.n * max(l, W) * 8 if alg != "single_pass" else cfg.n * cfg.l2 * 8
         n_gram = 2 * ((v + 1) // 2) + 2
-        # side-M share of the between-view flops: Gram + apply of the m-side blocks vs the n-side ones
+        # side-M share of the tall-skinny work (Grams, applies of the m-side blocks)
         m_side = (cfg.m if not inp else cfg.n)
         n_side = (cfg.n if not inp else cfg.m)
         frac_m = m_side / (m_side + n_side)
         row = {"cfg": name, "call": f"{alg} v={v}" + (" input=A^T" if inp else ""), "T1_ms": t1 * 1e3,
-               "views_ms": V * 1e3, "rest_ms": rest * 1e3}
+               "views_ms": V * 1e3, "rest_ms": rest * 1e3, "repl_ms": (repl + gaps) * 1e3, "tall_ms": tall * 1e3}
         for N in (1, 2, 4, 8):
             comm = 0.0 if N == 1 else (2 * (N - 1) / N * co_bytes / BUS + (n_co + n_gram) * LAT)
-            tN = V / N + rest * frac_m / N + rest * (1 - frac_m) + comm
+            tN = (V / N + tall * frac_m / N + tall * (1 - frac_m) + repl + gaps + comm) if N > 1 else t1
             row[f"T{N}_ms"] = tN * 1e3
             row[f"x{N}"] = t1 / tN
         rows_out.append(row)
@@ -83,8 +116,8 @@ for name, runs in (("C4", [("krylov", 3, 0), ("single_pass", 1, 0), ("subspace",
     del A
     torch.cuda.empty_cache()
 
-print("| config | call | 1-GPU ms | views ms | between-views ms | 2 GPUs | 4 GPUs | 8 GPUs |")
-print("|---|---|---|---|---|---|---|---|")
+print("| config | call | 1-GPU ms | views ms | replicated ms | tall-skinny ms | 2 GPUs | 4 GPUs | 8 GPUs |")
+print("|---|---|---|---|---|---|---|---|---|")
 for r in rows_out:
-    print(f"| {r['cfg']} | {r['call']} | {r['T1_ms']:.1f} | {r['views_ms']:.1f} | {r['rest_ms']:.1f} | "
+    print(f"| {r['cfg']} | {r['call']} | {r['T1_ms']:.1f} | {r['views_ms']:.1f} | {r['repl_ms']:.1f} | {r['tall_ms']:.1f} | "
           f"{r['T2_ms']:.1f} ({r['x2']:.2f}x) | {r['T4_ms']:.1f} ({r['x4']:.2f}x) | {r['T8_ms']:.1f} ({r['x8']:.2f}x) |")
