@@ -147,6 +147,10 @@ int launch_fill(double* dst, int64_t count, double v, cudaStream_t st);
 // out (rows x c) += T (rows x c), column-major
 int launch_add_cols(const double* T, int64_t ldt, double* out, int64_t ldo, int64_t rows, int c, cudaStream_t st);
 // out (rows x c) -= T (rows x c), column-major
+// F (n x w, ld ldf, column-major) -> (to_chunks) / <- chunked layout: chunk q = rows [q cs, (q+1) cs)
+// as a column-major cs x w block at buf + q cs w; rows >= n are zero in the chunks
+int launch_rows_chunk(double* F, int64_t ldf, int64_t n, double* buf, int64_t cs, int nchunks, int w, int to_chunks,
+                      cudaStream_t st);
 int launch_sub_cols(const double* T, int64_t ldt, double* out, int64_t ldo, int64_t rows, int c, cudaStream_t st);
 // triangular-system helpers for Alg. 7: out (c x c) = upper-triangular inverse of R (c x c)
 int launch_tri_inv(const double* R, int c, double* Rinv, DevStatus* status, cudaStream_t st);

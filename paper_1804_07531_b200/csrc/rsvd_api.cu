@@ -162,6 +162,12 @@ struct Exec {
   int dtype = RSVD_F64;
   int64_t lda = 0, m = 0, n = 0;
   int64_t m_glob = 0;   // global row count of A (m = this rank's rows)
+  // n-side sharding (Alg. 2 / 9 under a communicator of N > 1 ranks): side-N blocks
+  // hold only this rank's chunk of rows [n0, n0 + n_loc) of the n-long side, stored with ld = n_cs
+  // (the chunk size, a multiple of 32, equal on every rank).  A^T Y is a local full-length partial
+  // followed by a reduce-scatter; A X first all-gathers X; Grams of side-N blocks are all-reduced.
+  bool shard_n = false;
+  int64_t n_cs = 0, n0 = 0, n_loc = 0;
   // host-transfer plan (executed outside the graph); esz = element bytes (8, or 4 for fp32)
   struct H2D { void* dst; int64_t ldd; const void* src; int64_t lds; int64_t rows; int64_t cols; int esz = 8; };
   struct D2H { void* dst; int64_t ldd; const void* src; int64_t lds; int64_t rows; int64_t cols; int esz = 8; };
@@ -191,11 +197,13 @@ struct Exec {
   void chk(int r) {
     if (rc == RSVD_OK && r != RSVD_OK) rc = r;
   }
-  int64_t side_rows(Side s) const { return s == SIDE_M ? m : n; }
+  int64_t side_rows(Side s) const { return s == SIDE_M ? m : (shard_n ? n_loc : n); }
+  // global length of a side (sharded or not)
+  int64_t side_rows_glob(Side s) const { return s == SIDE_M ? m_glob : n; }
   TS new_ts(Side s, int w) {
     TS t;
     t.rows = side_rows(s);
-    t.ld = round_up(std::max<int64_t>(t.rows, 1), 32);
+    t.ld = (s == SIDE_N && shard_n) ? n_cs : round_up(std::max<int64_t>(t.rows, 1), 32);
     t.w = w;
     t.p = alloc(t.ld * w);
     return t;
@@ -209,7 +217,53 @@ struct Exec {
   // a communicator exists (rsvd_comm_init; also with one rank, which runs the sharded code path
   // on one GPU: sharded CholeskyQR, all-reduced Grams and A^T Y partials, NCCL in the graph)
   bool collective() const { return ctx->comm != nullptr; }
-  bool sharded(Side s) const { return s == SIDE_M && collective(); }
+  bool sharded(Side s) const { return s == SIDE_M ? collective() : shard_n; }
+  // enable n-side sharding for this call (after bind_A): every rank must own >= 1 row of side N
+  void plan_shard_n() {
+    shard_n = false;
+    if (!collective() || ctx->nranks < 2 || getenv_flag("RSVD_NO_SHARD_N")) return;
+    const int N = ctx->nranks;
+    const int64_t cs = round_up((n + N - 1) / N, 32);
+    if ((N - 1) * cs >= n) return;
+    shard_n = true;
+    n_cs = cs;
+    n0 = (int64_t)ctx->rank * cs;
+    n_loc = std::min<int64_t>(cs, n - n0);
+  }
+  // full (n x w) copy of an n-sharded side-N block: all-gather of the chunks
+  TS gather_n(const TS& X) {
+    TS F;
+    F.rows = n;
+    F.ld = round_up(n, 32);
+    F.w = X.w;
+    F.p = alloc(F.ld * X.w);
+    gather_n_into(X, F.p, F.ld);
+    return F;
+  }
+  void gather_n_into(const TS& X, double* dst, int64_t ldd) {
+    double* buf = alloc(n_cs * X.w * ctx->nranks);
+    if (!live()) return;
+    std::string e;
+    const int r = ctx->comm->allgather(X.p, buf, (size_t)(n_cs * X.w), st, &e);
+    if (r != RSVD_OK) {
+      set_err(ctx, "%s", e.c_str());
+      chk(r);
+      return;
+    }
+    chk(launch_rows_chunk(dst, ldd, n, buf, n_cs, ctx->nranks, X.w, 0, st));
+  }
+  // Y (this rank's chunk, ld n_cs) = sum over ranks of the full-length partials F, chunk n0
+  void reduce_scatter_n(const TS& F, const TS& Y) {
+    double* buf = alloc(n_cs * F.w * ctx->nranks);
+    if (!live()) return;
+    chk(launch_rows_chunk(F.p, F.ld, n, buf, n_cs, ctx->nranks, F.w, 1, st));
+    std::string e;
+    const int r = ctx->comm->reduce_scatter(buf, Y.p, (size_t)(n_cs * F.w), st, &e);
+    if (r != RSVD_OK) {
+      set_err(ctx, "%s", e.c_str());
+      chk(r);
+    }
+  }
 
   void allreduce(double* p, int64_t count) {
     if (!live()) return;
@@ -236,10 +290,30 @@ struct Exec {
   // One view of A (or, with nr >= 0, of its row panel [r0, r0 + nr): then Y / X are the panel's
   // row slices, nothing is all-reduced, and a_keep loads the panel with evict_last for a re-read).
   void view(Side from, const TS& X, const TS& Y, int64_t r0 = 0, int64_t nr = -1, int a_keep = 0) {
+    if (shard_n && nr < 0) {
+      const size_t mk = mark();
+      if (from == SIDE_N) {                  // A X: X all-gathered to full length first
+        TS F = gather_n(X);
+        view_local(from, F, Y, 0, -1, 0, false);
+      } else {                               // A^T Y: full-length local partial, reduce-scatter
+        TS F;
+        F.rows = n;
+        F.ld = round_up(n, 32);
+        F.w = Y.w;
+        F.p = alloc(F.ld * Y.w);
+        view_local(from, X, F, 0, -1, 0, false);
+        reduce_scatter_n(F, Y);
+      }
+      release(mk);
+      return;
+    }
+    view_local(from, X, Y, r0, nr, a_keep, true);
+  }
+  void view_local(Side from, const TS& X, const TS& Y, int64_t r0, int64_t nr, int a_keep, bool reduce) {
     const bool panel = nr >= 0;
     const int64_t rows_v = panel ? nr : m;
     if (dtype == RSVD_F32) {
-      view32(from, X, Y, r0, nr);
+      view32(from, X, Y, r0, nr, reduce);
       return;
     }
     const int w = X.w;
@@ -278,11 +352,11 @@ struct Exec {
       }
       release(mk);
     }
-    if (from == SIDE_M && collective() && !panel) allreduce(Y.p, Y.ld * Y.w);
+    if (from == SIDE_M && collective() && !panel && reduce) allreduce(Y.p, Y.ld * Y.w);
   }
 
   // fp32 A: split X into tf32 hi / lo parts, tcgen05 3xTF32 view into fp64 partial slots
-  void view32(Side from, const TS& X, const TS& Y, int64_t r0 = 0, int64_t nr = -1) {
+  void view32(Side from, const TS& X, const TS& Y, int64_t r0, int64_t nr, bool reduce) {
     const bool panel = nr >= 0;
     const int64_t rows_v = panel ? nr : m;
     const int w = X.w;
@@ -328,7 +402,7 @@ struct Exec {
       }
       release(mk);
     }
-    if (from == SIDE_M && collective() && !panel) allreduce(Y.p, Y.ld * Y.w);
+    if (from == SIDE_M && collective() && !panel && reduce) allreduce(Y.p, Y.ld * Y.w);
   }
 
   // G (a x b, col-major ld a) = Xa^T Xb over the side's rows (+ all-reduce when sharded)
@@ -434,7 +508,7 @@ struct Exec {
       R0s = R0;
       double* R0i = alloc((int64_t)w * w);
       // the shift must be identical on every rank: the GLOBAL row count of a sharded side
-      const double rows_all = (double)(sharded(s) ? m_glob : Y.rows);
+      const double rows_all = (double)(sharded(s) ? side_rows_glob(s) : Y.rows);
       const double coef = 11.0 * (rows_all * w + (double)w * (w + 1)) * 1.1102230246251565e-16;
       cross(s, Y, Y, G);
       if (live()) chk(launch_chol_ref(G, nullptr, w, 0.0, R0, R0i, nullptr, st, coef));
@@ -569,6 +643,8 @@ struct Exec {
   TS stage_in(Side s, const void* src, int64_t ld_user, int w, PtrKind kind) {
     (void)kind;
     TS t = new_ts(s, w);
+    if (s == SIDE_N && shard_n && src)   // this rank's chunk of the caller's n-long array
+      src = static_cast<const char*>(src) + n0 * (dtype == RSVD_F32 ? 4 : 8);
     if (dtype == RSVD_F32) {
       float* f = alloc_f(t.ld * w);
       h2d.push_back({f, t.ld, src, ld_user, t.rows, w, 4});
@@ -624,8 +700,16 @@ void write_outputs(Exec& E, Side side_c, Side side_r, const TS& Qc, const TS& Qr
     } else {
       if (c.kV == PTR_NULL) return;
       int64_t ld;
-      double* o = E.out_ptr(c.V, c.ldv, Q.rows, k, c.kV, &ld);
-      E.lift(Q, M, k, o, ld);
+      double* o = E.out_ptr(c.V, c.ldv, E.n, k, c.kV, &ld);
+      if (E.shard_n) {   // lift this rank's chunk, all-gather the full V
+        const size_t mk = E.mark();
+        TS L = E.new_ts(SIDE_N, k);
+        E.lift(Q, M, k, L.p, L.ld);
+        E.gather_n_into(L, o, ld);
+        E.release(mk);
+      } else {
+        E.lift(Q, M, k, o, ld);
+      }
     }
   };
   emit(side_c, Qc, Uh);
@@ -1468,6 +1552,8 @@ void bind_A(Exec& E, const Call& call) {
     E.A32 = reinterpret_cast<const float*>(E.A);
     E.A = nullptr;
   }
+  // the n-long side is sharded too for the generalized subspace iteration and block Krylov
+  if (call.alg == 0 || call.alg == 1) E.plan_shard_n();
 }
 
 // Wait for the ctx stream.  With a communicator: its wait (NCCL polls ncclCommGetAsyncError and

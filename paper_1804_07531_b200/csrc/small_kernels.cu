@@ -926,6 +926,29 @@ int launch_copy_cols(const double* src, int64_t lds, double* dst, int64_t ldd, i
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
+// n-side sharding (rsvd_api.cu Exec::gather_n / reduce_scatter_n): a column-major n x w block F
+// (ld ldf) <-> the chunked layout of the collectives, chunk q = global rows [q cs, (q + 1) cs) as
+// a column-major cs x w block at buf + q cs w (rows >= n zero in the chunked copy)
+__global__ void k_rows_chunk(double* __restrict__ F, int64_t ldf, int64_t n, double* __restrict__ buf, int64_t cs,
+                             int w, int64_t total, int to_chunks) {
+  const int64_t gr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (gr >= total) return;
+  const int64_t q = gr / cs, il = gr - q * cs;
+  double* b = buf + q * cs * w + (int64_t)j * cs + il;
+  if (to_chunks) *b = gr < n ? F[(int64_t)j * ldf + gr] : 0.0;
+  else if (gr < n) F[(int64_t)j * ldf + gr] = *b;
+}
+
+int launch_rows_chunk(double* F, int64_t ldf, int64_t n, double* buf, int64_t cs, int nchunks, int w, int to_chunks,
+                      cudaStream_t st) {
+  const int64_t total = cs * nchunks;
+  if (total <= 0 || w <= 0) return RSVD_OK;
+  k_rows_chunk<<<dim3((unsigned)((total + 255) / 256), (unsigned)w), 256, 0, st>>>(F, ldf, n, buf, cs, w, total,
+                                                                                    to_chunks);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
 __global__ void k_fill(double* dst, int64_t n, double v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[i] = v;

@@ -265,6 +265,43 @@ def test_sharded_equals_unsharded(lib, N):
     check(A, U, s, V, host(U1), host(s1), host(V1))
 
 
+@pytest.mark.parametrize("N", NS)
+@pytest.mark.parametrize("alg,v,inp,dt", [("subspace", 3, 0, "f64"), ("subspace", 4, 1, "f64"), ("krylov", 4, 0, "f64"),
+                                          ("krylov", 5, 1, "f64"), ("krylov", 4, 0, "f32")])
+def test_shard_n_equals_replicated_n(lib, N, alg, v, inp, dt, monkeypatch):
+    """n-side sharding (Alg. 2 / 9 under a communicator: side-N blocks split into 32-aligned row
+    chunks, A^T Y reduce-scattered, X all-gathered before A X, V all-gathered at the end) against
+    the replicated side-N schedule (RSVD_NO_SHARD_N=1) on the same shards: rounding only, and V
+    full length and bitwise equal on all ranks.  n = 2300 gives every rank a chunk at N = 2, 3, 8
+    (the last one ragged)."""
+    cfg, A = problem("C2", 2600, 2300, dt)
+    m, n = A.shape
+    rows = m if inp else n
+    Om = S.gaussian_test_matrix(rows, cfg.l, cfg, S.ROLE_OMEGA_M if inp else S.ROLE_OMEGA)
+    if dt == "f32":
+        Om = Om.astype(np.float32)
+    Ad, Omd = torch.from_numpy(A).cuda(), colmajor_dev(Om)
+
+    def fn(ctx, sh):
+        As = Ad[sh.row0:sh.row0 + sh.m_local]
+        Os = Omd[sh.row0:sh.row0 + sh.m_local] if inp else Omd
+        f = ctx.subspace if alg == "subspace" else ctx.block_krylov
+        return f(As, cfg.k, cfg.p, v, Os, input=inp, m=m, row0=sh.row0)[:3]
+
+    shards, outs = run_sharded(lib, N, m, fn)
+    U, s, V = assemble(shards, outs)
+    assert V.shape == (n, cfg.k)
+    monkeypatch.setenv("RSVD_NO_SHARD_N", "1")
+    shards, outs = run_sharded(lib, N, m, fn)
+    Ur, sr, Vr = assemble(shards, outs)
+    A64 = A.astype(np.float64)
+    check(A64, U, s, V, Ur, sr, Vr, dt=dt)
+    if dt == "f64":   # rounding-level agreement (fp64 views: only the reduction order differs)
+        assert np.max(np.abs(s - sr) / sr) <= 1e-12
+    Uo, so, Vo, _ = O.svd_of(A64, alg, cfg.k, cfg.p, v=v, Omega=Om.astype(np.float64), transpose=bool(inp))
+    check(A64, U, s, V, Uo, so, Vo, dt=dt)
+
+
 def test_loopback_failing_rank_releases_peers(lib):
     """A rank whose call fails (here: an invalid argument detected on the device side of the call,
     a zero-row shard) must not leave its peers blocked: they return RSVD_E_NCCL."""

@@ -7,11 +7,17 @@ CUPTI (torch.profiler) and classified:
           small products) plus the launch gaps (T_1 minus the summed kernel time);
   tall  : everything else, including the view kernels that run the Grams / applies of wide
           tall-skinny blocks (profiled k_view_* time minus V), slot sums, copies; split by the side-M
-          share of the rows (side-M blocks are row-sharded: / N; side-N blocks replicated).
-    T_N = V / N + tall_M / N + tall_N + repl + comm(N)
-comm(N)  : per co-range view an all-reduce of the n x w partial, per side-M orthonormalisation two
-           w x w Gram all-reduces: 2 (N-1)/N bytes / 725 GB/s (measured 8-rank NVLink bus
-           bandwidth, B200_PROFILING.md) + 25 us latency each.
+          share of the rows.  Alg. 2 / 9 shard BOTH sides (side M by A's row shards, side N by
+          32-aligned row chunks, Exec::plan_shard_n): all of it / N.  The single pass keeps side N
+          replicated: side-M share / N, side-N share replicated.
+    T_N = V / N + tall / N + repl + comm(N)                     (Alg. 2 / 9)
+    T_N = V / N + tall_M / N + tall_N + repl + comm(N)          (single pass)
+comm(N)  : Alg. 2 / 9: per co-range view a reduce-scatter of the n x w partial, per range view after
+           the first an all-gather of the n x w basis, the final all-gather of V (n x k), plus the
+           chunk / unchunk copies of those blocks at HBM speed; single pass: the all-reduce of
+           Y_r (n x l2).  Every w x w Gram is all-reduced (latency only).  Bytes moved:
+           (N-1)/N per reduce-scatter / all-gather, 2 (N-1)/N per all-reduce, at 725 GB/s (measured
+           8-rank NVLink bus bandwidth, B200_PROFILING.md) + 25 us latency each.
 Usage: python tools/scaling_projection.py > profiles/scaling_projection_r02.md"""
 import os
 import statistics
@@ -24,6 +30,7 @@ import synth as S  # noqa: E402
 from paper_1804_07531_b200 import build, rsvd  # noqa: E402
 
 BUS = 725e9
+HBM = 6.0e12
 LAT = 25e-6
 build.build()
 dev = torch.device("cuda", 0)
@@ -99,15 +106,25 @@ for name, runs in (("C4", [("krylov", 3, 0), ("single_pass", 1, 0), ("subspace",
         # co-range views (partials all-reduced): input A -> even views; sizes n x width
         n_co = v // 2 if not inp else (v + 1) // 2
         co_bytes = n_co * cfg.n * max(l, W) * 8 if alg != "single_pass" else cfg.n * cfg.l2 * 8
-        n_gram = 2 * ((v + 1) // 2) + 2
+        n_gram = 3 * v + 4
         # side-M share of the tall-skinny work (Grams, applies of the m-side blocks)
         m_side = (cfg.m if not inp else cfg.n)
         n_side = (cfg.n if not inp else cfg.m)
-        frac_m = m_side / (m_side + n_side)
+        frac_m = m_side / (m_side + n_side) if alg == "single_pass" else 1.0
+        width = max(l, W)
+        n_ax = (v + 1) // 2 if not inp else v // 2          # range views (X all-gathered after the first)
         row = {"cfg": name, "call": f"{alg} v={v}" + (" input=A^T" if inp else ""), "T1_ms": t1 * 1e3,
                "views_ms": V * 1e3, "rest_ms": rest * 1e3, "repl_ms": (repl + gaps) * 1e3, "tall_ms": tall * 1e3}
         for N in (1, 2, 4, 8):
-            comm = 0.0 if N == 1 else (2 * (N - 1) / N * co_bytes / BUS + (n_co + n_gram) * LAT)
+            if N == 1:
+                comm = 0.0
+            elif alg == "single_pass":
+                comm = 2 * (N - 1) / N * co_bytes / BUS + (1 + n_gram) * LAT
+            else:
+                nb = cfg.n * width * 8                          # one side-N block
+                moved = n_co * nb + max(n_ax - (0 if inp else 1), 0) * nb + cfg.n * cfg.k * 8
+                n_coll = n_co + max(n_ax - (0 if inp else 1), 0) + 1
+                comm = (N - 1) / N * moved / BUS + (n_coll + n_gram) * LAT + 2 * 2 * moved / HBM
             tN = (V / N + tall * frac_m / N + tall * (1 - frac_m) + repl + gaps + comm) if N > 1 else t1
             row[f"T{N}_ms"] = tN * 1e3
             row[f"x{N}"] = t1 / tN
