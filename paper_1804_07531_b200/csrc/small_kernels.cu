@@ -253,6 +253,8 @@ __global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, con
   }
 }
 
+int launch_chol_cl(const double* G, const double* ref, int w, double tol, double* R, double* Rinv, DevStatus* status,
+                   cudaStream_t st, double shift_coef);
 int launch_chol_big(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
                     DevStatus* status, cudaStream_t st, double shift_coef);
 
@@ -262,6 +264,12 @@ int launch_chol_ref(const double* G, const double* ref, int w, double tol, doubl
     const char* e = getenv("RSVD_CHOL_BIG_FROM");
     return e ? atoi(e) : kCholMaxW + 1;
   }();
+  // the cluster kernel above cl_from (RSVD_CHOL_CL_FROM, default 65; 0 disables it)
+  static const int cl_from = [] {
+    const char* e = getenv("RSVD_CHOL_CL_FROM");
+    return e ? atoi(e) : 65;
+  }();
+  if (cl_from > 0 && w >= cl_from && w >= 33) return launch_chol_cl(G, ref, w, tol, R, Rinv, status, st, shift_coef);
   if (w > kCholMaxW || w >= big_from) return launch_chol_big(G, ref, w, tol, R, Rinv, status, st, shift_coef);
   if (w < 1) return RSVD_E_ARG;
   const size_t smem = (size_t)w * w * 8 + (size_t)w * 4 + 16;
