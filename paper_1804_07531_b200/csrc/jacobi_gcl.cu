@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     k_jacobi_gcl(const double* __restrict__ M, int64_t ldm, int trans, int r, int c, int nb, int RS,
                  double* __restrict__ Ul, double* __restrict__ Sv, double* __restrict__ Vr, double* __restrict__ W,
                  double* __restrict__ J, double* __restrict__ sval_g, int* __restrict__ flags, double tol,
-                 int max_sweeps, int want_j, int once, int flags_mode, DevStatus* status) {
+                 int max_sweeps, int want_j, int once, int flags_mode, int cross, DevStatus* status) {
   constexpr int b = B2 / 2;
   constexpr int NT = B2 / 8;
   constexpr int T = NT * (NT + 1) / 2;             // 8 x 8 Gram tiles on and above the diagonal
@@ -293,6 +293,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
       // symmetric G (upper triangle's partial sums, fixed slice order), J_l = I, and the fresh
       // one-sided test on every pair of the block pair (diagonals summed by the testing thread)
       int need = 0, big = 0;
+      // cross-pair rounds (every block round but a sweep's first, `cross` mode) rotate and test only
+      // the pairs (p in P, q in Q); the sweep's first block round runs the full 2b-column sweep,
+      // which covers every pair inside each block once per sweep
+      const bool full = !cross || br == 0;
       for (int e = tid; e < B2 * B2; e += kGThreads) {
         const int i = e / B2, j = e - i * B2;
         const int lo = i < j ? i : j, hi = i < j ? j : i;
@@ -305,7 +309,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
         Gb[i * LG + j] = s;
         Jl[j * LJ + i] = (i == j) ? 1.0 : 0.0;
-        if (i < j && s != 0.0 && s * s > tol2 * (gi * gj)) {
+        if (i < j && (full || (i < b && j >= b)) && s != 0.0 && s * s > tol2 * (gi * gj)) {
           need = 1;
           if (s * s > 1e-20 * (gi * gj)) big = 1;
         }
@@ -320,12 +324,14 @@ __global__ void __launch_bounds__(kGThreads, 1)
         // kInner threads take part (named barrier 1)
         if (tid < kInner) {
           int gc = 0;
-          for (int ir = 0; ir < B2 - 1; ++ir) {
+          const int nround = full ? B2 - 1 : b;
+          for (int ir = 0; ir < nround; ++ir) {
             if (once) {
               // the round's b rotations formed once (fewer fp64 MUFU ops: 8 b^2 -> 4 b)
               if (tid < b) {
                 int p, q;
-                gpair_of(ir, tid, B2, &p, &q);
+                if (full) gpair_of(ir, tid, B2, &p, &q);
+                else { p = tid; q = b + (tid + ir) % b; }
                 const double* G = Gb + gc * B2 * LG;
                 grot(G[p * LG + p], G[q * LG + q], G[p * LG + q], tol2, &s_cs[tid], &s_sn[tid]);
               }
@@ -334,8 +340,13 @@ __global__ void __launch_bounds__(kGThreads, 1)
             if (tid < b * b) {
               const int k1 = tid / b, k2 = tid - (tid / b) * b;
               int p1, q1, p2, q2;
-              gpair_of(ir, k1, B2, &p1, &q1);
-              gpair_of(ir, k2, B2, &p2, &q2);
+              if (full) {
+                gpair_of(ir, k1, B2, &p1, &q1);
+                gpair_of(ir, k2, B2, &p2, &q2);
+              } else {
+                p1 = k1; q1 = b + (k1 + ir) % b;
+                p2 = k2; q2 = b + (k2 + ir) % b;
+              }
               const double* G = Gb + gc * B2 * LG;
               double* Gn = Gb + (gc ^ 1) * B2 * LG;
               double c1, s1, c2, s2;
@@ -524,6 +535,15 @@ static int gcl_once(int B2) {
 }
 
 // bit 0: no early exit on small cosines (RSVD_GCL_MODE)
+// cross-pair block rounds (RSVD_GCL_CROSS, default 1)
+static int gcl_cross() {
+  static const int env = [] {
+    const char* e = getenv("RSVD_GCL_CROSS");
+    return e ? atoi(e) : 1;
+  }();
+  return env;
+}
+
 static int gcl_mode() {
   static const int env = [] {
     const char* e = getenv("RSVD_GCL_MODE");
@@ -564,7 +584,7 @@ int launch_gcl_t(int C, const double* M, int64_t ldm, int trans, int r, int c, d
   const double tol = 2.220446049250313e-16 * sqrt((double)r);
   const int nb = 2 * C;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, k_jacobi_gcl<B2, DSM>, M, ldm, trans, r, c, nb, RS, Ul, S, Vr, W, J,
-                                           sval, flags, tol, 60, want_j, gcl_once(B2), gcl_mode(), status);
+                                           sval, flags, tol, 60, want_j, gcl_once(B2), gcl_mode(), gcl_cross(), status);
   return e == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
