@@ -2,9 +2,12 @@
 
 * shard planning, unique-id broadcast and max-over-ranks timing (paper_1804_07531_b200.sharding);
 * the row-sharded SCHEDULE (include/rsvd.h MULTI-GPU) as a NumPy emulation with
-  gloo all-reduces: A X local, A^T Y and every Gram / cross product of a row-sharded block
+  gloo collectives: A X local, A^T Y and every Gram / cross product of a row-sharded block
   all-reduced, column-side blocks replicated.  Each rank runs Alg. 2 / 9 / 7 / 8, the extended
   sketch and the row-wise single pass on its row block;
+* the n-side sharding of Alg. 2 / 9 (rsvd_api.cu Exec::plan_shard_n): side-N blocks in 32-aligned
+  row chunks, A^T Y reduced and scattered to the chunks, X all-gathered before A X, side-N Grams
+  all-reduced, the shifted CholeskyQR3 shift from the global length n, V all-gathered at the end;
   the gathered result must equal the single-process oracle (the schedule is exact algebra, so the
   same 1e-10 / 1e-9 tolerances as GPU parity apply).
   This checks the decomposition, not librsvd: the library's own sharded code path (unequal shards,
@@ -71,19 +74,29 @@ class ShardedOps:
         dist.all_reduce(t)
         return t.numpy()
 
+    def sharded(self, side):
+        return side == "M"
+
+    def local_n(self, X):                     # a caller's n-long array -> this rank's side-N block
+        return X
+
+    def finish_n(self, X):                    # this rank's side-N block -> the full n-long output
+        return X
+
     def view(self, from_side, X):             # from N: A X (local, side M); from M: A^T X (all-reduced)
         return self.A @ X if from_side == "N" else self.allreduce(self.A.T @ X)
 
     def cross(self, side, Xa, Xb):
         G = Xa.T @ Xb
-        return self.allreduce(G) if side == "M" else G
+        return self.allreduce(G) if self.sharded(side) else G
+
 
     def orth(self, side, Y, shifted=False):
         """CholeskyQR2 (shifted CholeskyQR3 if `shifted`) with the Gram all-reduced on the sharded
         side; R replicated.  Mirrors Exec::orth / orth_fused."""
         R = np.eye(Y.shape[1])
         if shifted:
-            rows = self.allreduce(np.array([float(Y.shape[0])]))[0] if side == "M" else Y.shape[0]
+            rows = self.allreduce(np.array([float(Y.shape[0])]))[0] if self.sharded(side) else Y.shape[0]
             G = self.cross(side, Y, Y)
             w = Y.shape[1]
             G = G + 11.0 * (rows * w + w * (w + 1)) * 1.1102230246251565e-16 * np.trace(G) * np.eye(w)
@@ -98,8 +111,40 @@ class ShardedOps:
         return Y, R
 
 
+class ShardedOpsN(ShardedOps):
+    """ShardedOps with the n-long side sharded too (Alg. 2 / 9 under N > 1 ranks): chunk size
+    cs = round_up(ceil(n / N), 32), rank r owns rows [r cs, min((r + 1) cs, n)) of every side-N block."""
+
+    def __init__(self, A_local, n, world, rank):
+        super().__init__(A_local)
+        self.n, self.world = n, world
+        self.cs = -(-(-(-n // world)) // 32) * 32
+        assert (world - 1) * self.cs < n          # every rank owns a chunk (as plan_shard_n requires)
+        self.n0 = rank * self.cs
+        self.n_loc = min(self.cs, n - self.n0)
+
+    def sharded(self, side):
+        return True
+
+    def local_n(self, X):
+        return X[self.n0:self.n0 + self.n_loc]
+
+    def finish_n(self, X):
+        pad = np.zeros((self.cs, X.shape[1]))
+        pad[:X.shape[0]] = X
+        parts = [torch.zeros(self.cs, X.shape[1], dtype=torch.float64) for _ in range(self.world)]
+        dist.all_gather(parts, torch.from_numpy(pad))
+        return np.vstack([t.numpy() for t in parts])[:self.n]
+
+    def view(self, from_side, X):
+        if from_side == "N":                      # all-gather X's chunks, then A X (local rows)
+            return self.A @ self.finish_n(X)
+        full = self.allreduce(self.A.T @ X)       # reduce (gloo has no reduce-scatter) ...
+        return full[self.n0:self.n0 + self.n_loc]   # ... and keep this rank's chunk
+
+
 def _alg2_sharded(ops, k, p, v, Om):
-    Qr = Om.copy()
+    Qr = ops.local_n(Om).copy()
     Qc = Rc = Rr = None
     for j in range(1, v + 1):
         if j % 2:
@@ -108,14 +153,14 @@ def _alg2_sharded(ops, k, p, v, Om):
             Qr, Rr = ops.orth("N", ops.view("M", Qc))
     if v % 2 == 0:
         Vw, lam, Uwt = np.linalg.svd(Rr)
-        return Qc @ Uwt.T[:, :k], lam[:k], Qr @ Vw[:, :k]
+        return Qc @ Uwt.T[:, :k], lam[:k], ops.finish_n(Qr @ Vw[:, :k])
     Uw, lam, Vwt = np.linalg.svd(Rc)
-    return Qc @ Uw[:, :k], lam[:k], Qr @ Vwt.T[:, :k]
+    return Qc @ Uw[:, :k], lam[:k], ops.finish_n(Qr @ Vwt.T[:, :k])
 
 
 def _alg9_sharded(ops, k, p, v, Om):
     l = Om.shape[1]
-    blocks, prev = [], Om
+    blocks, prev = [], ops.local_n(Om)
     for j in range(1, v):
         B = ops.view("N", prev) if j % 2 else ops.view("M", prev)
         side = "M" if j % 2 else "N"
@@ -137,10 +182,10 @@ def _alg9_sharded(ops, k, p, v, Om):
     if v % 2 == 0:
         Qr, Rr = ops.orth("N", ops.view("M", Q))
         Vw, lam, Uwt = np.linalg.svd(Rr)
-        return Q @ Uwt.T[:, :k], lam[:k], Qr @ Vw[:, :k]
+        return Q @ Uwt.T[:, :k], lam[:k], ops.finish_n(Qr @ Vw[:, :k])
     Qc, Rc = ops.orth("M", ops.view("N", Q))
     Uw, lam, Vwt = np.linalg.svd(Rc)
-    return Qc @ Uw[:, :k], lam[:k], Q @ Vwt.T[:, :k]
+    return Qc @ Uw[:, :k], lam[:k], ops.finish_n(Q @ Vwt.T[:, :k])
 
 
 def _alg7_sharded(ops, k, p, Om, Phi_local):
@@ -208,7 +253,9 @@ CASES = [("subspace", "C1", 2, None, None), ("subspace", "C1", 3, None, None),
          ("subspace", "C2", 4, 1200, 900), ("krylov", "C1", 4, None, None),
          ("krylov", "C2", 5, 1200, 900), ("single_pass", "C1", 1, None, None),
          ("single_pass", "C3", 1, 1500, 700), ("row", "C2", 1, 1200, 900), ("row", "C1", 1, None, None),
-         ("woolfe", "C2", 1, 1200, 900), ("bwz", "C1", 1, None, None), ("bwz2", "C2", 1, 1200, 900)]
+         ("woolfe", "C2", 1, 1200, 900), ("bwz", "C1", 1, None, None), ("bwz2", "C2", 1, 1200, 900),
+         ("subspace_n", "C2", 4, 1200, 900), ("subspace_n", "C1", 3, None, None), ("krylov_n", "C2", 5, 1200, 900),
+         ("krylov_n", "C2", 4, 1200, 901)]
 
 
 def _one_case(rank, world, case):
@@ -218,7 +265,10 @@ def _one_case(rank, world, case):
     Om = S.gaussian_test_matrix(A.shape[1], cfg.l, cfg, S.ROLE_OMEGA)
     Phi = S.gaussian_test_matrix(A.shape[0], cfg.l2, cfg, S.ROLE_PHI)
     sh = shard_rows(A.shape[0], world, rank)
-    ops = ShardedOps(A[sh.row0:sh.row0 + sh.m_local])
+    nshard = alg.endswith("_n")
+    alg = alg[:-2] if nshard else alg
+    A_l = A[sh.row0:sh.row0 + sh.m_local]
+    ops = ShardedOpsN(A_l, A.shape[1], world, rank) if nshard else ShardedOps(A_l)
     Phi_l = Phi[sh.row0:sh.row0 + sh.m_local]
     s_ext = min(A.shape[0], A.shape[1], 2 * cfg.l)
     Xr, Xc = S.srft_matrix(A.shape[0], s_ext, 7), S.srft_matrix(A.shape[1], s_ext, 8)
