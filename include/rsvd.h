@@ -47,7 +47,13 @@
  *   row-sharded (rank r holds rows [row0, row0 + m_local), the shards tiling [0, m) in rank
  *   order); U is returned row-sharded like A; S and V are replicated and bitwise identical on
  *   all ranks.  Gram matrices and the partial co-range views A^T Y are summed with NCCL
- *   all-reduce.  A call waits for its collectives by polling ncclCommGetAsyncError: an
+ *   all-reduce.  rsvd_subspace / rsvd_block_krylov with N > 1 ranks also shard the n-long side
+ *   (SURVEY §8(e)): every n x w block lives as N row chunks of ceil(n / N) rounded up to 32 rows
+ *   (rank r: rows [r cs, min((r + 1) cs, n))); A^T Y is reduce-scattered into the chunks, the
+ *   basis is all-gathered before the next A X, V is all-gathered before it is returned
+ *   (replicated, bitwise equal on all ranks).  Not used when some rank would own no chunk
+ *   (n <= (N - 1) cs) or with RSVD_NO_SHARD_N=1 (environment); the caller's Omega (n x l) is
+ *   passed whole on every rank either way.  A call waits for its collectives by polling ncclCommGetAsyncError: an
  *   asynchronous NCCL error, or no completion within RSVD_COMM_TIMEOUT_S seconds (environment,
  *   default 600), aborts the communicator and returns RSVD_E_NCCL (the ctx then needs a new one).
  * DETERMINISM.  Bitwise run-to-run reproducible for fixed inputs, rank count and SM budget

@@ -377,3 +377,52 @@ def test_invalid_rank_rejected(ctx):
         with pytest.raises(rsvd.RsvdError) as e:
             ctx.subspace(A, k, p, 2, Om)
         assert e.value.code == -1
+
+
+# ------------------------------------------------------------------ cluster Cholesky (k_chol_cl)
+# 64 < w <= 512: one 32-column panel per CTA; ragged last panels (w = 65: a 1-column panel),
+# the largest cluster (w = 512, 16 CTAs) and the near-identity second pass all go through it.
+@pytest.mark.parametrize("rows,w", [(2000, 65), (3000, 96), (3000, 97), (4000, 129), (5000, 255), (5000, 256),
+                                    (5000, 257), (6000, 511), (6000, 512)])
+def test_orth_cluster_cholesky_widths(ctx, rows, w):
+    Y = S.random_gaussian_matrix(rows, w, seed=7 * w + rows) * np.logspace(0, -4, w)
+    Q, R, info = ctx.orth(colmajor_dev(Y))
+    Q, R = host(Q), host(R)
+    np.testing.assert_allclose(Q.T @ Q, np.eye(w), atol=5e-14 * np.sqrt(w))
+    assert np.all(np.tril(R, -1) == 0) and np.all(np.diag(R) > 0)
+    assert np.linalg.norm(Q @ R - Y) <= 1e-13 * np.linalg.norm(Y)
+    Qo, Ro = O.qr(Y)
+    assert np.linalg.norm(R - Ro) <= 1e-11 * np.linalg.norm(Ro)
+    assert info.rank_deficient_cols == 0
+
+
+@pytest.mark.parametrize("w,r", [(97, 61), (300, 190), (512, 333)])
+def test_orth_cluster_cholesky_rank_deficient(ctx, w, r):
+    """The guard inside the cluster kernel's register-resident diagonal factorisation: deficient
+    pivots in every panel position zero their row of R and their column of R^-1 (reading R10)."""
+    rows = 3000
+    X, _ = S.exact_rank_factors(rows, w, r, seed=11)
+    Y = X @ S.random_gaussian_matrix(r, w, seed=12)
+    Q, R, info = ctx.orth(colmajor_dev(Y))
+    Q, R = host(Q), host(R)
+    kept = np.linalg.norm(Q, axis=0) > 0.5
+    assert r <= kept.sum() <= r + 2 and info.rank_deficient_cols >= w - r - 2
+    assert np.all(np.abs(R[~kept]).max(axis=1) == 0)      # rows of dropped pivots are exactly zero
+    Qk = Q[:, kept]
+    np.testing.assert_allclose(Qk.T @ Qk, np.eye(kept.sum()), atol=1e-12)
+    assert np.linalg.norm(X - Qk @ (Qk.T @ X)) < 1e-10
+
+
+@pytest.mark.parametrize("rows,w", [(5000, 300), (6000, 500)])
+def test_orth_cluster_cholesky_shifted(ctx, rows, w):
+    """Shifted CholeskyQR3 through the cluster kernel (shift pass + two guarded passes), kappa ~ 1e10."""
+    from paper_1804_07531_b200 import rsvd
+
+    Y = S.random_gaussian_matrix(rows, w, seed=rows + 5 * w) * np.logspace(0, -10, w)
+    Q, R, info = ctx.orth(colmajor_dev(Y), flags=rsvd.RSVD_ORTH_SHIFTED)
+    Q, R = host(Q), host(R)
+    np.testing.assert_allclose(Q.T @ Q, np.eye(w), atol=5e-14 * np.sqrt(w))
+    assert np.all(np.tril(R, -1) == 0) and np.all(np.diag(R) >= 0)
+    assert np.linalg.norm(Q @ R - Y) <= 1e-13 * np.linalg.norm(Y)
+    Qo, Ro = O.qr(Y)
+    assert np.linalg.norm(R - Ro) <= 1e-12 * np.linalg.norm(Ro)
