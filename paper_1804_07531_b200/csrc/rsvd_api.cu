@@ -26,6 +26,7 @@
 #include "internal.h"
 
 namespace rsvd {
+bool chol_reads_upper_only(int w);
 int launch_chol_ref(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
                     DevStatus* status, cudaStream_t st, double shift_coef = 0.0);
 int launch_jacobi_t(const double* M, int64_t ldm, int trans, int r, int c, double* Ul, double* S, double* Vr,
@@ -431,22 +432,26 @@ struct Exec {
 
   // one view launch (fp64) on the row-major matrix Ar (ar x nr, lda), X column-major (kdim x w, ldx);
   // result column-major (out_rows x w) into dst (ldd), split-K partial slots summed in order
+  // tri: only the upper triangle of the result is needed (a Gram for the cluster Cholesky, VIEW_AX:
+  // rows < c0 + wc of column chunk c0) or X is upper triangular (R^-1 applies, VIEW_ATY: the
+  // reduction stops at row c0 + wc of X): the chunk's A rows are cut to c0 + wc
   void view_raw(int kind, const double* Ar, int64_t ar, int64_t nr, int64_t lda_r, const double* X, int64_t ldx,
-                int w, double* dst, int64_t ldd) {
+                int w, double* dst, int64_t ldd, bool tri = false) {
     for (int c0 = 0; c0 < w; c0 += kMaxWT * 8) {
       const int wc = std::min(kMaxWT * 8, w - c0);
       const size_t mk = mark();
+      const int64_t ar_c = tri ? std::min<int64_t>(ar, c0 + wc) : ar;
       ViewArgs a;
       a.A = Ar;
-      a.rows = ar;
+      a.rows = ar_c;
       a.n = nr;
       a.lda = lda_r;
       a.X = X + (int64_t)c0 * ldx;
       a.ldx = ldx;
       a.w = wc;
       a.grid_cap = ctx->sms;
-      plan_view(kind, ar, nr, wc, ctx->sms, &a.S, &a.KTS);
-      const int64_t orows = (kind == VIEW_AX) ? ar : nr;
+      plan_view(kind, ar_c, nr, wc, ctx->sms, &a.S, &a.KTS);
+      const int64_t orows = (kind == VIEW_AX) ? ar_c : nr;
       double* d = dst + (int64_t)c0 * ldd;
       double* slots = (a.S == 1) ? d : alloc((int64_t)a.S * ldd * wc);
       a.out = slots;
@@ -460,20 +465,33 @@ struct Exec {
     }
   }
 
-  // G (a x b, col-major ld a) = Xa^T Xb over the rows (no all-reduce here)
-  void gram_dmma(const TS& Xa, const TS& Xb, double* G) {
-    view_raw(VIEW_AX, Xa.p, Xa.w, Xa.rows, Xa.ld, Xb.p, Xb.ld, Xb.w, G, Xa.w);
+  // G (a x b, col-major ld a) = Xa^T Xb over the rows (no all-reduce here); upper: only the upper
+  // triangle of a square Gram is formed (the rest of G is undefined)
+  void gram_dmma(const TS& Xa, const TS& Xb, double* G, bool upper = false) {
+    view_raw(VIEW_AX, Xa.p, Xa.w, Xa.rows, Xa.ld, Xb.p, Xb.ld, Xb.w, G, Xa.w, upper);
+  }
+  // Gram G = Y^T Y for a Cholesky: the upper triangle only when the Cholesky that consumes it
+  // reads nothing else (k_chol_cl), on the DMMA views (w >= 65 and a large block)
+  void gram_chol(Side s, const TS& Y, double* G) {
+    if (chol_reads_upper_only(Y.w) && big_skinny(Y.rows, Y.w, Y.w) && Y.w >= 8) {
+      const size_t mk = mark();
+      gram_dmma(Y, Y, G, true);
+      release(mk);
+      if (sharded(s)) allreduce(G, (int64_t)Y.w * Y.w);
+      return;
+    }
+    cross(s, Y, Y, G);
   }
 
   // out (rows x c, ldo) = in (rows x w, ldi) M (w x c, ldm); mode 1: out -= in M
   void tsmm(const double* in, int64_t ldi, int64_t rows, int w, const double* M, int64_t ldm, int c, double* out,
-            int64_t ldo, int mode) {
+            int64_t ldo, int mode, bool m_upper = false) {
     if (!big_skinny(rows, w, c) || w < 8 || ((ldm * 8) & 15) || (reinterpret_cast<uintptr_t>(M) & 15)) {
       if (live()) chk(launch_ts_gemm(in, ldi, rows, w, M, ldm, c, out, ldo, mode, st));
       return;
     }
     if (mode == 0) {
-      view_raw(VIEW_ATY, in, w, rows, ldi, M, ldm, c, out, ldo);
+      view_raw(VIEW_ATY, in, w, rows, ldi, M, ldm, c, out, ldo, m_upper && c == w);
       return;
     }
     const size_t mk = mark();
@@ -510,17 +528,17 @@ struct Exec {
       // the shift must be identical on every rank: the GLOBAL row count of a sharded side
       const double rows_all = (double)(sharded(s) ? side_rows_glob(s) : Y.rows);
       const double coef = 11.0 * (rows_all * w + (double)w * (w + 1)) * 1.1102230246251565e-16;
-      cross(s, Y, Y, G);
+      gram_chol(s, Y, G);
       if (live()) chk(launch_chol_ref(G, nullptr, w, 0.0, R0, R0i, nullptr, st, coef));
-      tsmm(Y.p, Y.ld, Y.rows, w, R0i, w, w, T.p, T.ld, 0);
+      tsmm(Y.p, Y.ld, Y.rows, w, R0i, w, w, T.p, T.ld, 0, true);
       if (live()) chk(launch_copy_cols(T.p, T.ld, Y.p, Y.ld, Y.rows, w, st));
     }
-    cross(s, Y, Y, G);
+    gram_chol(s, Y, G);
     if (live()) chk(launch_chol_ref(G, ref, w, 1e-12, R1, R1i, ctx->dstat, st));
-    tsmm(Y.p, Y.ld, Y.rows, w, R1i, w, w, T.p, T.ld, 0);
-    cross(s, T, T, G);
+    tsmm(Y.p, Y.ld, Y.rows, w, R1i, w, w, T.p, T.ld, 0, true);
+    gram_chol(s, T, G);
     if (live()) chk(launch_chol_ref(G, nullptr, w, 1e-12, R2, R2i, nullptr, st));
-    tsmm(T.p, T.ld, T.rows, w, R2i, w, w, Y.p, Y.ld, 0);
+    tsmm(T.p, T.ld, T.rows, w, R2i, w, w, Y.p, Y.ld, 0, true);
     if (live() && R_out) {
       if (shifted) {  // R = R2 R1 R0 (R1i is free now)
         chk(launch_small_gemm(0, 0, w, w, w, R1, w, R0s, w, R1i, w, st));

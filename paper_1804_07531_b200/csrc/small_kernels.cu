@@ -258,18 +258,25 @@ int launch_chol_cl(const double* G, const double* ref, int w, double tol, double
 int launch_chol_big(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
                     DevStatus* status, cudaStream_t st, double shift_coef);
 
+static int chol_cl_from() {
+  static const int v = [] {
+    const char* e = getenv("RSVD_CHOL_CL_FROM");
+    return e ? atoi(e) : 65;
+  }();
+  return v;
+}
+
+// launch_chol_ref takes the cluster kernel for this width: it reads only G's upper triangle
+bool chol_reads_upper_only(int w) { return chol_cl_from() > 0 && w >= chol_cl_from() && w >= 33 && w <= 512; }
+
 int launch_chol_ref(const double* G, const double* ref, int w, double tol, double* R, double* Rinv,
                     DevStatus* status, cudaStream_t st, double shift_coef) {
   static const int big_from = [] {
     const char* e = getenv("RSVD_CHOL_BIG_FROM");
     return e ? atoi(e) : kCholMaxW + 1;
   }();
-  // the cluster kernel above cl_from (RSVD_CHOL_CL_FROM, default 65; 0 disables it)
-  static const int cl_from = [] {
-    const char* e = getenv("RSVD_CHOL_CL_FROM");
-    return e ? atoi(e) : 65;
-  }();
-  if (cl_from > 0 && w >= cl_from && w >= 33) return launch_chol_cl(G, ref, w, tol, R, Rinv, status, st, shift_coef);
+  // the cluster kernel above RSVD_CHOL_CL_FROM (default 65; 0 disables it)
+  if (chol_reads_upper_only(w)) return launch_chol_cl(G, ref, w, tol, R, Rinv, status, st, shift_coef);
   if (w > kCholMaxW || w >= big_from) return launch_chol_big(G, ref, w, tol, R, Rinv, status, st, shift_coef);
   if (w < 1) return RSVD_E_ARG;
   const size_t smem = (size_t)w * w * 8 + (size_t)w * 4 + 16;
