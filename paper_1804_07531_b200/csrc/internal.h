@@ -160,7 +160,10 @@ int launch_pinv_svd(const double* U, const double* s, const double* V, int w, do
 int launch_scale_cols(double* X, int64_t ld, int rows, int cols, const double* d, cudaStream_t st);
 // zero the columns j of X (rows x w) with G_jj <= tol * ref_j (dependent after a block projection)
 int launch_zero_dep_cols(double* X, int64_t ld, int64_t rows, int w, const double* G, const double* ref, double tol,
-                         DevStatus* status, cudaStream_t st);
+                         DevStatus* status, cudaStream_t st,
+                         int64_t gstride = -1);   // G's diagonal stride (-1: a w x w Gram)
+// d[j] = squared norm of column j of X (rows x w, ld)
+int launch_colnorm2(const double* X, int64_t ld, int64_t rows, int w, double* d, cudaStream_t st);
 // S[i] <- S[i]^2
 int launch_square(double* S, int n, cudaStream_t st);
 // Nystrom (Alg. 4) helpers: nu = 2.2e-16 ||Y_r||_2 from the Gram of Y_r (power iteration);

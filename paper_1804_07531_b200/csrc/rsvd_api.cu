@@ -619,15 +619,14 @@ struct Exec {
         // (removes the components the normalisation amplified), then CholeskyQR2.
         TS Qp = slice(K, 0, c0);
         double* C = alloc((int64_t)c0 * wc);
-        double* G = alloc((int64_t)wc * wc);
         double* ref = alloc(wc);
-        cross(s, Wb, Wb, G);
-        if (live()) chk(launch_diag(G, wc, ref, st));
+        double* nrm = alloc(wc);
+        colnorm2(s, Wb, ref);                               // |w_j|^2 before the projection
         cross(s, Qp, Wb, C);
         tsmm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1);
-        cross(s, Wb, Wb, G);
+        colnorm2(s, Wb, nrm);                               // ... and after it
         constexpr double kDepTol = (64.0 * 1.1102230246251565e-16) * (64.0 * 1.1102230246251565e-16);
-        if (live()) chk(launch_zero_dep_cols(Wb.p, Wb.ld, Wb.rows, wc, G, ref, kDepTol, ctx->dstat, st));
+        if (live()) chk(launch_zero_dep_cols(Wb.p, Wb.ld, Wb.rows, wc, nrm, ref, kDepTol, ctx->dstat, st, 1));
         orth(s, Wb, nullptr, nullptr, /*shifted=*/true);
         cross(s, Qp, Wb, C);
         tsmm(Qp.p, Qp.ld, Qp.rows, c0, C, c0, wc, Wb.p, Wb.ld, 1);
@@ -637,6 +636,12 @@ struct Exec {
       }
       release(mk);
     }
+  }
+
+  // d[j] = |X_j|^2 over the side's rows (+ all-reduce when sharded): the diagonal of X^T X alone
+  void colnorm2(Side s, const TS& X, double* d) {
+    if (live()) chk(launch_colnorm2(X.p, X.ld, X.rows, X.w, d, st));
+    if (sharded(s)) allreduce(d, X.w);
   }
 
   // out (rows x k, ldo) = Q (rows x w) * Mk (w x k, ld w)

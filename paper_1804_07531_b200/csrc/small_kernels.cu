@@ -991,20 +991,52 @@ int launch_square(double* S, int n, cudaStream_t st) {
 // columns are set to exactly zero (they then stay zero through the shifted and the guarded
 // Cholesky passes); their count goes to status->deficient.  G: the w x w Gram after projection.
 __global__ void k_zero_dep_cols(double* __restrict__ X, int64_t ld, int64_t rows, int w, const double* __restrict__ G,
-                                const double* __restrict__ ref, double tol, DevStatus* status) {
+                                int64_t gstride, const double* __restrict__ ref, double tol, DevStatus* status) {
   const int j = blockIdx.y;
   if (j >= w) return;
-  if (!(G[(int64_t)j * w + j] <= tol * ref[j])) return;
+  if (!(G[(int64_t)j * gstride] <= tol * ref[j])) return;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
     X[(int64_t)j * ld + r] = 0.0;
   if (blockIdx.x == 0 && threadIdx.x == 0 && status) atomicAdd(&status->deficient, 1);
 }
 
 int launch_zero_dep_cols(double* X, int64_t ld, int64_t rows, int w, const double* G, const double* ref, double tol,
-                         DevStatus* status, cudaStream_t st) {
+                         DevStatus* status, cudaStream_t st, int64_t gstride) {
   if (rows <= 0 || w <= 0) return RSVD_OK;
   const unsigned bx = (unsigned)std::min<int64_t>((rows + 255) / 256, 64);
-  k_zero_dep_cols<<<dim3(bx, (unsigned)w), 256, 0, st>>>(X, ld, rows, w, G, ref, tol, status);
+  k_zero_dep_cols<<<dim3(bx, (unsigned)w), 256, 0, st>>>(X, ld, rows, w, G, gstride < 0 ? w + 1 : gstride, ref, tol,
+                                                          status);
+  return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
+}
+
+// squared column norms d[j] = sum_r X(r, j)^2 (the diagonal of X^T X without forming it): one CTA
+// per column, fixed-order per-thread sums and a fixed reduction tree (deterministic)
+__global__ void __launch_bounds__(256) k_colnorm2(const double* __restrict__ X, int64_t ld, int64_t rows,
+                                                  double* __restrict__ d) {
+  __shared__ double part[8];
+  const int j = blockIdx.x, tid = threadIdx.x;
+  const double* x = X + (int64_t)j * ld;
+  double s0 = 0.0, s1 = 0.0;
+  int64_t r = tid;
+  for (; r + 256 < rows; r += 512) {
+    const double a = x[r], b = x[r + 256];
+    s0 = fma(a, a, s0);
+    s1 = fma(b, b, s1);
+  }
+  if (r < rows) s0 = fma(x[r], x[r], s0);
+  double s = warp_sum(s0 + s1);
+  if ((tid & 31) == 0) part[tid >> 5] = s;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 8; ++i) t += part[i];
+    d[j] = t;
+  }
+}
+
+int launch_colnorm2(const double* X, int64_t ld, int64_t rows, int w, double* d, cudaStream_t st) {
+  if (w <= 0) return RSVD_OK;
+  k_colnorm2<<<w, 256, 0, st>>>(X, ld, rows, d);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
