@@ -316,13 +316,6 @@ __device__ __forceinline__ void cl_sync() {
 // X = R^-1 (ld 33), defi[p].  Pivot p: d = D(p,p) after the previous updates; deficient when
 // d <= tol * ref_p (ref_p = gd[p], + shift without a caller reference): R's row p and R^-1's row
 // and column p are zero.  Row p of R = D(p, :) / sqrt(d) (rsqrt, as k_chol).
-__device__ __forceinline__ double rsqrt_nr(double d) {
-  // MUFU seed (~2^-22) and one third-order step (-> ~2^-64): no IEEE slow-path subroutine
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-  const double e = fma(-d * y, y, 1.0);
-  return fma(y * e, fma(0.375, e, 0.5), y);
-}
 
 __device__ void factor_inv_warp(double* D, int jb, const double* gd, bool has_ref, double tol, double shift,
                                 int* defi, double* X, double* sb, double* dinv) {

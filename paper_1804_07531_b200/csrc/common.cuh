@@ -115,6 +115,15 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return ldexp(y, -e);
 }
 
+// 1/sqrt(d), d > 0 normal: the MUFU seed (rsqrt.approx.f64, ~2^-22) and one third-order Newton
+// step (~2^-64 before rounding) — a short dependent chain, no slow-path branch of the IEEE rsqrt
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  const double e = fma(-d * y, y, 1.0);
+  return fma(y * e, fma(0.375, e, 0.5), y);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

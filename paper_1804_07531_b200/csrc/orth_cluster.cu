@@ -103,7 +103,7 @@ __device__ int chol_inv_cols(double* G, int w, double shift, double tol, double*
         const double d = bc[192], rf = bc[193];
         const bool def = !(d > tol * rf) || !(rf > 0.0);
         ndef += (def && p < w) ? 1 : 0;
-        const double inv = def ? 0.0 : rsqrt(d);
+        const double inv = def ? 0.0 : rsqrt_nr(d);
         const double rpj = (j > p) ? c[k] * inv : ((j == p) ? d * inv : 0.0);
         if (act && j >= p) G[j * W + p] = def ? 0.0 : rpj;  // R(p, j)
         if (j == p) invd[p] = inv;

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(1024) k_chol(const double* __restrict__ G, con
     const double d = S[j * w + j];
     const double rf = ref ? s_ref[j] : (s_ref[j] + s_shift * (shift_coef > 0.0));
     const bool def = !(d > tol * rf) || !(rf > 0.0);
-    const double inv = def ? 0.0 : rsqrt(d);
+    const double inv = def ? 0.0 : rsqrt_nr(d);
     // row j of R: R(j,i) = S(j,i) / R_jj, i > j  (S(j,i) at S[i*w + j])
     for (int i = j + 1 + tid; i < w; i += nt) S[i * w + j] *= inv;
     __syncthreads();  // row j complete; everyone has read S(j,j)
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(kJacThreads) k_jacobi(const double* __restrict
           } else {
             t = copysign(1.0, d) * e / (ad + sqrt(fma(d, d, e * e)));
           }
-          const double cs = rsqrt(fma(t, t, 1.0));
+          const double cs = rsqrt_nr(fma(t, t, 1.0));
           const double sn = cs * t;
 #pragma unroll
           for (int t = 0; t < RPL; ++t) {
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(LPP == 4 ? 256 : 512) k_jacobi_mid(const doubl
           asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rsq) : "d"(s1));
           asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rt) : "d"(fma(s1, rsq, 1.0)));
           const double t = (d < 0.0 ? -rho : rho) * rt;
-          const double cs = rsqrt(fma(t, t, 1.0));
+          const double cs = rsqrt_nr(fma(t, t, 1.0));
           const double sn = cs * t;
 #pragma unroll
           for (int k = 0; k < RW; ++k) {
@@ -1207,7 +1207,7 @@ __device__ void cta_chol_inv(double* S, double* X, int w, const double* ref, dou
         tg[a][b] = (i > j && k >= i && k < w) ? S[k * lw + i] : 0.0;
       }
     const bool def = !(d > tol * ref[j]) || !(ref[j] > 0.0);
-    const double inv = def ? 0.0 : rsqrt(d);
+    const double inv = def ? 0.0 : rsqrt_nr(d);
     if (tid == 0) { defi[j] = def; invd[j] = inv; }
     const double inv2 = inv * inv;
 #pragma unroll
@@ -1642,7 +1642,7 @@ __global__ void __launch_bounds__(256) k_jacobi_small(const double* __restrict__
           asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rsq) : "d"(s1));
           asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rt) : "d"(fma(s1, rsq, 1.0)));
           const double t = (d < 0.0 ? -rho : rho) * rt;
-          const double cs = rsqrt(fma(t, t, 1.0));
+          const double cs = rsqrt_nr(fma(t, t, 1.0));
           const double sn = cs * t;
 #pragma unroll
           for (int k = 0; k < RW; ++k) {
