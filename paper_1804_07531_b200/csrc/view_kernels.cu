@@ -690,7 +690,9 @@ void plan_view(int kind, int64_t rows, int64_t n, int w, int grid_cap, int* S, i
   if (kind == VIEW_AX) {
     const int RB = (int)((rows + bm - 1) / bm);
     const int KT = (int)((n + kBK - 1) / kBK);
-    choose_split(RB, KT, grid_cap, 64, S, KTS);
+    // one or two row blocks (a tall-skinny Gram X^T X as a view of X^T): split the long reduction
+    // over every SM rather than 64 of them
+    choose_split(RB, KT, grid_cap, RB <= 2 ? grid_cap : 64, S, KTS);
   } else if (kind == VIEW_ATY) {
     const int CB = (int)((n + bm - 1) / bm);
     const int KT = (int)((rows + kBK - 1) / kBK);
