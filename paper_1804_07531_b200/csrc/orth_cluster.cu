@@ -76,7 +76,13 @@ __device__ int chol_inv_cols(double* G, int w, double shift, double tol, double*
 #pragma unroll
   for (int i = 0; i < W; ++i) c[i] = act ? G[j * W + i] : 0.0;
   const double sj = (j < w) ? shift : 0.0;
-  if (j < 2 * W && j >= W) rrow[j] = 0.0;
+  // W <= 32: the pivot and the broadcast row are double-buffered by pivot parity (rows at bc and
+  // bc + 64, pivots at bc[192..195]), so a pivot needs two barriers instead of three
+  constexpr bool DB = (W <= 32);
+  if (j < 2 * W && j >= W) {
+    rrow[j] = 0.0;
+    if (DB) rrow[64 + j] = 0.0;
+  }
   double refj = 0.0;
 #pragma unroll
   for (int i = 0; i < W; ++i)
@@ -94,25 +100,28 @@ __device__ int chol_inv_cols(double* G, int w, double shift, double tol, double*
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int p = p0 + k;
+        double* rr = rrow + (DB ? 64 * (k & 1) : 0);
+        double* pv = bc + 192 + (DB ? 2 * (k & 1) : 0);
         if (j == p) {
           c[k] += sj;
-          bc[192] = c[k];
-          bc[193] = refj;
+          pv[0] = c[k];
+          pv[1] = refj;
         }
         csync<W>();
-        const double d = bc[192], rf = bc[193];
+        const double d = pv[0], rf = pv[1];
         const bool def = !(d > tol * rf) || !(rf > 0.0);
         ndef += (def && p < w) ? 1 : 0;
         const double inv = def ? 0.0 : rsqrt_nr(d);
         const double rpj = (j > p) ? c[k] * inv : ((j == p) ? d * inv : 0.0);
         if (act && j >= p) G[j * W + p] = def ? 0.0 : rpj;  // R(p, j)
         if (j == p) invd[p] = inv;
-        if (act) rrow[j] = rpj;
+        if (act) rr[j] = rpj;
         csync<W>();
-        const double* rp = rrow + p0;  // rp[i] = R(p, p0 + i)
+        const double* rp = rr + p0;  // rp[i] = R(p, p0 + i)
+        // a deficient pivot has rpj = 0: the update leaves c unchanged (no select needed)
 #pragma unroll
-        for (int i = k + 1; i < W; ++i) c[i] = def ? c[i] : fma(-rp[i], rpj, c[i]);
-        csync<W>();
+        for (int i = k + 1; i < W; ++i) c[i] = fma(-rp[i], rpj, c[i]);
+        if (!DB) csync<W>();
       }
 #pragma unroll
       for (int i = 0; i < W - 8; ++i) c[i] = c[i + 8];
