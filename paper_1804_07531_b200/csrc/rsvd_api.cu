@@ -318,8 +318,12 @@ struct Exec {
       return;
     }
     const int w = X.w;
-    for (int c0 = 0; c0 < w; c0 += kMaxWT * 8) {
-      const int wc = std::min(kMaxWT * 8, w - c0);
+    // balanced column chunks of <= kMaxWT * 8 (each chunk streams A once: w = 140 as 72 + 68, two
+    // tensor-bound launches, not 128 + an HBM-bound 12)
+    const int nchunk = (w + kMaxWT * 8 - 1) / (kMaxWT * 8);
+    const int cw = std::min(kMaxWT * 8, ((w + nchunk - 1) / nchunk + 7) / 8 * 8);
+    for (int c0 = 0; c0 < w; c0 += cw) {
+      const int wc = std::min(cw, w - c0);
       const size_t mk = mark();
       ViewArgs a;
       a.A = A + (panel ? r0 * lda : 0);
