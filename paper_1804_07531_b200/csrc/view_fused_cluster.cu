@@ -322,7 +322,15 @@ int make_map_fc(CUtensorMap* map, const double* base, int64_t inner, int64_t out
   return r == CUDA_SUCCESS ? RSVD_OK : RSVD_E_CUDA;
 }
 
-int cluster_size_for(int64_t n) { return (n + kFBN - 1) / kFBN >= 32 ? 16 : 8; }
+int cluster_size_for(int64_t n) {
+  static const int force = [] {   // RSVD_FC_CL=8 / 16: A/B of the cluster size (measurement only)
+    const char* e = getenv("RSVD_FC_CL");
+    const int v = e ? atoi(e) : 0;
+    return (v == 8 || v == 16) ? v : 0;
+  }();
+  if (force) return force;
+  return (n + kFBN - 1) / kFBN >= 32 ? 16 : 8;
+}
 
 template <int L2T, int LTC>
 int launch_fc_t(const FusedClArgs& a, cudaStream_t st) {
