@@ -123,7 +123,11 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 // KIND == VIEW_ATY: out rows = cols of A (M), reduction over rows. tmA box {32 cols, 16 rows},
 //                   128B swizzle with 32B atoms (MN-major tf32 operand layout)
 // tmXh / tmXl: X^T (resp. Y^T) pre-split, fp32 [w x K] with K contiguous, box {16, min(WP,256)}
-template <int KIND>
+// TRUNC: A_hi is A itself (the tensor core reads the upper 19 bits of the fp32 container, i.e.
+// truncates to tf32), so the raw tile stays as TMA wrote it and only A_lo = A - trunc(A) (the
+// low 13 mantissa bits, exact in fp32) is formed and stored; else A_hi = rna(A) in place and
+// A_lo = rna(A - A_hi).  (RSVD_TF32_RNA=1 selects the rounded split for A/B.)
+template <int KIND, int TRUNC>
 __global__ void __launch_bounds__(kThreads, 1)
     k_view_tf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
                 const __grid_constant__ CUtensorMap tmXl, float* __restrict__ out, int64_t ldo,
@@ -270,15 +274,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         float4* raw = reinterpret_cast<float4*>(st);
         float4* lo = reinterpret_cast<float4*>(st + G.a_bytes);
         const int n4 = G.a_bytes / 16;
-        for (int i = ct; i < n4; i += 128) {
-          const float4 v = raw[i];
-          float4 h, l;
-          h.x = rna_tf32(v.x); l.x = rna_tf32(v.x - h.x);
-          h.y = rna_tf32(v.y); l.y = rna_tf32(v.y - h.y);
-          h.z = rna_tf32(v.z); l.z = rna_tf32(v.z - h.z);
-          h.w = rna_tf32(v.w); l.w = rna_tf32(v.w - h.w);
-          raw[i] = h;
-          lo[i] = l;
+        if (TRUNC) {
+          for (int i = ct; i < n4; i += 128) {
+            const float4 v = raw[i];
+            float4 l;
+            l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+            l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+            l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+            l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
+            lo[i] = l;
+          }
+        } else {
+          for (int i = ct; i < n4; i += 128) {
+            const float4 v = raw[i];
+            float4 h, l;
+            h.x = rna_tf32(v.x); l.x = rna_tf32(v.x - h.x);
+            h.y = rna_tf32(v.y); l.y = rna_tf32(v.y - h.y);
+            h.z = rna_tf32(v.z); l.z = rna_tf32(v.z - h.z);
+            h.w = rna_tf32(v.w); l.w = rna_tf32(v.w - h.w);
+            raw[i] = h;
+            lo[i] = l;
+          }
         }
         fence_async_smem();
         __syncwarp();
@@ -424,20 +440,27 @@ int launch_view_tf32(const ViewArgs32& a, cudaStream_t st) {
   const int grid = std::min(U, a.grid_cap);
   const int smem = G.smem();
   const int chunk = kTf32Chunk;
-  static std::atomic<bool> attr[2] = {{false}, {false}};
-  if (!attr[ax ? 0 : 1]) {
-    if (ax)
-      cudaFuncSetAttribute(k_view_tf32<VIEW_AX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
-    else
-      cudaFuncSetAttribute(k_view_tf32<VIEW_ATY>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
-    attr[ax ? 0 : 1] = true;
+  static const bool rna = [] {
+    const char* e = getenv("RSVD_TF32_RNA");
+    return e && e[0] == '1';
+  }();
+  static std::atomic<bool> attr{false};
+  if (!attr) {
+    cudaFuncSetAttribute(k_view_tf32<VIEW_AX, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
+    cudaFuncSetAttribute(k_view_tf32<VIEW_ATY, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
+    cudaFuncSetAttribute(k_view_tf32<VIEW_AX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
+    cudaFuncSetAttribute(k_view_tf32<VIEW_ATY, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 2048);
+    attr = true;
   }
-  if (ax)
-    k_view_tf32<VIEW_AX><<<grid, kThreads, smem, st>>>(tmA, tmXh, tmXl, a.out, a.ldo, a.slot_stride, (int)out_rows,
-                                                        a.w, MT, NB, a.S, KT, a.KTS, chunk);
-  else
-    k_view_tf32<VIEW_ATY><<<grid, kThreads, smem, st>>>(tmA, tmXh, tmXl, a.out, a.ldo, a.slot_stride, (int)out_rows,
-                                                         a.w, MT, NB, a.S, KT, a.KTS, chunk);
+#define TF32_LAUNCH(K, T)                                                                                        \
+  k_view_tf32<K, T><<<grid, kThreads, smem, st>>>(tmA, tmXh, tmXl, a.out, a.ldo, a.slot_stride, (int)out_rows, \
+                                                  a.w, MT, NB, a.S, KT, a.KTS, chunk)
+  if (ax) {
+    if (rna) TF32_LAUNCH(VIEW_AX, 0); else TF32_LAUNCH(VIEW_AX, 1);
+  } else {
+    if (rna) TF32_LAUNCH(VIEW_ATY, 0); else TF32_LAUNCH(VIEW_ATY, 1);
+  }
+#undef TF32_LAUNCH
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
