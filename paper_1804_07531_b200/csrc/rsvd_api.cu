@@ -978,8 +978,17 @@ void alg_single_pass(Exec& E) {
   double* R2 = E.alloc((int64_t)lp * lp);
   double* R2i = E.alloc((int64_t)lp * lp);
   double* Cq = E.alloc((int64_t)l2 * lp);
+  double* Rw = E.alloc(3 * (int64_t)lp * lp);
+  static const bool qr_small_chain = getenv_flag("RSVD_QR_SMALL_CHAIN");
   auto qr_small = [&](double* X, int64_t ldx, double* Rhi_out) {
     if (!E.live()) return;
+    if (!qr_small_chain && orth_cluster_fits(l2, lp)) {
+      // the same CholeskyQR2 (guarded passes, closed-form second pass) in one cluster launch,
+      // Qh over X and Rh = R2 R1; Rh^-1 by back substitution (zero pivots -> zero rows/columns)
+      E.chk(launch_orth_cluster(X, ldx, l2, lp, 0, 0.0, R1, Rw, E.ctx->dstat, E.st));
+      E.chk(launch_tri_inv(R1, lp, Rhi_out, nullptr, E.st));
+      return;
+    }
     E.chk(launch_small_gemm(1, 0, lp, lp, l2, X, ldx, X, ldx, G, lp, E.st));
     E.chk(launch_chol_ref(G, nullptr, lp, 1e-12, R1, R1i, E.ctx->dstat, E.st));
     E.chk(launch_small_gemm(0, 0, l2, lp, lp, X, ldx, R1i, lp, Cq, l2, E.st));
@@ -1067,7 +1076,13 @@ void small_qr(Exec& E, double* X, int rows, int w, double* R) {
   double* R2 = E.alloc((int64_t)w * w);
   double* R2i = E.alloc((int64_t)w * w);
   double* T = E.alloc((int64_t)rows * w);
+  double* Rw = E.alloc(3 * (int64_t)w * w);
   if (!E.live()) return;
+  if (!getenv_flag("RSVD_QR_SMALL_CHAIN") && orth_cluster_fits(rows, w)) {
+    // the same guarded CholeskyQR2 in one cluster launch (R = R2 R1 written by the kernel)
+    E.chk(launch_orth_cluster(X, rows, rows, w, 0, 0.0, R, Rw, nullptr, E.st));
+    return;
+  }
   E.chk(launch_small_gemm(1, 0, w, w, rows, X, rows, X, rows, G, w, E.st));
   E.chk(launch_chol_ref(G, nullptr, w, 1e-12, R1, R1i, nullptr, E.st));
   E.chk(launch_small_gemm(0, 0, rows, w, w, X, rows, R1i, w, T, rows, E.st));

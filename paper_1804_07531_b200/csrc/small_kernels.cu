@@ -285,6 +285,8 @@ int launch_chol_ref(const double* G, const double* ref, int w, double tol, doubl
     cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholMaxW * kCholMaxW * 8 + kCholMaxW * 4 + 16);
     attr = true;
   }
+  // 1024 threads: a 128 / 256-thread CTA (fewer warps per barrier) measured slower at w = 30
+  // (C2 single pass: 2 x 22.4 us vs 2 x 20.0 us), the pivot chain is not barrier-bound
   k_chol<<<1, 1024, smem, st>>>(G, ref, w, tol, shift_coef, R, Rinv, status);
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
@@ -850,9 +852,43 @@ __global__ void k_tri_inv(const double* __restrict__ R, int c, double* __restric
   }
 }
 
+// The same inverse for c <= 64 with R staged in shared memory and one warp per column j of X,
+// column-oriented: b = e_j; for i = j..0: x_i = b_i / R_ii, then b_t -= R_ti x_i (t < i, lanes
+// over t, rows t and t + 32 in two registers).  The chain is one shuffle, one division and one
+// fma per step (the thread-per-column loop above paid an L2 round trip per dot-product term:
+// ~20 us at c = 30).  Zero pivots give zero rows / columns, as above.
+__global__ void __launch_bounds__(1024) k_tri_inv_warp(const double* __restrict__ R, int c, double* __restrict__ X) {
+  __shared__ double Rs[64 * 65];
+  const int ld = c + 1;
+  for (int e = threadIdx.x; e < c * c; e += blockDim.x) {
+    const int i = e % c, k = e / c;
+    Rs[k * ld + i] = R[e];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = threadIdx.x >> 5; j < c; j += nw) {
+    double b0 = lane == j ? 1.0 : 0.0, b1 = lane + 32 == j ? 1.0 : 0.0;
+    for (int i = j; i >= 0; --i) {
+      const double bi = __shfl_sync(0xffffffffu, i < 32 ? b0 : b1, i & 31);
+      const double rii = Rs[i * ld + i];
+      const double xi = rii != 0.0 ? bi / rii : 0.0;
+      if (lane == i) b0 = xi;
+      if (lane + 32 == i) b1 = xi;
+      if (lane < i) b0 = fma(-Rs[i * ld + lane], xi, b0);
+      if (lane + 32 < i) b1 = fma(-Rs[i * ld + lane + 32], xi, b1);
+    }
+    if (lane < c) X[(int64_t)j * c + lane] = lane <= j ? b0 : 0.0;
+    if (lane + 32 < c) X[(int64_t)j * c + lane + 32] = lane + 32 <= j ? b1 : 0.0;
+  }
+}
+
 int launch_tri_inv(const double* R, int c, double* Rinv, DevStatus* /*status*/, cudaStream_t st) {
   if (c < 1) return RSVD_E_ARG;
-  k_tri_inv<<<1, 128, 0, st>>>(R, c, Rinv);
+  if (c <= 64) {
+    k_tri_inv_warp<<<1, 32 * min(c, 32), 0, st>>>(R, c, Rinv);
+  } else {
+    k_tri_inv<<<1, 128, 0, st>>>(R, c, Rinv);
+  }
   return cudaPeekAtLastError() == cudaSuccess ? RSVD_OK : RSVD_E_CUDA;
 }
 
