@@ -149,6 +149,158 @@ __global__ void __launch_bounds__(256) k_jac(const double* __restrict__ M, int r
   }
 }
 
+
+// Register-resident variant: thread group T keeps the "plus" column of its pair in registers
+// across rounds and only the "minus" column moves through shared memory (round-robin positions:
+// logical pair g holds plus = r+g, minus = r-g (mod m1), g = 0: (r, fixed)).  Moves per round:
+// plus[g] -> plus[g-1] (stays in the thread group, whose logical index is (T - r) mod npairs),
+// plus[0] -> minus[1], minus[g] -> minus[g+1], minus[npairs-1] -> plus[npairs-1], minus[0] stays
+// at logical 0.  Slots Sp / Sm indexed by the NEW logical index, double-buffered by round parity.
+template <int LPP, int RW>
+__global__ void __launch_bounds__(256) k_jac_reg(const double* __restrict__ M, int r, int c, double* __restrict__ S,
+                                                 int* sweeps_out, double tol) {
+  constexpr int RS = LPP * RW + 4;
+  extern __shared__ double sm[];
+  double* Sm = sm;               // 2 x 32 x RS
+  double* Sp = sm + 2 * 32 * RS; // 2 x RS (only logical npairs-1 uses it)
+  double* Wf = Sp + 2 * RS;      // 64 x RS final columns
+  const int tid = threadIdx.x;
+  const int T = tid / LPP, sl = tid % LPP;
+  const int ce = c + (c & 1);
+  const int npairs = ce >> 1, m1 = ce - 1;
+  const bool active = T < npairs;
+  double x[RW], y[RW];
+  auto colv = [&](int col, int i) -> double { return (i < r && col < c) ? M[(int64_t)col * r + i] : 0.0; };
+  {
+    const int pc = T, mc = T == 0 ? m1 : m1 - T;
+#pragma unroll
+    for (int t = 0; t < RW; ++t) {
+      x[t] = active ? colv(pc, sl + LPP * t) : 0.0;
+      y[t] = active ? colv(mc, sl + LPP * t) : 0.0;
+    }
+  }
+  const double tol2 = tol * tol;
+  int sweep = 0, R = 0;
+  for (; sweep < 60; ++sweep) {
+    int rotated = 0;
+    for (int round = 0; round < m1; ++round, ++R) {
+      const int h = active ? ((T - (R % npairs)) % npairs + npairs) % npairs : 0;
+      double a0 = 0.0, b0 = 0.0, c0 = 0.0, a1 = 0.0, b1 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int t = 0; t < RW; t += 2) {
+        a0 = fma(x[t], x[t], a0); b0 = fma(y[t], y[t], b0); c0 = fma(x[t], y[t], c0);
+        if (t + 1 < RW) { a1 = fma(x[t + 1], x[t + 1], a1); b1 = fma(y[t + 1], y[t + 1], b1); c1 = fma(x[t + 1], y[t + 1], c1); }
+      }
+      double a = a0 + a1, b = b0 + b1, cc = c0 + c1;
+      __syncwarp();
+#pragma unroll
+      for (int o = LPP / 2; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o, LPP);
+        b += __shfl_xor_sync(0xffffffffu, b, o, LPP);
+        cc += __shfl_xor_sync(0xffffffffu, cc, o, LPP);
+      }
+      if (active && cc * cc > tol2 * (a * b) && cc != 0.0) {
+        rotated = 1;
+        const double d = b - a;
+        double rd, rs, rt;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(fmax(fabs(d), 1e-300)));
+        const double rho = fmin(fmax(2.0 * cc * rd, -1e100), 1e100);
+        const double s1 = fma(rho, rho, 1.0);
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(s1));
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rt) : "d"(1.0 + s1 * rs));
+        const double tt = (d < 0.0 ? -rho : rho) * rt;
+        const double cs = rsqrt(fma(tt, tt, 1.0));
+        const double sn = cs * tt;
+#pragma unroll
+        for (int k = 0; k < RW; ++k) {
+          const double u = x[k], v = y[k];
+          x[k] = cs * u - sn * v;
+          y[k] = sn * u + cs * v;
+        }
+      }
+      // hand the moving columns to their next owners (slots by NEW logical index)
+      double* sm_w = Sm + (R & 1) * 32 * RS;
+      double* sp_w = Sp + (R & 1) * RS;
+      if (active) {
+        if (h == 0) {
+          if (npairs > 1) {
+#pragma unroll
+            for (int t = 0; t < RW; ++t) { sm_w[1 * RS + sl + LPP * t] = x[t]; sm_w[0 * RS + sl + LPP * t] = y[t]; }
+          }
+        } else if (h == npairs - 1) {
+#pragma unroll
+          for (int t = 0; t < RW; ++t) sp_w[sl + LPP * t] = y[t];
+        } else {
+#pragma unroll
+          for (int t = 0; t < RW; ++t) sm_w[(h + 1) * RS + sl + LPP * t] = y[t];
+        }
+      }
+      __syncthreads();
+      if (active && npairs > 1) {
+        const int hn = h == 0 ? npairs - 1 : h - 1;
+        if (h == 0) {
+#pragma unroll
+          for (int t = 0; t < RW; ++t) { x[t] = sp_w[sl + LPP * t]; y[t] = sm_w[hn * RS + sl + LPP * t]; }
+        } else {
+#pragma unroll
+          for (int t = 0; t < RW; ++t) y[t] = sm_w[hn * RS + sl + LPP * t];
+        }
+      }
+    }
+    if (!__syncthreads_or(rotated)) { ++sweep; break; }
+  }
+  if (active) {
+    const int h = ((T - (R % npairs)) % npairs + npairs) % npairs;
+    const int rr = R % m1;
+    const int pc = h == 0 ? rr : (rr + h) % m1, mc = h == 0 ? m1 : ((rr - h) % m1 + m1) % m1;
+#pragma unroll
+    for (int t = 0; t < RW; ++t) { Wf[pc * RS + sl + LPP * t] = x[t]; Wf[mc * RS + sl + LPP * t] = y[t]; }
+  }
+  __syncthreads();
+  for (int j = tid; j < c; j += blockDim.x) {
+    double s = 0;
+    for (int i = 0; i < r; ++i) s = fma(Wf[j * RS + i], Wf[j * RS + i], s);
+    S[j] = sqrt(s);
+  }
+  if (tid == 0) *sweeps_out = sweep;
+}
+
+template <int LPP, int RW>
+void run_reg(const char* name, const double* dM, int r, int c, const std::vector<double>& ref) {
+  constexpr int RS = LPP * RW + 4;
+  const int smem = (2 * 32 + 2 + 64) * RS * 8;
+  cudaFuncSetAttribute(k_jac_reg<LPP, RW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  double* dS;
+  int* dsw;
+  cudaMalloc(&dS, 128 * 8);
+  cudaMalloc(&dsw, 4);
+  const int ce = c + (c & 1);
+  const int threads = ((LPP * (ce / 2)) + 31) / 32 * 32;
+  const double tol = 2.220446049250313e-16 * sqrt((double)r);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_jac_reg<LPP, RW><<<1, threads, smem>>>(dM, r, c, dS, dsw, tol);
+  cudaEventRecord(e0);
+  const int reps = 5;
+  for (int i = 0; i < reps; ++i) k_jac_reg<LPP, RW><<<1, threads, smem>>>(dM, r, c, dS, dsw, tol);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  std::vector<double> S(c);
+  int sw;
+  cudaMemcpy(S.data(), dS, c * 8, cudaMemcpyDeviceToHost);
+  cudaMemcpy(&sw, dsw, 4, cudaMemcpyDeviceToHost);
+  std::sort(S.begin(), S.end(), [](double a, double b) { return a > b; });
+  double err = 0;
+  for (int i = 0; i < c; ++i) err = std::max(err, fabs(S[i] - ref[i]) / ref[0]);
+  printf("%-22s r=%d c=%d threads=%d  %8.1f us  sweeps=%d  err=%.2e  (%s)\n", name, r, c, threads, 1000.0 * ms / reps, sw,
+         err, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(dS);
+  cudaFree(dsw);
+}
+
 template <int LPP, int RW, int FAST>
 void run(const char* name, const double* dM, int r, int c, const std::vector<double>& ref) {
   constexpr int RS = LPP * RW + 4;
@@ -234,6 +386,8 @@ int main(int argc, char** argv) {
     if (w <= 32) {
       run<8, 4, 0>("lpp8 rw4 ieee", dM, r, c, ref);
       run<8, 4, 2>("lpp8 rw4 mufu64", dM, r, c, ref);
+      run_reg<8, 4>("REG lpp8 rw4", dM, r, c, ref);
+      run_reg<4, 8>("REG lpp4 rw8", dM, r, c, ref);
       run<8, 4, 3>("lpp8 rw4 mufu64+f32n", dM, r, c, ref);
       run<4, 8, 2>("lpp4 rw8 mufu64", dM, r, c, ref);
       run<4, 8, 3>("lpp4 rw8 mufu64+f32n", dM, r, c, ref);
@@ -245,6 +399,8 @@ int main(int argc, char** argv) {
       run<8, 8, 3>("lpp8 rw8 mufu64+f32n", dM, r, c, ref);
       run<4, 16, 0>("lpp4 rw16 ieee", dM, r, c, ref);
       run<4, 16, 2>("lpp4 rw16 mufu64", dM, r, c, ref);
+      run_reg<4, 16>("REG lpp4 rw16", dM, r, c, ref);
+      run_reg<8, 8>("REG lpp8 rw8", dM, r, c, ref);
       run<4, 16, 3>("lpp4 rw16 mufu64+f32n", dM, r, c, ref);
     }
     cudaFree(dM);
