@@ -180,11 +180,10 @@ __global__ void __launch_bounds__(256) k_jac_reg(const double* __restrict__ M, i
     }
   }
   const double tol2 = tol * tol;
-  int sweep = 0, R = 0;
+  int sweep = 0, R = 0, h = active ? T : 0;
   for (; sweep < 60; ++sweep) {
     int rotated = 0;
     for (int round = 0; round < m1; ++round, ++R) {
-      const int h = active ? ((T - (R % npairs)) % npairs + npairs) % npairs : 0;
       double a0 = 0.0, b0 = 0.0, c0 = 0.0, a1 = 0.0, b1 = 0.0, c1 = 0.0;
 #pragma unroll
       for (int t = 0; t < RW; t += 2) {
@@ -218,39 +217,33 @@ __global__ void __launch_bounds__(256) k_jac_reg(const double* __restrict__ M, i
           y[k] = sn * u + cs * v;
         }
       }
-      // hand the moving columns to their next owners (slots by NEW logical index)
+      // hand the moving columns to their next owners (slots by NEW logical index); predicated,
+      // no divergent branches (a warp reaching the next round's shuffles diverged is very slow)
       double* sm_w = Sm + (R & 1) * 32 * RS;
       double* sp_w = Sp + (R & 1) * RS;
-      if (active) {
-        if (h == 0) {
-          if (npairs > 1) {
+      {
+        const bool h0 = h == 0, hl = (h == npairs - 1) && !h0, two = npairs > 1;
+        double* ydst = h0 ? sm_w : (hl ? sp_w : sm_w + (h + 1) * RS);
 #pragma unroll
-            for (int t = 0; t < RW; ++t) { sm_w[1 * RS + sl + LPP * t] = x[t]; sm_w[0 * RS + sl + LPP * t] = y[t]; }
-          }
-        } else if (h == npairs - 1) {
-#pragma unroll
-          for (int t = 0; t < RW; ++t) sp_w[sl + LPP * t] = y[t];
-        } else {
-#pragma unroll
-          for (int t = 0; t < RW; ++t) sm_w[(h + 1) * RS + sl + LPP * t] = y[t];
+        for (int t = 0; t < RW; ++t) {
+          if (active) ydst[sl + LPP * t] = y[t];
+          if (active && h0 && two) sm_w[RS + sl + LPP * t] = x[t];
         }
-      }
-      __syncthreads();
-      if (active && npairs > 1) {
-        const int hn = h == 0 ? npairs - 1 : h - 1;
-        if (h == 0) {
+        __syncthreads();
+        const int hn = h0 ? npairs - 1 : h - 1;
+        const double* ysrc = sm_w + hn * RS;
 #pragma unroll
-          for (int t = 0; t < RW; ++t) { x[t] = sp_w[sl + LPP * t]; y[t] = sm_w[hn * RS + sl + LPP * t]; }
-        } else {
-#pragma unroll
-          for (int t = 0; t < RW; ++t) y[t] = sm_w[hn * RS + sl + LPP * t];
+        for (int t = 0; t < RW; ++t) {
+          const double yn = ysrc[sl + LPP * t];
+          y[t] = (active && two) ? yn : y[t];
+          if (active && h0 && two) x[t] = sp_w[sl + LPP * t];
         }
+        h = active ? hn : 0;
       }
     }
     if (!__syncthreads_or(rotated)) { ++sweep; break; }
   }
   if (active) {
-    const int h = ((T - (R % npairs)) % npairs + npairs) % npairs;
     const int rr = R % m1;
     const int pc = h == 0 ? rr : (rr + h) % m1, mc = h == 0 ? m1 : ((rr - h) % m1 + m1) % m1;
 #pragma unroll
